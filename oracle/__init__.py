@@ -1,0 +1,228 @@
+"""CPU oracle for the arXiv 2411.06465 memory estimator (ctypes over
+oracle/me_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  The product
+package paper_2411_06465_b200 never imports it, and it never imports the
+product.  Parity status per function is listed in DESIGN.md §3 ("parity
+unpinned" for readings R8, R19, R20 beyond their reductions to the paper).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+SRC = HERE / "me_oracle.c"
+LIB = HERE / "libme_oracle.so"
+
+OK, EINVAL, EDIV, EOVERFLOW, ENOMEM, ERANGE = 0, 1, 2, 3, 4, 7
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, what=""):
+        super().__init__(f"oracle status {status} {what}")
+        self.status = status
+
+
+def build(force: bool = False) -> Path:
+    if force or not LIB.exists() or LIB.stat().st_mtime < max(SRC.stat().st_mtime,
+                                                               (HERE / "me_oracle.h").stat().st_mtime):
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-Wall", "-shared", "-fPIC", "-pthread",
+                               str(SRC), "-o", str(LIB)])
+    return LIB
+
+
+class Model(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in ("h", "f", "L", "a", "k", "v")]
+
+
+class Cfg(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in ("d", "t", "p", "c", "b", "s", "gbs", "L0")] + [
+        ("rc", ctypes.c_uint8), ("dopt", ctypes.c_uint8), ("uneven", ctypes.c_uint8),
+        ("pad_", ctypes.c_uint8)]
+
+
+class Breakdown(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in
+                ("params", "grads", "optim", "act_layers", "act_embed", "act_head", "total")]
+
+
+TERMS = ("params", "grads", "optim", "act_layers", "act_embed", "act_head", "total")
+
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+
+
+class SpaceC(ctypes.Structure):
+    _fields_ = [("models", ctypes.POINTER(Model)), ("n_models", ctypes.c_uint32),
+                ("world", _u32p), ("n_world", ctypes.c_uint32),
+                ("cap_bytes", _u64p), ("n_caps", ctypes.c_uint32),
+                ("gpus_per_node", ctypes.c_uint32),
+                ("mbs", _u32p), ("n_mbs", ctypes.c_uint32),
+                ("seq", _u32p), ("n_seq", ctypes.c_uint32),
+                ("rc_mask", ctypes.c_uint8), ("do_mask", ctypes.c_uint8),
+                ("uneven", ctypes.c_uint8), ("pad_", ctypes.c_uint8),
+                ("gbs", ctypes.c_uint32), ("max_t", ctypes.c_uint32), ("max_c", ctypes.c_uint32),
+                ("max_p", ctypes.c_uint32), ("thr_num", ctypes.c_uint32),
+                ("thr_den", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(str(build()))
+        P = ctypes.POINTER
+        for name in ("or_attention_params", "or_ffn_params", "or_total_params"):
+            getattr(_lib, name).argtypes = [P(Model), _u64p]
+        _lib.or_stage0_params.argtypes = [P(Model), ctypes.c_uint32, ctypes.c_uint32,
+                                          ctypes.c_uint32, _u64p]
+        _lib.or_activation_per_layer.argtypes = [P(Model), ctypes.c_uint32, ctypes.c_uint32, _u64p]
+        _lib.or_first_stage_layers.argtypes = [P(Model), P(Cfg)]
+        _lib.or_first_stage_layers.restype = ctypes.c_uint32
+        _lib.or_estimate.argtypes = [P(Model), P(Cfg), P(Breakdown)]
+        _lib.or_cap_mask.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_uint32, ctypes.c_uint32,
+                                     ctypes.c_uint32]
+        _lib.or_cap_mask.restype = ctypes.c_uint32
+        _lib.or_space_size.argtypes = [P(SpaceC), _u64p]
+        _lib.or_decode.argtypes = [P(SpaceC), ctypes.c_uint64, _u32p, _u32p, P(Cfg)]
+        _lib.or_sweep.argtypes = [P(SpaceC), ctypes.c_uint64, ctypes.c_uint64, _u64p,
+                                  P(Breakdown), ctypes.c_uint64, _u64p, _u64p, ctypes.c_int]
+    return _lib
+
+
+def _model(shape) -> Model:
+    return Model(*[int(x) for x in shape])
+
+
+def _scalar(fn, shape, *args):
+    out = ctypes.c_uint64()
+    st = fn(ctypes.byref(_model(shape)), *args, ctypes.byref(out))
+    if st:
+        raise OracleError(st, fn.__name__)
+    return out.value
+
+
+def attention_params(shape):
+    return _scalar(lib().or_attention_params, shape)
+
+
+def ffn_params(shape):
+    return _scalar(lib().or_ffn_params, shape)
+
+
+def total_params(shape):
+    return _scalar(lib().or_total_params, shape)
+
+
+def stage0_params(shape, t, p, L0):
+    return _scalar(lib().or_stage0_params, shape, t, p, L0)
+
+
+def activation_per_layer(shape, s, b):
+    return _scalar(lib().or_activation_per_layer, shape, s, b)
+
+
+def make_cfg(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0) -> Cfg:
+    return Cfg(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, 0)
+
+
+def first_stage_layers(shape, **cfg):
+    return lib().or_first_stage_layers(ctypes.byref(_model(shape)), ctypes.byref(make_cfg(**cfg)))
+
+
+def estimate(shape, **cfg) -> dict:
+    """Eq.18 terms for one config; raises OracleError on a precondition failure."""
+    out = Breakdown()
+    st = lib().or_estimate(ctypes.byref(_model(shape)), ctypes.byref(make_cfg(**cfg)),
+                           ctypes.byref(out))
+    if st:
+        raise OracleError(st, str(cfg))
+    return {k: getattr(out, k) for k in TERMS}
+
+
+def estimate_status(shape, **cfg) -> int:
+    out = Breakdown()
+    return lib().or_estimate(ctypes.byref(_model(shape)), ctypes.byref(make_cfg(**cfg)),
+                             ctypes.byref(out))
+
+
+def cap_mask(total, cap_bytes, num=4, den=5) -> int:
+    caps = (ctypes.c_uint64 * max(1, len(cap_bytes)))(*cap_bytes)
+    return lib().or_cap_mask(total, caps, len(cap_bytes), num, den)
+
+
+class _SpaceHolder:
+    """Keeps the ctypes arrays alive for the lifetime of the struct."""
+
+    def __init__(self, sp):
+        self.models = (Model * len(sp.models))(*[_model(m) for m in sp.models])
+        self.world = (ctypes.c_uint32 * len(sp.world))(*sp.world)
+        cb = sp.cap_bytes
+        self.caps = (ctypes.c_uint64 * max(1, len(cb)))(*cb)
+        self.mbs = (ctypes.c_uint32 * len(sp.mbs))(*sp.mbs)
+        self.seq = (ctypes.c_uint32 * len(sp.seq))(*sp.seq)
+        self.c = SpaceC(self.models, len(sp.models), self.world, len(sp.world), self.caps, len(cb),
+                        sp.gpus_per_node, self.mbs, len(sp.mbs), self.seq, len(sp.seq),
+                        sp.rc_mask, sp.do_mask, sp.uneven, 0, sp.gbs, sp.max_t, sp.max_c,
+                        sp.max_p, sp.thr_num, sp.thr_den)
+
+
+def space_size(sp) -> int:
+    h = _SpaceHolder(sp)
+    n = ctypes.c_uint64()
+    st = lib().or_space_size(ctypes.byref(h.c), ctypes.byref(n))
+    if st:
+        raise OracleError(st, "space_size")
+    return n.value
+
+
+def decode(sp, index):
+    h = _SpaceHolder(sp)
+    mid, world, cfg = ctypes.c_uint32(), ctypes.c_uint32(), Cfg()
+    st = lib().or_decode(ctypes.byref(h.c), index, ctypes.byref(mid), ctypes.byref(world),
+                         ctypes.byref(cfg))
+    if st:
+        raise OracleError(st, f"decode {index}")
+    return mid.value, world.value, {k: getattr(cfg, k) for k in
+                                    ("d", "t", "p", "c", "b", "s", "gbs", "rc", "dopt")}
+
+
+def sweep(sp, begin=0, end=0, rows=True, threads=None, max_rows=None):
+    """Survivors of [begin, end) in ascending index order.
+
+    Returns (idx_mask uint64[n], rows uint64[n, 7] or None, count, cap_counts)."""
+    h = _SpaceHolder(sp)
+    threads = threads or 1
+    count = ctypes.c_uint64()
+    cc = (ctypes.c_uint64 * 8)()
+    if rows:
+        if max_rows is None:
+            n_all = (end or space_size(sp)) - begin
+            max_rows = max(1, n_all)
+        idx = np.zeros(max_rows, dtype=np.uint64)
+        rw = np.zeros((max_rows, 7), dtype=np.uint64)
+        st = lib().or_sweep(ctypes.byref(h.c), begin, end, idx.ctypes.data_as(_u64p),
+                            rw.ctypes.data_as(ctypes.POINTER(Breakdown)), max_rows,
+                            ctypes.byref(count), cc, threads)
+    else:
+        st = lib().or_sweep(ctypes.byref(h.c), begin, end, None, None, 0, ctypes.byref(count), cc,
+                            threads)
+    if st:
+        raise OracleError(st, "sweep")
+    n = count.value
+    caps = [cc[i] for i in range(len(sp.caps_gb))]
+    if rows:
+        return idx[:n].copy(), rw[:n].copy(), n, caps
+    return None, None, n, caps
+
+
+def default_threads() -> int:
+    return max(1, len(os.sched_getaffinity(0)))

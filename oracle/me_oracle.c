@@ -1,0 +1,592 @@
+/*
+ * me_oracle.c -- plain, slow, obviously-correct CPU oracle (see me_oracle.h).
+ *
+ * TEST INFRASTRUCTURE ONLY (tests/, __graft_entry__.smoke(), bench.py
+ * cpu_baseline / --impl reference).  Shares nothing with the CUDA path.
+ *
+ * Each estimator step below follows the printed equation it cites, as an exact
+ * rational; no factoring, hoisting or reordering beyond what the equation says.
+ */
+#include "me_oracle.h"
+
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef __int128 i128;
+
+/* ------------------------------------------------------------------ */
+/* exact rationals                                                     */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    i128 n, d; /* d > 0, gcd(|n|, d) = 1 */
+} rat;
+
+static __thread int g_overflow; /* set when a rational step overflows 127 bits */
+
+static i128 gcd128(i128 a, i128 b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b) {
+        i128 r = a % b;
+        a = b;
+        b = r;
+    }
+    return a;
+}
+
+static rat R(i128 n, i128 d) {
+    rat r;
+    if (d == 0) { g_overflow = 1; r.n = 0; r.d = 1; return r; }
+    if (d < 0) { n = -n; d = -d; }
+    i128 g = gcd128(n, d);
+    if (g == 0) g = 1;
+    r.n = n / g;
+    r.d = d / g;
+    return r;
+}
+static rat RI(i128 n) { return R(n, 1); }
+
+static i128 mul128(i128 a, i128 b) {
+    i128 r;
+    if (__builtin_mul_overflow(a, b, &r)) g_overflow = 1;
+    return r;
+}
+static i128 add128(i128 a, i128 b) {
+    i128 r;
+    if (__builtin_add_overflow(a, b, &r)) g_overflow = 1;
+    return r;
+}
+static rat radd(rat x, rat y) { return R(add128(mul128(x.n, y.d), mul128(y.n, x.d)), mul128(x.d, y.d)); }
+static rat rmul(rat x, rat y) {
+    /* cross-reduce first so products stay small */
+    i128 g1 = gcd128(x.n, y.d), g2 = gcd128(y.n, x.d);
+    if (g1 == 0) g1 = 1;
+    if (g2 == 0) g2 = 1;
+    return R(mul128(x.n / g1, y.n / g2), mul128(x.d / g2, y.d / g1));
+}
+static rat rdiv(rat x, rat y) { return rmul(x, R(y.d, y.n)); }
+
+/* integer value of an exact rational; sets *bad if it is not an integer or
+ * does not fit below 2^63 */
+static uint64_t to_u64(rat x, int* bad) {
+    if (x.d != 1) { *bad = OR_EDIV; return 0; }
+    if (x.n < 0 || x.n >= ((i128)1 << 63)) { *bad = OR_EOVERFLOW; return 0; }
+    return (uint64_t)x.n;
+}
+
+/* ------------------------------------------------------------------ */
+/* parameter counts                                                    */
+/* ------------------------------------------------------------------ */
+
+static int model_ok(const or_model* m) {
+    if (!m) return OR_EINVAL;
+    if (!m->h || !m->f || !m->L || !m->a || !m->k || !m->v) return OR_EINVAL;
+    /* SPEC S:38-42 / Table "Variable names": k | a (GQA group size), a | h */
+    if (m->a % m->k || m->h % m->a) return OR_EINVAL;
+    return OR_OK;
+}
+
+/* Eq.1: W_Q, W_O are (h, h); W_K, W_V are (h, h/g), g = a/k.
+ * Attention parameters per layer = 2 h^2 (1 + k/a). */
+static rat eq1_attention(const or_model* m) {
+    rat h = RI(m->h);
+    return rmul(RI(2), rmul(rmul(h, h), radd(RI(1), R(m->k, m->a))));
+}
+
+/* Eq.2: up (h, h_ffn), gate (h, h_ffn), down (h_ffn, h) = 3 h h_ffn */
+static rat eq2_ffn(const or_model* m) { return rmul(RI(3), rmul(RI(m->h), RI(m->f))); }
+
+/* Eq.3, first line: 2hv + L(2h^2(1+k/a) + 3h^2 h_ffn/h + 2h) + h */
+static rat eq3_total(const or_model* m) {
+    rat h = RI(m->h), v = RI(m->v), L = RI(m->L);
+    rat ffn = rmul(RI(3), rmul(rmul(h, h), R(m->f, m->h)));
+    rat per_layer = radd(radd(eq1_attention(m), ffn), rmul(RI(2), h));
+    return radd(radd(rmul(RI(2), rmul(h, v)), rmul(L, per_layer)), h);
+}
+
+int or_attention_params(const or_model* m, uint64_t* out) {
+    int st = model_ok(m);
+    if (st) return st;
+    g_overflow = 0;
+    int bad = 0;
+    uint64_t r = to_u64(eq1_attention(m), &bad);
+    if (g_overflow) return OR_EOVERFLOW;
+    if (bad) return bad;
+    *out = r;
+    return OR_OK;
+}
+int or_ffn_params(const or_model* m, uint64_t* out) {
+    int st = model_ok(m);
+    if (st) return st;
+    g_overflow = 0;
+    int bad = 0;
+    uint64_t r = to_u64(eq2_ffn(m), &bad);
+    if (g_overflow) return OR_EOVERFLOW;
+    if (bad) return bad;
+    *out = r;
+    return OR_OK;
+}
+int or_total_params(const or_model* m, uint64_t* out) {
+    int st = model_ok(m);
+    if (st) return st;
+    g_overflow = 0;
+    int bad = 0;
+    uint64_t r = to_u64(eq3_total(m), &bad);
+    if (g_overflow) return OR_EOVERFLOW;
+    if (bad) return bad;
+    *out = r;
+    return OR_OK;
+}
+
+/* Stage-0 parameter shard Psi_s.
+ *  p = 1: Eq.6  2hv/t + h + 2 L h^2 ((1 + k/a + 3/2 h_ffn/h)/t + 1/h)
+ *         (reading R4: both vocab matrices and the final norm live on the only stage;
+ *          Eq.18 prints hv/t, which the tables reject)
+ *  p > 1: Eq.7  hv/t + 2 (L/p) h^2 ((1 + k/a + 3/2 h_ffn/h)/t + 1/h)
+ *         (reading R5: no final norm on the first stage)
+ * with L/p replaced by the first-stage layer count L0 (R19; L0 = L/p when p | L). */
+static rat psi_stage0(const or_model* m, uint32_t t, uint32_t p, uint32_t L0) {
+    rat h = RI(m->h), v = RI(m->v), T = RI(t);
+    rat inner = radd(radd(RI(1), R(m->k, m->a)), rmul(R(3, 2), R(m->f, m->h)));
+    rat bracket = radd(rdiv(inner, T), R(1, m->h));
+    rat layers = rmul(rmul(RI(2), RI(L0)), rmul(rmul(h, h), bracket));
+    if (p == 1) return radd(radd(rdiv(rmul(RI(2), rmul(h, v)), T), h), layers);
+    return radd(rdiv(rmul(h, v), T), layers);
+}
+
+int or_stage0_params(const or_model* m, uint32_t t, uint32_t p, uint32_t L0, uint64_t* out) {
+    int st = model_ok(m);
+    if (st) return st;
+    if (!t || !p || !L0) return OR_EINVAL;
+    g_overflow = 0;
+    int bad = 0;
+    uint64_t r = to_u64(psi_stage0(m, t, p, L0), &bad);
+    if (g_overflow) return OR_EOVERFLOW;
+    if (bad) return bad;
+    *out = r;
+    return OR_OK;
+}
+
+/* Eq.12: sbh (12 + 4 k/a + 8 h_ffn/h) */
+static rat eq12_bracket(const or_model* m) {
+    return radd(radd(RI(12), rmul(RI(4), R(m->k, m->a))), rmul(RI(8), R(m->f, m->h)));
+}
+
+int or_activation_per_layer(const or_model* m, uint32_t s, uint32_t b, uint64_t* out) {
+    int st = model_ok(m);
+    if (st) return st;
+    g_overflow = 0;
+    int bad = 0;
+    rat sbh = rmul(rmul(RI(s), RI(b)), RI(m->h));
+    uint64_t r = to_u64(rmul(sbh, eq12_bracket(m)), &bad);
+    if (g_overflow) return OR_EOVERFLOW;
+    if (bad) return bad;
+    *out = r;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* preconditions                                                       */
+/* ------------------------------------------------------------------ */
+
+/* R19: first-stage layers.  p = 1 -> L (Eq.6); p | L -> L/p (Eq.7);
+ * uneven allowed -> ceil(L/p) (the largest stage of any split); an explicit L0
+ * must leave at least one layer for each of the other p-1 stages. */
+uint32_t or_first_stage_layers(const or_model* m, const or_cfg* c) {
+    if (!m || !c || !c->p || c->p > m->L) return 0;
+    if (c->L0) {
+        if (c->p == 1) return c->L0 == m->L ? c->L0 : 0;
+        if (c->L0 > m->L - (c->p - 1)) return 0;
+        return c->L0;
+    }
+    if (c->p == 1) return m->L;
+    if (m->L % c->p == 0) return m->L / c->p;
+    if (c->uneven) return (m->L + c->p - 1) / c->p;
+    return 0;
+}
+
+static int cfg_check(const or_model* m, const or_cfg* c) {
+    int st = model_ok(m);
+    if (st) return st;
+    if (!c || !c->d || !c->t || !c->p || !c->c || !c->b || !c->s) return OR_EINVAL;
+    /* R10: t | k (then t | a because k | a), t | v, t | h_ffn */
+    if (m->k % c->t || m->v % c->t || m->f % c->t) return OR_EDIV;
+    /* Eq.17: c splits the sequence */
+    if (c->s % c->c) return OR_EDIV;
+    if (c->p > m->L) return OR_EDIV;
+    if (!or_first_stage_layers(m, c)) return OR_EDIV;
+    /* R17: with a global batch the DP replicas must split it evenly */
+    if (c->gbs && c->gbs % ((uint64_t)c->d * c->b)) return OR_EDIV;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Eq.18 with its parts                                                */
+/* ------------------------------------------------------------------ */
+int or_estimate(const or_model* m, const or_cfg* c, or_breakdown* out) {
+    int st = cfg_check(m, c);
+    if (st) return st;
+    g_overflow = 0;
+    int bad = 0;
+    uint32_t L0 = or_first_stage_layers(m, c);
+
+    /* in-flight microbatches on stage 0: Eq.16 holds p; R17 caps it
+     * at m = gbs/(d b) when a global batch is given */
+    uint64_t n_inf = c->p;
+    if (c->gbs) {
+        uint64_t mb = c->gbs / ((uint64_t)c->d * c->b);
+        if (mb < n_inf) n_inf = mb;
+    }
+
+    /* model states: ledger P:192-199 (weight BF16 2 B, grad FP32 4 B, Adam
+     * master/momentum/variance FP32 4+4+4 B), sharding Eq.5 / Eq.10 (optimizer
+     * over d*c; R9: gradients not sharded), Eq.4 when the distributed optimizer
+     * is off (R21) */
+    rat psi = psi_stage0(m, c->t, c->p, L0);
+    uint64_t psi_s = to_u64(psi, &bad);
+    rat params = rmul(RI(2), psi);
+    rat grads = rmul(RI(4), psi);
+    rat optim;
+    if (c->dopt) {
+        rat share = rdiv(psi, RI((i128)c->d * c->c)); /* Psi_s / (d c) */
+        /* R8: the largest d*c rank holds ceil(Psi_s/(d c)) whole parameters */
+        i128 ceil_share = (share.n + share.d - 1) / share.d;
+        optim = rmul(RI(12), RI(ceil_share));
+    } else {
+        optim = rmul(RI(12), psi);
+    }
+
+    /* activations: Eq.17, generalised per DESIGN.md §3:
+     *   sbh/(tc) * ( (12 + 4k/a + 8h_ffn/h) n_inf L0 + 8 n_inf + delta_{p,1} 4(1 + v/h) )
+     * n_inf L0 = L in paper mode (R16); the 8p embedding term keeps its printed h
+     * (R13); the LM-head term only at p = 1 (R14).  Recompute (R20, extension):
+     * the layer part becomes 2 n_inf L0 + (12 + 4k/a + 8h_ffn/h). */
+    rat sbh_tc = R((i128)c->s * c->b * m->h, (i128)c->t * c->c);
+    rat br = eq12_bracket(m);
+    rat layers;
+    if (c->rc)
+        layers = rmul(sbh_tc, radd(RI((i128)2 * n_inf * L0), br));
+    else
+        layers = rmul(sbh_tc, rmul(br, RI((i128)n_inf * L0)));
+    rat embed = rmul(sbh_tc, RI((i128)8 * n_inf));
+    rat head = RI(0);
+    if (c->p == 1) head = rmul(sbh_tc, rmul(RI(4), radd(RI(1), R(m->v, m->h))));
+
+    or_breakdown r;
+    r.params = to_u64(params, &bad);
+    r.grads = to_u64(grads, &bad);
+    r.optim = to_u64(optim, &bad);
+    r.act_layers = to_u64(layers, &bad);
+    r.act_embed = to_u64(embed, &bad);
+    r.act_head = to_u64(head, &bad);
+    (void)psi_s;
+    rat total = radd(radd(radd(params, grads), radd(optim, layers)), radd(embed, head));
+    r.total = to_u64(total, &bad);
+    if (g_overflow) return OR_EOVERFLOW;
+    if (bad) return bad;
+    *out = r;
+    return OR_OK;
+}
+
+/* 80% rule (reading R2/R3): feasible for capacity j iff
+ * total <= (num/den) * cap_j, compared exactly */
+uint32_t or_cap_mask(uint64_t total, const uint64_t* cap_bytes, uint32_t n_caps, uint32_t num,
+                     uint32_t den) {
+    uint32_t mask = 0;
+    for (uint32_t j = 0; j < n_caps; j++)
+        if ((i128)total * den <= (i128)cap_bytes[j] * num) mask |= 1u << j;
+    return mask;
+}
+
+/* ------------------------------------------------------------------ */
+/* canonical enumeration                                */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    uint32_t t, c, p, d;
+    uint64_t w; /* configs per (model, N, t, c, p): valid (b, s) pairs x rc x do */
+} tup;
+
+typedef struct {
+    tup* v;
+    uint32_t n;
+} tuplist;
+
+static int popc2(uint32_t mask) { return (mask & 1) + ((mask >> 1) & 1); }
+
+/* all (t, c, p) with t*c*p | N in ascending (t, c, p) order and their inner size */
+static int build_tuples(const or_space* sp, uint32_t N, tuplist* out) {
+    uint32_t cap = 64, n = 0;
+    tup* v = (tup*)malloc(cap * sizeof(tup));
+    if (!v) return OR_ENOMEM;
+    for (uint32_t t = 1; t <= N; t++) {
+        if (N % t) continue;
+        for (uint32_t c = 1; c <= N / t; c++) {
+            if ((N / t) % c) continue;
+            for (uint32_t p = 1; p <= N / t / c; p++) {
+                if ((N / t / c) % p) continue;
+                uint32_t d = N / t / c / p;
+                uint64_t pairs = 0;
+                for (uint32_t bi = 0; bi < sp->n_mbs; bi++)
+                    for (uint32_t si = 0; si < sp->n_seq; si++) {
+                        uint32_t b = sp->mbs[bi], s = sp->seq[si];
+                        if (s % c) continue;
+                        if (sp->gbs && sp->gbs % ((uint64_t)d * b)) continue;
+                        pairs++;
+                    }
+                if (n == cap) {
+                    cap *= 2;
+                    tup* nv = (tup*)realloc(v, cap * sizeof(tup));
+                    if (!nv) { free(v); return OR_ENOMEM; }
+                    v = nv;
+                }
+                v[n].t = t; v[n].c = c; v[n].p = p; v[n].d = d;
+                v[n].w = pairs * popc2(sp->rc_mask) * popc2(sp->do_mask);
+                n++;
+            }
+        }
+    }
+    out->v = v;
+    out->n = n;
+    return OR_OK;
+}
+
+static int valid_static(const or_space* sp, const or_model* m, const tup* u) {
+    if (m->k % u->t || m->v % u->t || m->f % u->t) return 0;
+    if (u->p > m->L) return 0;
+    if (!sp->uneven && m->L % u->p) return 0;
+    if (sp->max_t && u->t > sp->max_t) return 0;
+    if (sp->max_c && u->c > sp->max_c) return 0;
+    if (sp->max_p && u->p > sp->max_p) return 0;
+    if (sp->gpus_per_node && u->t > sp->gpus_per_node) return 0;
+    return 1;
+}
+
+static int space_ok(const or_space* sp) {
+    if (!sp || !sp->models || !sp->n_models || !sp->world || !sp->n_world || !sp->mbs ||
+        !sp->n_mbs || !sp->seq || !sp->n_seq)
+        return OR_EINVAL;
+    if (sp->n_caps > 8 || (sp->n_caps && !sp->cap_bytes)) return OR_EINVAL;
+    if (!(sp->rc_mask & 3) || !(sp->do_mask & 3)) return OR_EINVAL;
+    if (!sp->thr_num || !sp->thr_den || sp->thr_num > 1024 || sp->thr_den > 1024) return OR_EINVAL;
+    for (uint32_t i = 0; i < sp->n_models; i++)
+        if (model_ok(&sp->models[i])) return OR_EINVAL;
+    for (uint32_t i = 0; i < sp->n_world; i++)
+        if (!sp->world[i]) return OR_EINVAL;
+    for (uint32_t i = 0; i < sp->n_mbs; i++)
+        if (!sp->mbs[i]) return OR_EINVAL;
+    for (uint32_t i = 0; i < sp->n_seq; i++)
+        if (!sp->seq[i]) return OR_EINVAL;
+    return OR_OK;
+}
+
+typedef struct {
+    tuplist* tl; /* one per world size */
+    uint32_t n;
+} tables;
+
+static void free_tables(tables* T) {
+    for (uint32_t i = 0; i < T->n; i++) free(T->tl[i].v);
+    free(T->tl);
+}
+static int build_tables(const or_space* sp, tables* T) {
+    T->n = sp->n_world;
+    T->tl = (tuplist*)calloc(sp->n_world, sizeof(tuplist));
+    if (!T->tl) return OR_ENOMEM;
+    for (uint32_t i = 0; i < sp->n_world; i++) {
+        int st = build_tuples(sp, sp->world[i], &T->tl[i]);
+        if (st) { free_tables(T); return st; }
+    }
+    return OR_OK;
+}
+
+int or_space_size(const or_space* sp, uint64_t* n) {
+    int st = space_ok(sp);
+    if (st) return st;
+    tables T;
+    if ((st = build_tables(sp, &T))) return st;
+    uint64_t idx = 0;
+    for (uint32_t mi = 0; mi < sp->n_models; mi++)
+        for (uint32_t ni = 0; ni < sp->n_world; ni++)
+            for (uint32_t j = 0; j < T.tl[ni].n; j++)
+                if (valid_static(sp, &sp->models[mi], &T.tl[ni].v[j])) idx += T.tl[ni].v[j].w;
+    free_tables(&T);
+    *n = idx;
+    return OR_OK;
+}
+
+/* sink for survivors of one contiguous index range */
+typedef struct {
+    const or_space* sp;
+    const tables* T;
+    uint64_t begin, end;
+    int want_rows;
+    uint64_t* idx;
+    or_breakdown* rows;
+    uint64_t n, cap;
+    uint64_t cap_counts[8];
+    int status;
+    /* decode target */
+    int decode_only;
+    uint32_t dec_model, dec_world;
+    or_cfg dec_cfg;
+} walk_t;
+
+static int push(walk_t* w, uint64_t idx_mask, const or_breakdown* r) {
+    if (!w->want_rows) { w->n++; return OR_OK; }
+    if (w->n == w->cap) {
+        uint64_t nc = w->cap ? w->cap * 2 : 1024;
+        uint64_t* ni = (uint64_t*)realloc(w->idx, nc * sizeof(uint64_t));
+        if (!ni) return OR_ENOMEM;
+        w->idx = ni;
+        or_breakdown* nr = (or_breakdown*)realloc(w->rows, nc * sizeof(or_breakdown));
+        if (!nr) return OR_ENOMEM;
+        w->rows = nr;
+        w->cap = nc;
+    }
+    w->idx[w->n] = idx_mask;
+    w->rows[w->n] = *r;
+    w->n++;
+    return OR_OK;
+}
+
+/* The canonical nested loops: model -> N -> (t asc, c asc, p asc) -> b -> s ->
+ * rc -> do.  Tuples failing valid_static and (b, s) pairs failing c | s or
+ * (d b) | gbs consume no index. */
+static void walk(walk_t* w) {
+    const or_space* sp = w->sp;
+    uint64_t idx = 0;
+    for (uint32_t mi = 0; mi < sp->n_models; mi++) {
+        const or_model* m = &sp->models[mi];
+        for (uint32_t ni = 0; ni < sp->n_world; ni++) {
+            const tuplist* tl = &w->T->tl[ni];
+            for (uint32_t j = 0; j < tl->n; j++) {
+                const tup* u = &tl->v[j];
+                if (!valid_static(sp, m, u)) continue;
+                if (idx + u->w <= w->begin) { idx += u->w; continue; }
+                if (idx >= w->end) return;
+                for (uint32_t bi = 0; bi < sp->n_mbs; bi++)
+                    for (uint32_t si = 0; si < sp->n_seq; si++) {
+                        uint32_t b = sp->mbs[bi], s = sp->seq[si];
+                        if (s % u->c) continue;
+                        if (sp->gbs && sp->gbs % ((uint64_t)u->d * b)) continue;
+                        for (uint32_t rc = 0; rc < 2; rc++) {
+                            if (!((sp->rc_mask >> rc) & 1)) continue;
+                            for (uint32_t dopt = 0; dopt < 2; dopt++) {
+                                if (!((sp->do_mask >> dopt) & 1)) continue;
+                                if (idx >= w->begin && idx < w->end) {
+                                    or_cfg c;
+                                    memset(&c, 0, sizeof c);
+                                    c.d = u->d; c.t = u->t; c.p = u->p; c.c = u->c;
+                                    c.b = b; c.s = s; c.gbs = sp->gbs; c.L0 = 0;
+                                    c.rc = (uint8_t)rc; c.dopt = (uint8_t)dopt;
+                                    c.uneven = sp->uneven;
+                                    if (w->decode_only) {
+                                        w->dec_model = mi;
+                                        w->dec_world = sp->world[ni];
+                                        w->dec_cfg = c;
+                                        w->status = OR_OK;
+                                        return;
+                                    }
+                                    or_breakdown r;
+                                    int st = or_estimate(m, &c, &r);
+                                    if (st) { w->status = st; return; }
+                                    uint32_t mask = or_cap_mask(r.total, sp->cap_bytes, sp->n_caps,
+                                                                sp->thr_num, sp->thr_den);
+                                    for (uint32_t q = 0; q < sp->n_caps; q++)
+                                        w->cap_counts[q] += (mask >> q) & 1;
+                                    if (mask) {
+                                        st = push(w, idx | ((uint64_t)mask << 56), &r);
+                                        if (st) { w->status = st; return; }
+                                    }
+                                }
+                                idx++;
+                                if (idx >= w->end) return;
+                            }
+                        }
+                    }
+            }
+        }
+    }
+}
+
+int or_decode(const or_space* sp, uint64_t index, uint32_t* model_id, uint32_t* world, or_cfg* cfg) {
+    int st = space_ok(sp);
+    if (st) return st;
+    tables T;
+    if ((st = build_tables(sp, &T))) return st;
+    walk_t w;
+    memset(&w, 0, sizeof w);
+    w.sp = sp; w.T = &T; w.begin = index; w.end = index + 1;
+    w.decode_only = 1;
+    w.status = OR_ERANGE; /* stays if index is past the end */
+    walk(&w);
+    free_tables(&T);
+    if (w.status) return w.status;
+    if (model_id) *model_id = w.dec_model;
+    if (world) *world = w.dec_world;
+    if (cfg) *cfg = w.dec_cfg;
+    return OR_OK;
+}
+
+static void* walk_thread(void* arg) {
+    walk((walk_t*)arg);
+    return NULL;
+}
+
+int or_sweep(const or_space* sp, uint64_t begin, uint64_t end, uint64_t* idx_mask,
+             or_breakdown* rows, uint64_t cap, uint64_t* count, uint64_t* cap_counts,
+             int n_threads) {
+    int st = space_ok(sp);
+    if (st) return st;
+    uint64_t total;
+    if ((st = or_space_size(sp, &total))) return st;
+    if (end == 0 || end > total) end = total;
+    if (begin > end) begin = end;
+    if (n_threads < 1) n_threads = 1;
+    if ((uint64_t)n_threads > end - begin) n_threads = (int)(end - begin ? end - begin : 1);
+    tables T;
+    if ((st = build_tables(sp, &T))) return st;
+    walk_t* ws = (walk_t*)calloc((size_t)n_threads, sizeof(walk_t));
+    pthread_t* th = (pthread_t*)calloc((size_t)n_threads, sizeof(pthread_t));
+    if (!ws || !th) { free(ws); free(th); free_tables(&T); return OR_ENOMEM; }
+    uint64_t len = end - begin;
+    for (int i = 0; i < n_threads; i++) {
+        ws[i].sp = sp;
+        ws[i].T = &T;
+        ws[i].begin = begin + len * (uint64_t)i / (uint64_t)n_threads;
+        ws[i].end = begin + len * (uint64_t)(i + 1) / (uint64_t)n_threads;
+        ws[i].want_rows = (idx_mask || rows) ? 1 : 0;
+        if (ws[i].end == ws[i].begin) continue;
+        if (n_threads == 1) walk(&ws[i]);
+        else pthread_create(&th[i], NULL, walk_thread, &ws[i]);
+    }
+    if (n_threads > 1)
+        for (int i = 0; i < n_threads; i++)
+            if (ws[i].end != ws[i].begin) pthread_join(th[i], NULL);
+    uint64_t n = 0;
+    uint64_t cc[8] = {0};
+    int status = OR_OK;
+    for (int i = 0; i < n_threads; i++) {
+        if (ws[i].status && !status) status = ws[i].status;
+        for (uint32_t q = 0; q < sp->n_caps; q++) cc[q] += ws[i].cap_counts[q];
+        for (uint64_t r = 0; r < ws[i].n && ws[i].want_rows; r++) {
+            if (n + r < cap) {
+                if (idx_mask) idx_mask[n + r] = ws[i].idx[r];
+                if (rows) rows[n + r] = ws[i].rows[r];
+            }
+        }
+        n += ws[i].n;
+        free(ws[i].idx);
+        free(ws[i].rows);
+    }
+    free(ws);
+    free(th);
+    free_tables(&T);
+    if (count) *count = n;
+    if (cap_counts)
+        for (uint32_t q = 0; q < sp->n_caps; q++) cap_counts[q] = cc[q];
+    if (status) return status;
+    if ((idx_mask || rows) && n > cap) return OR_ERANGE;
+    return OR_OK;
+}
