@@ -1,0 +1,362 @@
+"""Benchmark of the estimator hot path (BASELINE.json metric: estimator
+configs/sec at 1/2/4/8 B200, roofline fraction, bit-exact feasible set).
+
+Workload: C5 = BASELINE.json configs[4], the synthetic Llama
+grid (247,776 shapes) x world sizes 8..16384 x every 4D factorisation x
+mbs 1..16 x seq 4K..128K x recompute x distributed optimizer, uneven PP
+allowed, capacities 40/80/94/192 GiB -- 8.4e10 valid configurations, which the
+north star partitions over the 8 GPUs of one box.  One unit = one eighth of
+C5 (1.05e10 configs); rank r of N owns unit r, so per-GPU work is fixed as N
+grows ("scaling": "weak") and N = 8 sweeps the whole space every step.
+
+A step = one pass of the whole hot path over every rank's unit: decode ->
+estimate -> 80% filter -> order-preserving compaction into FULL records
+(8 u64 columns), in chunks of CHUNK configs per rank (each chunk's columns are
+written to HBM; two column sets alternate), with the NCCL allgather of the
+per-chunk survivor counts (global offsets) when N > 1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode full|index|count]
+  python bench.py --impl reference ...   (the CPU oracle on the host cores)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CHUNK = 1 << 28          # configs per rank per me_plan_sweep call
+UNITS = 8                # C5 is split into 8 units (one per GPU of the box)
+WORKLOAD = "C5"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--mode", default="full", choices=["full", "index", "count"])
+    ap.add_argument("--workload", default=WORKLOAD)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def unit_range(total, unit):
+    return total * unit // UNITS, total * (unit + 1) // UNITS
+
+
+class ClockSampler:
+    """NVML clocks and throttle reasons sampled during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def cpu_baseline(sp, begin, end, budget_s=12.0):
+    """The oracle (unchanged) on the host cores over a bounded, deterministic
+    sample of the workload: evenly spaced windows of the bench range."""
+    import oracle
+    threads = oracle.default_threads()
+    # calibrate
+    t = time.perf_counter()
+    cal = 200_000
+    oracle.sweep(sp, begin, begin + cal, rows=False, threads=threads)
+    dt = time.perf_counter() - t
+    rate = cal / max(dt, 1e-6)
+    n = int(min(end - begin, max(cal, rate * budget_s)))
+    wins = 16
+    per = max(1, n // wins)
+    done, t0 = 0, time.perf_counter()
+    for w in range(wins):
+        s = begin + (end - begin) * w // wins
+        oracle.sweep(sp, s, s + per, rows=False, threads=threads)
+        done += per
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": "configs/s", "cores": threads, "kind": "oracle",
+            "sample": f"{wins} evenly spaced windows of {per} configs of the rank-0 unit of {WORKLOAD} "
+                      f"(survivor counts, all estimator terms evaluated), {done} configs in {el:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import me_inputs as mi
+    import oracle
+    sp = mi.config(args.workload)
+    total = oracle.space_size(sp)
+    b, e = unit_range(total, 0)
+    threads = oracle.default_threads()
+    per = 2_000_000
+    times = []
+    for i in range(args.warmup + args.steps):
+        s = b + (e - b) * (i % 97) // 97
+        t = time.perf_counter()
+        oracle.sweep(sp, s, s + per, rows=False, threads=threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t)
+    el = sum(times)
+    v = per * args.steps / el
+    line = {"impl": "reference", "metric": "estimator configs/sec", "value": v, "unit": "configs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": {"workload": args.workload, "sample_per_step": per},
+            "cpu_baseline": {"value": v, "unit": "configs/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{per} consecutive configs per step at evenly spaced offsets of the "
+                                       f"rank-0 unit of {args.workload}"},
+            "e2e": {"value": v, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import me_inputs as mi
+    import paper_2411_06465_b200 as me
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "launch N>1 with torchrun"
+    torch.cuda.set_device(local)
+    dev = local
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    mode = {"full": me.ME_OUT_FULL, "index": me.ME_OUT_INDEX, "count": me.ME_OUT_COUNT}[args.mode]
+    ncols = {me.ME_OUT_FULL: 8, me.ME_OUT_INDEX: 1, me.ME_OUT_COUNT: 0}[mode]
+
+    sp = mi.config(args.workload)
+    stream = torch.cuda.Stream(device=dev)
+    plan = me.Plan(sp, device=dev, stream=stream.cuda_stream)
+    total = plan.size
+    # this job: units 0..world-1; each me_plan_sweep call covers world*CHUNK
+    # consecutive configs, split evenly over the ranks by the library
+    job_b, job_e = 0, unit_range(total, world - 1)[1]
+    calls = []
+    s = job_b
+    while s < job_e:
+        e = min(job_e, s + CHUNK * world)
+        calls.append((s, e))
+        s = e
+    comm = me.Comm(dev) if world > 1 else None
+    ring = [[torch.empty(CHUNK + 64, dtype=torch.int64, device=dev) for _ in range(ncols)] for _ in range(2)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(collect=None):
+        out = []
+        for q, (b, e) in enumerate(calls):
+            r = plan.sweep(b, e, mode=mode, out_cols=ring[q & 1] if ncols else None, comm=comm)
+            out.append(r)
+        return out
+
+    def drain(results, timings=None):
+        n_local = n_global = 0
+        for r in results:
+            if r.status() != 0:
+                raise RuntimeError("caller columns overflowed")
+            lo, gl, off = r.counts()
+            n_local += lo
+            n_global += gl
+            if timings is not None:
+                timings.append(r.timing())
+            r.free()
+        return n_local, n_global
+
+    # warmup
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            drain(step())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    timings = []
+    with clocks:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            all_res = []
+            for _ in range(args.steps):
+                flush.zero_()
+                all_res.append(step())
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    n_local = n_global = 0
+    for res in all_res:
+        lo, gl = drain(res, timings)
+        n_local += lo
+        n_global += gl
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    configs = (job_e - job_b) * args.steps
+    value = configs / (ms_max / 1e3)
+
+    # per-kernel device times (CUDA events on the sweep stream)
+    count_ms = sum(x[1] for x in timings)
+    write_ms = sum(x[3] for x in timings)
+    scan_ms = sum(x[2] for x in timings)
+    n_launch = len(timings)
+    survivors_local_per_step = n_local // args.steps
+    peaks, peak_src = measured_peaks()
+    if mode != me.ME_OUT_COUNT:
+        bytes_write = survivors_local_per_step * 8 * ncols * args.steps
+        achieved = bytes_write / (write_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": f"sweep_kernel<{2 if ncols == 8 else 1},4> (write pass)",
+                "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "traffic": None, "peak_source": f"{peak_src} hbm_gbs (copy)",
+                "algorithmic_bytes_per_launch": bytes_write / max(1, n_launch),
+                "avg_launch_ms": write_ms / max(1, n_launch)}
+    else:
+        roof = {"bound": "alu", "kernel": "sweep_kernel<0,4> (count pass)", "achieved": None, "peak": None,
+                "unit": "warp-instr/s", "frac": None, "traffic": None}
+    line = {
+        "metric": "estimator configs/sec", "value": value, "unit": "configs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "space_configs": total, "configs_per_gpu_per_step": (job_e - job_b) // world,
+                   "unit": "1/8 of C5 per GPU", "mode": args.mode, "chunk_configs_per_rank": CHUNK,
+                   "caps_gib": sp.caps_gb, "threshold": "4/5", "l2": "flushed (256 MiB write) before every step; "
+                   "outputs (GBs per step) also exceed L2", "parallelism": f"index-space partition x{world}"},
+        "feasible_per_step": n_global // args.steps,
+        "kernel_ms_per_step": {"count": count_ms / args.steps, "scan": scan_ms / args.steps,
+                               "write": write_ms / args.steps},
+        "roofline": roof,
+        "gpu_launches": 3 * n_launch if mode != me.ME_OUT_COUNT else 2 * n_launch,
+        "clocks": clocks.summary(),
+    }
+
+    # e2e: the public API with host buffers -- plan creation (host tables +
+    # H2D) and a D2H of every survivor column inside the timed region
+    if not args.no_e2e:
+        e2e_ms, h2d, d2h = e2e_run(me, sp, dev, world, comm, calls, mode, ncols, args.e2e_steps, stream)
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        line["e2e"] = {"value": (job_e - job_b) * args.e2e_steps / (float(t.item()) / 1e3), "unit": "configs/s",
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps}
+    if rank == 0 and not args.no_cpu:
+        b0, e0 = unit_range(total, 0)
+        line["cpu_baseline"] = cpu_baseline(sp, b0, e0)
+    if comm:
+        comm.destroy()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_run(me, sp, dev, world, comm, calls, mode, ncols, steps, stream):
+    """End to end through the C ABI: host description in, host columns out."""
+    import ctypes
+
+    import torch
+    HOST_ROWS = 1 << 26
+    host = [torch.empty(HOST_ROWS, dtype=torch.int64, pin_memory=True) for _ in range(ncols)]
+    ring = [torch.empty(CHUNK + 64, dtype=torch.int64, device=dev) for _ in range(ncols)]
+    h2d = d2h = 0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        plan = me.Plan(sp, device=dev, stream=stream.cuda_stream)
+        h2d += plan.table_bytes  # enumeration tables built on the host and uploaded
+        for (b, e) in calls:
+            r = plan.sweep(b, e, mode=mode, out_cols=ring if ncols else None, comm=comm)
+            lo, gl, off = r.counts()
+            if ncols:
+                arr = (ctypes.c_void_p * 8)(*([h.data_ptr() for h in host] + [None] * (8 - ncols)))
+                for first in range(0, lo, HOST_ROWS):
+                    n = min(HOST_ROWS, lo - first)
+                    me.check(me.lib().me_result_copy_to_host(r.h, first, n, arr), "me_result_copy_to_host")
+                d2h += lo * 8 * ncols
+            d2h += 8
+            r.free()
+        plan.free()
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) * 1e3
+    return el, h2d // steps, d2h // steps
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,241 @@
+/*
+ * me.h -- C ABI of libme.so: batched, exact-integer evaluation of the per-GPU
+ * memory estimator of Fujii, Watanabe, Yokota, "Accelerating Large Language
+ * Model Training with 4D Parallelism and Memory Consumption Estimator"
+ * (arXiv 2411.06465) on NVIDIA B200 (sm_100a), with the paper's 80%-of-HBM
+ * feasibility filter and order-preserving compaction of the survivors.
+ *
+ * Citations: P:n = line n of the paper's LaTeX source; Eq.k is the
+ * k-th numbered equation in source order; R1..R26 are the readings of the
+ * paper listed in DESIGN.md §3.
+ *
+ * Conventions for every call
+ *  - Every call returns an int status (ME_OK = 0); out-parameters are left
+ *    untouched on error.  No C++ exception crosses this boundary.
+ *  - Inputs are borrowed for the duration of the call (the library copies what
+ *    it keeps).  Plans and results are owned by the library until their _free
+ *    call; their device memory comes from the caller's allocator callback when
+ *    one is given, else from cudaMallocAsync.
+ *  - All arithmetic on the device is unsigned 64-bit integer; there is no
+ *    floating point and no CPU fallback: without a usable CUDA device the
+ *    compute calls return ME_ECUDA.
+ *  - Calls are thread-safe on distinct plan / result / comm handles.  Sweeps of
+ *    one plan reuse its scratch memory and must be issued on one stream.
+ *  - me_last_error_detail() returns a thread-local human-readable message for
+ *    the last failing call on the calling thread.
+ */
+#ifndef ME_H
+#define ME_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    ME_OK = 0,
+    ME_EINVAL = 1,    /* NULL pointer, zero field, k not dividing a, a not dividing h,
+                         bad mask or threshold, more than 8 capacities, input
+                         outside the exact-u64 domain of the sweep (me_plan_create) */
+    ME_EDIV = 2,      /* estimator precondition (R10, Eq.17, R17, R19):
+                         t must divide k, v and h_ffn; c must divide s; p <= L;
+                         p | L unless allow_uneven_pp; (d*b) | gbs when gbs > 0 */
+    ME_EOVERFLOW = 3, /* a term would reach 2^63, or a flat index 2^56 */
+    ME_ENOMEM = 4,
+    ME_ECUDA = 5,     /* no device, launch or runtime failure */
+    ME_ENCCL = 6,
+    ME_ERANGE = 7     /* caller buffer too small, or index past the end */
+};
+
+/* Model shape, Table "Variable names": h, h_ffn, L, a, k, v.
+ * Requires all fields > 0, k | a (GQA groups), a | h. */
+typedef struct {
+    uint32_t hidden, ffn_hidden, layers, heads, kv_heads, vocab;
+} me_model;
+
+/* One training configuration.  dp, tp, pp, cp = d, t, p, c; mbs = b; seq = s.
+ *  gbs                 0 = paper mode: p microbatches in flight on stage 0
+ *                      (Eq.16); >0 = min(p, gbs/(d*b)) in flight (R17)
+ *  first_stage_layers  0 = auto: L if p = 1, L/p if p | L, ceil(L/p) if uneven
+ *                      splits are allowed (R19); else explicit, 1..L-(p-1)
+ *                      (= L when p = 1)
+ *  recompute           1 = full activation recompute (R20, extension)
+ *  dist_opt            1 = distributed optimizer, 12 B/param sharded over d*c
+ *                      (Eq.5, Eq.10; ceil rule R8); 0 = Eq.4 (18 B/param) */
+typedef struct {
+    uint32_t dp, tp, pp, cp, mbs, seq;
+    uint32_t gbs;
+    uint32_t first_stage_layers;
+    uint8_t recompute, dist_opt, allow_uneven_pp, _pad;
+} me_parallel;
+
+/* Stage-0 per-GPU bytes (Eq.18 split by the ledger of P:192-199):
+ * params = 2 Psi_s (BF16), grads = 4 Psi_s (FP32, not sharded, R9),
+ * optim = 12 ceil(Psi_s/(d c)) or 12 Psi_s, act_layers / act_embed / act_head
+ * = the three groups of Eq.17, total = their sum. */
+typedef struct {
+    uint64_t params, grads, optim, act_layers, act_embed, act_head, total;
+} me_breakdown;
+
+/* feasible for capacity j <=> total <= floor(cap_j * num / den); the paper's
+ * rule is num/den = 4/5.  1 <= num, den <= 1024. */
+typedef struct {
+    uint32_t num, den;
+} me_threshold;
+
+typedef struct {
+    const me_model* models;
+    uint32_t n_models;
+} me_model_range;
+
+/* world_sizes: the N axis, in enumeration order.  capacity_bytes: up to 8 HBM
+ * capacities in bytes (the paper's "40GB"/"94GB" are GiB, R2: pass GB * 2^30).
+ * gpus_per_node > 0 keeps only t <= gpus_per_node. */
+typedef struct {
+    const uint32_t* world_sizes;
+    uint32_t n_world;
+    const uint64_t* capacity_bytes;
+    uint32_t n_cap;
+    uint32_t gpus_per_node;
+} me_cluster;
+
+/* The remaining axes.  recompute_mask / dist_opt_mask: bit0 = off, bit1 = on
+ * (each must be 1, 2 or 3).  max_tp/max_cp/max_pp: 0 = unlimited. */
+typedef struct {
+    const uint32_t* mbs;
+    uint32_t n_mbs;
+    const uint32_t* seq;
+    uint32_t n_seq;
+    uint8_t recompute_mask, dist_opt_mask, allow_uneven_pp, _pad;
+    uint32_t gbs, max_tp, max_cp, max_pp;
+} me_cfg_range;
+
+/* Output modes of a sweep:
+ *  COUNT  survivor counts only (total and per capacity)
+ *  INDEX  one u64 column: flat index | (capacity mask << 56)
+ *  FULL   eight u64 columns (structure of arrays): index|mask, params, grads,
+ *         optim, act_layers, act_embed, act_head, total */
+typedef enum { ME_OUT_COUNT = 0, ME_OUT_INDEX = 1, ME_OUT_FULL = 2 } me_out_mode;
+
+#define ME_N_COLS 8
+
+/* Allocator callbacks (e.g. PyTorch's caching allocator).  Device memory of
+ * `bytes` bytes usable on `stream`; free receives the same stream. */
+typedef void* (*me_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*me_free_fn)(void* p, void* stream, void* ctx);
+
+typedef struct me_comm me_comm;
+typedef struct me_plan me_plan;
+typedef struct me_result me_result;
+
+typedef struct {
+    uint64_t begin, end;   /* flat index range; end = 0 -> end of the space.
+                              With comm, [begin, end) is split into nranks
+                              contiguous equal parts and this rank does its own. */
+    me_out_mode mode;
+    int device;            /* CUDA device ordinal (me_sweep only; a plan keeps its own) */
+    void* stream;          /* cudaStream_t; NULL = the legacy default stream */
+    me_alloc_fn alloc;     /* NULL -> cudaMallocAsync / cudaFreeAsync (me_sweep only) */
+    me_free_fn free;
+    void* alloc_ctx;
+    me_comm* comm;         /* NULL = single GPU */
+    uint32_t gather;       /* with comm: 1 = every rank receives all ranks'
+                              columns in global order (NCCL broadcasts over NVLink) */
+    uint32_t _pad;
+    /* Optional caller-owned output columns: device pointers, ME_N_COLS of
+     * them for FULL, 1 for INDEX (NULL = the library allocates exactly, which
+     * synchronises the host once).  With caller columns the call is fully
+     * asynchronous: survivors beyond out_capacity are counted but not written
+     * and me_result_status() then returns ME_ERANGE. */
+    uint64_t* const* out_cols;
+    uint64_t out_capacity;
+} me_sweep_opts;
+
+/* me_estimate: Eq.18 and its parts for one configuration, evaluated by the same
+ * device code as the sweep (one GPU thread; synchronous).  Checks EINVAL then
+ * EDIV then EOVERFLOW as listed above.  Uses the current CUDA device. */
+int me_estimate(const me_model* model, const me_parallel* cfg, me_breakdown* out);
+
+/* me_estimate_batch: n configurations, cfgs[i] against models[model_ids[i]]
+ * (model_ids may be NULL: model 0).  Every array may be host or device memory
+ * (detected per pointer).  out (n rows), cap_mask (n bytes: bit j = feasible for
+ * capacity j) and status (n bytes: per-config ME_* code) may each be NULL.
+ * Synchronous.  Returns ME_OK, or the first per-config failure when status is
+ * NULL. */
+int me_estimate_batch(const me_model* models, uint32_t n_models, const uint32_t* model_ids,
+                      const me_parallel* cfgs, uint64_t n, const uint64_t* capacity_bytes,
+                      uint32_t n_cap, me_threshold thr, me_breakdown* out, uint8_t* cap_mask,
+                      uint8_t* status, void* stream);
+
+/* Number of valid configurations of the space (the canonical enumeration of
+ * model -> N -> t, c, p ascending with t*c*p | N -> b -> s -> rc
+ * -> do; invalid tuples consume no index).  Host-only. */
+int me_space_size(const me_model_range* models, const me_cluster* cluster,
+                  const me_cfg_range* cfg, uint64_t* n);
+
+/* Configuration at a flat index (host-only).  ME_ERANGE past the end. */
+int me_decode(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
+              uint64_t index, uint32_t* model_id, uint32_t* world_size, me_parallel* out);
+
+/* A plan = the space's enumeration tables resident on one device (built on the
+ * host, uploaded once) plus reusable scratch.  Domain of exact u64 evaluation
+ * (ME_EINVAL outside it): h <= 2^15, h_ffn <= 2^17, L <= 2^8, v <= 2^19,
+ * s <= 2^20, b <= 2^6, N <= 2^20 and < 2^56 configurations; then every term
+ * is < 2^58. */
+int me_plan_create(const me_model_range* models, const me_cluster* cluster,
+                   const me_cfg_range* cfg, me_threshold thr, int device, void* stream,
+                   me_alloc_fn alloc, me_free_fn free, void* alloc_ctx, me_plan** out);
+int me_plan_size(const me_plan* plan, uint64_t* n);
+/* bytes of enumeration tables the plan uploaded to the device (H2D) */
+int me_plan_table_bytes(const me_plan* plan, uint64_t* bytes);
+/* evaluate every configuration of opts->[begin, end), keep those whose
+ * capacity mask is non-zero, in ascending index order (the feasible set of
+ * the 80% rule) */
+int me_plan_sweep(me_plan* plan, const me_sweep_opts* opts, me_result** out);
+void me_plan_free(me_plan* plan);
+
+/* one-shot: me_plan_create + me_plan_sweep (+ free of the plan's tables) */
+int me_sweep(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
+             me_threshold thr, const me_sweep_opts* opts, me_result** out);
+
+/* Survivors: this rank's (local) and all ranks' (global) counts; without comm
+ * they are equal.  rank_offset = global position of this rank's first row.
+ * Waits for the sweep to finish. */
+int me_result_counts(me_result* r, uint64_t* local, uint64_t* global, uint64_t* rank_offset);
+/* per-capacity survivor counts (n_cap entries), global when comm is set */
+int me_result_cap_counts(me_result* r, uint64_t* per_cap);
+/* device pointers of the output columns (NULL entries for COUNT mode / unused
+ * columns).  With comm+gather these are the gathered global columns, else this
+ * rank's.  n_rows = rows visible in those columns. */
+int me_result_columns(me_result* r, uint64_t** cols /* ME_N_COLS */, uint64_t* n_rows);
+/* copy rows [first, first+n) of the visible columns to host arrays; cols_host[j]
+ * receives column j and may be NULL.  ME_ERANGE if out of bounds. */
+int me_result_copy_to_host(me_result* r, uint64_t first, uint64_t n, uint64_t* const* cols_host);
+/* ME_OK, or ME_ERANGE when caller columns overflowed.  Waits. */
+int me_result_status(me_result* r);
+/* wait for the result's work on its stream to finish */
+int me_result_wait(me_result* r);
+/* device time in ms from CUDA events on the sweep's stream: [0] whole sweep,
+ * [1] count pass, [2] scan, [3] write pass (0 when not run).  Waits. */
+int me_result_timing(me_result* r, float* ms4);
+void me_result_free(me_result* r);
+
+/* NCCL communicator over nranks processes (one per GPU).  rank 0 creates the
+ * unique id with me_comm_unique_id and the caller distributes it (e.g. with
+ * torch.distributed); every rank then calls me_comm_init collectively. */
+int me_comm_unique_id(uint8_t id[128]);
+int me_comm_init(const uint8_t id[128], int rank, int nranks, int device, me_comm** out);
+int me_comm_rank(const me_comm* c, int* rank, int* nranks);
+void me_comm_destroy(me_comm* c);
+
+const char* me_strerror(int status);
+const char* me_last_error_detail(void);
+/* library version string */
+const char* me_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ME_H */

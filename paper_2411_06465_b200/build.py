@@ -1,0 +1,61 @@
+"""Build libme.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels
+with the repo snapshot to the GPU box)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libme.so"
+SOURCES = ["me_space.cpp", "me_kernels.cu", "me_abi.cu"]
+HEADERS = ["me_space.hpp", "me_kernels.cuh"]
+
+
+def nccl_root() -> Path:
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        p = Path(list(spec.submodule_search_locations)[0])
+        if (p / "include" / "nccl.h").exists():
+            return p
+    raise RuntimeError("NCCL headers (nvidia.nccl) not found")
+
+
+def nvcc() -> str:
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if c and (Path(c).exists() or c == "nvcc"):
+            return c
+    return "nvcc"
+
+
+def stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "me.h", Path(__file__)]
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not stale():
+        return LIB
+    nr = nccl_root()
+    cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-lineinfo",
+           "-gencode", "arch=compute_100a,code=sm_100a",
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-I", str(ROOT / "include"), "-I", str(nr / "include"),
+           *[str(CSRC / s) for s in SOURCES],
+           "-L", str(nr / "lib"), "-l:libnccl.so.2", f"-Xlinker=-rpath={nr / 'lib'}",
+           "-o", str(LIB) + ".tmp"]
+    subprocess.check_call(cmd)
+    os.replace(str(LIB) + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force=True, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,713 @@
+// me_abi.cu -- the extern "C" boundary of libme.so (see include/me.h).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/me.h"
+#include "me_kernels.cuh"
+#include "me_space.hpp"
+
+namespace me {
+uint32_t ncap_stride(uint32_t n_cap);
+}
+
+using namespace me;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_detail;
+
+static int err(int st, const std::string& msg) {
+    g_detail = msg;
+    return st;
+}
+static int cuda_err(cudaError_t e, const char* where) {
+    return err(ME_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CU(call)                                            \
+    do {                                                    \
+        cudaError_t e_ = (call);                            \
+        if (e_ != cudaSuccess) return cuda_err(e_, #call);  \
+    } while (0)
+
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// allocation
+// ---------------------------------------------------------------------------
+struct Alloc {
+    me_alloc_fn alloc = nullptr;
+    me_free_fn free = nullptr;
+    void* ctx = nullptr;
+    cudaStream_t stream = nullptr;
+
+    void* get(size_t bytes) {
+        if (!bytes) bytes = 8;
+        if (alloc) return alloc(bytes, (void*)stream, ctx);
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) return nullptr;
+        return p;
+    }
+    void put(void* p) {
+        if (!p) return;
+        if (free) free(p, (void*)stream, ctx);
+        else cudaFreeAsync(p, stream);
+    }
+};
+
+template <typename T>
+static int upload(Alloc& A, const std::vector<T>& v, T** out) {
+    *out = (T*)A.get(v.size() * sizeof(T));
+    if (!*out) return err(ME_ENOMEM, "device allocation of a table failed");
+    if (!v.empty()) CU(cudaMemcpyAsync(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, A.stream));
+    return ME_OK;
+}
+
+// ---------------------------------------------------------------------------
+// comm
+// ---------------------------------------------------------------------------
+struct me_comm {
+    ncclComm_t nccl = nullptr;
+    int rank = 0, nranks = 1, device = 0;
+};
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct me_plan {
+    HostSpace hs;
+    DevSpace ds{};
+    Alloc A;
+    int device = 0;
+    std::vector<void*> owned;  // device allocations owned by the plan
+    // scratch, sized for max warps
+    uint32_t max_blocks = 0;
+    uint32_t* warp_count = nullptr;
+    uint32_t* warp_caps = nullptr;
+    uint64_t* warp_off = nullptr;
+};
+
+struct me_result {
+    me_plan* plan = nullptr;
+    bool own_plan = false;
+    Alloc A;
+    cudaStream_t stream = nullptr;
+    me_out_mode mode = ME_OUT_COUNT;
+    uint32_t n_cap = 0;
+    uint64_t begin = 0, end = 0;
+    uint64_t* stats = nullptr;       // device: [0] count, [1..8] per-cap
+    uint64_t* gathered = nullptr;    // device: nranks * 9 (comm)
+    uint64_t* cols[ME_N_COLS] = {};  // this rank's columns
+    bool own_cols = false;
+    uint64_t capacity = 0;
+    uint64_t* gcols[ME_N_COLS] = {};  // gathered columns (comm + gather)
+    uint64_t g_rows = 0;
+    me_comm* comm = nullptr;
+    bool gather = false;
+    cudaEvent_t ev[5] = {};
+    bool ran_count = false, ran_write = false;
+    // host-side results (valid after `resolved`)
+    bool resolved = false;
+    uint64_t local = 0, global = 0, offset = 0;
+    uint64_t caps[8] = {};
+};
+
+static uint32_t blocks_for(uint64_t len, uint32_t max_blocks) {
+    // >= 8 rounds of 32 per warp before spreading wider
+    uint64_t want = (len + (uint64_t)kThreads * 8 - 1) / ((uint64_t)kThreads * 8);
+    if (want < 1) want = 1;
+    return (uint32_t)(want < max_blocks ? want : max_blocks);
+}
+
+static int plan_create(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
+                       me_threshold thr, int device, void* stream, me_alloc_fn al, me_free_fn fr, void* ctx,
+                       me_plan** out) {
+    if (!out) return err(ME_EINVAL, "null out");
+    if (thr.num < 1 || thr.den < 1 || thr.num > 1024 || thr.den > 1024)
+        return err(ME_EINVAL, "threshold num/den must be in [1, 1024]");
+    me_plan* P = new (std::nothrow) me_plan();
+    if (!P) return err(ME_ENOMEM, "host allocation");
+    std::string detail;
+    int st = P->hs.build(models, cluster, cfg, true, &detail);
+    if (st) {
+        delete P;
+        return err(st, detail);
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        delete P;
+        return err(ME_ECUDA, "no CUDA device");
+    }
+    if (device < 0 || device >= ndev) {
+        delete P;
+        return err(ME_EINVAL, "bad device ordinal");
+    }
+    DeviceGuard g(device);
+    P->device = device;
+    P->A.alloc = al;
+    P->A.free = fr;
+    P->A.ctx = ctx;
+    P->A.stream = (cudaStream_t)stream;
+    const HostSpace& H = P->hs;
+    DevSpace& D = P->ds;
+    me_model* dm;
+    uint32_t *dcls, *dlo, *dlt;
+    uint64_t *dsp, *dlp;
+    DevTuple* dtu;
+    DevPair* dpr;
+    if ((st = upload(P->A, H.models, &dm)) || (P->owned.push_back(dm), false) ||
+        (st = upload(P->A, H.model_class, &dcls)) || (P->owned.push_back(dcls), false) ||
+        (st = upload(P->A, H.seg_prefix, &dsp)) || (P->owned.push_back(dsp), false) ||
+        (st = upload(P->A, H.list_off, &dlo)) || (P->owned.push_back(dlo), false) ||
+        (st = upload(P->A, H.list_tuple, &dlt)) || (P->owned.push_back(dlt), false) ||
+        (st = upload(P->A, H.list_prefix, &dlp)) || (P->owned.push_back(dlp), false) ||
+        (st = upload(P->A, H.tuples, &dtu)) || (P->owned.push_back(dtu), false) ||
+        (st = upload(P->A, H.pairs, &dpr)) || (P->owned.push_back(dpr), false)) {
+        me_plan_free(P);
+        return st;
+    }
+    D.models = dm;
+    D.model_class = dcls;
+    D.seg_prefix = dsp;
+    D.list_off = dlo;
+    D.list_tuple = dlt;
+    D.list_prefix = dlp;
+    D.tuples = dtu;
+    D.pairs = dpr;
+    D.n_seg = (uint32_t)(H.seg_prefix.size() - 1);
+    D.n_world = (uint32_t)H.world.size();
+    D.lg_rcdo = H.lg_rcdo;
+    D.rcdo_rc = H.rcdo_rc;
+    D.rcdo_do = H.rcdo_do;
+    D.n_cap = (uint32_t)H.caps.size();
+    for (int q = 0; q < 8; q++) D.thr[q] = 0;
+    for (size_t q = 0; q < H.caps.size(); q++)
+        D.thr[q] = (uint64_t)(((unsigned __int128)H.caps[q] * thr.num) / thr.den);
+    // scratch: 8 resident blocks of 256 threads per SM
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    P->max_blocks = (uint32_t)sms * 8;
+    const uint32_t max_warps = P->max_blocks * kWarpsPerBlock;
+    P->warp_count = (uint32_t*)P->A.get((size_t)max_warps * 4);
+    P->warp_caps = (uint32_t*)P->A.get((size_t)max_warps * 8 * 4);
+    P->warp_off = (uint64_t*)P->A.get((size_t)(max_warps + 1) * 8);
+    P->owned.push_back(P->warp_count);
+    P->owned.push_back(P->warp_caps);
+    P->owned.push_back(P->warp_off);
+    if (!P->warp_count || !P->warp_caps || !P->warp_off) {
+        me_plan_free(P);
+        return err(ME_ENOMEM, "scratch allocation");
+    }
+    *out = P;
+    return ME_OK;
+}
+
+extern "C" int me_plan_create(const me_model_range* models, const me_cluster* cluster,
+                              const me_cfg_range* cfg, me_threshold thr, int device, void* stream,
+                              me_alloc_fn alloc, me_free_fn free, void* alloc_ctx, me_plan** out) {
+    return plan_create(models, cluster, cfg, thr, device, stream, alloc, free, alloc_ctx, out);
+}
+
+extern "C" int me_plan_size(const me_plan* plan, uint64_t* n) {
+    if (!plan || !n) return err(ME_EINVAL, "null argument");
+    *n = plan->hs.total;
+    return ME_OK;
+}
+
+extern "C" int me_plan_table_bytes(const me_plan* plan, uint64_t* bytes) {
+    if (!plan || !bytes) return err(ME_EINVAL, "null argument");
+    const HostSpace& H = plan->hs;
+    *bytes = H.models.size() * sizeof(me_model) + H.model_class.size() * 4 + H.seg_prefix.size() * 8 +
+             H.list_off.size() * 4 + H.list_tuple.size() * 4 + H.list_prefix.size() * 8 +
+             H.tuples.size() * sizeof(DevTuple) + H.pairs.size() * sizeof(DevPair);
+    return ME_OK;
+}
+
+extern "C" void me_plan_free(me_plan* P) {
+    if (!P) return;
+    {
+        DeviceGuard g(P->device);
+        for (void* p : P->owned) P->A.put(p);
+    }
+    delete P;
+}
+
+static void result_release(me_result* R) {
+    if (!R) return;
+    DeviceGuard g(R->plan ? R->plan->device : -1);
+    for (int i = 0; i < 5; i++)
+        if (R->ev[i]) cudaEventDestroy(R->ev[i]);
+    R->A.put(R->stats);
+    R->A.put(R->gathered);
+    if (R->own_cols)
+        for (int j = 0; j < ME_N_COLS; j++) R->A.put(R->cols[j]);
+    for (int j = 0; j < ME_N_COLS; j++) R->A.put(R->gcols[j]);
+    if (R->own_plan) me_plan_free(R->plan);
+    delete R;
+}
+
+static int n_cols_of(me_out_mode m) { return m == ME_OUT_FULL ? ME_N_COLS : (m == ME_OUT_INDEX ? 1 : 0); }
+
+static int resolve(me_result* R);
+
+static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_result** out) {
+    if (!P || !o || !out) return err(ME_EINVAL, "null argument");
+    if (o->mode != ME_OUT_COUNT && o->mode != ME_OUT_INDEX && o->mode != ME_OUT_FULL)
+        return err(ME_EINVAL, "bad output mode");
+    DeviceGuard g(P->device);
+    cudaStream_t st = (cudaStream_t)o->stream;
+    uint64_t total = P->hs.total;
+    uint64_t b = o->begin, e = o->end ? o->end : total;
+    if (e > total) e = total;
+    if (b > e) b = e;
+    if (o->comm) {
+        const uint64_t len = e - b;
+        const int r = o->comm->rank, n = o->comm->nranks;
+        const uint64_t q = len / n, rem = len % n;
+        const uint64_t lo = b + q * r + (rem * r) / n, hi = b + q * (r + 1) + (rem * (r + 1)) / n;
+        b = lo;
+        e = hi;
+    }
+    me_result* R = new (std::nothrow) me_result();
+    if (!R) return err(ME_ENOMEM, "host allocation");
+    R->plan = P;
+    R->A = P->A;
+    R->A.stream = st;
+    R->stream = st;
+    R->mode = o->mode;
+    R->n_cap = P->ds.n_cap;
+    R->begin = b;
+    R->end = e;
+    R->comm = o->comm;
+    R->gather = o->comm && o->gather;
+    int rc = ME_OK;
+    auto fail = [&](int s) {
+        R->own_plan = false;
+        result_release(R);
+        return s;
+    };
+    for (int i = 0; i < 5; i++)
+        if (cudaEventCreate(&R->ev[i]) != cudaSuccess) return fail(cuda_err(cudaErrorUnknown, "cudaEventCreate"));
+    R->stats = (uint64_t*)R->A.get(9 * 8);
+    if (!R->stats) return fail(err(ME_ENOMEM, "stats allocation"));
+    if (cudaMemsetAsync(R->stats, 0, 9 * 8, st) != cudaSuccess) return fail(cuda_err(cudaErrorUnknown, "memset"));
+
+    const uint64_t len = e - b;
+    const uint32_t nb = blocks_for(len, P->max_blocks);
+    const uint32_t n_warps = nb * kWarpsPerBlock;
+    cudaEventRecord(R->ev[0], st);
+    if (len) {
+        cudaError_t ce = launch_count(P->ds, b, e, nb, P->warp_count, P->warp_caps, st);
+        if (ce != cudaSuccess) return fail(cuda_err(ce, "count kernel"));
+        R->ran_count = true;
+    }
+    cudaEventRecord(R->ev[1], st);
+    if (len) {
+        cudaError_t ce = launch_scan(P->warp_count, P->warp_caps, n_warps, P->ds.n_cap, P->warp_off, R->stats, st);
+        if (ce != cudaSuccess) return fail(cuda_err(ce, "scan kernel"));
+    }
+    cudaEventRecord(R->ev[2], st);
+    const int nc = n_cols_of(o->mode);
+    if (nc && len) {
+        if (o->out_cols) {
+            for (int j = 0; j < nc; j++) {
+                R->cols[j] = o->out_cols[j];
+                if (!R->cols[j]) return fail(err(ME_EINVAL, "null caller column"));
+            }
+            R->capacity = o->out_capacity;
+        } else {
+            uint64_t cnt = 0;
+            if (cudaMemcpyAsync(&cnt, R->stats, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess)
+                return fail(cuda_err(cudaGetLastError(), "count readback"));
+            R->own_cols = true;
+            for (int j = 0; j < nc; j++) {
+                R->cols[j] = (uint64_t*)R->A.get(cnt * 8);
+                if (!R->cols[j]) return fail(err(ME_ENOMEM, "result column allocation"));
+            }
+            R->capacity = cnt;
+        }
+        Cols cols{};
+        for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
+        cudaError_t ce = launch_write(P->ds, b, e, nb, P->warp_off, o->mode, cols, R->capacity, st);
+        if (ce != cudaSuccess) return fail(cuda_err(ce, "write kernel"));
+        R->ran_write = true;
+    }
+    cudaEventRecord(R->ev[3], st);
+    if (o->comm) {
+        R->gathered = (uint64_t*)R->A.get((size_t)o->comm->nranks * 9 * 8);
+        if (!R->gathered) return fail(err(ME_ENOMEM, "gather buffer"));
+        ncclResult_t nr = ncclAllGather(R->stats, R->gathered, 9, ncclUint64, o->comm->nccl, st);
+        if (nr != ncclSuccess) return fail(err(ME_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr)));
+        if (R->gather && nc) {
+            if ((rc = resolve(R))) return fail(rc);
+            // variable-size allgather of the columns: one broadcast per rank
+            std::vector<uint64_t> cnt(o->comm->nranks), off(o->comm->nranks + 1, 0);
+            std::vector<uint64_t> h(o->comm->nranks * 9);
+            if (cudaMemcpy(h.data(), R->gathered, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return fail(cuda_err(cudaGetLastError(), "gathered readback"));
+            for (int r = 0; r < o->comm->nranks; r++) {
+                cnt[r] = h[r * 9];
+                off[r + 1] = off[r] + cnt[r];
+            }
+            R->g_rows = off[o->comm->nranks];
+            for (int j = 0; j < nc; j++) {
+                R->gcols[j] = (uint64_t*)R->A.get(R->g_rows * 8);
+                if (!R->gcols[j]) return fail(err(ME_ENOMEM, "gathered column allocation"));
+            }
+            if (R->capacity < R->local) return fail(err(ME_ERANGE, "caller columns overflowed; cannot gather"));
+            ncclGroupStart();
+            for (int j = 0; j < nc; j++)
+                for (int r = 0; r < o->comm->nranks; r++) {
+                    if (!cnt[r]) continue;
+                    nr = ncclBroadcast(r == o->comm->rank ? (const void*)R->cols[j] : nullptr,
+                                       R->gcols[j] + off[r], cnt[r], ncclUint64, r, o->comm->nccl, st);
+                    if (nr != ncclSuccess) break;
+                }
+            ncclResult_t ng = ncclGroupEnd();
+            if (nr != ncclSuccess || ng != ncclSuccess)
+                return fail(err(ME_ENCCL, std::string("ncclBroadcast: ") + ncclGetErrorString(nr != ncclSuccess ? nr : ng)));
+        }
+    }
+    cudaEventRecord(R->ev[4], st);
+    R->own_plan = own_plan;
+    *out = R;
+    return ME_OK;
+}
+
+extern "C" int me_plan_sweep(me_plan* plan, const me_sweep_opts* opts, me_result** out) {
+    return plan_sweep(plan, opts, false, out);
+}
+
+extern "C" int me_sweep(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
+                        me_threshold thr, const me_sweep_opts* opts, me_result** out) {
+    if (!opts || !out) return err(ME_EINVAL, "null argument");
+    me_plan* P = nullptr;
+    int st = plan_create(models, cluster, cfg, thr, opts->device, opts->stream, opts->alloc, opts->free,
+                         opts->alloc_ctx, &P);
+    if (st) return st;
+    st = plan_sweep(P, opts, true, out);
+    if (st) me_plan_free(P);
+    return st;
+}
+
+// read device stats (waits)
+static int resolve(me_result* R) {
+    if (R->resolved) return ME_OK;
+    DeviceGuard g(R->plan->device);
+    CU(cudaStreamSynchronize(R->stream));
+    uint64_t h[9];
+    CU(cudaMemcpy(h, R->stats, sizeof h, cudaMemcpyDeviceToHost));
+    R->local = h[0];
+    for (int q = 0; q < 8; q++) R->caps[q] = h[1 + q];
+    R->global = R->local;
+    R->offset = 0;
+    if (R->comm) {
+        std::vector<uint64_t> all((size_t)R->comm->nranks * 9);
+        CU(cudaMemcpy(all.data(), R->gathered, all.size() * 8, cudaMemcpyDeviceToHost));
+        R->global = 0;
+        for (int q = 0; q < 8; q++) R->caps[q] = 0;
+        for (int r = 0; r < R->comm->nranks; r++) {
+            if (r < R->comm->rank) R->offset += all[(size_t)r * 9];
+            R->global += all[(size_t)r * 9];
+            for (int q = 0; q < 8; q++) R->caps[q] += all[(size_t)r * 9 + 1 + q];
+        }
+    }
+    R->resolved = true;
+    return ME_OK;
+}
+
+extern "C" int me_result_wait(me_result* R) {
+    if (!R) return err(ME_EINVAL, "null result");
+    DeviceGuard g(R->plan->device);
+    CU(cudaEventSynchronize(R->ev[4]));
+    return ME_OK;
+}
+
+extern "C" int me_result_counts(me_result* R, uint64_t* local, uint64_t* global, uint64_t* rank_offset) {
+    if (!R) return err(ME_EINVAL, "null result");
+    int st = resolve(R);
+    if (st) return st;
+    if (local) *local = R->local;
+    if (global) *global = R->global;
+    if (rank_offset) *rank_offset = R->offset;
+    return ME_OK;
+}
+
+extern "C" int me_result_cap_counts(me_result* R, uint64_t* per_cap) {
+    if (!R || !per_cap) return err(ME_EINVAL, "null argument");
+    int st = resolve(R);
+    if (st) return st;
+    for (uint32_t q = 0; q < R->n_cap; q++) per_cap[q] = R->caps[q];
+    return ME_OK;
+}
+
+extern "C" int me_result_status(me_result* R) {
+    if (!R) return err(ME_EINVAL, "null result");
+    int st = resolve(R);
+    if (st) return st;
+    if (n_cols_of(R->mode) && R->local > R->capacity)
+        return err(ME_ERANGE, "caller columns too small: need " + std::to_string(R->local) + " rows");
+    return ME_OK;
+}
+
+extern "C" int me_result_columns(me_result* R, uint64_t** cols, uint64_t* n_rows) {
+    if (!R || !cols) return err(ME_EINVAL, "null argument");
+    int st = resolve(R);
+    if (st) return st;
+    const bool g = R->gather && n_cols_of(R->mode);
+    for (int j = 0; j < ME_N_COLS; j++) cols[j] = g ? R->gcols[j] : R->cols[j];
+    if (n_rows) {
+        uint64_t n = g ? R->g_rows : R->local;
+        if (!g && n > R->capacity) n = R->capacity;
+        *n_rows = n_cols_of(R->mode) ? n : 0;
+    }
+    return ME_OK;
+}
+
+extern "C" int me_result_copy_to_host(me_result* R, uint64_t first, uint64_t n, uint64_t* const* cols_host) {
+    if (!R || !cols_host) return err(ME_EINVAL, "null argument");
+    uint64_t* cols[ME_N_COLS];
+    uint64_t rows = 0;
+    int st = me_result_columns(R, cols, &rows);
+    if (st) return st;
+    if (first > rows || n > rows - first) return err(ME_ERANGE, "rows out of bounds");
+    if (!n) return ME_OK;
+    DeviceGuard g(R->plan->device);
+    for (int j = 0; j < ME_N_COLS; j++) {
+        if (!cols_host[j]) continue;
+        if (!cols[j]) return err(ME_EINVAL, "column not produced in this mode");
+        CU(cudaMemcpyAsync(cols_host[j], cols[j] + first, n * 8, cudaMemcpyDeviceToHost, R->stream));
+    }
+    CU(cudaStreamSynchronize(R->stream));
+    return ME_OK;
+}
+
+extern "C" int me_result_timing(me_result* R, float* ms) {
+    if (!R || !ms) return err(ME_EINVAL, "null argument");
+    DeviceGuard g(R->plan->device);
+    CU(cudaEventSynchronize(R->ev[4]));
+    CU(cudaEventElapsedTime(&ms[0], R->ev[0], R->ev[4]));
+    CU(cudaEventElapsedTime(&ms[1], R->ev[0], R->ev[1]));
+    CU(cudaEventElapsedTime(&ms[2], R->ev[1], R->ev[2]));
+    CU(cudaEventElapsedTime(&ms[3], R->ev[2], R->ev[3]));
+    if (!R->ran_write) ms[3] = 0.f;
+    return ME_OK;
+}
+
+extern "C" void me_result_free(me_result* R) { result_release(R); }
+
+// ---------------------------------------------------------------------------
+// single estimates
+// ---------------------------------------------------------------------------
+static bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+extern "C" int me_estimate_batch(const me_model* models, uint32_t n_models, const uint32_t* ids,
+                                 const me_parallel* cfgs, uint64_t n, const uint64_t* caps, uint32_t n_cap,
+                                 me_threshold thr, me_breakdown* out, uint8_t* mask, uint8_t* status,
+                                 void* stream) {
+    if (!models || !n_models || !cfgs) return err(ME_EINVAL, "null argument");
+    if (n_cap > 8 || (n_cap && !caps)) return err(ME_EINVAL, "n_cap must be <= 8");
+    if (thr.num < 1 || thr.den < 1 || thr.num > 1024 || thr.den > 1024)
+        return err(ME_EINVAL, "threshold num/den must be in [1, 1024]");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return err(ME_ECUDA, "no CUDA device");
+    }
+    if (!n) return ME_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<void*> tmp;
+    auto stage_in = [&](const void* p, size_t bytes, const void** dp) -> int {
+        if (!p) { *dp = nullptr; return ME_OK; }
+        if (is_device_ptr(p)) { *dp = p; return ME_OK; }
+        void* d = nullptr;
+        CU(cudaMalloc(&d, bytes));
+        tmp.push_back(d);
+        CU(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, st));
+        *dp = d;
+        return ME_OK;
+    };
+    auto stage_out = [&](void* p, size_t bytes, void** dp) -> int {
+        if (!p) { *dp = nullptr; return ME_OK; }
+        if (is_device_ptr(p)) { *dp = p; return ME_OK; }
+        void* d = nullptr;
+        CU(cudaMalloc(&d, bytes));
+        tmp.push_back(d);
+        *dp = d;
+        return ME_OK;
+    };
+    uint64_t thr_h[8] = {0};
+    for (uint32_t q = 0; q < n_cap; q++) {
+        uint64_t c;
+        if (is_device_ptr(caps)) {
+            CU(cudaMemcpy(&c, caps + q, 8, cudaMemcpyDeviceToHost));
+        } else {
+            c = caps[q];
+        }
+        thr_h[q] = (uint64_t)(((unsigned __int128)c * thr.num) / thr.den);
+    }
+    const void *dm, *di, *dc, *dt;
+    void *dout, *dmask, *dstat;
+    int rc;
+    auto cleanup = [&]() {
+        for (void* p : tmp) cudaFree(p);
+    };
+    if ((rc = stage_in(models, (size_t)n_models * sizeof(me_model), &dm)) ||
+        (rc = stage_in(ids, n * 4, &di)) || (rc = stage_in(cfgs, n * sizeof(me_parallel), &dc)) ||
+        (rc = stage_in(thr_h, sizeof thr_h, &dt)) || (rc = stage_out(out, n * sizeof(me_breakdown), &dout)) ||
+        (rc = stage_out(mask, n, &dmask))) {
+        cleanup();
+        return rc;
+    }
+    // per-config status is always produced on the device
+    if (status && is_device_ptr(status)) {
+        dstat = status;
+    } else {
+        if (cudaMalloc(&dstat, n) != cudaSuccess) { cleanup(); return cuda_err(cudaGetLastError(), "cudaMalloc"); }
+        tmp.push_back(dstat);
+    }
+    cudaError_t ce = launch_estimate((const me_model*)dm, n_models, (const uint32_t*)di, (const me_parallel*)dc,
+                                     n, (const uint64_t*)dt, n_cap, (me_breakdown*)dout, (uint8_t*)dmask,
+                                     (uint8_t*)dstat, st);
+    if (ce != cudaSuccess) { cleanup(); return cuda_err(ce, "estimate kernel"); }
+    std::vector<uint8_t> hstat(n);
+    int first_bad = ME_OK;
+    ce = cudaMemcpyAsync(hstat.data(), dstat, n, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && out && dout != out)
+        ce = cudaMemcpyAsync(out, dout, n * sizeof(me_breakdown), cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && mask && dmask != mask) ce = cudaMemcpyAsync(mask, dmask, n, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess && status && dstat != status) ce = cudaMemcpyAsync(status, dstat, n, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    cleanup();
+    if (ce != cudaSuccess) return cuda_err(ce, "estimate readback");
+    for (uint64_t i = 0; i < n; i++)
+        if (hstat[i]) { first_bad = hstat[i]; break; }
+    if (!status && first_bad) return err(first_bad, "a configuration failed its preconditions");
+    return ME_OK;
+}
+
+extern "C" int me_estimate(const me_model* model, const me_parallel* cfg, me_breakdown* out) {
+    if (!model || !cfg || !out) return err(ME_EINVAL, "null argument");
+    me_breakdown b;
+    uint8_t s = 0;
+    me_threshold thr{4, 5};
+    int st = me_estimate_batch(model, 1, nullptr, cfg, 1, nullptr, 0, thr, &b, nullptr, &s, nullptr);
+    if (st) return st;
+    if (s) return err(s, "estimator precondition failed");
+    *out = b;
+    return ME_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-only space queries
+// ---------------------------------------------------------------------------
+extern "C" int me_space_size(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
+                             uint64_t* n) {
+    if (!n) return err(ME_EINVAL, "null out");
+    HostSpace H;
+    std::string d;
+    int st = H.build(models, cluster, cfg, false, &d);
+    if (st) return err(st, d);
+    *n = H.total;
+    return ME_OK;
+}
+
+extern "C" int me_decode(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
+                         uint64_t index, uint32_t* model_id, uint32_t* world_size, me_parallel* out) {
+    HostSpace H;
+    std::string d;
+    int st = H.build(models, cluster, cfg, false, &d);
+    if (st) return err(st, d);
+    st = H.decode(index, model_id, world_size, out);
+    if (st) return err(st, "index past the end of the space");
+    return ME_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL
+// ---------------------------------------------------------------------------
+extern "C" int me_comm_unique_id(uint8_t id[128]) {
+    if (!id) return err(ME_EINVAL, "null id");
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) return err(ME_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(id, &u, 128);
+    return ME_OK;
+}
+
+extern "C" int me_comm_init(const uint8_t id[128], int rank, int nranks, int device, me_comm** out) {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return err(ME_EINVAL, "bad comm arguments");
+    DeviceGuard g(device);
+    me_comm* c = new (std::nothrow) me_comm();
+    if (!c) return err(ME_ENOMEM, "host allocation");
+    ncclUniqueId u;
+    memcpy(&u, id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return err(ME_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = device;
+    *out = c;
+    return ME_OK;
+}
+
+extern "C" int me_comm_rank(const me_comm* c, int* rank, int* nranks) {
+    if (!c) return err(ME_EINVAL, "null comm");
+    if (rank) *rank = c->rank;
+    if (nranks) *nranks = c->nranks;
+    return ME_OK;
+}
+
+extern "C" void me_comm_destroy(me_comm* c) {
+    if (!c) return;
+    if (c->nccl) ncclCommDestroy(c->nccl);
+    delete c;
+}
+
+// ---------------------------------------------------------------------------
+extern "C" const char* me_strerror(int s) {
+    switch (s) {
+        case ME_OK: return "ok";
+        case ME_EINVAL: return "invalid argument";
+        case ME_EDIV: return "estimator precondition (divisibility) failed";
+        case ME_EOVERFLOW: return "value outside the exact 64-bit range";
+        case ME_ENOMEM: return "out of memory";
+        case ME_ECUDA: return "CUDA error";
+        case ME_ENCCL: return "NCCL error";
+        case ME_ERANGE: return "out of range / buffer too small";
+        default: return "unknown status";
+    }
+}
+
+extern "C" const char* me_last_error_detail(void) { return g_detail.c_str(); }
+
+extern "C" const char* me_version(void) { return "me-b200 0.1.0 sm_100a"; }

@@ -1,0 +1,140 @@
+// me_kernels.cuh -- device code of the estimator sweep (sm_100a).
+//
+// One pass of the hot path = decode flat index -> evaluate the six stage-0
+// byte terms of Eq.18 in exact u64 -> compare with floor(0.8 * capacity) ->
+// compact the survivors in index order.  Integer-only: no tensor cores, no FP.
+#pragma once
+#include <cstdint>
+
+#include "../../include/me.h"
+#include "me_space.hpp"
+
+namespace me {
+
+// Table pointers handed to the kernels (all device memory, read-only).
+struct DevSpace {
+    const me_model* models;
+    const uint32_t* model_class;
+    const uint64_t* seg_prefix;   // n_seg + 1
+    const uint32_t* list_off;     // n_class * n_world + 1
+    const uint32_t* list_tuple;
+    const uint64_t* list_prefix;
+    const DevTuple* tuples;
+    const DevPair* pairs;
+    uint32_t n_seg, n_world;
+    uint32_t lg_rcdo, rcdo_rc, rcdo_do;
+    uint32_t n_cap;
+    uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
+};
+
+// Per (model, tuple) coefficients: every estimator term of a config in this
+// row is an affine function of its tokens-per-microbatch u and in-flight count.
+template <typename U>
+struct RowCoefT {
+    U psi;        // Psi_s, Eq.6 (p = 1) / Eq.7 (p > 1) with L/p -> L0
+    U optim1;     // 12 ceil(Psi_s / (d c))   (Eq.10 + reading R8)
+    U ms0, ms1;   // model-state bytes with the distributed optimizer off / on
+    U lam0;       // L0 * B_t                 (rc = 0 layer bytes per token per mb)
+    U lam1;       // 2 ht L0                  (rc = 1: kept layer inputs, R20)
+    U bt;         // B_t = 12 ht + 4 hd k/t + 8 h_ffn/t   (Eq.12 / Eq.15 per token)
+    U e8;         // 8 ht                     (Eq.13 per token per mb, reading R13)
+    U hc;         // [p = 1] 4 (ht + v/t)     (Eq.14, delta_{p,1} of Eq.16)
+    uint32_t p;
+};
+using RowCoef = RowCoefT<uint64_t>;
+
+__host__ __device__ inline uint32_t first_stage_layers_auto(uint32_t L, uint32_t p) {
+    // R19: L (p = 1), L/p when p | L, ceil(L/p) otherwise -- one formula
+    return (L + p - 1) / p;
+}
+
+// Row coefficients.  All divisions are exact under the validity rules
+// (t | k | a | h, t | v, t | h_ffn) except the optimizer ceil (R8).
+template <typename U>
+__device__ __forceinline__ void make_row(const me_model& M, uint32_t t, uint32_t c, uint32_t p,
+                                         uint32_t d, uint32_t L0, RowCoefT<U>& R) {
+    const uint32_t h = M.hidden;
+    const uint32_t ht = h / t, kt = M.kv_heads / t, hd = h / M.heads, vt = M.vocab / t,
+                   ft = M.ffn_hidden / t;
+    // per-layer shard: W_Q + W_O (2 h ht), W_K + W_V (2 h hd k/t), up/gate/down
+    // (3 h h_ffn/t), two replicated RMSNorms (2h)  -- Eq.1, Eq.2, Eq.6
+    const U per_layer = (U)2 * h * ht + (U)2 * h * hd * kt + (U)3 * h * ft + (U)2 * h;
+    const U ends = (p == 1) ? ((U)2 * h * vt + h) : (U)h * vt;
+    R.psi = ends + (U)L0 * per_layer;
+    const uint32_t dc = d * c;
+    U share;
+    if ((dc & (dc - 1)) == 0) {
+        const uint32_t sh = __ffs(dc) - 1;
+        share = (R.psi + dc - 1) >> sh;
+    } else {
+        share = (R.psi + dc - 1) / dc;
+    }
+    R.optim1 = (U)12 * share;
+    R.ms0 = (U)18 * R.psi;
+    R.ms1 = (U)6 * R.psi + R.optim1;
+    R.bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft;
+    R.lam0 = (U)L0 * R.bt;
+    R.lam1 = (U)2 * ht * L0;
+    R.e8 = (U)8 * ht;
+    R.hc = (p == 1) ? (U)4 * ((U)ht + vt) : (U)0;
+    R.p = p;
+}
+
+template <typename U>
+struct TermsT {
+    U params, grads, optim, layers, embed, head, total;
+};
+
+// total only (count pass): model states + u * (n_inf * a_rc + b_rc)
+__device__ __forceinline__ uint64_t config_total(const RowCoef& R, uint32_t u, uint32_t m,
+                                                 uint32_t rc, uint32_t dopt) {
+    const uint32_t n_inf = min(R.p, m);
+    const uint64_t a = rc ? (R.lam1 + R.e8) : (R.lam0 + R.e8);
+    const uint64_t b = rc ? (R.bt + R.hc) : R.hc;
+    const uint64_t K = (uint64_t)n_inf * a + b;
+    return (dopt ? R.ms1 : R.ms0) + (uint64_t)u * K;
+}
+
+// all six terms (write pass, single estimates); total = their sum, equal to
+// config_total term by term
+template <typename U>
+__device__ __forceinline__ TermsT<U> config_terms(const RowCoefT<U>& R, uint32_t u, uint32_t m,
+                                                  uint32_t rc, uint32_t dopt) {
+    const uint32_t n_inf = min(R.p, m);
+    TermsT<U> T;
+    T.params = (U)2 * R.psi;
+    T.grads = (U)4 * R.psi;
+    T.optim = dopt ? R.optim1 : (U)12 * R.psi;
+    T.layers = (U)u * (rc ? ((U)n_inf * R.lam1 + R.bt) : (U)n_inf * R.lam0);
+    T.embed = (U)u * ((U)n_inf * R.e8);
+    T.head = (U)u * R.hc;
+    T.total = T.params + T.grads + T.optim + T.layers + T.embed + T.head;
+    return T;
+}
+
+// ---- launch wrappers (me_kernels.cu) ------------------------------------
+struct Cols {
+    uint64_t* c[ME_N_COLS];
+};
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerBlock = kThreads / 32;
+
+// count pass: per-warp survivor counts and per-capacity counts
+cudaError_t launch_count(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_blocks,
+                         uint32_t* warp_count, uint32_t* warp_caps, cudaStream_t st);
+// exclusive scan of the warp counts -> warp_off[n_warps + 1]; stats[0] = total,
+// stats[1 + j] = survivors for capacity j
+cudaError_t launch_scan(const uint32_t* warp_count, const uint32_t* warp_caps, uint32_t n_warps,
+                        uint32_t n_cap, uint64_t* warp_off, uint64_t* stats, cudaStream_t st);
+// write pass: survivors of each warp span at warp_off[w] ...
+cudaError_t launch_write(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_blocks,
+                         const uint64_t* warp_off, me_out_mode mode, Cols cols, uint64_t capacity,
+                         cudaStream_t st);
+// single configurations (me_estimate / me_estimate_batch)
+cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,
+                            const me_parallel* cfgs, uint64_t n, const uint64_t* thr,
+                            uint32_t n_cap, me_breakdown* out, uint8_t* mask, uint8_t* status,
+                            cudaStream_t st);
+
+}  // namespace me

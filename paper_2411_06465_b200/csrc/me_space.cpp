@@ -1,0 +1,233 @@
+// me_space.cpp -- builds the HostSpace tables (see me_space.hpp).
+#include "me_space.hpp"
+
+#include <algorithm>
+#include <map>
+#include <unordered_map>
+
+namespace me {
+
+static int fail(std::string* detail, int st, const std::string& msg) {
+    if (detail) *detail = msg;
+    return st;
+}
+
+static int popc2(uint32_t m) { return (m & 1) + ((m >> 1) & 1); }
+
+int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cfg_range* cr,
+                     bool for_sweep, std::string* detail) {
+    if (!mr || !cl || !cr || !mr->models || !mr->n_models || !cl->world_sizes || !cl->n_world ||
+        !cr->mbs || !cr->n_mbs || !cr->seq || !cr->n_seq)
+        return fail(detail, ME_EINVAL, "null or empty axis");
+    if (cl->n_cap > 8 || (cl->n_cap && !cl->capacity_bytes))
+        return fail(detail, ME_EINVAL, "n_cap must be <= 8");
+    if (!(cr->recompute_mask & 3) || (cr->recompute_mask & ~3u) || !(cr->dist_opt_mask & 3) ||
+        (cr->dist_opt_mask & ~3u))
+        return fail(detail, ME_EINVAL, "recompute_mask / dist_opt_mask must be 1, 2 or 3");
+    models.assign(mr->models, mr->models + mr->n_models);
+    world.assign(cl->world_sizes, cl->world_sizes + cl->n_world);
+    caps.assign(cl->capacity_bytes, cl->capacity_bytes + cl->n_cap);
+    mbs.assign(cr->mbs, cr->mbs + cr->n_mbs);
+    seq.assign(cr->seq, cr->seq + cr->n_seq);
+    gpus_per_node = cl->gpus_per_node;
+    gbs = cr->gbs;
+    max_t = cr->max_tp;
+    max_c = cr->max_cp;
+    max_p = cr->max_pp;
+    rc_mask = cr->recompute_mask;
+    do_mask = cr->dist_opt_mask;
+    uneven = cr->allow_uneven_pp ? 1 : 0;
+
+    for (size_t i = 0; i < models.size(); i++) {
+        const me_model& m = models[i];
+        if (!m.hidden || !m.ffn_hidden || !m.layers || !m.heads || !m.kv_heads || !m.vocab)
+            return fail(detail, ME_EINVAL, "model " + std::to_string(i) + ": zero field");
+        if (m.heads % m.kv_heads || m.hidden % m.heads)
+            return fail(detail, ME_EINVAL, "model " + std::to_string(i) + ": needs k | a and a | h");
+        if (for_sweep && (m.hidden > Limits::h || m.ffn_hidden > Limits::f ||
+                          m.layers > Limits::L || m.vocab > Limits::v))
+            return fail(detail, ME_EINVAL,
+                        "model " + std::to_string(i) + " outside the exact-u64 sweep domain");
+    }
+    for (uint32_t N : world) {
+        if (!N) return fail(detail, ME_EINVAL, "zero world size");
+        if (for_sweep && N > Limits::N) return fail(detail, ME_EINVAL, "world size > 2^20");
+    }
+    for (uint32_t b : mbs) {
+        if (!b) return fail(detail, ME_EINVAL, "zero mbs");
+        if (for_sweep && b > Limits::b) return fail(detail, ME_EINVAL, "mbs > 2^6");
+    }
+    for (uint32_t s : seq) {
+        if (!s) return fail(detail, ME_EINVAL, "zero seq");
+        if (for_sweep && s > Limits::s) return fail(detail, ME_EINVAL, "seq > 2^20");
+    }
+
+    // innermost (rc, do) digits, rc outer, do inner
+    n_rcdo = 0;
+    rcdo_rc = rcdo_do = 0;
+    for (uint32_t rc = 0; rc < 2; rc++) {
+        if (!((rc_mask >> rc) & 1)) continue;
+        for (uint32_t dd = 0; dd < 2; dd++) {
+            if (!((do_mask >> dd) & 1)) continue;
+            rcdo_rc |= rc << n_rcdo;
+            rcdo_do |= dd << n_rcdo;
+            n_rcdo++;
+        }
+    }
+    lg_rcdo = n_rcdo == 4 ? 2 : (n_rcdo == 2 ? 1 : 0);
+
+    // per world size: every (t, c, p) with t c p | N that passes the global
+    // limits, ascending; the pooled (b, s) pairs of each
+    tuples.clear();
+    pairs.clear();
+    tup_begin.assign(1, 0);
+    std::map<std::pair<uint32_t, uint32_t>, std::pair<uint32_t, uint32_t>> pool;  // (c, d|0) -> (off, n)
+    std::vector<uint32_t> tvals, pvals;
+    for (uint32_t N : world) {
+        for (uint32_t t = 1; t <= N; t++) {
+            if (N % t) continue;
+            if (max_t && t > max_t) continue;
+            if (gpus_per_node && t > gpus_per_node) continue;
+            for (uint32_t c = 1; c <= N / t; c++) {
+                if ((N / t) % c) continue;
+                if (max_c && c > max_c) continue;
+                for (uint32_t p = 1; p <= N / t / c; p++) {
+                    if ((N / t / c) % p) continue;
+                    if (max_p && p > max_p) continue;
+                    uint32_t d = N / t / c / p;
+                    auto key = std::make_pair(c, gbs ? d : 0u);
+                    auto it = pool.find(key);
+                    if (it == pool.end()) {
+                        uint32_t off = (uint32_t)pairs.size();
+                        for (uint32_t b : mbs)
+                            for (uint32_t s : seq) {
+                                if (s % c) continue;
+                                if (gbs && gbs % ((uint64_t)d * b)) continue;
+                                DevPair pr;
+                                pr.u = (s / c) * b;
+                                pr.m = gbs ? (uint32_t)(gbs / ((uint64_t)d * b)) : 0xFFFFFFFFu;
+                                pairs.push_back(pr);
+                            }
+                        it = pool.emplace(key, std::make_pair(off, (uint32_t)pairs.size() - off)).first;
+                    }
+                    DevTuple tu;
+                    tu.t = t; tu.c = c; tu.p = p; tu.d = d;
+                    tu.pair_off = it->second.first;
+                    tu.n_pairs = it->second.second;
+                    tu.w = tu.n_pairs * n_rcdo;
+                    tu.n_world = N;
+                    if (tu.w == 0) continue;  // no (b, s) pair survives: consumes no index
+                    tuples.push_back(tu);
+                    tvals.push_back(t);
+                    pvals.push_back(p);
+                }
+            }
+        }
+        tup_begin.push_back((uint32_t)tuples.size());
+    }
+    std::sort(tvals.begin(), tvals.end());
+    tvals.erase(std::unique(tvals.begin(), tvals.end()), tvals.end());
+    std::sort(pvals.begin(), pvals.end());
+    pvals.erase(std::unique(pvals.begin(), pvals.end()), pvals.end());
+
+    // validity classes: signature = (t | k, v, f) over tvals, (p <= L, p | L) over pvals
+    std::unordered_map<std::string, uint32_t> cls_of;
+    std::vector<std::string> cls_sig;
+    model_class.resize(models.size());
+    std::string sig(tvals.size() + pvals.size(), '0');
+    for (size_t i = 0; i < models.size(); i++) {
+        const me_model& m = models[i];
+        for (size_t q = 0; q < tvals.size(); q++) {
+            uint32_t t = tvals[q];
+            sig[q] = (m.kv_heads % t == 0 && m.vocab % t == 0 && m.ffn_hidden % t == 0) ? '1' : '0';
+        }
+        for (size_t q = 0; q < pvals.size(); q++) {
+            uint32_t p = pvals[q];
+            sig[tvals.size() + q] = (p <= m.layers && (uneven || m.layers % p == 0)) ? '1' : '0';
+        }
+        auto it = cls_of.find(sig);
+        if (it == cls_of.end()) {
+            it = cls_of.emplace(sig, (uint32_t)cls_sig.size()).first;
+            cls_sig.push_back(sig);
+        }
+        model_class[i] = it->second;
+    }
+    n_class = (uint32_t)cls_sig.size();
+
+    // per (class, N) tuple lists
+    const uint32_t nW = (uint32_t)world.size();
+    list_off.assign(1, 0);
+    list_tuple.clear();
+    list_prefix.clear();
+    class_seg.assign((size_t)n_class * nW, 0);
+    for (uint32_t k = 0; k < n_class; k++) {
+        const std::string& s = cls_sig[k];
+        for (uint32_t n = 0; n < nW; n++) {
+            uint64_t acc = 0;
+            for (uint32_t j = tup_begin[n]; j < tup_begin[n + 1]; j++) {
+                const DevTuple& tu = tuples[j];
+                size_t qt = std::lower_bound(tvals.begin(), tvals.end(), tu.t) - tvals.begin();
+                size_t qp = std::lower_bound(pvals.begin(), pvals.end(), tu.p) - pvals.begin();
+                if (s[qt] != '1' || s[tvals.size() + qp] != '1') continue;
+                list_tuple.push_back(j);
+                list_prefix.push_back(acc);
+                acc += tu.w;
+            }
+            list_off.push_back((uint32_t)list_tuple.size());
+            class_seg[(size_t)k * nW + n] = acc;
+        }
+    }
+
+    // segment prefix
+    seg_prefix.resize(models.size() * nW + 1);
+    uint64_t acc = 0;
+    for (size_t i = 0; i < models.size(); i++)
+        for (uint32_t n = 0; n < nW; n++) {
+            seg_prefix[i * nW + n] = acc;
+            acc += class_seg[(size_t)model_class[i] * nW + n];
+        }
+    seg_prefix[models.size() * nW] = acc;
+    total = acc;
+    if (for_sweep && total >= Limits::index)
+        return fail(detail, ME_EOVERFLOW, "space has >= 2^56 configurations");
+    return ME_OK;
+}
+
+int HostSpace::decode(uint64_t index, uint32_t* model_id, uint32_t* world_size,
+                      me_parallel* out) const {
+    if (index >= total) return ME_ERANGE;
+    const uint32_t nW = (uint32_t)world.size();
+    // last segment starting at or before index (it is non-empty)
+    size_t seg = std::upper_bound(seg_prefix.begin(), seg_prefix.end(), index) - seg_prefix.begin() - 1;
+    uint32_t mdl = (uint32_t)(seg / nW), n = (uint32_t)(seg % nW);
+    uint64_t within = index - seg_prefix[seg];
+    uint32_t cls = model_class[mdl];
+    uint32_t lb = list_off[(size_t)cls * nW + n], le = list_off[(size_t)cls * nW + n + 1];
+    size_t j = std::upper_bound(list_prefix.begin() + lb, list_prefix.begin() + le, within) -
+               list_prefix.begin() - 1;
+    uint64_t r = within - list_prefix[j];
+    const DevTuple& tu = tuples[list_tuple[j]];
+    uint32_t q = (uint32_t)(r >> lg_rcdo), sel = (uint32_t)(r & (n_rcdo - 1));
+    // recover (b, s) of the q-th valid pair in (b, s) order
+    uint32_t k = 0, b = 0, s = 0;
+    for (uint32_t bb : mbs) {
+        for (uint32_t ss : seq) {
+            if (ss % tu.c) continue;
+            if (gbs && gbs % ((uint64_t)tu.d * bb)) continue;
+            if (k == q) { b = bb; s = ss; }
+            k++;
+        }
+    }
+    me_parallel c{};
+    c.dp = tu.d; c.tp = tu.t; c.pp = tu.p; c.cp = tu.c; c.mbs = b; c.seq = s;
+    c.gbs = gbs; c.first_stage_layers = 0;
+    c.recompute = (uint8_t)((rcdo_rc >> sel) & 1);
+    c.dist_opt = (uint8_t)((rcdo_do >> sel) & 1);
+    c.allow_uneven_pp = uneven;
+    if (model_id) *model_id = mdl;
+    if (world_size) *world_size = world[n];
+    if (out) *out = c;
+    return ME_OK;
+}
+
+}  // namespace me

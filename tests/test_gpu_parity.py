@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact on every record: flat index, capacity mask, six terms and total
+(all integers; there is no tolerance).  Small spaces are compared in full;
+the BASELINE.json full-size spaces (C4, C5) on sampled windows in the same
+launch configuration bench.py uses, plus properties that hold at any size."""
+import numpy as np
+import pytest
+
+import me_inputs as mi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def me():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2411_06465_b200 import build
+    build.build()
+    import paper_2411_06465_b200 as me
+    torch.cuda.set_device(0)
+    return me
+
+
+def oracle_rows(oracle_mod, sp, begin=0, end=0, threads=8):
+    idx, rows, n, caps = oracle_mod.sweep(sp, begin, end, threads=threads)
+    return idx, rows, n, caps
+
+
+def assert_same(me, res, idx, rows, n, caps, mode):
+    lo, gl, off = res.counts()
+    assert lo == n and gl == n and off == 0
+    assert res.cap_counts() == caps
+    if mode == me.ME_OUT_COUNT:
+        return
+    got = res.to_host()
+    assert np.array_equal(got["index_mask"], idx)
+    if mode == me.ME_OUT_FULL:
+        for j, k in enumerate(me.TERMS):
+            assert np.array_equal(got[k], rows[:, j]), k
+
+
+# ---------------------------------------------------------------- single estimates
+def test_estimate_454_paper_cells(me, oracle_mod):
+    """C2 (BASELINE.json configs[1]): the paper's 454 cells through me_estimate_batch."""
+    cells = mi.paper_cells()
+    shapes = [mi.PRESETS["llama3.1-8b"], mi.PRESETS["llama3.1-70b"]]
+    ids = [0 if c["model"] == "llama3.1-8b" else 1 for c in cells]
+    for gbs in (0, 1024):
+        cfgs = [dict(d=c["d"], t=c["tp"], p=c["pp"], c=c["cp"], b=c["mbs"], s=c["seq"], gbs=gbs) for c in cells]
+        for cap in (40, 94):
+            rows, mask, status = me.me_estimate_batch(shapes, ids, cfgs, caps_bytes=[cap << 30])
+            assert not status.any()
+            for i, c in enumerate(cells):
+                e = oracle_mod.estimate(shapes[ids[i]], **cfgs[i])
+                assert rows[i].tolist() == [e[k] for k in oracle_mod.TERMS]
+                assert mask[i] == oracle_mod.cap_mask(e["total"], [cap << 30])
+    # the colour of the table the cell comes from (80% -> green)
+    rows, mask, _ = me.me_estimate_batch(shapes, ids, [dict(d=c["d"], t=c["tp"], p=c["pp"], c=c["cp"], b=c["mbs"],
+                                                            s=c["seq"]) for c in cells],
+                                         caps_bytes=[40 << 30, 94 << 30])
+    for i, c in enumerate(cells):
+        bit = 0 if c["gpu_gb"] == 40 else 1
+        assert bool(mask[i] >> bit & 1) == (c["colour"] == "green")
+
+
+def random_cfgs(rng, shape, n):
+    h, f, L, a, k, v = shape
+    out = []
+    for _ in range(n):
+        t = int(rng.choice([1, 2, 3, 4, 8, 16]))
+        c = int(rng.choice([1, 2, 3, 4, 8]))
+        p = int(rng.choice([1, 2, 3, 4, 5, 8, L, L + 1]))
+        d = int(rng.integers(1, 40))
+        b = int(rng.choice([1, 2, 3, 4, 16]))
+        s = int(rng.choice([1024, 3072, 4096, 8192, 12288]))
+        cfg = dict(d=d, t=t, p=p, c=c, b=b, s=s, gbs=int(rng.choice([0, 0, 96, 1024, 1000])),
+                   rc=int(rng.integers(0, 2)), dopt=int(rng.integers(0, 2)), uneven=int(rng.integers(0, 2)))
+        if rng.random() < 0.2 and p > 1:
+            cfg["L0"] = int(rng.integers(1, L + 1))
+        out.append(cfg)
+    return out
+
+
+def test_estimate_random_with_status(me, oracle_mod):
+    rng = np.random.default_rng(241106465)
+    shapes = mi.random_models(24, seed=5) + [mi.PRESETS[k] for k in ("llama2-7b", "llama2-13b", "llama3.1-70b")]
+    caps = [40 << 30, 80 << 30, 94 << 30, 192 << 30]
+    for si, shape in enumerate(shapes):
+        cfgs = random_cfgs(rng, shape, 200)
+        rows, mask, status = me.me_estimate_batch([shape], None, cfgs, caps_bytes=caps)
+        for i, cfg in enumerate(cfgs):
+            st = oracle_mod.estimate_status(shape, **cfg)
+            assert status[i] == st, (shape, cfg)
+            if st == 0:
+                e = oracle_mod.estimate(shape, **cfg)
+                assert rows[i].tolist() == [e[k] for k in oracle_mod.TERMS], (shape, cfg)
+                assert mask[i] == oracle_mod.cap_mask(e["total"], caps)
+
+
+def test_estimate_edge_cases(me, oracle_mod):
+    M8 = mi.PRESETS["llama3.1-8b"]
+    edge = [
+        ((1, 1, 1, 1, 1, 1), dict(d=1, t=1, p=1, c=1, b=1, s=1)),              # unit model
+        ((32768, 131072, 256, 256, 256, 524288), dict(d=1, t=1, p=1, c=1, b=64, s=1 << 20)),  # domain max
+        ((32768, 131072, 256, 256, 256, 524288), dict(d=1, t=256, p=256, c=1, b=64, s=1 << 20)),
+        ((65536, 131072, 4096, 512, 512, 1 << 22), dict(d=1, t=1, p=1, c=1, b=64, s=1 << 24)),  # overflow
+        (M8, dict(d=7, t=1, p=1, c=1, b=1, s=8192)),                            # ceil rule, d odd
+        (M8, dict(d=1, t=8, p=32, c=1, b=1, s=8192)),                           # p = L
+        (M8, dict(d=1, t=8, p=1, c=8192, b=1, s=8192)),                         # c = s
+        (M8, dict(d=1, t=1, p=2, c=1, b=4, s=8192, gbs=4)),                     # m = 1 < p
+        (M8, dict(d=1, t=1, p=3, c=1, b=1, s=8192, uneven=1)),
+        (M8, dict(d=1, t=1, p=3, c=1, b=1, s=8192, L0=30)),
+        (M8, dict(d=1, t=1, p=3, c=1, b=1, s=8192, L0=31)),                      # EDIV
+        (M8, dict(d=0, t=1, p=1, c=1, b=1, s=8192)),                            # EINVAL
+    ]
+    for shape, cfg in edge:
+        rows, mask, status = me.me_estimate_batch([shape], None, [cfg], caps_bytes=[80 << 30])
+        st = oracle_mod.estimate_status(shape, **cfg)
+        assert status[0] == st, (shape, cfg)
+        if st == 0:
+            e = oracle_mod.estimate(shape, **cfg)
+            assert rows[0].tolist() == [e[k] for k in oracle_mod.TERMS]
+    # me_estimate raises with the oracle's status
+    with pytest.raises(me.MEError) as ex:
+        me.me_estimate(M8, d=1, t=3, p=1, c=1, b=1, s=8192)
+    assert ex.value.status == oracle_mod.EDIV
+
+
+# ---------------------------------------------------------------- sweeps
+def small_spaces():
+    yield "C1", mi.config("C1")
+    yield "C3", mi.config("C3")
+    yield "C3u", mi.config("C3", uneven=1)
+    yield "gbs", mi.Space(models=mi.random_models(5, seed=21, small=True), world=[6, 8, 12, 24], caps_gb=[1, 2, 4],
+                          mbs=[1, 2, 3], seq=[8, 12, 16, 24], gbs=96, uneven=1, thr_num=9, thr_den=10)
+    yield "masks", mi.Space(models=mi.random_models(6, seed=22), world=mi.random_world_sizes(22, 5),
+                            caps_gb=[24, 40, 80, 94, 141, 180, 192, 288], mbs=[1, 2, 8], seq=[2048, 4096, 32768],
+                            rc_mask=2, do_mask=1, max_t=16, max_p=8)
+    yield "one_cap", mi.Space(models=[mi.PRESETS["llama2-70b"], mi.PRESETS["llama2-13b"]], world=[64, 48],
+                              caps_gb=[80], mbs=[1, 2], seq=[4096], gpus_per_node=8, rc_mask=1, do_mask=3)
+
+
+@pytest.mark.parametrize("name,sp", list(small_spaces()), ids=[n for n, _ in small_spaces()])
+@pytest.mark.parametrize("mode", [0, 1, 2], ids=["count", "index", "full"])
+def test_sweep_small_spaces(me, oracle_mod, name, sp, mode):
+    plan = me.Plan(sp)
+    assert plan.size == oracle_mod.space_size(sp)
+    res = plan.sweep(mode=mode)
+    assert res.status() == 0
+    assert_same(me, res, *oracle_rows(oracle_mod, sp), mode)
+
+
+def test_sweep_subranges(me, oracle_mod):
+    sp = mi.config("C3", uneven=1)
+    plan = me.Plan(sp)
+    rng = np.random.default_rng(3)
+    ranges = [(0, 1), (5, 5), (31, 33), (1000, 1031), (plan.size - 1, plan.size), (0, 0)]
+    ranges += [tuple(sorted(int(x) for x in rng.integers(0, plan.size, 2))) for _ in range(6)]
+    for b, e in ranges:
+        res = plan.sweep(b, e, mode=me.ME_OUT_FULL)
+        if (b, e) == (0, 0):
+            e = plan.size
+        assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), me.ME_OUT_FULL)
+
+
+def test_caller_columns_and_overflow(me, oracle_mod):
+    import torch
+    sp = mi.config("C3")
+    plan = me.Plan(sp)
+    idx, rows, n, caps = oracle_rows(oracle_mod, sp)
+    cols = [torch.full((n + 5,), -1, dtype=torch.int64, device="cuda") for _ in range(8)]
+    res = plan.sweep(mode=me.ME_OUT_FULL, out_cols=cols)
+    assert res.status() == 0
+    assert_same(me, res, idx, rows, n, caps, me.ME_OUT_FULL)
+    assert (cols[0][n:] == -1).all()
+    small = [torch.zeros(n // 2, dtype=torch.int64, device="cuda")]
+    res = plan.sweep(mode=me.ME_OUT_INDEX, out_cols=small)
+    assert res.status() == 7  # ME_ERANGE
+    assert res.counts()[0] == n
+    got = small[0].cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, idx[: n // 2])
+
+
+def test_random_model_grid(me, oracle_mod):
+    """Seeded random Llama shapes x non-power-of-two world sizes (ceil rule R8)."""
+    sp = mi.Space(models=mi.random_models(40, seed=99), world=[24, 96, 120, 1000], caps_gb=[40, 80, 94, 192],
+                  mbs=[1, 2, 4], seq=[4096, 8192, 131072], uneven=1)
+    plan = me.Plan(sp)
+    res = plan.sweep(mode=me.ME_OUT_FULL)
+    assert_same(me, res, *oracle_rows(oracle_mod, sp, threads=16), me.ME_OUT_FULL)
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_size_sampled(me, oracle_mod, name):
+    """BASELINE.json configs[3]/[4] at full size, in bench.py's launch
+    configuration (chunks of bench.CHUNK): windows compared record by record
+    with the oracle, sampled rows of whole chunks recomputed one by one, and
+    the properties every chunk must have."""
+    import torch
+
+    import bench
+    sp = mi.config(name)
+    plan = me.Plan(sp)
+    assert plan.size == oracle_mod.space_size(sp)
+    rng = np.random.default_rng(7 if name == "C4" else 8)
+    # exact windows (including the first and last indices of the space)
+    wins = [(0, 20_000), (plan.size - 20_000, plan.size)]
+    wins += [(s, s + 20_000) for s in (int(x) for x in rng.integers(0, plan.size - 20_000, 4))]
+    for b, e in wins:
+        res = plan.sweep(b, e, mode=me.ME_OUT_FULL)
+        assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), me.ME_OUT_FULL)
+    # whole bench chunks: sampled rows and ordering properties
+    chunk = bench.CHUNK
+    cols = [torch.empty(chunk, dtype=torch.int64, device="cuda") for _ in range(8)]
+    starts = [0, (plan.size // chunk // 2) * chunk, (plan.size - 1) // chunk * chunk]
+    for s in starts:
+        e = min(plan.size, s + chunk)
+        res = plan.sweep(s, e, mode=me.ME_OUT_FULL, out_cols=cols)
+        assert res.status() == 0
+        n = res.counts()[0]
+        assert 0 < n <= e - s
+        ix = cols[0][:n].cpu().numpy().view(np.uint64)
+        index = ix & np.uint64((1 << 56) - 1)
+        mask = ix >> np.uint64(56)
+        assert (np.diff(index.astype(np.int64)) > 0).all() and index[0] >= s and index[-1] < e
+        assert (mask > 0).all() and (mask < 16).all()
+        tot = [cols[j][:n].cpu().numpy().view(np.uint64) for j in range(1, 8)]
+        assert np.array_equal(tot[0] + tot[1] + tot[2] + tot[3] + tot[4] + tot[5], tot[6])
+        assert np.array_equal(tot[1], 2 * tot[0])
+        # masks are monotone in capacity: feasible at 40 GiB => feasible at 80, ...
+        m = mask.astype(np.int64)
+        assert ((m & 1) <= (m >> 1 & 1)).all() and ((m >> 1 & 1) <= (m >> 2 & 1)).all()
+        for k in rng.choice(n, size=64, replace=False):
+            i = int(index[k])
+            mid, N, cfg = oracle_mod.decode(sp, i)
+            e_ = oracle_mod.estimate(sp.models[mid], uneven=sp.uneven, **cfg)
+            assert [int(t[k]) for t in tot] == [e_[q] for q in oracle_mod.TERMS], i
+            assert int(mask[k]) == oracle_mod.cap_mask(e_["total"], sp.cap_bytes)
