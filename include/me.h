@@ -222,6 +222,17 @@ int me_result_wait(me_result* r);
 int me_result_timing(me_result* r, float* ms4);
 void me_result_free(me_result* r);
 
+/* Host logic of the multi-GPU path (host-only, no device needed).
+ * me_partition: rank's contiguous share [lo, hi) of [begin, end) with
+ * lo = begin + floor(len*rank/nranks), hi likewise for rank + 1.
+ * me_join_counts: from every rank's stats row (stride u64 per rank: survivor
+ * count then n_cap per-capacity counts, as allgathered by a comm sweep)
+ * compute this rank's global row offset, the global count and the global
+ * per-capacity counts (cap_global may be NULL). */
+int me_partition(uint64_t begin, uint64_t end, int rank, int nranks, uint64_t* lo, uint64_t* hi);
+int me_join_counts(const uint64_t* stats, int nranks, uint32_t stride, uint32_t n_cap, int rank,
+                   uint64_t* offset, uint64_t* global, uint64_t* cap_global);
+
 /* NCCL communicator over nranks processes (one per GPU).  rank 0 creates the
  * unique id with me_comm_unique_id and the caller distributes it (e.g. with
  * torch.distributed); every rank then calls me_comm_init collectively. */

@@ -18,6 +18,9 @@ uint32_t ncap_stride(uint32_t n_cap);
 
 using namespace me;
 
+extern "C" int me_partition(uint64_t, uint64_t, int, int, uint64_t*, uint64_t*);
+extern "C" int me_join_counts(const uint64_t*, int, uint32_t, uint32_t, int, uint64_t*, uint64_t*, uint64_t*);
+
 // ---------------------------------------------------------------------------
 // errors
 // ---------------------------------------------------------------------------
@@ -277,10 +280,8 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     if (e > total) e = total;
     if (b > e) b = e;
     if (o->comm) {
-        const uint64_t len = e - b;
-        const int r = o->comm->rank, n = o->comm->nranks;
-        const uint64_t q = len / n, rem = len % n;
-        const uint64_t lo = b + q * r + (rem * r) / n, hi = b + q * (r + 1) + (rem * (r + 1)) / n;
+        uint64_t lo = 0, hi = 0;
+        me_partition(b, e, o->comm->rank, o->comm->nranks, &lo, &hi);
         b = lo;
         e = hi;
     }
@@ -421,13 +422,7 @@ static int resolve(me_result* R) {
     if (R->comm) {
         std::vector<uint64_t> all((size_t)R->comm->nranks * 9);
         CU(cudaMemcpy(all.data(), R->gathered, all.size() * 8, cudaMemcpyDeviceToHost));
-        R->global = 0;
-        for (int q = 0; q < 8; q++) R->caps[q] = 0;
-        for (int r = 0; r < R->comm->nranks; r++) {
-            if (r < R->comm->rank) R->offset += all[(size_t)r * 9];
-            R->global += all[(size_t)r * 9];
-            for (int q = 0; q < 8; q++) R->caps[q] += all[(size_t)r * 9 + 1 + q];
-        }
+        me_join_counts(all.data(), R->comm->nranks, 9, 8, R->comm->rank, &R->offset, &R->global, R->caps);
     }
     R->resolved = true;
     return ME_OK;
@@ -645,6 +640,36 @@ extern "C" int me_decode(const me_model_range* models, const me_cluster* cluster
     if (st) return err(st, d);
     st = H.decode(index, model_id, world_size, out);
     if (st) return err(st, "index past the end of the space");
+    return ME_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU host logic (used by plan_sweep / resolve; exported for tests)
+// ---------------------------------------------------------------------------
+extern "C" int me_partition(uint64_t begin, uint64_t end, int rank, int nranks, uint64_t* lo, uint64_t* hi) {
+    if (!lo || !hi || nranks < 1 || rank < 0 || rank >= nranks || end < begin)
+        return err(ME_EINVAL, "bad partition arguments");
+    const uint64_t len = end - begin, n = (uint64_t)nranks, r = (uint64_t)rank;
+    const uint64_t q = len / n, rem = len % n;
+    *lo = begin + q * r + (rem * r) / n;
+    *hi = begin + q * (r + 1) + (rem * (r + 1)) / n;
+    return ME_OK;
+}
+
+extern "C" int me_join_counts(const uint64_t* stats, int nranks, uint32_t stride, uint32_t n_cap, int rank,
+                              uint64_t* offset, uint64_t* global, uint64_t* cap_global) {
+    if (!stats || nranks < 1 || rank < 0 || rank >= nranks || stride < 1 + n_cap)
+        return err(ME_EINVAL, "bad join arguments");
+    uint64_t off = 0, tot = 0;
+    for (uint32_t q = 0; q < n_cap && cap_global; q++) cap_global[q] = 0;
+    for (int r = 0; r < nranks; r++) {
+        const uint64_t* row = stats + (size_t)r * stride;
+        if (r < rank) off += row[0];
+        tot += row[0];
+        for (uint32_t q = 0; q < n_cap && cap_global; q++) cap_global[q] += row[1 + q];
+    }
+    if (offset) *offset = off;
+    if (global) *global = tot;
     return ME_OK;
 }
 
