@@ -127,12 +127,12 @@ def cpu_baseline(sp, begin, end, budget_s=12.0):
     threads = oracle.default_threads()
     # calibrate
     t = time.perf_counter()
-    cal = 200_000
+    cal = 1_000_000
     oracle.sweep(sp, begin, begin + cal, rows=False, threads=threads)
     dt = time.perf_counter() - t
     rate = cal / max(dt, 1e-6)
     n = int(min(end - begin, max(cal, rate * budget_s)))
-    wins = 16
+    wins = 4
     per = max(1, n // wins)
     done, t0 = 0, time.perf_counter()
     for w in range(wins):

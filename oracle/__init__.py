@@ -95,6 +95,7 @@ def lib():
         _lib.or_decode.argtypes = [P(SpaceC), ctypes.c_uint64, _u32p, _u32p, P(Cfg)]
         _lib.or_sweep.argtypes = [P(SpaceC), ctypes.c_uint64, ctypes.c_uint64, _u64p,
                                   P(Breakdown), ctypes.c_uint64, _u64p, _u64p, ctypes.c_int]
+        _lib.or_points.argtypes = [P(SpaceC), _u64p, ctypes.c_uint64, P(Breakdown), _u32p]
     return _lib
 
 
@@ -222,6 +223,23 @@ def sweep(sp, begin=0, end=0, rows=True, threads=None, max_rows=None):
     if rows:
         return idx[:n].copy(), rw[:n].copy(), n, caps
     return None, None, n, caps
+
+
+def points(sp, indices):
+    """Records (rows uint64[n, 7], masks uint32[n]) of the configurations at the
+    given indices, evaluated one by one in a single canonical walk."""
+    h = _SpaceHolder(sp)
+    order = np.argsort(np.asarray(indices, dtype=np.uint64), kind="stable")
+    pts = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64)[order])
+    rows = np.zeros((len(pts), 7), dtype=np.uint64)
+    masks = np.zeros(len(pts), dtype=np.uint32)
+    st = lib().or_points(ctypes.byref(h.c), pts.ctypes.data_as(_u64p), len(pts),
+                         rows.ctypes.data_as(ctypes.POINTER(Breakdown)), masks.ctypes.data_as(_u32p))
+    if st:
+        raise OracleError(st, "points")
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    return rows[inv], masks[inv]
 
 
 def default_threads() -> int:

@@ -529,6 +529,61 @@ int or_decode(const or_space* sp, uint64_t index, uint32_t* model_id, uint32_t* 
     return OR_OK;
 }
 
+/* The same canonical walk, visiting only the given ascending indices: every
+ * visited configuration is evaluated (feasible or not). */
+int or_points(const or_space* sp, const uint64_t* points, uint64_t n, or_breakdown* rows,
+              uint32_t* masks) {
+    int st = space_ok(sp);
+    if (st) return st;
+    for (uint64_t k = 1; k < n; k++)
+        if (points[k] <= points[k - 1]) return OR_EINVAL;
+    tables T;
+    if ((st = build_tables(sp, &T))) return st;
+    uint64_t idx = 0, k = 0;
+    for (uint32_t mi = 0; mi < sp->n_models && k < n; mi++) {
+        const or_model* m = &sp->models[mi];
+        for (uint32_t ni = 0; ni < sp->n_world && k < n; ni++) {
+            const tuplist* tl = &T.tl[ni];
+            for (uint32_t j = 0; j < tl->n && k < n; j++) {
+                const tup* u = &tl->v[j];
+                if (!valid_static(sp, m, u)) continue;
+                if (idx + u->w <= points[k]) { idx += u->w; continue; }
+                for (uint32_t bi = 0; bi < sp->n_mbs; bi++)
+                    for (uint32_t si = 0; si < sp->n_seq; si++) {
+                        uint32_t b = sp->mbs[bi], s = sp->seq[si];
+                        if (s % u->c) continue;
+                        if (sp->gbs && sp->gbs % ((uint64_t)u->d * b)) continue;
+                        for (uint32_t rc = 0; rc < 2; rc++) {
+                            if (!((sp->rc_mask >> rc) & 1)) continue;
+                            for (uint32_t dopt = 0; dopt < 2; dopt++) {
+                                if (!((sp->do_mask >> dopt) & 1)) continue;
+                                if (k < n && idx == points[k]) {
+                                    or_cfg c;
+                                    memset(&c, 0, sizeof c);
+                                    c.d = u->d; c.t = u->t; c.p = u->p; c.c = u->c;
+                                    c.b = b; c.s = s; c.gbs = sp->gbs;
+                                    c.rc = (uint8_t)rc; c.dopt = (uint8_t)dopt;
+                                    c.uneven = sp->uneven;
+                                    or_breakdown r;
+                                    st = or_estimate(m, &c, &r);
+                                    if (st) { free_tables(&T); return st; }
+                                    if (rows) rows[k] = r;
+                                    if (masks)
+                                        masks[k] = or_cap_mask(r.total, sp->cap_bytes, sp->n_caps,
+                                                               sp->thr_num, sp->thr_den);
+                                    k++;
+                                }
+                                idx++;
+                            }
+                        }
+                    }
+            }
+        }
+    }
+    free_tables(&T);
+    return k == n ? OR_OK : OR_ERANGE;
+}
+
 static void* walk_thread(void* arg) {
     walk((walk_t*)arg);
     return NULL;
@@ -539,9 +594,11 @@ int or_sweep(const or_space* sp, uint64_t begin, uint64_t end, uint64_t* idx_mas
              int n_threads) {
     int st = space_ok(sp);
     if (st) return st;
-    uint64_t total;
-    if ((st = or_space_size(sp, &total))) return st;
-    if (end == 0 || end > total) end = total;
+    if (end == 0) {
+        /* whole space: its size bounds the range (a given end may also lie
+           past the space; the walk then simply stops at its last index) */
+        if ((st = or_space_size(sp, &end))) return st;
+    }
     if (begin > end) begin = end;
     if (n_threads < 1) n_threads = 1;
     if ((uint64_t)n_threads > end - begin) n_threads = (int)(end - begin ? end - begin : 1);

@@ -99,6 +99,11 @@ int or_sweep(const or_space* sp, uint64_t begin, uint64_t end, uint64_t* idx_mas
              or_breakdown* rows, uint64_t cap, uint64_t* count, uint64_t* cap_counts,
              int n_threads);
 
+/* Evaluate the configurations at the given strictly ascending indices (one
+ * walk): rows[k] and masks[k] (either may be NULL) for points[k]. */
+int or_points(const or_space* sp, const uint64_t* points, uint64_t n, or_breakdown* rows,
+              uint32_t* masks);
+
 #ifdef __cplusplus
 }
 #endif

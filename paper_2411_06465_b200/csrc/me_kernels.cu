@@ -78,18 +78,26 @@ struct Walker {
     // move forward by `step` indices (the caller guarantees the target exists)
     __device__ __forceinline__ void advance(const DevSpace& S, uint32_t step) {
         r += step;
-        while (r >= w) {
-            r -= w;
-            ++j;
-            if (j == jend) {
-                uint32_t s = seg;
-                do {
-                    ++s;
-                } while (__ldg(S.seg_prefix + s + 1) == __ldg(S.seg_prefix + s));
-                enter_segment(S, s);
-            }
-            set_row(S);
+        while (r >= w) next_row(S);
+    }
+
+    // leave the current row (r >= w): next tuple of the list, next non-empty
+    // segment when the list is exhausted
+    __device__ __forceinline__ void next_row(const DevSpace& S) {
+        r -= w;
+        ++j;
+        if (j == jend) {
+            uint32_t s = seg;
+            do {
+                ++s;
+            } while (__ldg(S.seg_prefix + s + 1) == __ldg(S.seg_prefix + s));
+            enter_segment(S, s);
         }
+        set_row(S);
+    }
+
+    __device__ __forceinline__ uint2 pair(const DevSpace& S, uint32_t lg) const {
+        return __ldg(reinterpret_cast<const uint2*>(S.pairs) + pair_off + (r >> lg));
     }
 };
 
@@ -113,6 +121,96 @@ __device__ __forceinline__ uint32_t cap_mask(const DevSpace& S, uint64_t total) 
     return mask;
 }
 
+// Per-lane accumulators of the count pass: survivor count and 8-bit packed
+// per-capacity counters (mask * 0x00204081 spreads bits 0..3 to bytes 0..3).
+template <int NCAP>
+struct CountAcc {
+    uint32_t cnt = 0, lo = 0, hi = 0, round = 0;
+    uint32_t capc[NCAP];
+    __device__ __forceinline__ CountAcc() {
+#pragma unroll
+        for (int q = 0; q < NCAP; q++) capc[q] = 0;
+    }
+    __device__ __forceinline__ void flush() {
+#pragma unroll
+        for (int q = 0; q < NCAP; q++) capc[q] += ((q < 4 ? lo : hi) >> (8 * (q & 3))) & 255u;
+        lo = hi = 0;
+    }
+    __device__ __forceinline__ void add(uint32_t mask) {
+        cnt += mask ? 1u : 0u;
+        if (NCAP <= 4) {
+            lo += (mask * 0x00204081u) & 0x01010101u;
+        } else {
+            lo += ((mask & 15u) * 0x00204081u) & 0x01010101u;
+            hi += ((mask >> 4) * 0x00204081u) & 0x01010101u;
+        }
+        if ((++round & 255u) == 0) flush();
+    }
+};
+
+// One warp span.  RAGGED = the span does not start and end on multiples of 32
+// (only the first and last spans of a range), so lanes need range checks.
+// The pair of the next round is loaded before the current round is evaluated
+// (software pipelining of the only per-config memory access).
+template <int MODE, int NCAP, bool RAGGED>
+__device__ __forceinline__ void walk_span(const DevSpace& S, uint64_t sb, uint64_t se, uint32_t lane,
+                                          CountAcc<NCAP>& acc, uint64_t out, const Cols& cols,
+                                          uint64_t capacity) {
+    const uint64_t base = sb & ~31ull;
+    Walker W;
+    uint64_t pos = base + lane;
+    if (RAGGED && pos >= se) return;  // this lane never has work (its later positions are >= se too)
+    W.seek(S, pos);
+    const uint32_t rc_bits = S.rcdo_rc, do_bits = S.rcdo_do, lg = S.lg_rcdo;
+    const uint32_t sel_mask = (1u << lg) - 1;
+    uint2 pr = W.pair(S, lg);
+    for (uint64_t p0 = base; p0 < se; p0 += 32, pos += 32) {
+        // issue the next round's pair load first when it stays in this row
+        const uint32_t rn = W.r + 32;
+        const bool more = pos + 32 < se;
+        const bool in_row = rn < W.w;
+        uint2 prn = pr;
+        if (in_row && more) prn = __ldg(reinterpret_cast<const uint2*>(S.pairs) + W.pair_off + (rn >> lg));
+
+        const bool act = !RAGGED || (pos >= sb && pos < se);
+        const uint32_t sel = W.r & sel_mask;
+        const uint32_t rc = (rc_bits >> sel) & 1u, dopt = (do_bits >> sel) & 1u;
+        const uint64_t total = config_total(W.R, pr.x, pr.y, rc, dopt);
+        uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
+        if (MODE == 0) {
+            acc.add(mask);
+        } else {
+            const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
+            if (mask) {
+                const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
+                if (o < capacity) {
+                    cols.c[0][o] = pos | ((uint64_t)mask << 56);
+                    if (MODE == 2) {
+                        const TermsT<uint64_t> T = config_terms_no_total(W.R, pr.x, pr.y, rc, dopt);
+                        cols.c[1][o] = T.params;
+                        cols.c[2][o] = T.grads;
+                        cols.c[3][o] = T.optim;
+                        cols.c[4][o] = T.layers;
+                        cols.c[5][o] = T.embed;
+                        cols.c[6][o] = T.head;
+                        cols.c[7][o] = total;
+                    }
+                }
+            }
+            out += __popc(ballot);
+        }
+        if (more) {
+            if (in_row) {
+                W.r = rn;
+                pr = prn;
+            } else {
+                W.advance(S, 32);
+                pr = W.pair(S, lg);
+            }
+        }
+    }
+}
+
 // MODE 0 = count pass, 1 = INDEX write, 2 = FULL write
 template <int MODE, int NCAP>
 __global__ void __launch_bounds__(kThreads) sweep_kernel(const DevSpace S, const uint64_t begin,
@@ -127,82 +225,21 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const DevSpace S, const
     const uint64_t sb = span_start(begin, end, gw, n_warps);
     const uint64_t se = span_start(begin, end, gw + 1, n_warps);
 
-    uint32_t cnt = 0;
-    uint32_t packed_lo = 0, packed_hi = 0;  // 8-bit per-capacity counters
-    uint32_t capc[NCAP];
-#pragma unroll
-    for (int q = 0; q < NCAP; q++) capc[q] = 0;
+    CountAcc<NCAP> acc;
     uint64_t out = 0;
     if (MODE != 0) out = warp_off[gw];
-
     if (sb < se) {
-        const uint64_t base = sb & ~31ull;
-        Walker W;
-        uint64_t pos = base + lane;
-        if (pos < se) W.seek(S, pos);
-        const uint32_t rc_bits = S.rcdo_rc, do_bits = S.rcdo_do, lg = S.lg_rcdo;
-        const uint32_t sel_mask = (1u << lg) - 1;
-        uint32_t round = 0;
-        for (uint64_t p0 = base; p0 < se; p0 += 32, pos += 32) {
-            const bool live = pos < se;
-            const bool act = live && pos >= sb;
-            uint32_t mask = 0;
-            uint64_t total = 0;
-            uint32_t u = 0, m = 0, rc = 0, dopt = 0;
-            if (act) {
-                const uint2 pr = __ldg(reinterpret_cast<const uint2*>(S.pairs) + W.pair_off + (W.r >> lg));
-                const uint32_t sel = W.r & sel_mask;
-                u = pr.x;
-                m = pr.y;
-                rc = (rc_bits >> sel) & 1u;
-                dopt = (do_bits >> sel) & 1u;
-                total = config_total(W.R, u, m, rc, dopt);
-                mask = cap_mask<NCAP>(S, total);
-            }
-            if (MODE == 0) {
-                cnt += mask ? 1u : 0u;
-                if (NCAP <= 4) {
-                    packed_lo += (mask * 0x00204081u) & 0x01010101u;
-                } else {
-                    packed_lo += ((mask & 15u) * 0x00204081u) & 0x01010101u;
-                    packed_hi += ((mask >> 4) * 0x00204081u) & 0x01010101u;
-                }
-                if ((++round & 255u) == 0) {
-#pragma unroll
-                    for (int q = 0; q < NCAP; q++)
-                        capc[q] += ((q < 4 ? packed_lo : packed_hi) >> (8 * (q & 3))) & 255u;
-                    packed_lo = packed_hi = 0;
-                }
-            } else {
-                const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
-                if (mask) {
-                    const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
-                    if (o < capacity) {
-                        cols.c[0][o] = pos | ((uint64_t)mask << 56);
-                        if (MODE == 2) {
-                            const TermsT<uint64_t> T = config_terms(W.R, u, m, rc, dopt);
-                            cols.c[1][o] = T.params;
-                            cols.c[2][o] = T.grads;
-                            cols.c[3][o] = T.optim;
-                            cols.c[4][o] = T.layers;
-                            cols.c[5][o] = T.embed;
-                            cols.c[6][o] = T.head;
-                            cols.c[7][o] = T.total;
-                        }
-                    }
-                }
-                out += __popc(ballot);
-            }
-            if (pos + 32 < se) W.advance(S, 32);
-        }
+        if (((sb | se) & 31ull) == 0)
+            walk_span<MODE, NCAP, false>(S, sb, se, lane, acc, out, cols, capacity);
+        else
+            walk_span<MODE, NCAP, true>(S, sb, se, lane, acc, out, cols, capacity);
     }
     if (MODE == 0) {
+        acc.flush();
+        const uint32_t cnt = __reduce_add_sync(0xffffffffu, acc.cnt);
+        uint32_t capc[NCAP];
 #pragma unroll
-        for (int q = 0; q < NCAP; q++)
-            capc[q] += ((q < 4 ? packed_lo : packed_hi) >> (8 * (q & 3))) & 255u;
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-#pragma unroll
-        for (int q = 0; q < NCAP; q++) capc[q] = __reduce_add_sync(0xffffffffu, capc[q]);
+        for (int q = 0; q < NCAP; q++) capc[q] = __reduce_add_sync(0xffffffffu, acc.capc[q]);
         if (lane == 0) {
             warp_count[gw] = cnt;
 #pragma unroll

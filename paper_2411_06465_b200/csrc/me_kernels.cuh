@@ -95,8 +95,25 @@ __device__ __forceinline__ uint64_t config_total(const RowCoef& R, uint32_t u, u
     return (dopt ? R.ms1 : R.ms0) + (uint64_t)u * K;
 }
 
-// all six terms (write pass, single estimates); total = their sum, equal to
-// config_total term by term
+// the six terms without their sum (the write pass reuses config_total's value,
+// which equals the sum term by term)
+template <typename U>
+__device__ __forceinline__ TermsT<U> config_terms_no_total(const RowCoefT<U>& R, uint32_t u, uint32_t m,
+                                                           uint32_t rc, uint32_t dopt) {
+    const uint32_t n_inf = min(R.p, m);
+    TermsT<U> T;
+    T.params = (U)2 * R.psi;
+    T.grads = (U)4 * R.psi;
+    T.optim = dopt ? R.optim1 : (U)12 * R.psi;
+    T.layers = (U)u * (rc ? ((U)n_inf * R.lam1 + R.bt) : (U)n_inf * R.lam0);
+    T.embed = (U)u * ((U)n_inf * R.e8);
+    T.head = (U)u * R.hc;
+    T.total = 0;
+    return T;
+}
+
+// all six terms (single estimates); total = their sum, equal to config_total
+// term by term
 template <typename U>
 __device__ __forceinline__ TermsT<U> config_terms(const RowCoefT<U>& R, uint32_t u, uint32_t m,
                                                   uint32_t rc, uint32_t dopt) {

@@ -233,9 +233,8 @@ def test_full_size_sampled(me, oracle_mod, name):
         # masks are monotone in capacity: feasible at 40 GiB => feasible at 80, ...
         m = mask.astype(np.int64)
         assert ((m & 1) <= (m >> 1 & 1)).all() and ((m >> 1 & 1) <= (m >> 2 & 1)).all()
-        for k in rng.choice(n, size=64, replace=False):
-            i = int(index[k])
-            mid, N, cfg = oracle_mod.decode(sp, i)
-            e_ = oracle_mod.estimate(sp.models[mid], uneven=sp.uneven, **cfg)
-            assert [int(t[k]) for t in tot] == [e_[q] for q in oracle_mod.TERMS], i
-            assert int(mask[k]) == oracle_mod.cap_mask(e_["total"], sp.cap_bytes)
+        ks = np.sort(rng.choice(n, size=256, replace=False))
+        o_rows, o_masks = oracle_mod.points(sp, index[ks])
+        for q, k in enumerate(ks):
+            assert [int(t[k]) for t in tot] == o_rows[q].tolist(), int(index[k])
+            assert int(mask[k]) == int(o_masks[q])

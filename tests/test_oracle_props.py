@@ -6,6 +6,8 @@ against an itertools re-statement of the canonical order and
 the closed-form tuple counts of the configs."""
 import itertools
 
+import numpy as np
+
 import pytest
 
 import me_inputs as mi
@@ -222,3 +224,13 @@ def test_sweep_matches_pointwise(oracle_mod):
     a = oracle_mod.sweep(sp, 0, 77)[0]
     b = oracle_mod.sweep(sp, 77, 240)[0]
     assert list(a) + list(b) == list(idx)
+
+
+def test_points_match_sweep(oracle_mod):
+    sp = mi.config("C3")
+    idx, rows, n, caps = oracle_mod.sweep(sp)
+    index = (idx & np.uint64((1 << 56) - 1))
+    pick = index[::97]
+    r2, m2 = oracle_mod.points(sp, pick[::-1])
+    assert (r2[::-1] == rows[::97]).all()
+    assert (m2[::-1] == (idx[::97] >> np.uint64(56))).all()
