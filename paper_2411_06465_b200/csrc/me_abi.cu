@@ -99,11 +99,23 @@ struct me_plan {
     Alloc A;
     int device = 0;
     std::vector<void*> owned;  // device allocations owned by the plan
-    // scratch, sized for max warps
-    uint32_t max_blocks = 0;
-    uint32_t* warp_count = nullptr;
-    uint32_t* warp_caps = nullptr;
-    uint64_t* warp_off = nullptr;
+    // Launch shape.  The range of a sweep is cut into n_spans warp spans (fixes
+    // the output offsets); the count and write passes run on their own grids.
+    int sms = 148;
+    uint32_t max_spans = 0;
+    uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
+    // Two scratch sets, alternated by successive sweeps, so that the count pass
+    // of sweep i+1 (on the plan's count stream) overlaps the write pass of sweep
+    // i (on the caller's stream).
+    struct Scratch {
+        uint32_t* warp_count = nullptr;
+        uint32_t* warp_caps = nullptr;
+        uint64_t* warp_off = nullptr;
+        cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
+    } scratch[2];
+    uint32_t turn = 0;
+    cudaStream_t cstream = nullptr;     // count + scan passes
+    cudaEvent_t ready_ev = nullptr;     // tables uploaded
 };
 
 struct me_result {
@@ -130,13 +142,6 @@ struct me_result {
     uint64_t local = 0, global = 0, offset = 0;
     uint64_t caps[8] = {};
 };
-
-static uint32_t blocks_for(uint64_t len, uint32_t max_blocks) {
-    // >= 8 rounds of 32 per warp before spreading wider
-    uint64_t want = (len + (uint64_t)kThreads * 8 - 1) / ((uint64_t)kThreads * 8);
-    if (want < 1) want = 1;
-    return (uint32_t)(want < max_blocks ? want : max_blocks);
-}
 
 static int plan_create(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
                        me_threshold thr, int device, void* stream, me_alloc_fn al, me_free_fn fr, void* ctx,
@@ -202,21 +207,40 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     for (int q = 0; q < 8; q++) D.thr[q] = 0;
     for (size_t q = 0; q < H.caps.size(); q++)
         D.thr[q] = (uint64_t)(((unsigned __int128)H.caps[q] * thr.num) / thr.den);
-    // scratch: 8 resident blocks of 256 threads per SM
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    P->max_blocks = (uint32_t)sms * 8;
-    const uint32_t max_warps = P->max_blocks * kWarpsPerBlock;
-    P->warp_count = (uint32_t*)P->A.get((size_t)max_warps * 4);
-    P->warp_caps = (uint32_t*)P->A.get((size_t)max_warps * 8 * 4);
-    P->warp_off = (uint64_t*)P->A.get((size_t)(max_warps + 1) * 8);
-    P->owned.push_back(P->warp_count);
-    P->owned.push_back(P->warp_caps);
-    P->owned.push_back(P->warp_off);
-    if (!P->warp_count || !P->warp_caps || !P->warp_off) {
-        me_plan_free(P);
-        return err(ME_ENOMEM, "scratch allocation");
+    // launch shape: spans = 96 per SM (divisible by every grid of 1..4
+    // resident 8-warp blocks per SM, so the grid-stride over spans is even)
+    cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
+    P->max_spans = (uint32_t)P->sms * 96;
+    const int occ_c = sweep_blocks_per_sm(0, D.n_cap), occ_w = sweep_blocks_per_sm(2, D.n_cap);
+    P->write_bps = (uint32_t)(occ_w > 1 ? occ_w - 1 : 1);
+    P->count_bps = (uint32_t)(occ_c - (int)P->write_bps > 0 ? occ_c - (int)P->write_bps : 1);
+    if (const char* e = getenv("ME_WRITE_BPS")) P->write_bps = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_COUNT_BPS")) P->count_bps = (uint32_t)atoi(e);
+    if (P->write_bps < 1) P->write_bps = 1;
+    if (P->count_bps < 1) P->count_bps = 1;
+    for (auto& sc : P->scratch) {
+        sc.warp_count = (uint32_t*)P->A.get((size_t)P->max_spans * 4);
+        sc.warp_caps = (uint32_t*)P->A.get((size_t)P->max_spans * 8 * 4);
+        sc.warp_off = (uint64_t*)P->A.get((size_t)(P->max_spans + 1) * 8);
+        P->owned.push_back(sc.warp_count);
+        P->owned.push_back(sc.warp_caps);
+        P->owned.push_back(sc.warp_off);
+        if (!sc.warp_count || !sc.warp_caps || !sc.warp_off) {
+            me_plan_free(P);
+            return err(ME_ENOMEM, "scratch allocation");
+        }
+        if (cudaEventCreateWithFlags(&sc.free_ev, cudaEventDisableTiming) != cudaSuccess) {
+            me_plan_free(P);
+            return cuda_err(cudaGetLastError(), "cudaEventCreate");
+        }
+        cudaEventRecord(sc.free_ev, (cudaStream_t)stream);
     }
+    if (cudaStreamCreateWithFlags(&P->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ready_ev, cudaEventDisableTiming) != cudaSuccess) {
+        me_plan_free(P);
+        return cuda_err(cudaGetLastError(), "count stream");
+    }
+    cudaEventRecord(P->ready_ev, (cudaStream_t)stream);
     *out = P;
     return ME_OK;
 }
@@ -246,7 +270,12 @@ extern "C" void me_plan_free(me_plan* P) {
     if (!P) return;
     {
         DeviceGuard g(P->device);
+        if (P->cstream) cudaStreamSynchronize(P->cstream);
         for (void* p : P->owned) P->A.put(p);
+        for (auto& sc : P->scratch)
+            if (sc.free_ev) cudaEventDestroy(sc.free_ev);
+        if (P->ready_ev) cudaEventDestroy(P->ready_ev);
+        if (P->cstream) cudaStreamDestroy(P->cstream);
     }
     delete P;
 }
@@ -254,6 +283,9 @@ extern "C" void me_plan_free(me_plan* P) {
 static void result_release(me_result* R) {
     if (!R) return;
     DeviceGuard g(R->plan ? R->plan->device : -1);
+    // the count stream and the caller's stream may still use the buffers
+    if (R->ev[2]) cudaEventSynchronize(R->ev[2]);
+    if (R->ev[4]) cudaEventSynchronize(R->ev[4]);
     for (int i = 0; i < 5; i++)
         if (R->ev[i]) cudaEventDestroy(R->ev[i]);
     R->A.put(R->stats);
@@ -307,23 +339,36 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         if (cudaEventCreate(&R->ev[i]) != cudaSuccess) return fail(cuda_err(cudaErrorUnknown, "cudaEventCreate"));
     R->stats = (uint64_t*)R->A.get(9 * 8);
     if (!R->stats) return fail(err(ME_ENOMEM, "stats allocation"));
-    if (cudaMemsetAsync(R->stats, 0, 9 * 8, st) != cudaSuccess) return fail(cuda_err(cudaErrorUnknown, "memset"));
 
+    // count + scan on the plan's count stream; it waits only for the tables and
+    // for the write pass that last used this scratch set, so it can run while
+    // the caller's stream is still writing the previous sweep's columns
+    me_plan::Scratch& sc = P->scratch[P->turn++ & 1];
+    cudaStream_t cs = P->cstream;
+    cudaStreamWaitEvent(cs, P->ready_ev, 0);
+    cudaStreamWaitEvent(cs, sc.free_ev, 0);
+    if (cudaMemsetAsync(R->stats, 0, 9 * 8, cs) != cudaSuccess) return fail(cuda_err(cudaErrorUnknown, "memset"));
     const uint64_t len = e - b;
-    const uint32_t nb = blocks_for(len, P->max_blocks);
-    const uint32_t n_warps = nb * kWarpsPerBlock;
-    cudaEventRecord(R->ev[0], st);
+    // spans: at least 8 rounds of 32 each, at most max_spans
+    uint64_t want = (len + 255) / 256;
+    const uint32_t n_spans = (uint32_t)(want < 1 ? 1 : (want < P->max_spans ? want : P->max_spans));
+    auto grid = [&](uint32_t bps) {
+        uint32_t gb = (uint32_t)P->sms * bps, need = (n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        return gb < need ? gb : need;
+    };
+    cudaEventRecord(R->ev[0], cs);
     if (len) {
-        cudaError_t ce = launch_count(P->ds, b, e, nb, P->warp_count, P->warp_caps, st);
+        cudaError_t ce = launch_count(P->ds, b, e, n_spans, grid(P->count_bps), sc.warp_count, sc.warp_caps, cs);
         if (ce != cudaSuccess) return fail(cuda_err(ce, "count kernel"));
         R->ran_count = true;
     }
-    cudaEventRecord(R->ev[1], st);
+    cudaEventRecord(R->ev[1], cs);
     if (len) {
-        cudaError_t ce = launch_scan(P->warp_count, P->warp_caps, n_warps, P->ds.n_cap, P->warp_off, R->stats, st);
+        cudaError_t ce = launch_scan(sc.warp_count, sc.warp_caps, n_spans, P->ds.n_cap, sc.warp_off, R->stats, cs);
         if (ce != cudaSuccess) return fail(cuda_err(ce, "scan kernel"));
     }
-    cudaEventRecord(R->ev[2], st);
+    cudaEventRecord(R->ev[2], cs);
+    cudaStreamWaitEvent(st, R->ev[2], 0);
     const int nc = n_cols_of(o->mode);
     if (nc && len) {
         if (o->out_cols) {
@@ -346,11 +391,13 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
         Cols cols{};
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
-        cudaError_t ce = launch_write(P->ds, b, e, nb, P->warp_off, o->mode, cols, R->capacity, st);
+        cudaError_t ce = launch_write(P->ds, b, e, n_spans, grid(P->write_bps), sc.warp_off, o->mode, cols,
+                                      R->capacity, st);
         if (ce != cudaSuccess) return fail(cuda_err(ce, "write kernel"));
         R->ran_write = true;
     }
     cudaEventRecord(R->ev[3], st);
+    cudaEventRecord(sc.free_ev, st);  // scratch set reusable after this point of the caller's stream
     if (o->comm) {
         R->gathered = (uint64_t*)R->A.get((size_t)o->comm->nranks * 9 * 8);
         if (!R->gathered) return fail(err(ME_ENOMEM, "gather buffer"));

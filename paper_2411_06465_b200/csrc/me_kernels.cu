@@ -211,39 +211,42 @@ __device__ __forceinline__ void walk_span(const DevSpace& S, uint64_t sb, uint64
     }
 }
 
-// MODE 0 = count pass, 1 = INDEX write, 2 = FULL write
+// MODE 0 = count pass, 1 = INDEX write, 2 = FULL write.  The range is cut
+// into n_spans spans; warp w of the grid handles spans w, w + n_warps, ...
+// (the span decomposition, not the grid, fixes the output offsets, so the
+// two passes may run with different grids).
 template <int MODE, int NCAP>
 __global__ void __launch_bounds__(kThreads) sweep_kernel(const DevSpace S, const uint64_t begin,
-                                                         const uint64_t end,
+                                                         const uint64_t end, const uint32_t n_spans,
                                                          uint32_t* __restrict__ warp_count,
                                                          uint32_t* __restrict__ warp_caps,
                                                          const uint64_t* __restrict__ warp_off,
                                                          const Cols cols, const uint64_t capacity) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
-    const uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    const uint64_t sb = span_start(begin, end, gw, n_warps);
-    const uint64_t se = span_start(begin, end, gw + 1, n_warps);
-
-    CountAcc<NCAP> acc;
-    uint64_t out = 0;
-    if (MODE != 0) out = warp_off[gw];
-    if (sb < se) {
-        if (((sb | se) & 31ull) == 0)
-            walk_span<MODE, NCAP, false>(S, sb, se, lane, acc, out, cols, capacity);
-        else
-            walk_span<MODE, NCAP, true>(S, sb, se, lane, acc, out, cols, capacity);
-    }
-    if (MODE == 0) {
-        acc.flush();
-        const uint32_t cnt = __reduce_add_sync(0xffffffffu, acc.cnt);
-        uint32_t capc[NCAP];
+    for (uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); gw < n_spans; gw += n_warps) {
+        const uint64_t sb = span_start(begin, end, gw, n_spans);
+        const uint64_t se = span_start(begin, end, gw + 1, n_spans);
+        CountAcc<NCAP> acc;
+        uint64_t out = 0;
+        if (MODE != 0) out = warp_off[gw];
+        if (sb < se) {
+            if (((sb | se) & 31ull) == 0)
+                walk_span<MODE, NCAP, false>(S, sb, se, lane, acc, out, cols, capacity);
+            else
+                walk_span<MODE, NCAP, true>(S, sb, se, lane, acc, out, cols, capacity);
+        }
+        if (MODE == 0) {
+            acc.flush();
+            const uint32_t cnt = __reduce_add_sync(0xffffffffu, acc.cnt);
+            uint32_t capc[NCAP];
 #pragma unroll
-        for (int q = 0; q < NCAP; q++) capc[q] = __reduce_add_sync(0xffffffffu, acc.capc[q]);
-        if (lane == 0) {
-            warp_count[gw] = cnt;
+            for (int q = 0; q < NCAP; q++) capc[q] = __reduce_add_sync(0xffffffffu, acc.capc[q]);
+            if (lane == 0) {
+                warp_count[gw] = cnt;
 #pragma unroll
-            for (int q = 0; q < NCAP; q++) warp_caps[(size_t)gw * NCAP + q] = capc[q];
+                for (int q = 0; q < NCAP; q++) warp_caps[(size_t)gw * NCAP + q] = capc[q];
+            }
         }
     }
 }
@@ -365,29 +368,42 @@ __global__ void estimate_kernel(const me_model* __restrict__ models, uint32_t n_
     }
 }
 
+inline uint32_t ncap_stride_(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
+
 template <int MODE>
-cudaError_t launch_mode(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_blocks,
-                        uint32_t* wc, uint32_t* wcap, const uint64_t* woff, Cols cols,
-                        uint64_t capacity, cudaStream_t st) {
-    const uint32_t nc = S.n_cap <= 1 ? 1 : S.n_cap <= 2 ? 2 : S.n_cap <= 4 ? 4 : 8;
-    dim3 g(n_blocks), b(kThreads);
-    switch (nc) {
-        case 1: sweep_kernel<MODE, 1><<<g, b, 0, st>>>(S, begin, end, wc, wcap, woff, cols, capacity); break;
-        case 2: sweep_kernel<MODE, 2><<<g, b, 0, st>>>(S, begin, end, wc, wcap, woff, cols, capacity); break;
-        case 4: sweep_kernel<MODE, 4><<<g, b, 0, st>>>(S, begin, end, wc, wcap, woff, cols, capacity); break;
-        default: sweep_kernel<MODE, 8><<<g, b, 0, st>>>(S, begin, end, wc, wcap, woff, cols, capacity); break;
+void* kernel_for(uint32_t n_cap) {
+    switch (ncap_stride_(n_cap)) {
+        case 1: return reinterpret_cast<void*>(&sweep_kernel<MODE, 1>);
+        case 2: return reinterpret_cast<void*>(&sweep_kernel<MODE, 2>);
+        case 4: return reinterpret_cast<void*>(&sweep_kernel<MODE, 4>);
+        default: return reinterpret_cast<void*>(&sweep_kernel<MODE, 8>);
     }
-    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_mode(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans,
+                        uint32_t n_blocks, uint32_t* wc, uint32_t* wcap, const uint64_t* woff, Cols cols,
+                        uint64_t capacity, cudaStream_t st) {
+    void* args[] = {(void*)&S, (void*)&begin, (void*)&end, (void*)&n_spans, (void*)&wc,
+                    (void*)&wcap, (void*)&woff, (void*)&cols, (void*)&capacity};
+    return cudaLaunchKernel(kernel_for<MODE>(S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
 }  // namespace
 
-uint32_t ncap_stride(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
+uint32_t ncap_stride(uint32_t n_cap) { return ncap_stride_(n_cap); }
 
-cudaError_t launch_count(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_blocks,
+int sweep_blocks_per_sm(int pass, uint32_t n_cap) {
+    void* fn = pass == 0 ? kernel_for<0>(n_cap) : (pass == 1 ? kernel_for<1>(n_cap) : kernel_for<2>(n_cap));
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_count(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
                          uint32_t* warp_count, uint32_t* warp_caps, cudaStream_t st) {
     Cols none{};
-    return launch_mode<0>(S, begin, end, n_blocks, warp_count, warp_caps, nullptr, none, 0, st);
+    return launch_mode<0>(S, begin, end, n_spans, n_blocks, warp_count, warp_caps, nullptr, none, 0, st);
 }
 
 cudaError_t launch_scan(const uint32_t* warp_count, const uint32_t* warp_caps, uint32_t n_warps,
@@ -397,12 +413,12 @@ cudaError_t launch_scan(const uint32_t* warp_count, const uint32_t* warp_caps, u
     return cudaGetLastError();
 }
 
-cudaError_t launch_write(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_blocks,
+cudaError_t launch_write(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
                          const uint64_t* warp_off, me_out_mode mode, Cols cols, uint64_t capacity,
                          cudaStream_t st) {
     if (mode == ME_OUT_FULL)
-        return launch_mode<2>(S, begin, end, n_blocks, nullptr, nullptr, warp_off, cols, capacity, st);
-    return launch_mode<1>(S, begin, end, n_blocks, nullptr, nullptr, warp_off, cols, capacity, st);
+        return launch_mode<2>(S, begin, end, n_spans, n_blocks, nullptr, nullptr, warp_off, cols, capacity, st);
+    return launch_mode<1>(S, begin, end, n_spans, n_blocks, nullptr, nullptr, warp_off, cols, capacity, st);
 }
 
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,

@@ -138,14 +138,17 @@ constexpr int kThreads = 256;
 constexpr int kWarpsPerBlock = kThreads / 32;
 
 // count pass: per-warp survivor counts and per-capacity counts
-cudaError_t launch_count(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_blocks,
+cudaError_t launch_count(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
                          uint32_t* warp_count, uint32_t* warp_caps, cudaStream_t st);
+// resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
+int sweep_blocks_per_sm(int pass, uint32_t n_cap);
+uint32_t ncap_stride(uint32_t n_cap);
 // exclusive scan of the warp counts -> warp_off[n_warps + 1]; stats[0] = total,
 // stats[1 + j] = survivors for capacity j
 cudaError_t launch_scan(const uint32_t* warp_count, const uint32_t* warp_caps, uint32_t n_warps,
                         uint32_t n_cap, uint64_t* warp_off, uint64_t* stats, cudaStream_t st);
 // write pass: survivors of each warp span at warp_off[w] ...
-cudaError_t launch_write(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_blocks,
+cudaError_t launch_write(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
                          const uint64_t* warp_off, me_out_mode mode, Cols cols, uint64_t capacity,
                          cudaStream_t st);
 // single configurations (me_estimate / me_estimate_batch)
