@@ -99,18 +99,21 @@ struct me_plan {
     Alloc A;
     int device = 0;
     std::vector<void*> owned;  // device allocations owned by the plan
-    // Launch shape.  The range of a sweep is cut into n_spans warp spans (fixes
-    // the output offsets); the count and write passes run on their own grids.
+    // Launch shape.  A sweep is processed in sub-ranges of <= kMaxSub indices;
+    // each is cut into tiles of kTile indices (they fix the output offsets) and
+    // the count pass walks n_spans spans of whole tiles.  The count and write
+    // passes run on their own grids.
     int sms = 148;
-    uint32_t max_spans = 0;
+    uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    // Two scratch sets, alternated by successive sweeps, so that the count pass
-    // of sweep i+1 (on the plan's count stream) overlaps the write pass of sweep
-    // i (on the caller's stream).
+    // Two scratch sets, alternated by successive sub-ranges, so that the count
+    // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
+    // of sub-range i (on the caller's stream).
     struct Scratch {
-        uint32_t* warp_count = nullptr;
-        uint32_t* warp_caps = nullptr;
-        uint64_t* warp_off = nullptr;
+        uint32_t* tile_count = nullptr;
+        uint4* tile_ck = nullptr;
+        uint64_t* tile_off = nullptr;
+        uint32_t* span_caps = nullptr;
         cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
     } scratch[2];
     uint32_t turn = 0;
@@ -136,6 +139,7 @@ struct me_result {
     me_comm* comm = nullptr;
     bool gather = false;
     cudaEvent_t ev[5] = {};
+    std::vector<cudaEvent_t> tev;  // per sub-range: count start/end, scan end, write start/end
     bool ran_count = false, ran_write = false;
     // host-side results (valid after `resolved`)
     bool resolved = false;
@@ -204,6 +208,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.rcdo_rc = H.rcdo_rc;
     D.rcdo_do = H.rcdo_do;
     D.n_cap = (uint32_t)H.caps.size();
+    D.gbs_mode = H.gbs ? 1u : 0u;
     for (int q = 0; q < 8; q++) D.thr[q] = 0;
     for (size_t q = 0; q < H.caps.size(); q++)
         D.thr[q] = (uint64_t)(((unsigned __int128)H.caps[q] * thr.num) / thr.den);
@@ -211,6 +216,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     // resident 8-warp blocks per SM, so the grid-stride over spans is even)
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     P->max_spans = (uint32_t)P->sms * 96;
+    P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
     const int occ_c = sweep_blocks_per_sm(0, D.n_cap), occ_w = sweep_blocks_per_sm(2, D.n_cap);
     P->write_bps = (uint32_t)(occ_w > 1 ? occ_w - 1 : 1);
     P->count_bps = (uint32_t)(occ_c - (int)P->write_bps > 0 ? occ_c - (int)P->write_bps : 1);
@@ -219,13 +225,15 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (P->write_bps < 1) P->write_bps = 1;
     if (P->count_bps < 1) P->count_bps = 1;
     for (auto& sc : P->scratch) {
-        sc.warp_count = (uint32_t*)P->A.get((size_t)P->max_spans * 4);
-        sc.warp_caps = (uint32_t*)P->A.get((size_t)P->max_spans * 8 * 4);
-        sc.warp_off = (uint64_t*)P->A.get((size_t)(P->max_spans + 1) * 8);
-        P->owned.push_back(sc.warp_count);
-        P->owned.push_back(sc.warp_caps);
-        P->owned.push_back(sc.warp_off);
-        if (!sc.warp_count || !sc.warp_caps || !sc.warp_off) {
+        sc.tile_count = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
+        sc.tile_ck = (uint4*)P->A.get((size_t)P->max_tiles * 16);
+        sc.tile_off = (uint64_t*)P->A.get((size_t)P->max_tiles * 8);
+        sc.span_caps = (uint32_t*)P->A.get((size_t)P->max_spans * 8 * 4);
+        P->owned.push_back(sc.tile_count);
+        P->owned.push_back(sc.tile_ck);
+        P->owned.push_back(sc.tile_off);
+        P->owned.push_back(sc.span_caps);
+        if (!sc.tile_count || !sc.tile_ck || !sc.tile_off || !sc.span_caps) {
             me_plan_free(P);
             return err(ME_ENOMEM, "scratch allocation");
         }
@@ -288,6 +296,7 @@ static void result_release(me_result* R) {
     if (R->ev[4]) cudaEventSynchronize(R->ev[4]);
     for (int i = 0; i < 5; i++)
         if (R->ev[i]) cudaEventDestroy(R->ev[i]);
+    for (cudaEvent_t x : R->tev) cudaEventDestroy(x);
     R->A.put(R->stats);
     R->A.put(R->gathered);
     if (R->own_cols)
@@ -340,36 +349,53 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     R->stats = (uint64_t*)R->A.get(9 * 8);
     if (!R->stats) return fail(err(ME_ENOMEM, "stats allocation"));
 
-    // count + scan on the plan's count stream; it waits only for the tables and
-    // for the write pass that last used this scratch set, so it can run while
-    // the caller's stream is still writing the previous sweep's columns
-    me_plan::Scratch& sc = P->scratch[P->turn++ & 1];
+    // Sub-ranges of <= kMaxSub indices.  Count + scan run on the plan's count
+    // stream, which waits only for the tables and for the write pass that last
+    // used the scratch set, so the count of sub-range i+1 runs while the
+    // caller's stream still writes the columns of sub-range i.
     cudaStream_t cs = P->cstream;
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
-    cudaStreamWaitEvent(cs, sc.free_ev, 0);
-    if (cudaMemsetAsync(R->stats, 0, 9 * 8, cs) != cudaSuccess) return fail(cuda_err(cudaErrorUnknown, "memset"));
+    const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
-    // spans: at least 8 rounds of 32 each, at most max_spans
-    uint64_t want = (len + 255) / 256;
-    const uint32_t n_spans = (uint32_t)(want < 1 ? 1 : (want < P->max_spans ? want : P->max_spans));
-    auto grid = [&](uint32_t bps) {
-        uint32_t gb = (uint32_t)P->sms * bps, need = (n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock;
-        return gb < need ? gb : need;
+    auto pipeline = [&](uint64_t* stats, bool write, Cols cols, uint64_t capacity) -> int {
+        if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
+        for (uint64_t lo = b; lo < e; lo += kMaxSub) {
+            const uint64_t hi = e - lo < kMaxSub ? e : lo + kMaxSub;
+            me_plan::Scratch& sc = P->scratch[P->turn++ & 1];
+            const uint32_t n_tiles = n_tiles_of(lo, hi);
+            const uint32_t n_spans = n_tiles < P->max_spans ? n_tiles : P->max_spans;
+            auto grid = [&](uint32_t bps, uint32_t units) {
+                uint32_t gb = (uint32_t)P->sms * bps, need = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
+                return gb < need ? gb : need;
+            };
+            cudaEvent_t tev[5];
+            for (auto& x : tev) {
+                if (cudaEventCreate(&x) != cudaSuccess) return cuda_err(cudaGetLastError(), "cudaEventCreate");
+                R->tev.push_back(x);
+            }
+            cudaStreamWaitEvent(cs, sc.free_ev, 0);
+            cudaEventRecord(tev[0], cs);
+            cudaError_t ce = launch_count(P->ds, lo, hi, n_spans, grid(P->count_bps, n_spans), sc.tile_count,
+                                          sc.tile_ck, sc.span_caps, cs);
+            if (ce != cudaSuccess) return cuda_err(ce, "count kernel");
+            cudaEventRecord(tev[1], cs);
+            ce = launch_scan(sc.tile_count, n_tiles, sc.span_caps, n_spans, P->ds.n_cap, sc.tile_off, stats, cs);
+            if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
+            cudaEventRecord(tev[2], cs);
+            cudaStreamWaitEvent(st, tev[2], 0);
+            cudaEventRecord(tev[3], st);
+            if (write) {
+                ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_off, o->mode, cols,
+                                  capacity, st);
+                if (ce != cudaSuccess) return cuda_err(ce, "write kernel");
+            }
+            cudaEventRecord(tev[4], st);
+            cudaEventRecord(sc.free_ev, st);  // scratch set reusable after this point of the caller's stream
+        }
+        return ME_OK;
     };
     cudaEventRecord(R->ev[0], cs);
-    if (len) {
-        cudaError_t ce = launch_count(P->ds, b, e, n_spans, grid(P->count_bps), sc.warp_count, sc.warp_caps, cs);
-        if (ce != cudaSuccess) return fail(cuda_err(ce, "count kernel"));
-        R->ran_count = true;
-    }
-    cudaEventRecord(R->ev[1], cs);
-    if (len) {
-        cudaError_t ce = launch_scan(sc.warp_count, sc.warp_caps, n_spans, P->ds.n_cap, sc.warp_off, R->stats, cs);
-        if (ce != cudaSuccess) return fail(cuda_err(ce, "scan kernel"));
-    }
-    cudaEventRecord(R->ev[2], cs);
-    cudaStreamWaitEvent(st, R->ev[2], 0);
-    const int nc = n_cols_of(o->mode);
+    Cols cols{};
     if (nc && len) {
         if (o->out_cols) {
             for (int j = 0; j < nc; j++) {
@@ -378,6 +404,8 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             }
             R->capacity = o->out_capacity;
         } else {
+            // exact allocation: a count-only pipeline first (synchronises the host once)
+            if ((rc = pipeline(R->stats, false, cols, 0))) return fail(rc);
             uint64_t cnt = 0;
             if (cudaMemcpyAsync(&cnt, R->stats, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
                 cudaStreamSynchronize(st) != cudaSuccess)
@@ -388,16 +416,16 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 if (!R->cols[j]) return fail(err(ME_ENOMEM, "result column allocation"));
             }
             R->capacity = cnt;
+            for (cudaEvent_t x : R->tev) cudaEventDestroy(x);
+            R->tev.clear();
         }
-        Cols cols{};
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
-        cudaError_t ce = launch_write(P->ds, b, e, n_spans, grid(P->write_bps), sc.warp_off, o->mode, cols,
-                                      R->capacity, st);
-        if (ce != cudaSuccess) return fail(cuda_err(ce, "write kernel"));
-        R->ran_write = true;
     }
+    if ((rc = pipeline(R->stats, nc != 0, cols, R->capacity))) return fail(rc);
+    R->ran_count = len != 0;
+    R->ran_write = nc && len;
+    cudaEventRecord(R->ev[2], cs);
     cudaEventRecord(R->ev[3], st);
-    cudaEventRecord(sc.free_ev, st);  // scratch set reusable after this point of the caller's stream
     if (o->comm) {
         R->gathered = (uint64_t*)R->A.get((size_t)o->comm->nranks * 9 * 8);
         if (!R->gathered) return fail(err(ME_ENOMEM, "gather buffer"));
@@ -546,9 +574,16 @@ extern "C" int me_result_timing(me_result* R, float* ms) {
     DeviceGuard g(R->plan->device);
     CU(cudaEventSynchronize(R->ev[4]));
     CU(cudaEventElapsedTime(&ms[0], R->ev[0], R->ev[4]));
-    CU(cudaEventElapsedTime(&ms[1], R->ev[0], R->ev[1]));
-    CU(cudaEventElapsedTime(&ms[2], R->ev[1], R->ev[2]));
-    CU(cudaEventElapsedTime(&ms[3], R->ev[2], R->ev[3]));
+    ms[1] = ms[2] = ms[3] = 0.f;
+    for (size_t k = 0; k + 5 <= R->tev.size(); k += 5) {
+        float a = 0, b = 0, c = 0;
+        CU(cudaEventElapsedTime(&a, R->tev[k], R->tev[k + 1]));
+        CU(cudaEventElapsedTime(&b, R->tev[k + 1], R->tev[k + 2]));
+        CU(cudaEventElapsedTime(&c, R->tev[k + 3], R->tev[k + 4]));
+        ms[1] += a;
+        ms[2] += b;
+        ms[3] += c;
+    }
     if (!R->ran_write) ms[3] = 0.f;
     return ME_OK;
 }

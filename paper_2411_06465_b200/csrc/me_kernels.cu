@@ -1,20 +1,24 @@
 // me_kernels.cu -- the sweep kernels (sm_100a).
 //
-// Work decomposition: the index range [begin, end) is split into one
-// contiguous span per warp (span boundaries aligned to multiples of 32 in
-// absolute index).  A warp walks its span in rounds of 32 consecutive
-// indices, lane l taking index base + 32 i + l, so a warp ballot yields the
-// survivors of a round in index order.  Each lane keeps an odometer over the
-// canonical enumeration (segment -> tuple row -> position in row); the only
-// search is one binary search per lane at span start.  Row coefficients
-// (Psi_s, model-state bytes, per-token activation coefficients) are computed
-// once per row; the per-config work is a pair lookup, a u32 x u64 multiply-add
-// and n_cap u64 compares.
+// The index range of one pass is cut into tiles of kTile = 512 consecutive
+// indices (16 rounds of 32).  A warp evaluates a round as 32 consecutive
+// indices, lane l taking index base + l, so a warp ballot yields the survivors
+// of a round in index order.  Each lane keeps an odometer over the canonical
+// enumeration (segment -> tuple row -> position in row); rows are entered with
+// all their estimator coefficients precomputed (LaneRow), so the per-config work
+// is one pair load, one u32 x u64 multiply-add and n_cap u64 compares.
 //
-// Two passes: the count pass stores per-warp survivor counts,
-// a one-block scan turns them into per-warp output offsets, and the write
-// pass re-walks the spans and stores the survivors' columns (structure of
-// arrays, 8-byte stores that are contiguous across the active lanes).
+// Passes:
+//  count  warps walk contiguous spans of whole tiles (one binary search per
+//         lane per span) and store, per tile, its survivor count and the
+//         walker state of the tile's first index (a checkpoint);
+//  scan   one block turns the tile counts into output offsets (adding the
+//         running total of earlier sub-ranges) and accumulates the totals;
+//  write  warps take tiles in grid-stride order -- at any moment the grid
+//         writes one compact window of the output columns, which keeps the
+//         DRAM write stream local -- restore the walker from the tile's
+//         checkpoint and store the survivors' columns (structure of arrays;
+//         the stores of a round are contiguous across the surviving lanes).
 #include <cuda_runtime.h>
 
 #include "me_kernels.cuh"
@@ -35,10 +39,45 @@ __device__ __forceinline__ uint32_t upper_bound_u64(const uint64_t* __restrict__
     return lo;
 }
 
-struct Walker {
-    uint32_t seg, j, jend, r, w, pair_off;
-    me_model M;
+// Per-lane row coefficients.  Lanes advance by 32 and every row length is a
+// multiple of the (rc, do) digit count (1, 2 or 4), so a lane's (rc, do) digits
+// never change along its walk: the rc / do selections of RowCoef are made once
+// per row, leaving per config only
+//   total = ms + u * (n_inf * a + b)          (n_inf = p in paper mode).
+struct LaneRow {
+    uint64_t ms;        // params + grads + optim for this lane's do
+    uint64_t a, b;      // per-token activation bytes = n_inf * a + b (this lane's rc)
+    uint64_t kp;        // p * a + b (paper mode: n_inf = p)
+    uint64_t psi;       // Psi_s
+    uint64_t optim;     // optimizer bytes for this lane's do
+    uint64_t lam, mu;   // per-token layer bytes = n_inf * lam + mu
+    uint64_t e8, hc;    // per-token embedding bytes = n_inf * e8; head bytes = hc
+    uint32_t p;
+};
+
+__device__ __forceinline__ void make_lane_row(const me_model& M, uint32_t t, uint32_t c, uint32_t p, uint32_t d,
+                                              uint32_t rc, uint32_t dopt, LaneRow& L) {
     RowCoef R;
+    make_row(M, t, c, p, d, first_stage_layers_auto(M.layers, p), R);
+    L.ms = dopt ? R.ms1 : R.ms0;
+    L.a = (rc ? R.lam1 : R.lam0) + R.e8;
+    L.b = rc ? R.bt + R.hc : R.hc;
+    L.kp = (uint64_t)p * L.a + L.b;
+    L.psi = R.psi;
+    L.optim = dopt ? R.optim1 : 12ull * R.psi;
+    L.lam = rc ? R.lam1 : R.lam0;
+    L.mu = rc ? R.bt : 0ull;
+    L.e8 = R.e8;
+    L.hc = R.hc;
+    L.p = p;
+}
+
+struct Walker {
+    uint32_t seg, j, jend, r, w;
+    const uint2* pp;    // this lane's current (b, s) pair
+    uint32_t rc, dopt;  // this lane's innermost digits (constant along its walk)
+    me_model M;
+    LaneRow L;
 
     __device__ __forceinline__ void enter_segment(const DevSpace& S, uint32_t s) {
         seg = s;
@@ -60,25 +99,14 @@ struct Walker {
         const uint4 a = __ldg(reinterpret_cast<const uint4*>(S.tuples + tid));      // t c p d
         const uint2 b = __ldg(reinterpret_cast<const uint2*>(S.tuples + tid) + 2);  // w pair_off
         w = b.x;
-        pair_off = b.y;
-        make_row(M, a.x, a.y, a.z, a.w, first_stage_layers_auto(M.layers, a.z), R);
+        pp = reinterpret_cast<const uint2*>(S.pairs) + b.y + (r >> S.lg_rcdo);
+        make_lane_row(M, a.x, a.y, a.z, a.w, rc, dopt, L);
     }
 
-    // position the walker on absolute index pos (< total)
-    __device__ __forceinline__ void seek(const DevSpace& S, uint64_t pos) {
-        const uint32_t s = upper_bound_u64(S.seg_prefix, S.n_seg + 1, pos) - 1;
-        enter_segment(S, s);
-        const uint64_t within = pos - __ldg(S.seg_prefix + s);
-        const uint32_t k = upper_bound_u64(S.list_prefix + j, jend - j, within) - 1;
-        j += k;
-        r = (uint32_t)(within - __ldg(S.list_prefix + j));
-        set_row(S);
-    }
-
-    // move forward by `step` indices (the caller guarantees the target exists)
-    __device__ __forceinline__ void advance(const DevSpace& S, uint32_t step) {
-        r += step;
-        while (r >= w) next_row(S);
+    __device__ __forceinline__ void set_digits(const DevSpace& S) {
+        const uint32_t sel = r & ((1u << S.lg_rcdo) - 1u);
+        rc = (S.rcdo_rc >> sel) & 1u;
+        dopt = (S.rcdo_do >> sel) & 1u;
     }
 
     // leave the current row (r >= w): next tuple of the list, next non-empty
@@ -96,22 +124,40 @@ struct Walker {
         set_row(S);
     }
 
-    __device__ __forceinline__ uint2 pair(const DevSpace& S, uint32_t lg) const {
-        return __ldg(reinterpret_cast<const uint2*>(S.pairs) + pair_off + (r >> lg));
+    // position on absolute index pos (< total) by binary search
+    __device__ __forceinline__ void seek(const DevSpace& S, uint64_t pos) {
+        const uint32_t s = upper_bound_u64(S.seg_prefix, S.n_seg + 1, pos) - 1;
+        enter_segment(S, s);
+        const uint64_t within = pos - __ldg(S.seg_prefix + s);
+        const uint32_t k = upper_bound_u64(S.list_prefix + j, jend - j, within) - 1;
+        j += k;
+        r = (uint32_t)(within - __ldg(S.list_prefix + j));
+        set_digits(S);
+        set_row(S);
+    }
+
+    // position on checkpoint (state of index x) + lane
+    __device__ __forceinline__ void restore(const DevSpace& S, uint4 ck, uint32_t lane) {
+        enter_segment(S, ck.x);
+        j = ck.y;
+        r = ck.z + lane;
+        set_digits(S);  // row lengths are multiples of the digit count
+        set_row(S);
+        while (r >= w) next_row(S);
+    }
+
+    // move forward by 32 indices (the caller guarantees the target exists)
+    __device__ __forceinline__ void advance32(const DevSpace& S, uint32_t pstep) {
+        r += 32;
+        if (r < w) {
+            pp += pstep;
+        } else {
+            do {
+                next_row(S);
+            } while (r >= w);
+        }
     }
 };
-
-// span of global warp gw: [span(gw), span(gw + 1)), 32-aligned in absolute index
-__device__ __forceinline__ uint64_t span_start(uint64_t begin, uint64_t end, uint32_t gw,
-                                               uint32_t n_warps) {
-    if (gw == 0) return begin;
-    if (gw >= n_warps) return end;
-    const uint64_t len = end - begin;
-    const uint64_t q = len / n_warps, rem = len % n_warps;
-    uint64_t s = begin + q * gw + (rem * gw) / n_warps;
-    s = (s + 31) & ~31ull;
-    return s < end ? s : end;
-}
 
 template <int NCAP>
 __device__ __forceinline__ uint32_t cap_mask(const DevSpace& S, uint64_t total) {
@@ -121,63 +167,57 @@ __device__ __forceinline__ uint32_t cap_mask(const DevSpace& S, uint64_t total) 
     return mask;
 }
 
-// Per-lane accumulators of the count pass: survivor count and 8-bit packed
-// per-capacity counters (mask * 0x00204081 spreads bits 0..3 to bytes 0..3).
+// 8-bit packed per-capacity counters (mask * 0x00204081 spreads bits 0..3 to
+// bytes 0..3); flushed to 32-bit counters every tile (16 rounds < 256)
 template <int NCAP>
-struct CountAcc {
-    uint32_t cnt = 0, lo = 0, hi = 0, round = 0;
+struct CapAcc {
+    uint32_t lo = 0, hi = 0;
     uint32_t capc[NCAP];
-    __device__ __forceinline__ CountAcc() {
+    __device__ __forceinline__ CapAcc() {
 #pragma unroll
         for (int q = 0; q < NCAP; q++) capc[q] = 0;
     }
-    __device__ __forceinline__ void flush() {
-#pragma unroll
-        for (int q = 0; q < NCAP; q++) capc[q] += ((q < 4 ? lo : hi) >> (8 * (q & 3))) & 255u;
-        lo = hi = 0;
-    }
     __device__ __forceinline__ void add(uint32_t mask) {
-        cnt += mask ? 1u : 0u;
         if (NCAP <= 4) {
             lo += (mask * 0x00204081u) & 0x01010101u;
         } else {
             lo += ((mask & 15u) * 0x00204081u) & 0x01010101u;
             hi += ((mask >> 4) * 0x00204081u) & 0x01010101u;
         }
-        if ((++round & 255u) == 0) flush();
+    }
+    __device__ __forceinline__ void flush() {
+#pragma unroll
+        for (int q = 0; q < NCAP; q++) capc[q] += ((q < 4 ? lo : hi) >> (8 * (q & 3))) & 255u;
+        lo = hi = 0;
     }
 };
 
-// One warp span.  RAGGED = the span does not start and end on multiples of 32
-// (only the first and last spans of a range), so lanes need range checks.
-// The pair of the next round is loaded before the current round is evaluated
-// (software pipelining of the only per-config memory access).
-template <int MODE, int NCAP, bool RAGGED>
-__device__ __forceinline__ void walk_span(const DevSpace& S, uint64_t sb, uint64_t se, uint32_t lane,
-                                          CountAcc<NCAP>& acc, uint64_t out, const Cols& cols,
-                                          uint64_t capacity) {
-    const uint64_t base = sb & ~31ull;
-    Walker W;
-    uint64_t pos = base + lane;
-    if (RAGGED && pos >= se) return;  // this lane never has work (its later positions are >= se too)
-    W.seek(S, pos);
-    const uint32_t rc_bits = S.rcdo_rc, do_bits = S.rcdo_do, lg = S.lg_rcdo;
-    const uint32_t sel_mask = (1u << lg) - 1;
-    uint2 pr = W.pair(S, lg);
-    for (uint64_t p0 = base; p0 < se; p0 += 32, pos += 32) {
-        // issue the next round's pair load first when it stays in this row
-        const uint32_t rn = W.r + 32;
-        const bool more = pos + 32 < se;
-        const bool in_row = rn < W.w;
+// Evaluate one tile's rounds starting at the walker's position (lane's index
+// = pos).  RAGGED: the tile is cut by lo/hi (first or last tile of a range).
+// GBS: a global batch bounds the in-flight microbatches (R17).  Returns with
+// the walker on the first index after the tile when `advance_out`.
+template <int MODE, int NCAP, bool RAGGED, bool GBS>
+__device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
+                                             uint64_t hi, uint32_t rounds, uint32_t lane, CapAcc<NCAP>& acc,
+                                             uint64_t out, const Cols& cols, uint64_t capacity,
+                                             bool advance_out) {
+    const uint32_t pstep = 32u >> S.lg_rcdo;
+    uint32_t cnt = 0;
+    uint2 pr = __ldg(W.pp);
+    for (uint32_t it = 0; it < rounds; it++, pos += 32) {
+        const bool more = (it + 1 < rounds) || advance_out;
+        const bool in_row = W.r + 32 < W.w;
         uint2 prn = pr;
-        if (in_row && more) prn = __ldg(reinterpret_cast<const uint2*>(S.pairs) + W.pair_off + (rn >> lg));
+        if (in_row && more) prn = __ldg(W.pp + pstep);  // next round's pair, issued early
 
-        const bool act = !RAGGED || (pos >= sb && pos < se);
-        const uint32_t sel = W.r & sel_mask;
-        const uint32_t rc = (rc_bits >> sel) & 1u, dopt = (do_bits >> sel) & 1u;
-        const uint64_t total = config_total(W.R, pr.x, pr.y, rc, dopt);
-        uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
+        const uint32_t u = pr.x;
+        const uint32_t n_inf = GBS ? min(W.L.p, pr.y) : W.L.p;
+        const uint64_t K = GBS ? (uint64_t)n_inf * W.L.a + W.L.b : W.L.kp;
+        const uint64_t total = W.L.ms + (uint64_t)u * K;
+        const bool act = !RAGGED || (pos >= lo && pos < hi);
+        const uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
         if (MODE == 0) {
+            cnt += mask ? 1u : 0u;
             acc.add(mask);
         } else {
             const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
@@ -186,90 +226,163 @@ __device__ __forceinline__ void walk_span(const DevSpace& S, uint64_t sb, uint64
                 if (o < capacity) {
                     cols.c[0][o] = pos | ((uint64_t)mask << 56);
                     if (MODE == 2) {
-                        const TermsT<uint64_t> T = config_terms_no_total(W.R, pr.x, pr.y, rc, dopt);
-                        cols.c[1][o] = T.params;
-                        cols.c[2][o] = T.grads;
-                        cols.c[3][o] = T.optim;
-                        cols.c[4][o] = T.layers;
-                        cols.c[5][o] = T.embed;
-                        cols.c[6][o] = T.head;
+                        cols.c[1][o] = 2ull * W.L.psi;
+                        cols.c[2][o] = 4ull * W.L.psi;
+                        cols.c[3][o] = W.L.optim;
+                        cols.c[4][o] = (uint64_t)u * ((uint64_t)n_inf * W.L.lam + W.L.mu);
+                        cols.c[5][o] = (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
+                        cols.c[6][o] = (uint64_t)u * W.L.hc;
                         cols.c[7][o] = total;
                     }
                 }
             }
             out += __popc(ballot);
         }
-        if (more) {
+        if (more && (!RAGGED || pos + 32 < hi)) {
             if (in_row) {
-                W.r = rn;
+                W.r += 32;
+                W.pp += pstep;
                 pr = prn;
             } else {
-                W.advance(S, 32);
-                pr = W.pair(S, lg);
+                W.advance32(S, pstep);
+                pr = __ldg(W.pp);
             }
         }
     }
+    return cnt;
 }
 
-// MODE 0 = count pass, 1 = INDEX write, 2 = FULL write.  The range is cut
-// into n_spans spans; warp w of the grid handles spans w, w + n_warps, ...
-// (the span decomposition, not the grid, fixes the output offsets, so the
-// two passes may run with different grids).
-template <int MODE, int NCAP>
-__global__ void __launch_bounds__(kThreads) sweep_kernel(const DevSpace S, const uint64_t begin,
-                                                         const uint64_t end, const uint32_t n_spans,
-                                                         uint32_t* __restrict__ warp_count,
-                                                         uint32_t* __restrict__ warp_caps,
-                                                         const uint64_t* __restrict__ warp_off,
-                                                         const Cols cols, const uint64_t capacity) {
+struct TileGeom {
+    uint64_t lo, hi, base;  // range [lo, hi); tiles start at base = lo & ~31
+    uint32_t n_tiles;
+    __device__ __forceinline__ uint64_t start(uint32_t t) const { return base + (uint64_t)t * kTile; }
+    __device__ __forceinline__ bool ragged(uint32_t t) const {
+        return (t == 0 && lo != base) || start(t) + kTile > hi;
+    }
+    __device__ __forceinline__ uint32_t rounds(uint32_t t) const {
+        const uint64_t e = start(t) + kTile < hi ? start(t) + kTile : hi;
+        return (uint32_t)((e - start(t) + 31) / 32);
+    }
+};
+
+__device__ __forceinline__ TileGeom geom(uint64_t lo, uint64_t hi) {
+    TileGeom g;
+    g.lo = lo;
+    g.hi = hi;
+    g.base = lo & ~31ull;
+    g.n_tiles = (uint32_t)((hi - g.base + kTile - 1) / kTile);
+    return g;
+}
+
+// count pass: span s = tiles [s*n/S, (s+1)*n/S)
+template <int NCAP, bool GBS>
+__device__ __forceinline__ void count_span(const DevSpace& S, const TileGeom& G, uint32_t t0, uint32_t t1,
+                                           uint32_t lane, uint32_t* __restrict__ tile_count,
+                                           uint4* __restrict__ tile_ck, CapAcc<NCAP>& acc) {
+    Walker W;
+    // a lane past the end of the range only takes part in the warp reductions:
+    // park it on the last index (its own positions stay inactive)
+    const uint64_t p0 = G.start(t0) + lane;
+    W.seek(S, p0 < G.hi ? p0 : G.hi - 1);
+    for (uint32_t t = t0; t < t1; t++) {
+        const uint64_t ts = G.start(t);
+        const uint4 ck = make_uint4(W.seg, W.j, W.r, 0u);
+        if (lane == 0) tile_ck[t] = ck;  // lane 0 is at the tile's first index
+        const bool last = t + 1 == t1;
+        uint32_t cnt;
+        if (G.ragged(t))
+            cnt = run_tile<0, NCAP, true, GBS>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{}, 0,
+                                               !last);
+        else
+            cnt = run_tile<0, NCAP, false, GBS>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0, Cols{}, 0,
+                                                !last);
+        acc.flush();
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) tile_count[t] = cnt;
+    }
+}
+
+template <int NCAP>
+__global__ void __launch_bounds__(kThreads) count_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+                                                         const uint32_t n_spans, uint32_t* __restrict__ tile_count,
+                                                         uint4* __restrict__ tile_ck,
+                                                         uint32_t* __restrict__ span_caps) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
-    for (uint32_t gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); gw < n_spans; gw += n_warps) {
-        const uint64_t sb = span_start(begin, end, gw, n_spans);
-        const uint64_t se = span_start(begin, end, gw + 1, n_spans);
-        CountAcc<NCAP> acc;
-        uint64_t out = 0;
-        if (MODE != 0) out = warp_off[gw];
-        if (sb < se) {
-            if (((sb | se) & 31ull) == 0)
-                walk_span<MODE, NCAP, false>(S, sb, se, lane, acc, out, cols, capacity);
-            else
-                walk_span<MODE, NCAP, true>(S, sb, se, lane, acc, out, cols, capacity);
+    const TileGeom G = geom(lo, hi);
+    for (uint32_t s = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); s < n_spans; s += n_warps) {
+        const uint32_t t0 = (uint32_t)((uint64_t)G.n_tiles * s / n_spans);
+        const uint32_t t1 = (uint32_t)((uint64_t)G.n_tiles * (s + 1) / n_spans);
+        CapAcc<NCAP> acc;
+        if (t0 < t1) {
+            if (S.gbs_mode) count_span<NCAP, true>(S, G, t0, t1, lane, tile_count, tile_ck, acc);
+            else count_span<NCAP, false>(S, G, t0, t1, lane, tile_count, tile_ck, acc);
         }
-        if (MODE == 0) {
-            acc.flush();
-            const uint32_t cnt = __reduce_add_sync(0xffffffffu, acc.cnt);
-            uint32_t capc[NCAP];
 #pragma unroll
-            for (int q = 0; q < NCAP; q++) capc[q] = __reduce_add_sync(0xffffffffu, acc.capc[q]);
-            if (lane == 0) {
-                warp_count[gw] = cnt;
-#pragma unroll
-                for (int q = 0; q < NCAP; q++) warp_caps[(size_t)gw * NCAP + q] = capc[q];
-            }
+        for (int q = 0; q < NCAP; q++) {
+            const uint32_t c = __reduce_add_sync(0xffffffffu, acc.capc[q]);
+            if (lane == 0) span_caps[(size_t)s * NCAP + q] = c;
         }
     }
 }
 
-// one block: exclusive scan of n warp counts (u32) into u64 offsets + totals
-__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__ warp_count,
-                                                    const uint32_t* __restrict__ warp_caps,
-                                                    uint32_t n, uint32_t ncap_stride,
-                                                    uint32_t n_cap, uint64_t* __restrict__ warp_off,
-                                                    uint64_t* __restrict__ stats) {
+// write pass: tiles in grid-stride order
+template <int MODE, int NCAP>
+__global__ void __launch_bounds__(kThreads) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+                                                         const uint4* __restrict__ tile_ck,
+                                                         const uint64_t* __restrict__ tile_off, const Cols cols,
+                                                         const uint64_t capacity) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
+    const TileGeom G = geom(lo, hi);
+    CapAcc<NCAP> none;
+    for (uint32_t t = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < G.n_tiles; t += n_warps) {
+        const uint64_t ts = G.start(t);
+        const uint64_t pos = ts + lane;
+        const uint64_t out = __ldg(tile_off + t);
+        Walker W;
+        const bool ragged = G.ragged(t);
+        // a lane past the end of the range is parked on the last index: it
+        // takes part in the ballots with inactive positions
+        W.restore(S, __ldg(tile_ck + t), pos < hi ? lane : (uint32_t)(hi - 1 - ts));
+        if (ragged) {
+            if (S.gbs_mode)
+                run_tile<MODE, NCAP, true, true>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols, capacity,
+                                                 false);
+            else
+                run_tile<MODE, NCAP, true, false>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
+                                                  capacity, false);
+        } else {
+            if (S.gbs_mode)
+                run_tile<MODE, NCAP, false, true>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
+                                                  capacity, false);
+            else
+                run_tile<MODE, NCAP, false, false>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
+                                                   capacity, false);
+        }
+    }
+}
+
+// one block: exclusive scan of the tile counts (u32) into u64 offsets starting
+// at the running total stats[0]; stats[0] and stats[1 + q] accumulate the
+// totals of this sub-range
+__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__ tile_count, uint32_t n,
+                                                    const uint32_t* __restrict__ span_caps, uint32_t n_spans,
+                                                    uint32_t ncap_stride, uint32_t n_cap,
+                                                    uint64_t* __restrict__ tile_off, uint64_t* __restrict__ stats) {
     __shared__ uint64_t s_warp[32];
     __shared__ uint64_t s_caps[8][32];
+    __shared__ uint64_t s_base;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_base = stats[0];
     const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = min(n, tid * chunk), hi = min(n, lo + chunk);
     uint64_t sum = 0;
+    for (uint32_t i = lo; i < hi; i++) sum += tile_count[i];
     uint64_t caps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t i = lo; i < hi; i++) {
-        sum += warp_count[i];
-        for (uint32_t q = 0; q < n_cap; q++) caps[q] += warp_caps[(size_t)i * ncap_stride + q];
-    }
-    // inclusive warp scan
-    uint64_t inc = sum;
+    for (uint32_t s = tid; s < n_spans; s += blockDim.x)
+        for (uint32_t q = 0; q < n_cap; q++) caps[q] += span_caps[(size_t)s * ncap_stride + q];
+    uint64_t inc = sum;  // inclusive warp scan
     for (int o = 1; o < 32; o <<= 1) {
         uint64_t v = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= (uint32_t)o) inc += v;
@@ -281,6 +394,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__
         if (lane == 0) s_caps[q][wid] = c;
     }
     __syncthreads();
+    const uint64_t base = s_base;
     if (wid == 0) {
         const uint32_t nw = blockDim.x >> 5;
         uint64_t v = lane < nw ? s_warp[lane] : 0;
@@ -290,20 +404,19 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__
             if (lane >= (uint32_t)o) x += y;
         }
         if (lane < nw) s_warp[lane] = x - v;  // exclusive
-        if (lane == 31) stats[0] = x;
+        if (lane == 31) stats[0] = base + x;
         for (uint32_t q = 0; q < n_cap; q++) {
             uint64_t c = lane < nw ? s_caps[q][lane] : 0;
             for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
-            if (lane == 0) stats[1 + q] = c;
+            if (lane == 0) stats[1 + q] += c;
         }
     }
     __syncthreads();
-    uint64_t run = s_warp[wid] + inc - sum;
+    uint64_t run = base + s_warp[wid] + inc - sum;
     for (uint32_t i = lo; i < hi; i++) {
-        warp_off[i] = run;
-        run += warp_count[i];
+        tile_off[i] = run;
+        run += tile_count[i];
     }
-    if (tid == blockDim.x - 1) warp_off[n] = s_warp[wid] + inc;
 }
 
 // ---- single configurations ----------------------------------------------
@@ -370,55 +483,61 @@ __global__ void estimate_kernel(const me_model* __restrict__ models, uint32_t n_
 
 inline uint32_t ncap_stride_(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
 
-template <int MODE>
-void* kernel_for(uint32_t n_cap) {
+void* count_kernel_for(uint32_t n_cap) {
     switch (ncap_stride_(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&sweep_kernel<MODE, 1>);
-        case 2: return reinterpret_cast<void*>(&sweep_kernel<MODE, 2>);
-        case 4: return reinterpret_cast<void*>(&sweep_kernel<MODE, 4>);
-        default: return reinterpret_cast<void*>(&sweep_kernel<MODE, 8>);
+        case 1: return reinterpret_cast<void*>(&count_kernel<1>);
+        case 2: return reinterpret_cast<void*>(&count_kernel<2>);
+        case 4: return reinterpret_cast<void*>(&count_kernel<4>);
+        default: return reinterpret_cast<void*>(&count_kernel<8>);
     }
 }
 
 template <int MODE>
-cudaError_t launch_mode(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans,
-                        uint32_t n_blocks, uint32_t* wc, uint32_t* wcap, const uint64_t* woff, Cols cols,
-                        uint64_t capacity, cudaStream_t st) {
-    void* args[] = {(void*)&S, (void*)&begin, (void*)&end, (void*)&n_spans, (void*)&wc,
-                    (void*)&wcap, (void*)&woff, (void*)&cols, (void*)&capacity};
-    return cudaLaunchKernel(kernel_for<MODE>(S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
+void* write_kernel_for(uint32_t n_cap) {
+    switch (ncap_stride_(n_cap)) {
+        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1>);
+        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2>);
+        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4>);
+        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8>);
+    }
 }
 
 }  // namespace
 
 uint32_t ncap_stride(uint32_t n_cap) { return ncap_stride_(n_cap); }
 
+uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
+    const uint64_t base = lo & ~31ull;
+    return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
+}
+
 int sweep_blocks_per_sm(int pass, uint32_t n_cap) {
-    void* fn = pass == 0 ? kernel_for<0>(n_cap) : (pass == 1 ? kernel_for<1>(n_cap) : kernel_for<2>(n_cap));
+    void* fn = pass == 0 ? count_kernel_for(n_cap) : (pass == 1 ? write_kernel_for<1>(n_cap) : write_kernel_for<2>(n_cap));
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 
-cudaError_t launch_count(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* warp_count, uint32_t* warp_caps, cudaStream_t st) {
-    Cols none{};
-    return launch_mode<0>(S, begin, end, n_spans, n_blocks, warp_count, warp_caps, nullptr, none, 0, st);
+cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
+                         uint32_t* tile_count, uint4* tile_ck, uint32_t* span_caps, cudaStream_t st) {
+    void* args[] = {(void*)&S, (void*)&lo, (void*)&hi, (void*)&n_spans, (void*)&tile_count, (void*)&tile_ck,
+                    (void*)&span_caps};
+    return cudaLaunchKernel(count_kernel_for(S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
-cudaError_t launch_scan(const uint32_t* warp_count, const uint32_t* warp_caps, uint32_t n_warps,
-                        uint32_t n_cap, uint64_t* warp_off, uint64_t* stats, cudaStream_t st) {
-    scan_kernel<<<1, 1024, 0, st>>>(warp_count, warp_caps, n_warps, ncap_stride(n_cap), n_cap,
-                                    warp_off, stats);
+cudaError_t launch_scan(const uint32_t* tile_count, uint32_t n_tiles, const uint32_t* span_caps, uint32_t n_spans,
+                        uint32_t n_cap, uint64_t* tile_off, uint64_t* stats, cudaStream_t st) {
+    scan_kernel<<<1, 1024, 0, st>>>(tile_count, n_tiles, span_caps, n_spans, ncap_stride(n_cap), n_cap, tile_off,
+                                    stats);
     return cudaGetLastError();
 }
 
-cudaError_t launch_write(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
-                         const uint64_t* warp_off, me_out_mode mode, Cols cols, uint64_t capacity,
-                         cudaStream_t st) {
-    if (mode == ME_OUT_FULL)
-        return launch_mode<2>(S, begin, end, n_spans, n_blocks, nullptr, nullptr, warp_off, cols, capacity, st);
-    return launch_mode<1>(S, begin, end, n_spans, n_blocks, nullptr, nullptr, warp_off, cols, capacity, st);
+cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
+                         const uint64_t* tile_off, me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st) {
+    void* args[] = {(void*)&S, (void*)&lo, (void*)&hi, (void*)&tile_ck, (void*)&tile_off, (void*)&cols,
+                    (void*)&capacity};
+    void* fn = mode == ME_OUT_FULL ? write_kernel_for<2>(S.n_cap) : write_kernel_for<1>(S.n_cap);
+    return cudaLaunchKernel(fn, dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,

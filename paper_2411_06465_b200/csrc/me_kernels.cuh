@@ -24,6 +24,7 @@ struct DevSpace {
     uint32_t n_seg, n_world;
     uint32_t lg_rcdo, rcdo_rc, rcdo_do;
     uint32_t n_cap;
+    uint32_t gbs_mode;            // 1 = a global batch bounds the in-flight microbatches (R17)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
 };
 
@@ -136,21 +137,25 @@ struct Cols {
 
 constexpr int kThreads = 256;
 constexpr int kWarpsPerBlock = kThreads / 32;
+constexpr uint32_t kTileRounds = 16;               // rounds of 32 indices per tile
+constexpr uint32_t kTile = kTileRounds * 32;       // 512 indices
+constexpr uint64_t kMaxSub = 1ull << 28;           // indices per count/scan/write sub-range
 
-// count pass: per-warp survivor counts and per-capacity counts
-cudaError_t launch_count(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* warp_count, uint32_t* warp_caps, cudaStream_t st);
+uint32_t ncap_stride(uint32_t n_cap);
+// tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
+uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
 // resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
 int sweep_blocks_per_sm(int pass, uint32_t n_cap);
-uint32_t ncap_stride(uint32_t n_cap);
-// exclusive scan of the warp counts -> warp_off[n_warps + 1]; stats[0] = total,
-// stats[1 + j] = survivors for capacity j
-cudaError_t launch_scan(const uint32_t* warp_count, const uint32_t* warp_caps, uint32_t n_warps,
-                        uint32_t n_cap, uint64_t* warp_off, uint64_t* stats, cudaStream_t st);
-// write pass: survivors of each warp span at warp_off[w] ...
-cudaError_t launch_write(const DevSpace& S, uint64_t begin, uint64_t end, uint32_t n_spans, uint32_t n_blocks,
-                         const uint64_t* warp_off, me_out_mode mode, Cols cols, uint64_t capacity,
-                         cudaStream_t st);
+// count pass over [lo, hi): per-tile survivor counts and walker checkpoints,
+// per-span per-capacity counts (n_spans spans of whole tiles)
+cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
+                         uint32_t* tile_count, uint4* tile_ck, uint32_t* span_caps, cudaStream_t st);
+// tile offsets = running total stats[0] + exclusive prefix; stats accumulate
+cudaError_t launch_scan(const uint32_t* tile_count, uint32_t n_tiles, const uint32_t* span_caps, uint32_t n_spans,
+                        uint32_t n_cap, uint64_t* tile_off, uint64_t* stats, cudaStream_t st);
+// write pass over [lo, hi): survivors of tile t stored from row tile_off[t]
+cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
+                         const uint64_t* tile_off, me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st);
 // single configurations (me_estimate / me_estimate_batch)
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,
                             const me_parallel* cfgs, uint64_t n, const uint64_t* thr,
