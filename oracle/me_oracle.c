@@ -300,6 +300,94 @@ uint32_t or_cap_mask(uint64_t total, const uint64_t* cap_bytes, uint32_t n_caps,
 }
 
 /* ------------------------------------------------------------------ */
+/* every pipeline stage (NEXT-1)                        */
+/* ------------------------------------------------------------------ */
+
+/* layers of stage i: stage 0 holds L0 (R19); the other p-1 stages split the
+ * remaining L - L0 layers as evenly as possible, earlier stages first */
+uint32_t or_stage_layers(const or_model* m, const or_cfg* c, uint32_t i) {
+    uint32_t L0 = or_first_stage_layers(m, c);
+    if (!L0 || i >= c->p) return 0;
+    if (i == 0) return L0;
+    uint32_t rest = m->L - L0, q = c->p - 1;
+    return rest / q + ((i - 1) < rest % q ? 1u : 0u);
+}
+
+/* Stage i's six terms:
+ *  parameters: Eq.6 (p = 1), Eq.7 (first), Eq.8 (middle), Eq.9 (last: hv/t + h)
+ *              with L/p -> L_i;
+ *  activations: Eq.17 with the stage's own 1F1B occupancy n_i = min(m, p - i)
+ *              ("the first pipeline stage has up to p microbatches ...
+ *              the last stage ... only one"), m = gbs/(d b) or
+ *              unbounded in paper mode; the embedding term on stage 0 only
+ *              (Eq.13), the LM-head term on the last stage only (Eq.14). */
+int or_estimate_stage(const or_model* m, const or_cfg* c, uint32_t i, or_breakdown* out) {
+    int st = cfg_check(m, c);
+    if (st) return st;
+    if (i >= c->p) return OR_EINVAL;
+    g_overflow = 0;
+    int bad = 0;
+    uint32_t Li = or_stage_layers(m, c, i);
+    int first = i == 0, last = i == c->p - 1;
+    uint64_t n_i = c->p - i;
+    if (c->gbs) {
+        uint64_t mb = c->gbs / ((uint64_t)c->d * c->b);
+        if (mb < n_i) n_i = mb;
+    }
+    rat h = RI(m->h), v = RI(m->v), T = RI(c->t);
+    rat inner = radd(radd(RI(1), R(m->k, m->a)), rmul(R(3, 2), R(m->f, m->h)));
+    rat layer_part = rmul(rmul(RI(2), RI(Li)), rmul(rmul(h, h), radd(rdiv(inner, T), R(1, m->h))));
+    rat psi = layer_part;                                          /* Eq.8 */
+    if (first && last) psi = radd(radd(rdiv(rmul(RI(2), rmul(h, v)), T), h), layer_part); /* Eq.6 */
+    else if (first) psi = radd(rdiv(rmul(h, v), T), layer_part);   /* Eq.7 */
+    else if (last) psi = radd(radd(rdiv(rmul(h, v), T), h), layer_part); /* Eq.9 */
+    rat params = rmul(RI(2), psi), grads = rmul(RI(4), psi), optim;
+    if (c->dopt) {
+        rat share = rdiv(psi, RI((i128)c->d * c->c));
+        optim = rmul(RI(12), RI((share.n + share.d - 1) / share.d)); /* R8 */
+    } else {
+        optim = rmul(RI(12), psi);
+    }
+    rat sbh_tc = R((i128)c->s * c->b * m->h, (i128)c->t * c->c);
+    rat br = eq12_bracket(m);
+    rat layers = c->rc ? rmul(sbh_tc, radd(RI((i128)2 * n_i * Li), br))
+                       : rmul(sbh_tc, rmul(br, RI((i128)n_i * Li)));
+    rat embed = first ? rmul(sbh_tc, RI((i128)8 * n_i)) : RI(0);
+    rat head = last ? rmul(RI((i128)n_i), rmul(sbh_tc, rmul(RI(4), radd(RI(1), R(m->v, m->h))))) : RI(0);
+    or_breakdown r;
+    r.params = to_u64(params, &bad);
+    r.grads = to_u64(grads, &bad);
+    r.optim = to_u64(optim, &bad);
+    r.act_layers = to_u64(layers, &bad);
+    r.act_embed = to_u64(embed, &bad);
+    r.act_head = to_u64(head, &bad);
+    r.total = to_u64(radd(radd(radd(params, grads), radd(optim, layers)), radd(embed, head)), &bad);
+    if (g_overflow) return OR_EOVERFLOW;
+    if (bad) return bad;
+    *out = r;
+    return OR_OK;
+}
+
+/* the stage with the largest total (the first one on ties) */
+int or_estimate_max(const or_model* m, const or_cfg* c, or_breakdown* out, uint32_t* stage) {
+    int st = cfg_check(m, c);
+    if (st) return st;
+    or_breakdown best;
+    uint32_t arg = 0;
+    for (uint32_t i = 0; i < c->p; i++) {
+        or_breakdown r;
+        if ((st = or_estimate_stage(m, c, i, &r))) return st;
+        if (i == 0 || r.total > best.total) {
+            best = r;
+            arg = i;
+        }
+    }
+    *out = best;
+    if (stage) *stage = arg;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
 /* canonical enumeration                                */
 /* ------------------------------------------------------------------ */
 typedef struct {

@@ -81,6 +81,11 @@ int or_activation_per_layer(const or_model* m, uint32_t s, uint32_t b, uint64_t*
 uint32_t or_first_stage_layers(const or_model* m, const or_cfg* c);
 /* Eq.18 + extensions: the six stage-0 terms and their sum */
 int or_estimate(const or_model* m, const or_cfg* c, or_breakdown* out);
+/* NEXT-1: layers of pipeline stage i, the six terms of stage i (Eq.6-9 with
+ * the stage's 1F1B occupancy min(m, p - i)), and the largest stage total */
+uint32_t or_stage_layers(const or_model* m, const or_cfg* c, uint32_t i);
+int or_estimate_stage(const or_model* m, const or_cfg* c, uint32_t i, or_breakdown* out);
+int or_estimate_max(const or_model* m, const or_cfg* c, or_breakdown* out, uint32_t* stage);
 /* capacity bitmask: bit j set <=> total * den <= cap_j * num (80% rule) */
 uint32_t or_cap_mask(uint64_t total, const uint64_t* cap_bytes, uint32_t n_caps,
                      uint32_t num, uint32_t den);

@@ -192,15 +192,46 @@ struct CapAcc {
     }
 };
 
+// Shared-memory staging of a warp's survivor columns (write pass): the
+// survivors of a round are put into a 64-entry ring per column; whenever 32
+// rows are pending, the warp stores them with one full-warp, contiguous
+// 256-byte store per column.  The write kernel can also store directly from
+// the lanes (ME_WRITE_STAGE=0, for comparison).
+template <int NC>
+struct Stager {
+    uint64_t* buf;      // NC x 64 ring entries of this warp
+    uint32_t head = 0, pend = 0;
+    uint64_t grow = 0;  // output row of the first pending entry
+    __device__ __forceinline__ void put(uint32_t slot, uint32_t col, uint64_t v) {
+        buf[col * 64 + ((head + pend + slot) & 63u)] = v;
+    }
+    __device__ __forceinline__ void flush(const Cols& cols, uint64_t capacity, uint32_t lane, uint32_t n) {
+        __syncwarp();
+        if (lane < n) {
+            const uint32_t idx = (head + lane) & 63u;
+            const uint64_t row = grow + lane;
+            if (row < capacity) {
+#pragma unroll
+                for (int c = 0; c < NC; c++) cols.c[c][row] = buf[c * 64 + idx];
+            }
+        }
+        __syncwarp();
+        head = (head + n) & 63u;
+        pend -= n;
+        grow += n;
+    }
+};
+
 // Evaluate one tile's rounds starting at the walker's position (lane's index
 // = pos).  RAGGED: the tile is cut by lo/hi (first or last tile of a range).
 // GBS: a global batch bounds the in-flight microbatches (R17).  Returns with
 // the walker on the first index after the tile when `advance_out`.
-template <int MODE, int NCAP, bool RAGGED, bool GBS>
+template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STAGE>
 __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
                                              uint64_t hi, uint32_t rounds, uint32_t lane, CapAcc<NCAP>& acc,
                                              uint64_t out, const Cols& cols, uint64_t capacity,
-                                             bool advance_out) {
+                                             bool advance_out, Stager<MODE == 2 ? 8 : 1>* sg) {
+    constexpr int NC = MODE == 2 ? 8 : 1;
     const uint32_t pstep = 32u >> S.lg_rcdo;
     uint32_t cnt = 0;
     uint2 pr = __ldg(W.pp);
@@ -221,19 +252,30 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
             acc.add(mask);
         } else {
             const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
-            if (mask) {
-                const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
+            const uint32_t rank = __popc(ballot & ((1u << lane) - 1u));
+            uint64_t v[NC];
+            v[0] = pos | ((uint64_t)mask << 56);
+            if (MODE == 2) {
+                v[1] = 2ull * W.L.psi;
+                v[2] = 4ull * W.L.psi;
+                v[3] = W.L.optim;
+                v[4] = (uint64_t)u * ((uint64_t)n_inf * W.L.lam + W.L.mu);
+                v[5] = (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
+                v[6] = (uint64_t)u * W.L.hc;
+                v[7] = total;
+            }
+            if (STAGE) {
+                if (mask) {
+#pragma unroll
+                    for (int c = 0; c < NC; c++) sg->put(rank, c, v[c]);
+                }
+                sg->pend += __popc(ballot);
+                if (sg->pend >= 32) sg->flush(cols, capacity, lane, 32);
+            } else if (mask) {
+                const uint64_t o = out + rank;
                 if (o < capacity) {
-                    cols.c[0][o] = pos | ((uint64_t)mask << 56);
-                    if (MODE == 2) {
-                        cols.c[1][o] = 2ull * W.L.psi;
-                        cols.c[2][o] = 4ull * W.L.psi;
-                        cols.c[3][o] = W.L.optim;
-                        cols.c[4][o] = (uint64_t)u * ((uint64_t)n_inf * W.L.lam + W.L.mu);
-                        cols.c[5][o] = (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
-                        cols.c[6][o] = (uint64_t)u * W.L.hc;
-                        cols.c[7][o] = total;
-                    }
+#pragma unroll
+                    for (int c = 0; c < NC; c++) cols.c[c][o] = v[c];
                 }
             }
             out += __popc(ballot);
@@ -274,38 +316,44 @@ __device__ __forceinline__ TileGeom geom(uint64_t lo, uint64_t hi) {
     return g;
 }
 
-// count pass: span s = tiles [s*n/S, (s+1)*n/S)
+// count pass over span s = tiles [t0, t1): per tile its checkpoint
+// {seg, j, r, s} and its first survivor's rank inside the span; the span total
 template <int NCAP, bool GBS>
-__device__ __forceinline__ void count_span(const DevSpace& S, const TileGeom& G, uint32_t t0, uint32_t t1,
-                                           uint32_t lane, uint32_t* __restrict__ tile_count,
-                                           uint4* __restrict__ tile_ck, CapAcc<NCAP>& acc) {
+__device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom& G, uint32_t s, uint32_t t0,
+                                               uint32_t t1, uint32_t lane, uint32_t* __restrict__ tile_rel,
+                                               uint4* __restrict__ tile_ck, CapAcc<NCAP>& acc) {
     Walker W;
     // a lane past the end of the range only takes part in the warp reductions:
     // park it on the last index (its own positions stay inactive)
     const uint64_t p0 = G.start(t0) + lane;
     W.seek(S, p0 < G.hi ? p0 : G.hi - 1);
+    uint32_t run = 0;
+    Stager<1>* nosg = nullptr;
     for (uint32_t t = t0; t < t1; t++) {
         const uint64_t ts = G.start(t);
-        const uint4 ck = make_uint4(W.seg, W.j, W.r, 0u);
-        if (lane == 0) tile_ck[t] = ck;  // lane 0 is at the tile's first index
+        if (lane == 0) {  // lane 0 is at the tile's first index
+            tile_ck[t] = make_uint4(W.seg, W.j, W.r, s);
+            tile_rel[t] = run;
+        }
         const bool last = t + 1 == t1;
         uint32_t cnt;
         if (G.ragged(t))
-            cnt = run_tile<0, NCAP, true, GBS>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{}, 0,
-                                               !last);
+            cnt = run_tile<0, NCAP, true, GBS, false>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{},
+                                                      0, !last, nosg);
         else
-            cnt = run_tile<0, NCAP, false, GBS>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0, Cols{}, 0,
-                                                !last);
+            cnt = run_tile<0, NCAP, false, GBS, false>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
+                                                       Cols{}, 0, !last, nosg);
         acc.flush();
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0) tile_count[t] = cnt;
+        run += __reduce_add_sync(0xffffffffu, cnt);
     }
+    return run;
 }
 
 template <int NCAP>
-__global__ void __launch_bounds__(kThreads) count_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
-                                                         const uint32_t n_spans, uint32_t* __restrict__ tile_count,
+__global__ void __launch_bounds__(kThreads, 4) count_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+                                                         const uint32_t n_spans, uint32_t* __restrict__ tile_rel,
                                                          uint4* __restrict__ tile_ck,
+                                                         uint32_t* __restrict__ span_count,
                                                          uint32_t* __restrict__ span_caps) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
@@ -314,10 +362,12 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const DevSpace S, const
         const uint32_t t0 = (uint32_t)((uint64_t)G.n_tiles * s / n_spans);
         const uint32_t t1 = (uint32_t)((uint64_t)G.n_tiles * (s + 1) / n_spans);
         CapAcc<NCAP> acc;
+        uint32_t n = 0;
         if (t0 < t1) {
-            if (S.gbs_mode) count_span<NCAP, true>(S, G, t0, t1, lane, tile_count, tile_ck, acc);
-            else count_span<NCAP, false>(S, G, t0, t1, lane, tile_count, tile_ck, acc);
+            if (S.gbs_mode) n = count_span<NCAP, true>(S, G, s, t0, t1, lane, tile_rel, tile_ck, acc);
+            else n = count_span<NCAP, false>(S, G, s, t0, t1, lane, tile_rel, tile_ck, acc);
         }
+        if (lane == 0) span_count[s] = n;
 #pragma unroll
         for (int q = 0; q < NCAP; q++) {
             const uint32_t c = __reduce_add_sync(0xffffffffu, acc.capc[q]);
@@ -327,49 +377,59 @@ __global__ void __launch_bounds__(kThreads) count_kernel(const DevSpace S, const
 }
 
 // write pass: tiles in grid-stride order
-template <int MODE, int NCAP>
-__global__ void __launch_bounds__(kThreads) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+template <int MODE, int NCAP, bool STAGE>
+__global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                          const uint4* __restrict__ tile_ck,
-                                                         const uint64_t* __restrict__ tile_off, const Cols cols,
+                                                         const uint32_t* __restrict__ tile_rel,
+                                                         const uint64_t* __restrict__ span_off, const Cols cols,
                                                          const uint64_t capacity) {
-    const uint32_t lane = threadIdx.x & 31;
+    constexpr int NC = MODE == 2 ? 8 : 1;
+    __shared__ uint64_t s_stage[STAGE ? kWarpsPerBlock * NC * 64 : 1];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
     const TileGeom G = geom(lo, hi);
     CapAcc<NCAP> none;
-    for (uint32_t t = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < G.n_tiles; t += n_warps) {
+    Stager<NC> sg;
+    sg.buf = s_stage + (STAGE ? wid * NC * 64 : 0);
+    for (uint32_t t = blockIdx.x * kWarpsPerBlock + wid; t < G.n_tiles; t += n_warps) {
         const uint64_t ts = G.start(t);
         const uint64_t pos = ts + lane;
-        const uint64_t out = __ldg(tile_off + t);
+        const uint4 ck = __ldg(tile_ck + t);
+        const uint64_t out = __ldg(span_off + ck.w) + __ldg(tile_rel + t);
+        sg.head = 0;
+        sg.pend = 0;
+        sg.grow = out;
         Walker W;
         const bool ragged = G.ragged(t);
         // a lane past the end of the range is parked on the last index: it
         // takes part in the ballots with inactive positions
-        W.restore(S, __ldg(tile_ck + t), pos < hi ? lane : (uint32_t)(hi - 1 - ts));
+        W.restore(S, ck, pos < hi ? lane : (uint32_t)(hi - 1 - ts));
         if (ragged) {
             if (S.gbs_mode)
-                run_tile<MODE, NCAP, true, true>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols, capacity,
-                                                 false);
+                run_tile<MODE, NCAP, true, true, STAGE>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
+                                                        capacity, false, &sg);
             else
-                run_tile<MODE, NCAP, true, false>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
-                                                  capacity, false);
+                run_tile<MODE, NCAP, true, false, STAGE>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
+                                                         capacity, false, &sg);
         } else {
             if (S.gbs_mode)
-                run_tile<MODE, NCAP, false, true>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
-                                                  capacity, false);
+                run_tile<MODE, NCAP, false, true, STAGE>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
+                                                         capacity, false, &sg);
             else
-                run_tile<MODE, NCAP, false, false>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
-                                                   capacity, false);
+                run_tile<MODE, NCAP, false, false, STAGE>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
+                                                          capacity, false, &sg);
         }
+        if (STAGE && sg.pend) sg.flush(cols, capacity, lane, sg.pend);
     }
 }
 
-// one block: exclusive scan of the tile counts (u32) into u64 offsets starting
-// at the running total stats[0]; stats[0] and stats[1 + q] accumulate the
-// totals of this sub-range
-__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__ tile_count, uint32_t n,
+// one block: exclusive scan of the span counts into u64 offsets starting at
+// the running total stats[0]; stats[0] and stats[1 + q] accumulate the totals
+// of this sub-range
+__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__ counts, uint32_t n,
                                                     const uint32_t* __restrict__ span_caps, uint32_t n_spans,
                                                     uint32_t ncap_stride, uint32_t n_cap,
-                                                    uint64_t* __restrict__ tile_off, uint64_t* __restrict__ stats) {
+                                                    uint64_t* __restrict__ offs, uint64_t* __restrict__ stats) {
     __shared__ uint64_t s_warp[32];
     __shared__ uint64_t s_caps[8][32];
     __shared__ uint64_t s_base;
@@ -378,7 +438,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__
     const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = min(n, tid * chunk), hi = min(n, lo + chunk);
     uint64_t sum = 0;
-    for (uint32_t i = lo; i < hi; i++) sum += tile_count[i];
+    for (uint32_t i = lo; i < hi; i++) sum += counts[i];
     uint64_t caps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (uint32_t s = tid; s < n_spans; s += blockDim.x)
         for (uint32_t q = 0; q < n_cap; q++) caps[q] += span_caps[(size_t)s * ncap_stride + q];
@@ -414,8 +474,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__
     __syncthreads();
     uint64_t run = base + s_warp[wid] + inc - sum;
     for (uint32_t i = lo; i < hi; i++) {
-        tile_off[i] = run;
-        run += tile_count[i];
+        offs[i] = run;
+        run += counts[i];
     }
 }
 
@@ -492,14 +552,19 @@ void* count_kernel_for(uint32_t n_cap) {
     }
 }
 
-template <int MODE>
+template <int MODE, bool STAGE>
 void* write_kernel_for(uint32_t n_cap) {
     switch (ncap_stride_(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1>);
-        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2>);
-        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4>);
-        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8>);
+        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1, STAGE>);
+        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2, STAGE>);
+        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4, STAGE>);
+        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8, STAGE>);
     }
+}
+
+void* write_fn(me_out_mode mode, uint32_t n_cap, bool stage) {
+    if (mode == ME_OUT_FULL) return stage ? write_kernel_for<2, true>(n_cap) : write_kernel_for<2, false>(n_cap);
+    return stage ? write_kernel_for<1, true>(n_cap) : write_kernel_for<1, false>(n_cap);
 }
 
 }  // namespace
@@ -511,33 +576,34 @@ uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
     return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
 }
 
-int sweep_blocks_per_sm(int pass, uint32_t n_cap) {
-    void* fn = pass == 0 ? count_kernel_for(n_cap) : (pass == 1 ? write_kernel_for<1>(n_cap) : write_kernel_for<2>(n_cap));
+int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool stage) {
+    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX, n_cap, stage);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* tile_count, uint4* tile_ck, uint32_t* span_caps, cudaStream_t st) {
-    void* args[] = {(void*)&S, (void*)&lo, (void*)&hi, (void*)&n_spans, (void*)&tile_count, (void*)&tile_ck,
-                    (void*)&span_caps};
+                         uint32_t* tile_rel, uint4* tile_ck, uint32_t* span_count, uint32_t* span_caps,
+                         cudaStream_t st) {
+    void* args[] = {(void*)&S,        (void*)&lo,      (void*)&hi,         (void*)&n_spans,
+                    (void*)&tile_rel, (void*)&tile_ck, (void*)&span_count, (void*)&span_caps};
     return cudaLaunchKernel(count_kernel_for(S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
-cudaError_t launch_scan(const uint32_t* tile_count, uint32_t n_tiles, const uint32_t* span_caps, uint32_t n_spans,
-                        uint32_t n_cap, uint64_t* tile_off, uint64_t* stats, cudaStream_t st) {
-    scan_kernel<<<1, 1024, 0, st>>>(tile_count, n_tiles, span_caps, n_spans, ncap_stride(n_cap), n_cap, tile_off,
+cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
+                        uint64_t* span_off, uint64_t* stats, cudaStream_t st) {
+    scan_kernel<<<1, 1024, 0, st>>>(span_count, n_spans, span_caps, n_spans, ncap_stride(n_cap), n_cap, span_off,
                                     stats);
     return cudaGetLastError();
 }
 
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
-                         const uint64_t* tile_off, me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st) {
-    void* args[] = {(void*)&S, (void*)&lo, (void*)&hi, (void*)&tile_ck, (void*)&tile_off, (void*)&cols,
-                    (void*)&capacity};
-    void* fn = mode == ME_OUT_FULL ? write_kernel_for<2>(S.n_cap) : write_kernel_for<1>(S.n_cap);
-    return cudaLaunchKernel(fn, dim3(n_blocks), dim3(kThreads), args, 0, st);
+                         const uint32_t* tile_rel, const uint64_t* span_off, me_out_mode mode, bool stage, Cols cols,
+                         uint64_t capacity, cudaStream_t st) {
+    void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,   (void*)&tile_ck,
+                    (void*)&tile_rel, (void*)&span_off, (void*)&cols, (void*)&capacity};
+    return cudaLaunchKernel(write_fn(mode, S.n_cap, stage), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,

@@ -145,17 +145,21 @@ uint32_t ncap_stride(uint32_t n_cap);
 // tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
 uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
 // resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
-int sweep_blocks_per_sm(int pass, uint32_t n_cap);
-// count pass over [lo, hi): per-tile survivor counts and walker checkpoints,
-// per-span per-capacity counts (n_spans spans of whole tiles)
+int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool stage);
+// count pass over [lo, hi) cut into n_spans spans of whole tiles: per tile its
+// walker checkpoint {seg, j, r, span} and the rank of its first survivor in the
+// span; per span its survivor count and per-capacity counts
 cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* tile_count, uint4* tile_ck, uint32_t* span_caps, cudaStream_t st);
-// tile offsets = running total stats[0] + exclusive prefix; stats accumulate
-cudaError_t launch_scan(const uint32_t* tile_count, uint32_t n_tiles, const uint32_t* span_caps, uint32_t n_spans,
-                        uint32_t n_cap, uint64_t* tile_off, uint64_t* stats, cudaStream_t st);
-// write pass over [lo, hi): survivors of tile t stored from row tile_off[t]
+                         uint32_t* tile_rel, uint4* tile_ck, uint32_t* span_count, uint32_t* span_caps,
+                         cudaStream_t st);
+// span offsets = running total stats[0] + exclusive prefix; stats accumulate
+cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
+                        uint64_t* span_off, uint64_t* stats, cudaStream_t st);
+// write pass over [lo, hi): survivors of tile t stored from row
+// span_off[span(t)] + tile_rel[t]; stage = through shared-memory staging
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
-                         const uint64_t* tile_off, me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st);
+                         const uint32_t* tile_rel, const uint64_t* span_off, me_out_mode mode, bool stage, Cols cols,
+                         uint64_t capacity, cudaStream_t st);
 // single configurations (me_estimate / me_estimate_batch)
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,
                             const me_parallel* cfgs, uint64_t n, const uint64_t* thr,

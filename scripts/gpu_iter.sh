@@ -13,6 +13,6 @@ $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "launch rc=$?"
 $CMD > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 6 -c 3 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"count_kernel|write_kernel" -s 8 -c 4 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
 fi
