@@ -96,6 +96,10 @@ def lib():
         _lib.or_sweep.argtypes = [P(SpaceC), ctypes.c_uint64, ctypes.c_uint64, _u64p,
                                   P(Breakdown), ctypes.c_uint64, _u64p, _u64p, ctypes.c_int]
         _lib.or_points.argtypes = [P(SpaceC), _u64p, ctypes.c_uint64, P(Breakdown), _u32p]
+        _lib.or_stage_layers.argtypes = [P(Model), P(Cfg), ctypes.c_uint32]
+        _lib.or_stage_layers.restype = ctypes.c_uint32
+        _lib.or_estimate_stage.argtypes = [P(Model), P(Cfg), ctypes.c_uint32, P(Breakdown)]
+        _lib.or_estimate_max.argtypes = [P(Model), P(Cfg), P(Breakdown), _u32p]
     return _lib
 
 
@@ -153,6 +157,30 @@ def estimate_status(shape, **cfg) -> int:
     out = Breakdown()
     return lib().or_estimate(ctypes.byref(_model(shape)), ctypes.byref(make_cfg(**cfg)),
                              ctypes.byref(out))
+
+
+def stage_layers(shape, stage, **cfg) -> int:
+    return lib().or_stage_layers(ctypes.byref(_model(shape)), ctypes.byref(make_cfg(**cfg)), stage)
+
+
+def estimate_stage(shape, stage, **cfg) -> dict:
+    """NEXT-1: the six terms of pipeline stage `stage` (Eq.6-9, 1F1B occupancy)."""
+    out = Breakdown()
+    st = lib().or_estimate_stage(ctypes.byref(_model(shape)), ctypes.byref(make_cfg(**cfg)), stage,
+                                 ctypes.byref(out))
+    if st:
+        raise OracleError(st, f"stage {stage} {cfg}")
+    return {k: getattr(out, k) for k in TERMS}
+
+
+def estimate_max(shape, **cfg):
+    """NEXT-1: (terms of the stage with the largest total, that stage)."""
+    out, stage = Breakdown(), ctypes.c_uint32()
+    st = lib().or_estimate_max(ctypes.byref(_model(shape)), ctypes.byref(make_cfg(**cfg)), ctypes.byref(out),
+                               ctypes.byref(stage))
+    if st:
+        raise OracleError(st, str(cfg))
+    return {k: getattr(out, k) for k in TERMS}, stage.value
 
 
 def cap_mask(total, cap_bytes, num=4, den=5) -> int:
