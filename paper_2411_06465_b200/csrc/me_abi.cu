@@ -106,12 +106,13 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t stage = 1;                     // write pass through shared-memory staging
+    uint32_t stage = 0;                     // write pass through shared-memory staging (ME_WRITE_STAGE=1)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
     // of sub-range i (on the caller's stream).
     struct Scratch {
         uint32_t* tile_rel = nullptr;   // rank of a tile's first survivor inside its span
+        uint32_t* tile_cnt = nullptr;   // survivors of a tile
         uint4* tile_ck = nullptr;       // walker checkpoint of a tile's first index
         uint32_t* span_count = nullptr;
         uint64_t* span_off = nullptr;
@@ -229,6 +230,8 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (P->count_bps < 1) P->count_bps = 1;
     for (auto& sc : P->scratch) {
         sc.tile_rel = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
+        sc.tile_cnt = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
+        P->owned.push_back(sc.tile_cnt);
         sc.tile_ck = (uint4*)P->A.get((size_t)P->max_tiles * 16);
         sc.span_count = (uint32_t*)P->A.get((size_t)P->max_spans * 4);
         sc.span_off = (uint64_t*)P->A.get((size_t)P->max_spans * 8);
@@ -238,7 +241,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         P->owned.push_back(sc.span_count);
         P->owned.push_back(sc.span_off);
         P->owned.push_back(sc.span_caps);
-        if (!sc.tile_rel || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps) {
+        if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps) {
             me_plan_free(P);
             return err(ME_ENOMEM, "scratch allocation");
         }
@@ -381,7 +384,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             cudaStreamWaitEvent(cs, sc.free_ev, 0);
             cudaEventRecord(tev[0], cs);
             cudaError_t ce = launch_count(P->ds, lo, hi, n_spans, grid(P->count_bps, n_spans), sc.tile_rel,
-                                          sc.tile_ck, sc.span_count, sc.span_caps, cs);
+                                          sc.tile_cnt, sc.tile_ck, sc.span_count, sc.span_caps, cs);
             if (ce != cudaSuccess) return cuda_err(ce, "count kernel");
             cudaEventRecord(tev[1], cs);
             ce = launch_scan(sc.span_count, sc.span_caps, n_spans, P->ds.n_cap, sc.span_off, stats, cs);
@@ -390,8 +393,8 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             cudaStreamWaitEvent(st, tev[2], 0);
             cudaEventRecord(tev[3], st);
             if (write) {
-                ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_rel, sc.span_off,
-                                  o->mode, P->stage != 0, cols, capacity, st);
+                ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_rel, sc.tile_cnt,
+                                  sc.span_off, o->mode, P->stage != 0, cols, capacity, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "write kernel");
             }
             cudaEventRecord(tev[4], st);

@@ -321,7 +321,8 @@ __device__ __forceinline__ TileGeom geom(uint64_t lo, uint64_t hi) {
 template <int NCAP, bool GBS>
 __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom& G, uint32_t s, uint32_t t0,
                                                uint32_t t1, uint32_t lane, uint32_t* __restrict__ tile_rel,
-                                               uint4* __restrict__ tile_ck, CapAcc<NCAP>& acc) {
+                                               uint32_t* __restrict__ tile_cnt, uint4* __restrict__ tile_ck,
+                                               CapAcc<NCAP>& acc) {
     Walker W;
     // a lane past the end of the range only takes part in the warp reductions:
     // park it on the last index (its own positions stay inactive)
@@ -344,7 +345,9 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
             cnt = run_tile<0, NCAP, false, GBS, false>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
                                                        Cols{}, 0, !last, nosg);
         acc.flush();
-        run += __reduce_add_sync(0xffffffffu, cnt);
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) tile_cnt[t] = cnt;
+        run += cnt;
     }
     return run;
 }
@@ -352,7 +355,7 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
 template <int NCAP>
 __global__ void __launch_bounds__(kThreads, 4) count_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                          const uint32_t n_spans, uint32_t* __restrict__ tile_rel,
-                                                         uint4* __restrict__ tile_ck,
+                                                         uint32_t* __restrict__ tile_cnt, uint4* __restrict__ tile_ck,
                                                          uint32_t* __restrict__ span_count,
                                                          uint32_t* __restrict__ span_caps) {
     const uint32_t lane = threadIdx.x & 31;
@@ -364,8 +367,8 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const DevSpace S, co
         CapAcc<NCAP> acc;
         uint32_t n = 0;
         if (t0 < t1) {
-            if (S.gbs_mode) n = count_span<NCAP, true>(S, G, s, t0, t1, lane, tile_rel, tile_ck, acc);
-            else n = count_span<NCAP, false>(S, G, s, t0, t1, lane, tile_rel, tile_ck, acc);
+            if (S.gbs_mode) n = count_span<NCAP, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+            else n = count_span<NCAP, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
         }
         if (lane == 0) span_count[s] = n;
 #pragma unroll
@@ -381,6 +384,7 @@ template <int MODE, int NCAP, bool STAGE>
 __global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                          const uint4* __restrict__ tile_ck,
                                                          const uint32_t* __restrict__ tile_rel,
+                                                         const uint32_t* __restrict__ tile_cnt,
                                                          const uint64_t* __restrict__ span_off, const Cols cols,
                                                          const uint64_t capacity) {
     constexpr int NC = MODE == 2 ? 8 : 1;
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, co
     Stager<NC> sg;
     sg.buf = s_stage + (STAGE ? wid * NC * 64 : 0);
     for (uint32_t t = blockIdx.x * kWarpsPerBlock + wid; t < G.n_tiles; t += n_warps) {
+        if (__ldg(tile_cnt + t) == 0) continue;  // no survivor: nothing to write
         const uint64_t ts = G.start(t);
         const uint64_t pos = ts + lane;
         const uint4 ck = __ldg(tile_ck + t);
@@ -584,10 +589,10 @@ int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool stage) {
 }
 
 cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* tile_rel, uint4* tile_ck, uint32_t* span_count, uint32_t* span_caps,
-                         cudaStream_t st) {
-    void* args[] = {(void*)&S,        (void*)&lo,      (void*)&hi,         (void*)&n_spans,
-                    (void*)&tile_rel, (void*)&tile_ck, (void*)&span_count, (void*)&span_caps};
+                         uint32_t* tile_rel, uint32_t* tile_cnt, uint4* tile_ck, uint32_t* span_count,
+                         uint32_t* span_caps, cudaStream_t st) {
+    void* args[] = {(void*)&S,       (void*)&lo,         (void*)&hi,       (void*)&n_spans, (void*)&tile_rel,
+                    (void*)&tile_cnt, (void*)&tile_ck, (void*)&span_count, (void*)&span_caps};
     return cudaLaunchKernel(count_kernel_for(S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
@@ -599,10 +604,10 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 }
 
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
-                         const uint32_t* tile_rel, const uint64_t* span_off, me_out_mode mode, bool stage, Cols cols,
-                         uint64_t capacity, cudaStream_t st) {
-    void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,   (void*)&tile_ck,
-                    (void*)&tile_rel, (void*)&span_off, (void*)&cols, (void*)&capacity};
+                         const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
+                         me_out_mode mode, bool stage, Cols cols, uint64_t capacity, cudaStream_t st) {
+    void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
+                    (void*)&tile_cnt, (void*)&span_off, (void*)&cols, (void*)&capacity};
     return cudaLaunchKernel(write_fn(mode, S.n_cap, stage), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 

@@ -150,16 +150,16 @@ int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool stage);
 // walker checkpoint {seg, j, r, span} and the rank of its first survivor in the
 // span; per span its survivor count and per-capacity counts
 cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* tile_rel, uint4* tile_ck, uint32_t* span_count, uint32_t* span_caps,
-                         cudaStream_t st);
+                         uint32_t* tile_rel, uint32_t* tile_cnt, uint4* tile_ck, uint32_t* span_count,
+                         uint32_t* span_caps, cudaStream_t st);
 // span offsets = running total stats[0] + exclusive prefix; stats accumulate
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st);
 // write pass over [lo, hi): survivors of tile t stored from row
 // span_off[span(t)] + tile_rel[t]; stage = through shared-memory staging
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
-                         const uint32_t* tile_rel, const uint64_t* span_off, me_out_mode mode, bool stage, Cols cols,
-                         uint64_t capacity, cudaStream_t st);
+                         const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
+                         me_out_mode mode, bool stage, Cols cols, uint64_t capacity, cudaStream_t st);
 // single configurations (me_estimate / me_estimate_batch)
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,
                             const me_parallel* cfgs, uint64_t n, const uint64_t* thr,
