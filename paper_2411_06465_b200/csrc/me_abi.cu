@@ -106,7 +106,7 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t stage = 0;                     // write pass through shared-memory staging (ME_WRITE_STAGE=1)
+    uint32_t stage = 1;                     // write pass through aligned shared-memory staging (ME_WRITE_STAGE)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
     // of sub-range i (on the caller's stream).

@@ -193,10 +193,12 @@ struct CapAcc {
 };
 
 // Shared-memory staging of a warp's survivor columns (write pass): the
-// survivors of a round are put into a 64-entry ring per column; whenever 32
-// rows are pending, the warp stores them with one full-warp, contiguous
-// 256-byte store per column.  The write kernel can also store directly from
-// the lanes (ME_WRITE_STAGE=0, for comparison).
+// survivors of a round are put into a 64-entry ring per column and leave it in
+// whole, aligned 128-byte lines (one full-warp 256-byte store per column per 32
+// rows); only the first and last line of a tile's output can be partial.
+// Measured on B200 (scripts/storebench.cu): aligned full-warp column stores
+// reach 5.7-6.1 TB/s, unaligned or partial ones 4.0-4.2 TB/s.  The write
+// kernel can also store directly from the lanes (ME_WRITE_STAGE=0).
 template <int NC>
 struct Stager {
     uint64_t* buf;      // NC x 64 ring entries of this warp
@@ -219,6 +221,16 @@ struct Stager {
         head = (head + n) & 63u;
         pend -= n;
         grow += n;
+    }
+    // store what can go out in whole 128-byte lines: first the rows up to the
+    // next line boundary, then groups of 32 rows (two full lines per column)
+    __device__ __forceinline__ void drain(const Cols& cols, uint64_t capacity, uint32_t lane) {
+        if (grow & 15u) {
+            const uint32_t a = 16u - (uint32_t)(grow & 15u);
+            if (pend < a) return;
+            flush(cols, capacity, lane, a);
+        }
+        while (pend >= 32) flush(cols, capacity, lane, 32);
     }
 };
 
@@ -270,7 +282,7 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
                     for (int c = 0; c < NC; c++) sg->put(rank, c, v[c]);
                 }
                 sg->pend += __popc(ballot);
-                if (sg->pend >= 32) sg->flush(cols, capacity, lane, 32);
+                if (sg->pend >= 16) sg->drain(cols, capacity, lane);
             } else if (mask) {
                 const uint64_t o = out + rank;
                 if (o < capacity) {
@@ -424,7 +436,8 @@ __global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, co
                 run_tile<MODE, NCAP, false, false, STAGE>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
                                                           capacity, false, &sg);
         }
-        if (STAGE && sg.pend) sg.flush(cols, capacity, lane, sg.pend);
+        if (STAGE)
+            while (sg.pend) sg.flush(cols, capacity, lane, sg.pend < 32 ? sg.pend : 32u);
     }
 }
 
