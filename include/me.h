@@ -102,13 +102,16 @@ typedef struct {
 } me_cluster;
 
 /* The remaining axes.  recompute_mask / dist_opt_mask: bit0 = off, bit1 = on
- * (each must be 1, 2 or 3).  max_tp/max_cp/max_pp: 0 = unlimited. */
+ * (each must be 1, 2 or 3).  max_tp/max_cp/max_pp: 0 = unlimited.
+ * stage_policy: ME_STAGE_FIRST (0) = the paper's first-stage estimate;
+ * ME_STAGE_MAX (1) = the largest stage total (NEXT-1: Eq.7/8/9 per stage with
+ * the stage's 1F1B occupancy; the record then holds that stage's terms). */
 typedef struct {
     const uint32_t* mbs;
     uint32_t n_mbs;
     const uint32_t* seq;
     uint32_t n_seq;
-    uint8_t recompute_mask, dist_opt_mask, allow_uneven_pp, _pad;
+    uint8_t recompute_mask, dist_opt_mask, allow_uneven_pp, stage_policy;
     uint32_t gbs, max_tp, max_cp, max_pp;
 } me_cfg_range;
 
@@ -118,6 +121,9 @@ typedef struct {
  *  FULL   eight u64 columns (structure of arrays): index|mask, params, grads,
  *         optim, act_layers, act_embed, act_head, total */
 typedef enum { ME_OUT_COUNT = 0, ME_OUT_INDEX = 1, ME_OUT_FULL = 2 } me_out_mode;
+
+enum { ME_STAGE_FIRST = 0, ME_STAGE_MAX = 1 };
+#define ME_STAGE_ARGMAX 0xFFFFFFFFu
 
 #define ME_N_COLS 8
 
@@ -157,6 +163,19 @@ typedef struct {
  * device code as the sweep (one GPU thread; synchronous).  Checks EINVAL then
  * EDIV then EOVERFLOW as listed above.  Uses the current CUDA device. */
 int me_estimate(const me_model* model, const me_parallel* cfg, me_breakdown* out);
+
+/* me_estimate_stage: the six terms of pipeline stage `stage` (0 .. p-1) of one
+ * configuration (NEXT-1, extension of the paper's first-stage estimate: Eq.6
+ * for p = 1, Eq.7 first, Eq.8 middle, Eq.9 last stage with the final norm and
+ * the LM head; stage i holds min(m, p - i) in-flight microbatches, m =
+ * gbs/(d b) or unbounded when gbs = 0; the embedding input lives on stage 0).
+ * stage = ME_STAGE_ARGMAX returns the stage with the largest total (the first
+ * such stage) and stores its index in *which (may be NULL).  Stage 0 equals
+ * me_estimate.  Layers: stage 0 holds L0 (see me_parallel), the other stages
+ * split L - L0 as evenly as possible, earlier stages first.  ME_EINVAL for
+ * stage >= p. */
+int me_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,
+                      uint32_t* which);
 
 /* me_estimate_batch: n configurations, cfgs[i] against models[model_ids[i]]
  * (model_ids may be NULL: model 0).  Every array may be host or device memory

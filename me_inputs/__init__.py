@@ -52,6 +52,7 @@ class Space:
     gpus_per_node: int = 0
     thr_num: int = 4
     thr_den: int = 5
+    stage_max: int = 0  # 1 = NEXT-1: feasibility of the largest pipeline stage
     name: str = ""
 
     @property

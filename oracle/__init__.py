@@ -66,7 +66,7 @@ class SpaceC(ctypes.Structure):
                 ("mbs", _u32p), ("n_mbs", ctypes.c_uint32),
                 ("seq", _u32p), ("n_seq", ctypes.c_uint32),
                 ("rc_mask", ctypes.c_uint8), ("do_mask", ctypes.c_uint8),
-                ("uneven", ctypes.c_uint8), ("pad_", ctypes.c_uint8),
+                ("uneven", ctypes.c_uint8), ("stage_max", ctypes.c_uint8),
                 ("gbs", ctypes.c_uint32), ("max_t", ctypes.c_uint32), ("max_c", ctypes.c_uint32),
                 ("max_p", ctypes.c_uint32), ("thr_num", ctypes.c_uint32),
                 ("thr_den", ctypes.c_uint32)]
@@ -200,7 +200,7 @@ class _SpaceHolder:
         self.seq = (ctypes.c_uint32 * len(sp.seq))(*sp.seq)
         self.c = SpaceC(self.models, len(sp.models), self.world, len(sp.world), self.caps, len(cb),
                         sp.gpus_per_node, self.mbs, len(sp.mbs), self.seq, len(sp.seq),
-                        sp.rc_mask, sp.do_mask, sp.uneven, 0, sp.gbs, sp.max_t, sp.max_c,
+                        sp.rc_mask, sp.do_mask, sp.uneven, getattr(sp, "stage_max", 0), sp.gbs, sp.max_t, sp.max_c,
                         sp.max_p, sp.thr_num, sp.thr_den)
 
 

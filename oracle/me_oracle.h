@@ -64,7 +64,8 @@ typedef struct {
     uint32_t gpus_per_node;                      /* 0 = no t <= node filter */
     const uint32_t* mbs; uint32_t n_mbs;
     const uint32_t* seq; uint32_t n_seq;
-    uint8_t rc_mask, do_mask, uneven, pad_;      /* masks: bit0 = off, bit1 = on */
+    uint8_t rc_mask, do_mask, uneven, stage_max; /* masks: bit0 = off, bit1 = on;
+                                                    stage_max: 1 = largest pipeline stage (NEXT-1) */
     uint32_t gbs, max_t, max_c, max_p;           /* 0 = unlimited */
     uint32_t thr_num, thr_den;                   /* feasible <=> total*den <= cap*num */
 } or_space;

@@ -45,6 +45,18 @@ def me_estimate(shape, **cfg) -> Dict[str, int]:
     return {k: getattr(out, k) for k in TERMS}
 
 
+STAGE_ARGMAX = 0xFFFFFFFF
+
+
+def me_estimate_stage(shape, stage, **cfg):
+    """NEXT-1: terms of pipeline stage `stage` (or STAGE_ARGMAX: the largest);
+    returns (terms, stage index)."""
+    out, which = me_breakdown(), ctypes.c_uint32()
+    check(lib().me_estimate_stage(ctypes.byref(me_model(*shape)), ctypes.byref(_parallel(**cfg)), stage,
+                                  ctypes.byref(out), ctypes.byref(which)), "me_estimate_stage")
+    return {k: getattr(out, k) for k in TERMS}, which.value
+
+
 def me_estimate_batch(shapes: Sequence, ids, cfgs: Sequence[dict], caps_bytes=(), thr=(4, 5), stream=None):
     """Batched single estimates.  Returns (rows uint64[n, 7], cap_mask uint8[n], status uint8[n])."""
     n = len(cfgs)
@@ -75,7 +87,8 @@ class _SpaceC:
         self.seq = (ctypes.c_uint32 * len(sp.seq))(*sp.seq)
         self.mr = me_model_range(self.models, len(sp.models))
         self.cl = me_cluster(self.world, len(sp.world), self.caps, len(cb), sp.gpus_per_node)
-        self.cr = me_cfg_range(self.mbs, len(sp.mbs), self.seq, len(sp.seq), sp.rc_mask, sp.do_mask, sp.uneven, 0,
+        self.cr = me_cfg_range(self.mbs, len(sp.mbs), self.seq, len(sp.seq), sp.rc_mask, sp.do_mask, sp.uneven,
+                               getattr(sp, "stage_max", 0),
                                sp.gbs, sp.max_t, sp.max_c, sp.max_p)
         self.thr = me_threshold(sp.thr_num, sp.thr_den)
         self.n_cap = len(cb)

@@ -45,7 +45,7 @@ class me_cluster(ctypes.Structure):
 
 class me_cfg_range(ctypes.Structure):
     _fields_ = [("mbs", P(u32)), ("n_mbs", u32), ("seq", P(u32)), ("n_seq", u32),
-                ("recompute_mask", u8), ("dist_opt_mask", u8), ("allow_uneven_pp", u8), ("_pad", u8),
+                ("recompute_mask", u8), ("dist_opt_mask", u8), ("allow_uneven_pp", u8), ("stage_policy", u8),
                 ("gbs", u32), ("max_tp", u32), ("max_cp", u32), ("max_pp", u32)]
 
 
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(str(LIB_PATH))
         sigs = {
             "me_estimate": ([P(me_model), P(me_parallel), P(me_breakdown)], ctypes.c_int),
+            "me_estimate_stage": ([P(me_model), P(me_parallel), u32, P(me_breakdown), P(u32)], ctypes.c_int),
             "me_estimate_batch": ([ctypes.c_void_p, u32, ctypes.c_void_p, ctypes.c_void_p, u64, ctypes.c_void_p,
                                    u32, me_threshold, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p], ctypes.c_int),
@@ -120,7 +121,7 @@ def lib() -> ctypes.CDLL:
 
 
 # every symbol include/me.h declares (checked by tests/test_abi.py)
-EXPORTS = ("me_estimate", "me_estimate_batch", "me_space_size", "me_decode", "me_plan_create", "me_plan_size", "me_plan_table_bytes",
+EXPORTS = ("me_estimate", "me_estimate_stage", "me_estimate_batch", "me_space_size", "me_decode", "me_plan_create", "me_plan_size", "me_plan_table_bytes",
            "me_plan_sweep", "me_plan_free", "me_sweep", "me_result_counts", "me_result_cap_counts",
            "me_result_columns", "me_result_copy_to_host", "me_result_status", "me_result_wait",
            "me_result_timing", "me_result_free", "me_partition", "me_join_counts", "me_comm_unique_id", "me_comm_init", "me_comm_rank",

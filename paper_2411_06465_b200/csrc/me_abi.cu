@@ -181,12 +181,14 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     P->A.stream = (cudaStream_t)stream;
     const HostSpace& H = P->hs;
     DevSpace& D = P->ds;
-    me_model* dm;
+    DevModel* dm;
+    std::vector<DevModel> dmodels;
+    for (const me_model& m : H.models) dmodels.push_back(dev_model(m));
     uint32_t *dcls, *dlo, *dlt;
     uint64_t *dsp, *dlp;
     DevTuple* dtu;
     DevPair* dpr;
-    if ((st = upload(P->A, H.models, &dm)) || (P->owned.push_back(dm), false) ||
+    if ((st = upload(P->A, dmodels, &dm)) || (P->owned.push_back(dm), false) ||
         (st = upload(P->A, H.model_class, &dcls)) || (P->owned.push_back(dcls), false) ||
         (st = upload(P->A, H.seg_prefix, &dsp)) || (P->owned.push_back(dsp), false) ||
         (st = upload(P->A, H.list_off, &dlo)) || (P->owned.push_back(dlo), false) ||

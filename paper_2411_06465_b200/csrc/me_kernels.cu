@@ -55,10 +55,10 @@ struct LaneRow {
     uint32_t p;
 };
 
-__device__ __forceinline__ void make_lane_row(const me_model& M, uint32_t t, uint32_t c, uint32_t p, uint32_t d,
+__device__ __forceinline__ void make_lane_row(const DevModel& M, uint32_t t, uint32_t c, uint32_t p, uint32_t d,
                                               uint32_t rc, uint32_t dopt, LaneRow& L) {
     RowCoef R;
-    make_row(M, t, c, p, d, first_stage_layers_auto(M.layers, p), R);
+    make_row(M, t, c, p, d, p == 1 ? M.layers : div_u32(M.layers + p - 1, p), R);
     L.ms = dopt ? R.ms1 : R.ms0;
     L.a = (rc ? R.lam1 : R.lam0) + R.e8;
     L.b = rc ? R.bt + R.hc : R.hc;
@@ -76,19 +76,15 @@ struct Walker {
     uint32_t seg, j, jend, r, w;
     const uint2* pp;    // this lane's current (b, s) pair
     uint32_t rc, dopt;  // this lane's innermost digits (constant along its walk)
-    me_model M;
+    DevModel M;
     LaneRow L;
 
     __device__ __forceinline__ void enter_segment(const DevSpace& S, uint32_t s) {
         seg = s;
         const uint32_t m = s / S.n_world, n = s - m * S.n_world;
-        const uint32_t* mp = reinterpret_cast<const uint32_t*>(S.models + m);
-        M.hidden = __ldg(mp + 0);
-        M.ffn_hidden = __ldg(mp + 1);
-        M.layers = __ldg(mp + 2);
-        M.heads = __ldg(mp + 3);
-        M.kv_heads = __ldg(mp + 4);
-        M.vocab = __ldg(mp + 5);
+        const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(S.models + m));
+        const uint4 m1 = __ldg(reinterpret_cast<const uint4*>(S.models + m) + 1);
+        M = DevModel{m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, 0u};
         const uint32_t cls = __ldg(S.model_class + m);
         j = __ldg(S.list_off + cls * S.n_world + n);
         jend = __ldg(S.list_off + cls * S.n_world + n + 1);
@@ -498,7 +494,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__
 }
 
 // ---- single configurations ----------------------------------------------
-__device__ int estimate_one(const me_model& M, const me_parallel& P, me_breakdown& out) {
+__device__ int estimate_one(const me_model& Min, const me_parallel& P, me_breakdown& out) {
+    const me_model& M = Min;
     if (!M.hidden || !M.ffn_hidden || !M.layers || !M.heads || !M.kv_heads || !M.vocab)
         return ME_EINVAL;
     if (M.heads % M.kv_heads || M.hidden % M.heads) return ME_EINVAL;
@@ -521,13 +518,14 @@ __device__ int estimate_one(const me_model& M, const me_parallel& P, me_breakdow
     const uint32_t m = P.gbs ? (uint32_t)(P.gbs / ((uint64_t)d * P.mbs)) : 0xFFFFFFFFu;
     // exact shadow in 128 bits for the overflow verdict; the values returned
     // come from the same u64 code the sweep runs
+    const DevModel DM = dev_model(M);
     RowCoefT<unsigned __int128> W;
-    make_row(M, t, c, p, d, L0, W);
+    make_row(DM, t, c, p, d, L0, W);
     const TermsT<unsigned __int128> T2 = config_terms(W, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u);
     const unsigned __int128 lim = (unsigned __int128)1 << 63;
     if (W.psi >= lim || W.ms0 >= lim || T2.total >= lim) return ME_EOVERFLOW;
     RowCoef R;
-    make_row(M, t, c, p, d, L0, R);
+    make_row(DM, t, c, p, d, L0, R);
     const TermsT<uint64_t> T = config_terms(R, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u);
     out.params = T.params;
     out.grads = T.grads;

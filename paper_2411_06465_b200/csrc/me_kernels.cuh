@@ -11,9 +11,19 @@
 
 namespace me {
 
+// Device copy of a model shape with the head dimension h/a precomputed (32 B).
+struct DevModel {
+    uint32_t hidden, ffn_hidden, layers, heads, kv_heads, vocab, head_dim, _pad;
+};
+
+__host__ __device__ inline DevModel dev_model(const me_model& m) {
+    return DevModel{m.hidden, m.ffn_hidden, m.layers, m.heads, m.kv_heads, m.vocab,
+                    m.heads ? m.hidden / m.heads : 0u, 0u};
+}
+
 // Table pointers handed to the kernels (all device memory, read-only).
 struct DevSpace {
-    const me_model* models;
+    const DevModel* models;
     const uint32_t* model_class;
     const uint64_t* seg_prefix;   // n_seg + 1
     const uint32_t* list_off;     // n_class * n_world + 1
@@ -49,14 +59,32 @@ __host__ __device__ inline uint32_t first_stage_layers_auto(uint32_t L, uint32_t
     return (L + p - 1) / p;
 }
 
+// x / d, a shift when d is a power of two (every t, c, p of a power-of-two
+// world size)
+__device__ __forceinline__ uint32_t div_u32(uint32_t x, uint32_t d) {
+    return (d & (d - 1)) == 0 ? x >> (__ffs(d) - 1) : x / d;
+}
+
 // Row coefficients.  All divisions are exact under the validity rules
 // (t | k | a | h, t | v, t | h_ffn) except the optimizer ceil (R8).
 template <typename U>
-__device__ __forceinline__ void make_row(const me_model& M, uint32_t t, uint32_t c, uint32_t p,
+__device__ __forceinline__ void make_row(const DevModel& M, uint32_t t, uint32_t c, uint32_t p,
                                          uint32_t d, uint32_t L0, RowCoefT<U>& R) {
     const uint32_t h = M.hidden;
-    const uint32_t ht = h / t, kt = M.kv_heads / t, hd = h / M.heads, vt = M.vocab / t,
-                   ft = M.ffn_hidden / t;
+    const uint32_t hd = M.head_dim;
+    uint32_t ht, kt, vt, ft;
+    if ((t & (t - 1)) == 0) {
+        const uint32_t lt = __ffs(t) - 1;
+        ht = h >> lt;
+        kt = M.kv_heads >> lt;
+        vt = M.vocab >> lt;
+        ft = M.ffn_hidden >> lt;
+    } else {
+        ht = h / t;
+        kt = M.kv_heads / t;
+        vt = M.vocab / t;
+        ft = M.ffn_hidden / t;
+    }
     // per-layer shard: W_Q + W_O (2 h ht), W_K + W_V (2 h hd k/t), up/gate/down
     // (3 h h_ffn/t), two replicated RMSNorms (2h)  -- Eq.1, Eq.2, Eq.6
     const U per_layer = (U)2 * h * ht + (U)2 * h * hd * kt + (U)3 * h * ft + (U)2 * h;
