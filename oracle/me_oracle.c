@@ -577,7 +577,8 @@ static void walk(walk_t* w) {
                                         return;
                                     }
                                     or_breakdown r;
-                                    int st = or_estimate(m, &c, &r);
+                                    int st = sp->stage_max ? or_estimate_max(m, &c, &r, NULL)
+                                                           : or_estimate(m, &c, &r);
                                     if (st) { w->status = st; return; }
                                     uint32_t mask = or_cap_mask(r.total, sp->cap_bytes, sp->n_caps,
                                                                 sp->thr_num, sp->thr_den);
@@ -653,7 +654,8 @@ int or_points(const or_space* sp, const uint64_t* points, uint64_t n, or_breakdo
                                     c.rc = (uint8_t)rc; c.dopt = (uint8_t)dopt;
                                     c.uneven = sp->uneven;
                                     or_breakdown r;
-                                    st = or_estimate(m, &c, &r);
+                                    st = sp->stage_max ? or_estimate_max(m, &c, &r, NULL)
+                                                       : or_estimate(m, &c, &r);
                                     if (st) { free_tables(&T); return st; }
                                     if (rows) rows[k] = r;
                                     if (masks)

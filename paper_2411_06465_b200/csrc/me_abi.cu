@@ -106,7 +106,6 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t stage = 1;                     // write pass through aligned shared-memory staging (ME_WRITE_STAGE)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
     // of sub-range i (on the caller's stream).
@@ -214,6 +213,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.rcdo_do = H.rcdo_do;
     D.n_cap = (uint32_t)H.caps.size();
     D.gbs_mode = H.gbs ? 1u : 0u;
+    D.stage_max = H.stage_max ? 1u : 0u;
     for (int q = 0; q < 8; q++) D.thr[q] = 0;
     for (size_t q = 0; q < H.caps.size(); q++)
         D.thr[q] = (uint64_t)(((unsigned __int128)H.caps[q] * thr.num) / thr.den);
@@ -222,8 +222,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     P->max_spans = (uint32_t)P->sms * 96;
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
-    if (const char* e = getenv("ME_WRITE_STAGE")) P->stage = (uint32_t)atoi(e);
-    const int occ_c = sweep_blocks_per_sm(0, D.n_cap, false), occ_w = sweep_blocks_per_sm(2, D.n_cap, P->stage != 0);
+    const int occ_c = sweep_blocks_per_sm(0, D.n_cap), occ_w = sweep_blocks_per_sm(2, D.n_cap);
     P->write_bps = (uint32_t)(occ_w > 1 ? occ_w - 1 : 1);
     P->count_bps = (uint32_t)(occ_c - (int)P->write_bps > 0 ? occ_c - (int)P->write_bps : 1);
     if (const char* e = getenv("ME_WRITE_BPS")) P->write_bps = (uint32_t)atoi(e);
@@ -396,7 +395,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             cudaEventRecord(tev[3], st);
             if (write) {
                 ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_rel, sc.tile_cnt,
-                                  sc.span_off, o->mode, P->stage != 0, cols, capacity, st);
+                                  sc.span_off, o->mode, cols, capacity, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "write kernel");
             }
             cudaEventRecord(tev[4], st);
@@ -695,6 +694,37 @@ extern "C" int me_estimate_batch(const me_model* models, uint32_t n_models, cons
     for (uint64_t i = 0; i < n; i++)
         if (hstat[i]) { first_bad = hstat[i]; break; }
     if (!status && first_bad) return err(first_bad, "a configuration failed its preconditions");
+    return ME_OK;
+}
+
+extern "C" int me_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,
+                                 uint32_t* which) {
+    if (!model || !cfg || !out) return err(ME_EINVAL, "null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return err(ME_ECUDA, "no CUDA device");
+    }
+    struct Buf {
+        me_model m;
+        me_parallel c;
+        me_breakdown b;
+        uint32_t which;
+        int status;
+    };
+    Buf h{};
+    h.m = *model;
+    h.c = *cfg;
+    Buf* d = nullptr;
+    CU(cudaMalloc(&d, sizeof(Buf)));
+    cudaError_t ce = cudaMemcpy(d, &h, sizeof(Buf), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = launch_estimate_stage(&d->m, &d->c, stage, &d->b, &d->which, &d->status, nullptr);
+    if (ce == cudaSuccess) ce = cudaMemcpy(&h, d, sizeof(Buf), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (ce != cudaSuccess) return cuda_err(ce, "me_estimate_stage");
+    if (h.status) return err(h.status, "estimator precondition failed");
+    *out = h.b;
+    if (which) *which = h.which;
     return ME_OK;
 }
 

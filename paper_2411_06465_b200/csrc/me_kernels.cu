@@ -53,12 +53,29 @@ struct LaneRow {
     uint64_t lam, mu;   // per-token layer bytes = n_inf * lam + mu
     uint64_t e8, hc;    // per-token embedding bytes = n_inf * e8; head bytes = hc
     uint32_t p;
+    // NEXT-1 (stage_max): the last pipeline stage (p >= 2), one microbatch in
+    // flight: total = msL + u * kL, layers = u * layL, head = u * hcL
+    bool two;
+    uint64_t msL, kL, psiL, optimL, layL, hcL;
 };
 
 __device__ __forceinline__ void make_lane_row(const DevModel& M, uint32_t t, uint32_t c, uint32_t p, uint32_t d,
-                                              uint32_t rc, uint32_t dopt, LaneRow& L) {
+                                              uint32_t rc, uint32_t dopt, bool stage_max, LaneRow& L) {
     RowCoef R;
-    make_row(M, t, c, p, d, p == 1 ? M.layers : div_u32(M.layers + p - 1, p), R);
+    const uint32_t L0 = p == 1 ? M.layers : div_u32(M.layers + p - 1, p);
+    make_row(M, t, c, p, d, L0, R);
+    L.two = stage_max && p >= 2;
+    if (L.two) {
+        // the last stage holds floor((L - L0) / (p - 1)) layers
+        const uint32_t Ll = (M.layers - L0) / (p - 1);
+        const TermsT<uint64_t> T = stage_terms<uint64_t>(M, t, c, d, false, true, Ll, 1u, 1u, rc, dopt);
+        L.psiL = T.params >> 1;
+        L.optimL = T.optim;
+        L.msL = T.params + T.grads + T.optim;
+        L.layL = T.layers;
+        L.hcL = T.head;
+        L.kL = T.layers + T.head;
+    }
     L.ms = dopt ? R.ms1 : R.ms0;
     L.a = (rc ? R.lam1 : R.lam0) + R.e8;
     L.b = rc ? R.bt + R.hc : R.hc;
@@ -96,7 +113,7 @@ struct Walker {
         const uint2 b = __ldg(reinterpret_cast<const uint2*>(S.tuples + tid) + 2);  // w pair_off
         w = b.x;
         pp = reinterpret_cast<const uint2*>(S.pairs) + b.y + (r >> S.lg_rcdo);
-        make_lane_row(M, a.x, a.y, a.z, a.w, rc, dopt, L);
+        make_lane_row(M, a.x, a.y, a.z, a.w, rc, dopt, S.stage_max != 0, L);
     }
 
     __device__ __forceinline__ void set_digits(const DevSpace& S) {
@@ -188,57 +205,23 @@ struct CapAcc {
     }
 };
 
-// Shared-memory staging of a warp's survivor columns (write pass): the
-// survivors of a round are put into a 64-entry ring per column and leave it in
-// whole, aligned 128-byte lines (one full-warp 256-byte store per column per 32
-// rows); only the first and last line of a tile's output can be partial.
-// Measured on B200 (scripts/storebench.cu): aligned full-warp column stores
-// reach 5.7-6.1 TB/s, unaligned or partial ones 4.0-4.2 TB/s.  The write
-// kernel can also store directly from the lanes (ME_WRITE_STAGE=0).
-template <int NC>
-struct Stager {
-    uint64_t* buf;      // NC x 64 ring entries of this warp
-    uint32_t head = 0, pend = 0;
-    uint64_t grow = 0;  // output row of the first pending entry
-    __device__ __forceinline__ void put(uint32_t slot, uint32_t col, uint64_t v) {
-        buf[col * 64 + ((head + pend + slot) & 63u)] = v;
-    }
-    __device__ __forceinline__ void flush(const Cols& cols, uint64_t capacity, uint32_t lane, uint32_t n) {
-        __syncwarp();
-        if (lane < n) {
-            const uint32_t idx = (head + lane) & 63u;
-            const uint64_t row = grow + lane;
-            if (row < capacity) {
-#pragma unroll
-                for (int c = 0; c < NC; c++) cols.c[c][row] = buf[c * 64 + idx];
-            }
-        }
-        __syncwarp();
-        head = (head + n) & 63u;
-        pend -= n;
-        grow += n;
-    }
-    // store what can go out in whole 128-byte lines: first the rows up to the
-    // next line boundary, then groups of 32 rows (two full lines per column)
-    __device__ __forceinline__ void drain(const Cols& cols, uint64_t capacity, uint32_t lane) {
-        if (grow & 15u) {
-            const uint32_t a = 16u - (uint32_t)(grow & 15u);
-            if (pend < a) return;
-            flush(cols, capacity, lane, a);
-        }
-        while (pend >= 32) flush(cols, capacity, lane, 32);
-    }
-};
-
 // Evaluate one tile's rounds starting at the walker's position (lane's index
 // = pos).  RAGGED: the tile is cut by lo/hi (first or last tile of a range).
-// GBS: a global batch bounds the in-flight microbatches (R17).  Returns with
+// GBS: a global batch bounds the in-flight microbatches (R17).  STMAX: the
+// largest pipeline stage decides (NEXT-1; middle stages never exceed stage 0,
+// so the larger of stage 0 and the last stage is the maximum).  Returns with
 // the walker on the first index after the tile when `advance_out`.
-template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STAGE>
+//
+// Write pass stores: each surviving lane stores its 8-byte value of every
+// column at its row; a round's rows are contiguous.  (Measured alternatives on
+// B200, scripts/storebench.cu and DESIGN.md §6: shared-memory staging into
+// aligned full-line stores lifts the store pattern itself from ~4.1 to ~5.7
+// TB/s but costs more issue slots than it saves in this kernel.)
+template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX>
 __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
                                              uint64_t hi, uint32_t rounds, uint32_t lane, CapAcc<NCAP>& acc,
                                              uint64_t out, const Cols& cols, uint64_t capacity,
-                                             bool advance_out, Stager<MODE == 2 ? 8 : 1>* sg) {
+                                             bool advance_out) {
     constexpr int NC = MODE == 2 ? 8 : 1;
     const uint32_t pstep = 32u >> S.lg_rcdo;
     uint32_t cnt = 0;
@@ -252,7 +235,13 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
         const uint32_t u = pr.x;
         const uint32_t n_inf = GBS ? min(W.L.p, pr.y) : W.L.p;
         const uint64_t K = GBS ? (uint64_t)n_inf * W.L.a + W.L.b : W.L.kp;
-        const uint64_t total = W.L.ms + (uint64_t)u * K;
+        uint64_t total = W.L.ms + (uint64_t)u * K;
+        bool last = false;
+        if (STMAX && W.L.two) {
+            const uint64_t tl = W.L.msL + (uint64_t)u * W.L.kL;
+            last = tl > total;
+            total = last ? tl : total;
+        }
         const bool act = !RAGGED || (pos >= lo && pos < hi);
         const uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
         if (MODE == 0) {
@@ -260,28 +249,21 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
             acc.add(mask);
         } else {
             const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
-            const uint32_t rank = __popc(ballot & ((1u << lane) - 1u));
-            uint64_t v[NC];
-            v[0] = pos | ((uint64_t)mask << 56);
-            if (MODE == 2) {
-                v[1] = 2ull * W.L.psi;
-                v[2] = 4ull * W.L.psi;
-                v[3] = W.L.optim;
-                v[4] = (uint64_t)u * ((uint64_t)n_inf * W.L.lam + W.L.mu);
-                v[5] = (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
-                v[6] = (uint64_t)u * W.L.hc;
-                v[7] = total;
-            }
-            if (STAGE) {
-                if (mask) {
-#pragma unroll
-                    for (int c = 0; c < NC; c++) sg->put(rank, c, v[c]);
-                }
-                sg->pend += __popc(ballot);
-                if (sg->pend >= 16) sg->drain(cols, capacity, lane);
-            } else if (mask) {
-                const uint64_t o = out + rank;
+            if (mask) {
+                const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
                 if (o < capacity) {
+                    uint64_t v[NC];
+                    v[0] = pos | ((uint64_t)mask << 56);
+                    if (MODE == 2) {
+                        const uint64_t psi = STMAX && last ? W.L.psiL : W.L.psi;
+                        v[1] = 2ull * psi;
+                        v[2] = 4ull * psi;
+                        v[3] = STMAX && last ? W.L.optimL : W.L.optim;
+                        v[4] = (uint64_t)u * (STMAX && last ? W.L.layL : (uint64_t)n_inf * W.L.lam + W.L.mu);
+                        v[5] = STMAX && last ? 0ull : (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
+                        v[6] = (uint64_t)u * (STMAX && last ? W.L.hcL : W.L.hc);
+                        v[7] = total;
+                    }
 #pragma unroll
                     for (int c = 0; c < NC; c++) cols.c[c][o] = v[c];
                 }
@@ -325,8 +307,9 @@ __device__ __forceinline__ TileGeom geom(uint64_t lo, uint64_t hi) {
 }
 
 // count pass over span s = tiles [t0, t1): per tile its checkpoint
-// {seg, j, r, s} and its first survivor's rank inside the span; the span total
-template <int NCAP, bool GBS>
+// {seg, j, r, s}, its survivor count and its first survivor's rank inside the
+// span; returns the span total
+template <int NCAP, bool GBS, bool STMAX>
 __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom& G, uint32_t s, uint32_t t0,
                                                uint32_t t1, uint32_t lane, uint32_t* __restrict__ tile_rel,
                                                uint32_t* __restrict__ tile_cnt, uint4* __restrict__ tile_ck,
@@ -337,7 +320,6 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
     const uint64_t p0 = G.start(t0) + lane;
     W.seek(S, p0 < G.hi ? p0 : G.hi - 1);
     uint32_t run = 0;
-    Stager<1>* nosg = nullptr;
     for (uint32_t t = t0; t < t1; t++) {
         const uint64_t ts = G.start(t);
         if (lane == 0) {  // lane 0 is at the tile's first index
@@ -347,11 +329,11 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
         const bool last = t + 1 == t1;
         uint32_t cnt;
         if (G.ragged(t))
-            cnt = run_tile<0, NCAP, true, GBS, false>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{},
-                                                      0, !last, nosg);
+            cnt = run_tile<0, NCAP, true, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{},
+                                                      0, !last);
         else
-            cnt = run_tile<0, NCAP, false, GBS, false>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
-                                                       Cols{}, 0, !last, nosg);
+            cnt = run_tile<0, NCAP, false, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
+                                                       Cols{}, 0, !last);
         acc.flush();
         cnt = __reduce_add_sync(0xffffffffu, cnt);
         if (lane == 0) tile_cnt[t] = cnt;
@@ -362,10 +344,11 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
 
 template <int NCAP>
 __global__ void __launch_bounds__(kThreads, 4) count_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
-                                                         const uint32_t n_spans, uint32_t* __restrict__ tile_rel,
-                                                         uint32_t* __restrict__ tile_cnt, uint4* __restrict__ tile_ck,
-                                                         uint32_t* __restrict__ span_count,
-                                                         uint32_t* __restrict__ span_caps) {
+                                                            const uint32_t n_spans, uint32_t* __restrict__ tile_rel,
+                                                            uint32_t* __restrict__ tile_cnt,
+                                                            uint4* __restrict__ tile_ck,
+                                                            uint32_t* __restrict__ span_count,
+                                                            uint32_t* __restrict__ span_caps) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
     const TileGeom G = geom(lo, hi);
@@ -375,8 +358,13 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const DevSpace S, co
         CapAcc<NCAP> acc;
         uint32_t n = 0;
         if (t0 < t1) {
-            if (S.gbs_mode) n = count_span<NCAP, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
-            else n = count_span<NCAP, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+            if (S.stage_max) {
+                if (S.gbs_mode) n = count_span<NCAP, true, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+                else n = count_span<NCAP, false, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+            } else {
+                if (S.gbs_mode) n = count_span<NCAP, true, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+                else n = count_span<NCAP, false, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+            }
         }
         if (lane == 0) span_count[s] = n;
 #pragma unroll
@@ -387,53 +375,47 @@ __global__ void __launch_bounds__(kThreads, 4) count_kernel(const DevSpace S, co
     }
 }
 
-// write pass: tiles in grid-stride order
-template <int MODE, int NCAP, bool STAGE>
+template <int MODE, int NCAP, bool GBS, bool STMAX>
+__device__ __forceinline__ void write_tile(const DevSpace& S, const TileGeom& G, Walker& W, uint32_t t, uint64_t pos,
+                                           uint32_t lane, uint64_t out, const Cols& cols, uint64_t capacity) {
+    CapAcc<NCAP> none;
+    if (G.ragged(t))
+        run_tile<MODE, NCAP, true, GBS, STMAX>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols, capacity,
+                                               false);
+    else
+        run_tile<MODE, NCAP, false, GBS, STMAX>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols, capacity,
+                                                false);
+}
+
+// write pass: tiles in grid-stride order (at any moment the grid writes one
+// compact window of the output columns)
+template <int MODE, int NCAP>
 __global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
-                                                         const uint4* __restrict__ tile_ck,
-                                                         const uint32_t* __restrict__ tile_rel,
-                                                         const uint32_t* __restrict__ tile_cnt,
-                                                         const uint64_t* __restrict__ span_off, const Cols cols,
-                                                         const uint64_t capacity) {
-    constexpr int NC = MODE == 2 ? 8 : 1;
-    __shared__ uint64_t s_stage[STAGE ? kWarpsPerBlock * NC * 64 : 1];
+                                                            const uint4* __restrict__ tile_ck,
+                                                            const uint32_t* __restrict__ tile_rel,
+                                                            const uint32_t* __restrict__ tile_cnt,
+                                                            const uint64_t* __restrict__ span_off, const Cols cols,
+                                                            const uint64_t capacity) {
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
     const TileGeom G = geom(lo, hi);
-    CapAcc<NCAP> none;
-    Stager<NC> sg;
-    sg.buf = s_stage + (STAGE ? wid * NC * 64 : 0);
     for (uint32_t t = blockIdx.x * kWarpsPerBlock + wid; t < G.n_tiles; t += n_warps) {
         if (__ldg(tile_cnt + t) == 0) continue;  // no survivor: nothing to write
         const uint64_t ts = G.start(t);
         const uint64_t pos = ts + lane;
         const uint4 ck = __ldg(tile_ck + t);
         const uint64_t out = __ldg(span_off + ck.w) + __ldg(tile_rel + t);
-        sg.head = 0;
-        sg.pend = 0;
-        sg.grow = out;
         Walker W;
-        const bool ragged = G.ragged(t);
         // a lane past the end of the range is parked on the last index: it
         // takes part in the ballots with inactive positions
         W.restore(S, ck, pos < hi ? lane : (uint32_t)(hi - 1 - ts));
-        if (ragged) {
-            if (S.gbs_mode)
-                run_tile<MODE, NCAP, true, true, STAGE>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
-                                                        capacity, false, &sg);
-            else
-                run_tile<MODE, NCAP, true, false, STAGE>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
-                                                         capacity, false, &sg);
+        if (S.stage_max) {
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, true>(S, G, W, t, pos, lane, out, cols, capacity);
+            else write_tile<MODE, NCAP, false, true>(S, G, W, t, pos, lane, out, cols, capacity);
         } else {
-            if (S.gbs_mode)
-                run_tile<MODE, NCAP, false, true, STAGE>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
-                                                         capacity, false, &sg);
-            else
-                run_tile<MODE, NCAP, false, false, STAGE>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
-                                                          capacity, false, &sg);
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, false>(S, G, W, t, pos, lane, out, cols, capacity);
+            else write_tile<MODE, NCAP, false, false>(S, G, W, t, pos, lane, out, cols, capacity);
         }
-        if (STAGE)
-            while (sg.pend) sg.flush(cols, capacity, lane, sg.pend < 32 ? sg.pend : 32u);
     }
 }
 
@@ -537,6 +519,50 @@ __device__ int estimate_one(const me_model& Min, const me_parallel& P, me_breakd
     return ME_OK;
 }
 
+// NEXT-1: stage `stage` of one configuration, or the largest stage (the first
+// of equal totals) when stage == 0xFFFFFFFF
+__device__ int estimate_stage_one(const me_model& M, const me_parallel& P, uint32_t stage, me_breakdown& out,
+                                  uint32_t& which) {
+    me_breakdown b0;
+    int st = estimate_one(M, P, b0);  // preconditions, overflow of stage 0
+    if (st) return st;
+    const uint32_t t = P.tp, c = P.cp, p = P.pp, d = P.dp, L = M.layers;
+    if (stage != 0xFFFFFFFFu && stage >= p) return ME_EINVAL;
+    const uint32_t L0 = P.first_stage_layers ? P.first_stage_layers : first_stage_layers_auto(L, p);
+    const uint32_t u = (P.seq / c) * P.mbs;
+    const uint64_t m = P.gbs ? P.gbs / ((uint64_t)d * P.mbs) : 0xFFFFFFFFull;
+    const DevModel DM = dev_model(M);
+    const unsigned __int128 lim = (unsigned __int128)1 << 63;
+    uint32_t lo = stage == 0xFFFFFFFFu ? 0 : stage, hi = stage == 0xFFFFFFFFu ? p : stage + 1;
+    bool have = false;
+    for (uint32_t i = lo; i < hi; i++) {
+        // stage 0 holds L0; the others split L - L0 evenly, earlier stages first
+        const uint32_t Li = i == 0 ? L0 : (L - L0) / (p - 1) + ((i - 1) < (L - L0) % (p - 1) ? 1u : 0u);
+        const uint32_t n_i = (uint32_t)((uint64_t)(p - i) < m ? (uint64_t)(p - i) : m);
+        const uint32_t rc = P.recompute ? 1u : 0u, dopt = P.dist_opt ? 1u : 0u;
+        const TermsT<unsigned __int128> W = stage_terms<unsigned __int128>(DM, t, c, d, i == 0, i == p - 1, Li, n_i,
+                                                                           u, rc, dopt);
+        if (W.total >= lim) return ME_EOVERFLOW;
+        const TermsT<uint64_t> T = stage_terms<uint64_t>(DM, t, c, d, i == 0, i == p - 1, Li, n_i, u, rc, dopt);
+        if (!have || T.total > out.total) {
+            out = me_breakdown{T.params, T.grads, T.optim, T.layers, T.embed, T.head, T.total};
+            which = i;
+            have = true;
+        }
+    }
+    return ME_OK;
+}
+
+__global__ void estimate_stage_kernel(const me_model* __restrict__ model, const me_parallel* __restrict__ cfg,
+                                      uint32_t stage, me_breakdown* __restrict__ out, uint32_t* __restrict__ which,
+                                      int* __restrict__ status) {
+    me_breakdown b = {0, 0, 0, 0, 0, 0, 0};
+    uint32_t w = 0;
+    *status = estimate_stage_one(*model, *cfg, stage, b, w);
+    *out = b;
+    *which = w;
+}
+
 __global__ void estimate_kernel(const me_model* __restrict__ models, uint32_t n_models,
                                 const uint32_t* __restrict__ ids,
                                 const me_parallel* __restrict__ cfgs, uint64_t n,
@@ -568,19 +594,18 @@ void* count_kernel_for(uint32_t n_cap) {
     }
 }
 
-template <int MODE, bool STAGE>
+template <int MODE>
 void* write_kernel_for(uint32_t n_cap) {
     switch (ncap_stride_(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1, STAGE>);
-        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2, STAGE>);
-        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4, STAGE>);
-        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8, STAGE>);
+        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1>);
+        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2>);
+        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4>);
+        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8>);
     }
 }
 
-void* write_fn(me_out_mode mode, uint32_t n_cap, bool stage) {
-    if (mode == ME_OUT_FULL) return stage ? write_kernel_for<2, true>(n_cap) : write_kernel_for<2, false>(n_cap);
-    return stage ? write_kernel_for<1, true>(n_cap) : write_kernel_for<1, false>(n_cap);
+void* write_fn(me_out_mode mode, uint32_t n_cap) {
+    return mode == ME_OUT_FULL ? write_kernel_for<2>(n_cap) : write_kernel_for<1>(n_cap);
 }
 
 }  // namespace
@@ -592,8 +617,8 @@ uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
     return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
 }
 
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool stage) {
-    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX, n_cap, stage);
+int sweep_blocks_per_sm(int pass, uint32_t n_cap) {
+    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX, n_cap);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
@@ -616,10 +641,16 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, bool stage, Cols cols, uint64_t capacity, cudaStream_t st) {
+                         me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st) {
     void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
                     (void*)&tile_cnt, (void*)&span_off, (void*)&cols, (void*)&capacity};
-    return cudaLaunchKernel(write_fn(mode, S.n_cap, stage), dim3(n_blocks), dim3(kThreads), args, 0, st);
+    return cudaLaunchKernel(write_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
+}
+
+cudaError_t launch_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,
+                                  uint32_t* which, int* status, cudaStream_t st) {
+    estimate_stage_kernel<<<1, 1, 0, st>>>(model, cfg, stage, out, which, status);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,

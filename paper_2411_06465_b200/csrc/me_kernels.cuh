@@ -35,6 +35,7 @@ struct DevSpace {
     uint32_t lg_rcdo, rcdo_rc, rcdo_do;
     uint32_t n_cap;
     uint32_t gbs_mode;            // 1 = a global batch bounds the in-flight microbatches (R17)
+    uint32_t stage_max;           // 1 = feasibility of the largest pipeline stage (NEXT-1)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
 };
 
@@ -114,6 +115,35 @@ struct TermsT {
     U params, grads, optim, layers, embed, head, total;
 };
 
+// NEXT-1: the six terms of pipeline stage i holding Li layers and n_i in-flight
+// microbatches -- Eq.6 (single stage), Eq.7 (first), Eq.8 (middle), Eq.9
+// (last: the final norm and the LM head); embedding input on the first stage,
+// LM-head activations on the last.  For the first stage this is make_row +
+// config_terms term by term.
+template <typename U>
+__device__ __forceinline__ TermsT<U> stage_terms(const DevModel& M, uint32_t t, uint32_t c, uint32_t d, bool first,
+                                                 bool last, uint32_t Li, uint32_t n_i, uint32_t u, uint32_t rc,
+                                                 uint32_t dopt) {
+    const uint32_t h = M.hidden, hd = M.head_dim;
+    const uint32_t ht = div_u32(h, t), kt = div_u32(M.kv_heads, t), vt = div_u32(M.vocab, t),
+                   ft = div_u32(M.ffn_hidden, t);
+    const U per_layer = (U)2 * h * ht + (U)2 * h * hd * kt + (U)3 * h * ft + (U)2 * h;
+    const U ends = first && last ? (U)2 * h * vt + h : (first ? (U)h * vt : (last ? (U)h * vt + h : (U)0));
+    const U psi = ends + (U)Li * per_layer;
+    const uint32_t dc = d * c;
+    const U share = (psi + dc - 1) / dc;
+    const U bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft;
+    TermsT<U> T;
+    T.params = (U)2 * psi;
+    T.grads = (U)4 * psi;
+    T.optim = dopt ? (U)12 * share : (U)12 * psi;
+    T.layers = (U)u * (rc ? (U)2 * ht * n_i * Li + bt : (U)n_i * Li * bt);
+    T.embed = first ? (U)u * ((U)8 * ht * n_i) : (U)0;
+    T.head = last ? (U)u * ((U)4 * ((U)ht + vt) * n_i) : (U)0;
+    T.total = T.params + T.grads + T.optim + T.layers + T.embed + T.head;
+    return T;
+}
+
 // total only (count pass): model states + u * (n_inf * a_rc + b_rc)
 __device__ __forceinline__ uint64_t config_total(const RowCoef& R, uint32_t u, uint32_t m,
                                                  uint32_t rc, uint32_t dopt) {
@@ -173,7 +203,7 @@ uint32_t ncap_stride(uint32_t n_cap);
 // tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
 uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
 // resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool stage);
+int sweep_blocks_per_sm(int pass, uint32_t n_cap);
 // count pass over [lo, hi) cut into n_spans spans of whole tiles: per tile its
 // walker checkpoint {seg, j, r, span} and the rank of its first survivor in the
 // span; per span its survivor count and per-capacity counts
@@ -184,10 +214,13 @@ cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st);
 // write pass over [lo, hi): survivors of tile t stored from row
-// span_off[span(t)] + tile_rel[t]; stage = through shared-memory staging
+// span_off[span(t)] + tile_rel[t]
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, bool stage, Cols cols, uint64_t capacity, cudaStream_t st);
+                         me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st);
+// one configuration, one stage or (stage = 0xFFFFFFFF) the largest stage (NEXT-1)
+cudaError_t launch_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,
+                                  uint32_t* which, int* status, cudaStream_t st);
 // single configurations (me_estimate / me_estimate_batch)
 cudaError_t launch_estimate(const me_model* models, uint32_t n_models, const uint32_t* ids,
                             const me_parallel* cfgs, uint64_t n, const uint64_t* thr,

@@ -37,6 +37,8 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
     rc_mask = cr->recompute_mask;
     do_mask = cr->dist_opt_mask;
     uneven = cr->allow_uneven_pp ? 1 : 0;
+    if (cr->stage_policy > 1) return fail(detail, ME_EINVAL, "stage_policy must be 0 or 1");
+    stage_max = cr->stage_policy;
 
     for (size_t i = 0; i < models.size(); i++) {
         const me_model& m = models[i];

@@ -238,3 +238,51 @@ def test_full_size_sampled(me, oracle_mod, name):
         for q, k in enumerate(ks):
             assert [int(t[k]) for t in tot] == o_rows[q].tolist(), int(index[k])
             assert int(mask[k]) == int(o_masks[q])
+
+
+# ---------------------------------------------------------------- NEXT-1: every stage
+def test_estimate_stage_matches_oracle(me, oracle_mod):
+    rng = np.random.default_rng(17)
+    shapes = mi.random_models(12, seed=13) + [mi.PRESETS["llama3.1-8b"], (1024, 2816, 16, 8, 8, 256000)]
+    for shape in shapes:
+        h, f, L, a, k, v = shape
+        for _ in range(25):
+            p = int(rng.integers(1, L + 1))
+            cfg = dict(d=int(rng.integers(1, 17)), t=1, p=p, c=int(rng.choice([1, 2])), b=int(rng.integers(1, 5)),
+                       s=int(rng.choice([4096, 8192])), gbs=int(rng.choice([0, 0, 64, 1024])),
+                       rc=int(rng.integers(0, 2)), dopt=int(rng.integers(0, 2)), uneven=1)
+            if cfg["gbs"] and cfg["gbs"] % (cfg["d"] * cfg["b"]):
+                cfg["gbs"] = 0
+            for i in sorted({0, p - 1, int(rng.integers(0, p))}):
+                got, which = me.me_estimate_stage(shape, i, **cfg)
+                assert which == i
+                assert got == oracle_mod.estimate_stage(shape, i, **cfg), (shape, cfg, i)
+            got, which = me.me_estimate_stage(shape, me.STAGE_ARGMAX, **cfg)
+            ref, arg = oracle_mod.estimate_max(shape, **cfg)
+            assert (got, which) == (ref, arg), (shape, cfg)
+    with pytest.raises(me.MEError):
+        me.me_estimate_stage(mi.PRESETS["llama3.1-8b"], 4, d=1, t=1, p=4, c=1, b=1, s=8192)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2], ids=["count", "index", "full"])
+@pytest.mark.parametrize("name", ["C3u", "gbs", "rand"])
+def test_sweep_stage_max(me, oracle_mod, name, mode):
+    """NEXT-1 sweeps: feasibility of the largest pipeline stage."""
+    if name == "C3u":
+        sp = mi.config("C3", uneven=1, stage_max=1)
+    elif name == "gbs":
+        sp = mi.Space(models=mi.random_models(5, seed=21, small=True), world=[6, 8, 12, 24], caps_gb=[1, 2, 4],
+                      mbs=[1, 2, 3], seq=[8, 12, 16, 24], gbs=96, uneven=1, thr_num=9, thr_den=10, stage_max=1)
+    else:
+        sp = mi.Space(models=mi.random_models(20, seed=23) + [(1024, 2816, 16, 8, 8, 256000)],
+                      world=[8, 24, 64], caps_gb=[24, 40, 80, 192], mbs=[1, 2, 8], seq=[4096, 32768],
+                      uneven=1, stage_max=1)
+    plan = me.Plan(sp)
+    res = plan.sweep(mode=mode)
+    assert res.status() == 0
+    assert_same(me, res, *oracle_rows(oracle_mod, sp), mode)
+    # the first-stage sweep of the same space differs (the last stage binds somewhere)
+    if name == "rand":
+        import dataclasses
+        r0 = me.Plan(dataclasses.replace(sp, stage_max=0)).sweep(mode=me.ME_OUT_COUNT)
+        assert r0.counts()[0] != res.counts()[0]
