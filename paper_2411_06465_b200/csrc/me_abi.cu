@@ -106,7 +106,8 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t bulk = 1;                      // write pass through shared memory + bulk copies (ME_WRITE_BULK)
+    uint32_t bulk = 0;                      // write pass through shared memory + bulk copies (ME_WRITE_BULK=1)
+    uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
     // of sub-range i (on the caller's stream).
@@ -224,6 +225,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     P->max_spans = (uint32_t)P->sms * 96;
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
     if (const char* e = getenv("ME_WRITE_BULK")) P->bulk = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
     const int occ_c = sweep_blocks_per_sm(0, D.n_cap, false), occ_w = sweep_blocks_per_sm(2, D.n_cap, P->bulk != 0);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
@@ -378,9 +380,12 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             me_plan::Scratch& sc = P->scratch[P->turn++ & 1];
             const uint32_t n_tiles = n_tiles_of(lo, hi);
             const uint32_t n_spans = n_tiles < P->max_spans ? n_tiles : P->max_spans;
+            // grid_mode 0: persistent grids of bps resident blocks per SM;
+            // 1: one unit (span / tile) per warp, so the block scheduler
+            // interleaves the blocks of the concurrent count and write passes
             auto grid = [&](uint32_t bps, uint32_t units) {
                 uint32_t gb = (uint32_t)P->sms * bps, need = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
-                return gb < need ? gb : need;
+                return P->grid_mode || gb > need ? need : gb;
             };
             cudaEvent_t tev[5];
             for (auto& x : tev) {
