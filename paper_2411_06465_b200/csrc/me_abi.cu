@@ -217,8 +217,11 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.gbs_mode = H.gbs ? 1u : 0u;
     D.stage_max = H.stage_max ? 1u : 0u;
     for (int q = 0; q < 8; q++) D.thr[q] = 0;
-    for (size_t q = 0; q < H.caps.size(); q++)
+    D.thr_max = 0;
+    for (size_t q = 0; q < H.caps.size(); q++) {
         D.thr[q] = (uint64_t)(((unsigned __int128)H.caps[q] * thr.num) / thr.den);
+        if (q == 0 || D.thr[q] > D.thr_max) D.thr_max = D.thr[q];
+    }
     // launch shape: spans = 96 per SM (divisible by every grid of 1..4
     // resident 8-warp blocks per SM, so the grid-stride over spans is even)
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);

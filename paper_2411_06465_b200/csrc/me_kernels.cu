@@ -180,28 +180,13 @@ __device__ __forceinline__ uint32_t cap_mask(const DevSpace& S, uint64_t total) 
     return mask;
 }
 
-// 8-bit packed per-capacity counters (mask * 0x00204081 spreads bits 0..3 to
-// bytes 0..3); flushed to 32-bit counters every tile (16 rounds < 256)
+// per-lane survivor counters per capacity (count pass)
 template <int NCAP>
 struct CapAcc {
-    uint32_t lo = 0, hi = 0;
     uint32_t capc[NCAP];
     __device__ __forceinline__ CapAcc() {
 #pragma unroll
         for (int q = 0; q < NCAP; q++) capc[q] = 0;
-    }
-    __device__ __forceinline__ void add(uint32_t mask) {
-        if (NCAP <= 4) {
-            lo += (mask * 0x00204081u) & 0x01010101u;
-        } else {
-            lo += ((mask & 15u) * 0x00204081u) & 0x01010101u;
-            hi += ((mask >> 4) * 0x00204081u) & 0x01010101u;
-        }
-    }
-    __device__ __forceinline__ void flush() {
-#pragma unroll
-        for (int q = 0; q < NCAP; q++) capc[q] += ((q < 4 ? lo : hi) >> (8 * (q & 3))) & 255u;
-        lo = hi = 0;
     }
 };
 
@@ -280,6 +265,7 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
                                              uint64_t out, const Cols& cols, uint64_t capacity,
                                              bool advance_out, BulkStager<MODE == 2 ? 8 : 1>* bs = nullptr) {
     constexpr int NC = MODE == 2 ? 8 : 1;
+    constexpr bool PREFETCH = MODE != 0;  // the write pass hides the pair load behind a round
     const uint32_t pstep = 32u >> S.lg_rcdo;
     uint32_t cnt = 0;
     uint2 pr = __ldg(W.pp);
@@ -287,7 +273,7 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
         const bool more = (it + 1 < rounds) || advance_out;
         const bool in_row = W.r + 32 < W.w;
         uint2 prn = pr;
-        if (in_row && more) prn = __ldg(W.pp + pstep);  // next round's pair, issued early
+        if (PREFETCH && in_row && more) prn = __ldg(W.pp + pstep);  // next round's pair, issued early
 
         const uint32_t u = pr.x;
         const uint32_t n_inf = GBS ? min(W.L.p, pr.y) : W.L.p;
@@ -300,11 +286,16 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
             total = last ? tl : total;
         }
         const bool act = !RAGGED || (pos >= lo && pos < hi);
-        const uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
         if (MODE == 0) {
-            cnt += mask ? 1u : 0u;
-            acc.add(mask);
+            // counts only: survivors (total <= the largest threshold) and
+            // survivors per capacity
+            if (act) {
+                cnt += total <= S.thr_max ? 1u : 0u;
+#pragma unroll
+                for (int q = 0; q < NCAP; q++) acc.capc[q] += total <= S.thr[q] ? 1u : 0u;
+            }
         } else {
+            const uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
             const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
             if (mask) {
                 const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
@@ -337,7 +328,7 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
             if (in_row) {
                 W.r += 32;
                 W.pp += pstep;
-                pr = prn;
+                pr = PREFETCH ? prn : __ldg(W.pp);
             } else {
                 W.advance32(S, pstep);
                 pr = __ldg(W.pp);
@@ -398,7 +389,6 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
         else
             cnt = run_tile<0, NCAP, false, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
                                                        Cols{}, 0, !last);
-        acc.flush();
         cnt = __reduce_add_sync(0xffffffffu, cnt);
         if (lane == 0) tile_cnt[t] = cnt;
         run += cnt;
@@ -407,7 +397,7 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
 }
 
 template <int NCAP>
-__global__ void __launch_bounds__(kThreads, 4) count_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+__global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                             const uint32_t n_spans, uint32_t* __restrict__ tile_rel,
                                                             uint32_t* __restrict__ tile_cnt,
                                                             uint4* __restrict__ tile_ck,

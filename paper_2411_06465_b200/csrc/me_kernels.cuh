@@ -37,6 +37,7 @@ struct DevSpace {
     uint32_t gbs_mode;            // 1 = a global batch bounds the in-flight microbatches (R17)
     uint32_t stage_max;           // 1 = feasibility of the largest pipeline stage (NEXT-1)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
+    uint64_t thr_max;             // the largest threshold: survivor <=> total <= thr_max
 };
 
 // Per (model, tuple) coefficients: every estimator term of a config in this
