@@ -241,6 +241,16 @@ int me_result_wait(me_result* r);
 int me_result_timing(me_result* r, float* ms4);
 void me_result_free(me_result* r);
 
+/* NEXT-2 planner (the search heuristics of P:552-593): for every
+ * (model, N) segment of the plan (n_models * n_world entries, model-major),
+ * the flat index of the best row of an INDEX or FULL result that is feasible
+ * for capacity `cap`, or UINT64_MAX when none is.  Rank key (DESIGN.md §9,
+ * reading R27): smallest t*c*p, largest micro batch (P:564,
+ * P:587), smallest p (bubble (p-1)/m), smallest t (CP before TP,
+ * P:580-582), recompute off, smallest index.  best_index: host array.
+ * Sharded multi-GPU results must have been gathered.  Synchronous. */
+int me_result_rank(me_result* r, uint32_t cap, uint64_t* best_index);
+
 /* Host logic of the multi-GPU path (host-only, no device needed).
  * me_partition: rank's contiguous share [lo, hi) of [begin, end) with
  * lo = begin + floor(len*rank/nranks), hi likewise for rank + 1.

@@ -208,6 +208,15 @@ class Result:
         check(lib().me_result_copy_to_host(self.h, first, n, hp), "me_result_copy_to_host")
         return dict(zip(COLUMNS, arrays))
 
+    def rank(self, cap: int = 0) -> np.ndarray:
+        """NEXT-2: best feasible flat index per (model, N) segment for capacity
+        `cap` (me_result_rank); UINT64_MAX where none."""
+        n_seg = len(self.plan.c.models) * len(self.plan.c.world)
+        out = np.zeros(n_seg, dtype=np.uint64)
+        check(lib().me_result_rank(self.h, cap, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))),
+              "me_result_rank")
+        return out
+
     def free(self):
         if self.h:
             lib().me_result_free(self.h)

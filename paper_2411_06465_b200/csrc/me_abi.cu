@@ -189,6 +189,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     uint64_t *dsp, *dlp;
     DevTuple* dtu;
     DevPair* dpr;
+    uint32_t* dpb;
     if ((st = upload(P->A, dmodels, &dm)) || (P->owned.push_back(dm), false) ||
         (st = upload(P->A, H.model_class, &dcls)) || (P->owned.push_back(dcls), false) ||
         (st = upload(P->A, H.seg_prefix, &dsp)) || (P->owned.push_back(dsp), false) ||
@@ -196,7 +197,8 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         (st = upload(P->A, H.list_tuple, &dlt)) || (P->owned.push_back(dlt), false) ||
         (st = upload(P->A, H.list_prefix, &dlp)) || (P->owned.push_back(dlp), false) ||
         (st = upload(P->A, H.tuples, &dtu)) || (P->owned.push_back(dtu), false) ||
-        (st = upload(P->A, H.pairs, &dpr)) || (P->owned.push_back(dpr), false)) {
+        (st = upload(P->A, H.pairs, &dpr)) || (P->owned.push_back(dpr), false) ||
+        (st = upload(P->A, H.pair_b, &dpb)) || (P->owned.push_back(dpb), false)) {
         me_plan_free(P);
         return st;
     }
@@ -208,6 +210,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.list_prefix = dlp;
     D.tuples = dtu;
     D.pairs = dpr;
+    D.pair_b = dpb;
     D.n_seg = (uint32_t)(H.seg_prefix.size() - 1);
     D.n_world = (uint32_t)H.world.size();
     D.lg_rcdo = H.lg_rcdo;
@@ -611,6 +614,32 @@ extern "C" int me_result_timing(me_result* R, float* ms) {
 }
 
 extern "C" void me_result_free(me_result* R) { result_release(R); }
+
+extern "C" int me_result_rank(me_result* R, uint32_t cap, uint64_t* best_index) {
+    if (!R || !best_index) return err(ME_EINVAL, "null argument");
+    if (cap >= R->n_cap) return err(ME_EINVAL, "capacity index out of range");
+    if (R->mode == ME_OUT_COUNT) return err(ME_EINVAL, "ranking needs an INDEX or FULL result");
+    if (R->comm && !R->gather) return err(ME_EINVAL, "ranking a sharded result needs gather = 1");
+    uint64_t* cols[ME_N_COLS];
+    uint64_t rows = 0;
+    int st = me_result_columns(R, cols, &rows);
+    if (st) return st;
+    me_plan* P = R->plan;
+    DeviceGuard g(P->device);
+    const size_t n_seg = P->hs.seg_prefix.size() - 1;
+    uint64_t *dkey = nullptr, *didx = nullptr;
+    CU(cudaMalloc(&dkey, n_seg * 8));
+    cudaError_t ce = cudaMalloc(&didx, n_seg * 8);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(dkey, 0xFF, n_seg * 8, R->stream);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(didx, 0xFF, n_seg * 8, R->stream);
+    if (ce == cudaSuccess) ce = launch_rank(P->ds, cols[0], rows, cap, dkey, didx, R->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(best_index, didx, n_seg * 8, cudaMemcpyDeviceToHost, R->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(R->stream);
+    cudaFree(dkey);
+    cudaFree(didx);
+    if (ce != cudaSuccess) return cuda_err(ce, "me_result_rank");
+    return ME_OK;
+}
 
 // ---------------------------------------------------------------------------
 // single estimates

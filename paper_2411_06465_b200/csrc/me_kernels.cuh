@@ -31,6 +31,7 @@ struct DevSpace {
     const uint64_t* list_prefix;
     const DevTuple* tuples;
     const DevPair* pairs;
+    const uint32_t* pair_b;       // micro-batch size of each pair (planner only)
     uint32_t n_seg, n_world;
     uint32_t lg_rcdo, rcdo_rc, rcdo_do;
     uint32_t n_cap;
@@ -220,6 +221,10 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint32_t* tile_bits,
                          const uint64_t* span_off, me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st);
+// NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
+// (rank key of DESIGN.md §9); best_key / best_index initialised to ~0
+cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint64_t n_rows, uint32_t cap,
+                        uint64_t* best_key, uint64_t* best_index, cudaStream_t st);
 // one configuration, one stage or (stage = 0xFFFFFFFF) the largest stage (NEXT-1)
 cudaError_t launch_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,
                                   uint32_t* which, int* status, cudaStream_t st);

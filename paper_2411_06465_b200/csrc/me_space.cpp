@@ -82,6 +82,7 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
     // limits, ascending; the pooled (b, s) pairs of each
     tuples.clear();
     pairs.clear();
+    pair_b.clear();
     tup_begin.assign(1, 0);
     std::map<std::pair<uint32_t, uint32_t>, std::pair<uint32_t, uint32_t>> pool;  // (c, d|0) -> (off, n)
     std::vector<uint32_t> tvals, pvals;
@@ -109,6 +110,7 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
                                 pr.u = (s / c) * b;
                                 pr.m = gbs ? (uint32_t)(gbs / ((uint64_t)d * b)) : 0xFFFFFFFFu;
                                 pairs.push_back(pr);
+                                pair_b.push_back(b);
                             }
                         it = pool.emplace(key, std::make_pair(off, (uint32_t)pairs.size() - off)).first;
                     }
