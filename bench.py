@@ -285,6 +285,17 @@ def main():
                 "traffic": None, "peak_source": f"{peak_src} hbm_gbs (copy)",
                 "algorithmic_bytes_per_launch": bytes_write / max(1, n_launch),
                 "avg_launch_ms": write_ms / max(1, n_launch)}
+        ncu = ROOT / "profiles" / "ncu_write_traffic.json"
+        if ncu.exists():  # one ncu --set full capture of one chunk (scripts/profile_chunk.py)
+            t = json.loads(ncu.read_text())
+            roof["traffic"] = t["dram_bytes_read"] + t["dram_bytes_write"]
+            roof["traffic_note"] = (f"ncu DRAM bytes of the write kernel of C5 chunk {t['chunk']} "
+                                    f"(algorithmic {t['algorithmic_write_bytes']} B for that launch)")
+        mb = ROOT / "profiles" / "r1_v4" / "microbench.json"
+        if mb.exists():
+            w = json.loads(mb.read_text())["write_only_gbs"]
+            roof["write_only_peak_gbs"] = w
+            roof["frac_of_write_only"] = achieved / w
     else:
         roof = {"bound": "alu", "kernel": "sweep_kernel<0,4> (count pass)", "achieved": None, "peak": None,
                 "unit": "warp-instr/s", "frac": None, "traffic": None}

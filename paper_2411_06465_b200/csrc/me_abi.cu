@@ -106,6 +106,7 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
+    uint32_t bulk = 0;                      // write pass through shared memory + bulk copies (ME_WRITE_BULK=1)
     uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
@@ -113,7 +114,6 @@ struct me_plan {
     struct Scratch {
         uint32_t* tile_rel = nullptr;   // rank of a tile's first survivor inside its span
         uint32_t* tile_cnt = nullptr;   // survivors of a tile
-        uint32_t* tile_bits = nullptr;  // survivor ballots of a tile's rounds
         uint4* tile_ck = nullptr;       // walker checkpoint of a tile's first index
         uint32_t* span_count = nullptr;
         uint64_t* span_off = nullptr;
@@ -230,8 +230,9 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     P->max_spans = (uint32_t)P->sms * 96;
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
+    if (const char* e = getenv("ME_WRITE_BULK")) P->bulk = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
-    const int occ_c = sweep_blocks_per_sm(0, D.n_cap), occ_w = sweep_blocks_per_sm(2, D.n_cap);
+    const int occ_c = sweep_blocks_per_sm(0, D.n_cap, false), occ_w = sweep_blocks_per_sm(2, D.n_cap, P->bulk != 0);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
     P->write_bps = (uint32_t)(occ_w > 2 ? 2 : occ_w);
@@ -244,8 +245,6 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         sc.tile_rel = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
         sc.tile_cnt = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
         P->owned.push_back(sc.tile_cnt);
-        sc.tile_bits = (uint32_t*)P->A.get((size_t)P->max_tiles * kTileRounds * 4);
-        P->owned.push_back(sc.tile_bits);
         sc.tile_ck = (uint4*)P->A.get((size_t)P->max_tiles * 16);
         sc.span_count = (uint32_t*)P->A.get((size_t)P->max_spans * 4);
         sc.span_off = (uint64_t*)P->A.get((size_t)P->max_spans * 8);
@@ -255,7 +254,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         P->owned.push_back(sc.span_count);
         P->owned.push_back(sc.span_off);
         P->owned.push_back(sc.span_caps);
-        if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_bits || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps) {
+        if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps) {
             me_plan_free(P);
             return err(ME_ENOMEM, "scratch allocation");
         }
@@ -379,6 +378,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
+    bool bulk = false;
     auto pipeline = [&](uint64_t* stats, bool write, Cols cols, uint64_t capacity) -> int {
         if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
         for (uint64_t lo = b; lo < e; lo += kMaxSub) {
@@ -401,7 +401,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             cudaStreamWaitEvent(cs, sc.free_ev, 0);
             cudaEventRecord(tev[0], cs);
             cudaError_t ce = launch_count(P->ds, lo, hi, n_spans, grid(P->count_bps, n_spans), sc.tile_rel,
-                                          sc.tile_cnt, sc.tile_ck, sc.tile_bits, sc.span_count, sc.span_caps, cs);
+                                          sc.tile_cnt, sc.tile_ck, sc.span_count, sc.span_caps, cs);
             if (ce != cudaSuccess) return cuda_err(ce, "count kernel");
             cudaEventRecord(tev[1], cs);
             ce = launch_scan(sc.span_count, sc.span_caps, n_spans, P->ds.n_cap, sc.span_off, stats, cs);
@@ -411,7 +411,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             cudaEventRecord(tev[3], st);
             if (write) {
                 ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_rel, sc.tile_cnt,
-                                  sc.tile_bits, sc.span_off, o->mode, cols, capacity, st);
+                                  sc.span_off, o->mode, bulk, cols, capacity, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "write kernel");
             }
             cudaEventRecord(tev[4], st);
@@ -446,6 +446,10 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
     }
+    // bulk copies need 16-byte aligned columns
+    bulk = P->bulk != 0;
+    for (int j = 0; j < nc; j++)
+        if (((uintptr_t)cols.c[j]) & 15u) bulk = false;
     if ((rc = pipeline(R->stats, nc != 0, cols, R->capacity))) return fail(rc);
     R->ran_count = len != 0;
     R->ran_write = nc && len;

@@ -190,6 +190,63 @@ struct CapAcc {
     }
 };
 
+// Bulk (TMA) staging of a warp's survivor columns for the write pass.  The
+// lanes put their rows into a per-warp shared-memory ring (kRing rows per
+// column, ring slot = row mod kRing, so a row's shared and global addresses
+// have the same 16-byte phase); whenever >= kSend rows are pending, one lane
+// hands them to the bulk-copy engine (cp.async.bulk shared -> global, one copy
+// per column and ring segment) -- full, contiguous transfers instead of the
+// 8-byte lane stores, whose unaligned ~200-byte runs cap the store rate at
+// ~4.1 TB/s on B200 (scripts/storebench.cu).  Single rows at odd ends go out
+// as plain stores (bulk copies move multiples of 16 bytes).
+constexpr uint32_t kRing = 128, kSend = 64;
+
+__device__ __forceinline__ void bulk_s2g(void* g, const void* sm, uint32_t bytes) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sm);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "r"(bytes)
+                 : "memory");
+}
+
+template <int NC>
+struct BulkStager {
+    uint64_t* ring;  // NC x kRing rows of this warp
+    uint64_t sent;   // first row not yet handed out
+    __device__ __forceinline__ void put(uint64_t row, int c, uint64_t v) { ring[c * kRing + (row & (kRing - 1))] = v; }
+    // hand rows [sent, upto) out; rows >= capacity are dropped
+    __device__ __forceinline__ void send(const Cols& cols, uint64_t upto, uint64_t capacity, uint32_t lane) {
+        uint64_t hi = upto < capacity ? upto : capacity;
+        if (sent < hi) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // lanes' STS -> async proxy
+            __syncwarp();
+            if (lane == 0) {
+                uint64_t lo = sent;
+                if (lo & 1) {
+#pragma unroll
+                    for (int c = 0; c < NC; c++) cols.c[c][lo] = ring[c * kRing + (lo & (kRing - 1))];
+                    lo++;
+                }
+                if ((hi - lo) & 1) {
+                    hi--;
+#pragma unroll
+                    for (int c = 0; c < NC; c++) cols.c[c][hi] = ring[c * kRing + (hi & (kRing - 1))];
+                }
+                while (lo < hi) {
+                    const uint64_t wrap = (lo | (kRing - 1)) + 1;
+                    const uint64_t e = hi < wrap ? hi : wrap;
+#pragma unroll
+                    for (int c = 0; c < NC; c++)
+                        bulk_s2g(cols.c[c] + lo, ring + c * kRing + (lo & (kRing - 1)), (uint32_t)(e - lo) * 8u);
+                    lo = e;
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // ring slots reusable
+            }
+            __syncwarp();
+        }
+        sent = upto;
+    }
+};
+
 // Evaluate one tile's rounds starting at the walker's position (lane's index
 // = pos).  RAGGED: the tile is cut by lo/hi (first or last tile of a range).
 // GBS: a global batch bounds the in-flight microbatches (R17).  STMAX: the
@@ -197,75 +254,88 @@ struct CapAcc {
 // so the larger of stage 0 and the last stage is the maximum).  Returns with
 // the walker on the first index after the tile when `advance_out`.
 //
-// bits[it] is the survivor ballot of round it: written by the count pass, read
-// by the write pass, which evaluates only the surviving lanes of non-empty
-// rounds (an empty round only advances the walker).
-//
 // Write pass stores: each surviving lane stores its 8-byte value of every
 // column at its row; a round's rows are contiguous.  (Measured alternatives on
 // B200, scripts/storebench.cu and DESIGN.md §6: shared-memory staging into
-// aligned full lines, plain or drained by cp.async.bulk, lifts the store
-// pattern itself from ~4.1 to ~5.7 TB/s but cost more than they saved here.)
-template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX>
+// aligned full-line stores lifts the store pattern itself from ~4.1 to ~5.7
+// TB/s but costs more issue slots than it saves in this kernel.)
+template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX, bool BULK = false>
 __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
                                              uint64_t hi, uint32_t rounds, uint32_t lane, CapAcc<NCAP>& acc,
-                                             uint32_t* __restrict__ bits, uint64_t out, const Cols& cols,
-                                             uint64_t capacity, bool advance_out) {
+                                             uint64_t out, const Cols& cols, uint64_t capacity,
+                                             bool advance_out, BulkStager<MODE == 2 ? 8 : 1>* bs = nullptr) {
     constexpr int NC = MODE == 2 ? 8 : 1;
+    constexpr bool PREFETCH = MODE != 0;  // the write pass hides the pair load behind a round
     const uint32_t pstep = 32u >> S.lg_rcdo;
     uint32_t cnt = 0;
+    uint2 pr = __ldg(W.pp);
     for (uint32_t it = 0; it < rounds; it++, pos += 32) {
         const bool more = (it + 1 < rounds) || advance_out;
-        const uint32_t ballot_in = MODE == 0 ? 0u : __ldg(bits + it);
-        if (MODE == 0 || ballot_in) {
-            const uint2 pr = __ldg(W.pp);
-            const uint32_t u = pr.x;
-            const uint32_t n_inf = GBS ? min(W.L.p, pr.y) : W.L.p;
-            const uint64_t K = GBS ? (uint64_t)n_inf * W.L.a + W.L.b : W.L.kp;
-            uint64_t total = W.L.ms + (uint64_t)u * K;
-            bool last = false;
-            if (STMAX && W.L.two) {
-                const uint64_t tl = W.L.msL + (uint64_t)u * W.L.kL;
-                last = tl > total;
-                total = last ? tl : total;
-            }
-            if (MODE == 0) {
-                // survivors (total <= the largest threshold): ballot per round;
-                // survivors per capacity: per-lane counters
-                const bool act = !RAGGED || (pos >= lo && pos < hi);
-                const uint32_t ballot = __ballot_sync(0xffffffffu, act && total <= S.thr_max);
-                if (lane == 0) bits[it] = ballot;
-                cnt += __popc(ballot);
-                if (act) {
+        const bool in_row = W.r + 32 < W.w;
+        uint2 prn = pr;
+        if (PREFETCH && in_row && more) prn = __ldg(W.pp + pstep);  // next round's pair, issued early
+
+        const uint32_t u = pr.x;
+        const uint32_t n_inf = GBS ? min(W.L.p, pr.y) : W.L.p;
+        const uint64_t K = GBS ? (uint64_t)n_inf * W.L.a + W.L.b : W.L.kp;
+        uint64_t total = W.L.ms + (uint64_t)u * K;
+        bool last = false;
+        if (STMAX && W.L.two) {
+            const uint64_t tl = W.L.msL + (uint64_t)u * W.L.kL;
+            last = tl > total;
+            total = last ? tl : total;
+        }
+        const bool act = !RAGGED || (pos >= lo && pos < hi);
+        if (MODE == 0) {
+            // counts only: survivors (total <= the largest threshold) and
+            // survivors per capacity
+            if (act) {
+                cnt += total <= S.thr_max ? 1u : 0u;
 #pragma unroll
-                    for (int q = 0; q < NCAP; q++) acc.capc[q] += total <= S.thr[q] ? 1u : 0u;
-                }
-            } else {
-                if ((ballot_in >> lane) & 1u) {
-                    const uint32_t mask = cap_mask<NCAP>(S, total);
-                    const uint64_t o = out + __popc(ballot_in & ((1u << lane) - 1u));
-                    if (o < capacity) {
-                        uint64_t v[NC];
-                        v[0] = pos | ((uint64_t)mask << 56);
-                        if (MODE == 2) {
-                            const uint64_t psi = STMAX && last ? W.L.psiL : W.L.psi;
-                            v[1] = 2ull * psi;
-                            v[2] = 4ull * psi;
-                            v[3] = STMAX && last ? W.L.optimL : W.L.optim;
-                            v[4] = (uint64_t)u * (STMAX && last ? W.L.layL : (uint64_t)n_inf * W.L.lam + W.L.mu);
-                            v[5] = STMAX && last ? 0ull : (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
-                            v[6] = (uint64_t)u * (STMAX && last ? W.L.hcL : W.L.hc);
-                            v[7] = total;
-                        }
+                for (int q = 0; q < NCAP; q++) acc.capc[q] += total <= S.thr[q] ? 1u : 0u;
+            }
+        } else {
+            const uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
+            const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
+            if (mask) {
+                const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
+                if (BULK || o < capacity) {
+                    uint64_t v[NC];
+                    v[0] = pos | ((uint64_t)mask << 56);
+                    if (MODE == 2) {
+                        const uint64_t psi = STMAX && last ? W.L.psiL : W.L.psi;
+                        v[1] = 2ull * psi;
+                        v[2] = 4ull * psi;
+                        v[3] = STMAX && last ? W.L.optimL : W.L.optim;
+                        v[4] = (uint64_t)u * (STMAX && last ? W.L.layL : (uint64_t)n_inf * W.L.lam + W.L.mu);
+                        v[5] = STMAX && last ? 0ull : (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
+                        v[6] = (uint64_t)u * (STMAX && last ? W.L.hcL : W.L.hc);
+                        v[7] = total;
+                    }
+                    if (BULK) {
+#pragma unroll
+                        for (int c = 0; c < NC; c++) bs->put(o, c, v[c]);
+                    } else {
 #pragma unroll
                         for (int c = 0; c < NC; c++) cols.c[c][o] = v[c];
                     }
                 }
-                out += __popc(ballot_in);
+            }
+            out += __popc(ballot);
+            if (BULK && out - bs->sent >= kSend) bs->send(cols, out, capacity, lane);
+        }
+        if (more && (!RAGGED || pos + 32 < hi)) {
+            if (in_row) {
+                W.r += 32;
+                W.pp += pstep;
+                pr = PREFETCH ? prn : __ldg(W.pp);
+            } else {
+                W.advance32(S, pstep);
+                pr = __ldg(W.pp);
             }
         }
-        if (more && (!RAGGED || pos + 32 < hi)) W.advance32(S, pstep);
     }
+    if (BULK) bs->send(cols, out, capacity, lane);
     return cnt;
 }
 
@@ -292,15 +362,15 @@ __device__ __forceinline__ TileGeom geom(uint64_t lo, uint64_t hi) {
 }
 
 // count pass over span s = tiles [t0, t1): per tile its checkpoint
-// {seg, j, r, s}, its 16 round ballots, its survivor count and its first
-// survivor's rank inside the span; returns the span total
+// {seg, j, r, s}, its survivor count and its first survivor's rank inside the
+// span; returns the span total
 template <int NCAP, bool GBS, bool STMAX>
 __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom& G, uint32_t s, uint32_t t0,
                                                uint32_t t1, uint32_t lane, uint32_t* __restrict__ tile_rel,
                                                uint32_t* __restrict__ tile_cnt, uint4* __restrict__ tile_ck,
-                                               uint32_t* __restrict__ tile_bits, CapAcc<NCAP>& acc) {
+                                               CapAcc<NCAP>& acc) {
     Walker W;
-    // a lane past the end of the range only takes part in the warp ballots:
+    // a lane past the end of the range only takes part in the warp reductions:
     // park it on the last index (its own positions stay inactive)
     const uint64_t p0 = G.start(t0) + lane;
     W.seek(S, p0 < G.hi ? p0 : G.hi - 1);
@@ -312,14 +382,14 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
             tile_rel[t] = run;
         }
         const bool last = t + 1 == t1;
-        uint32_t* bits = tile_bits + (size_t)t * kTileRounds;
         uint32_t cnt;
         if (G.ragged(t))
-            cnt = run_tile<0, NCAP, true, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, bits, 0,
-                                                      Cols{}, 0, !last);
+            cnt = run_tile<0, NCAP, true, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{},
+                                                      0, !last);
         else
-            cnt = run_tile<0, NCAP, false, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, bits, 0,
+            cnt = run_tile<0, NCAP, false, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
                                                        Cols{}, 0, !last);
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
         if (lane == 0) tile_cnt[t] = cnt;
         run += cnt;
     }
@@ -331,7 +401,6 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, co
                                                             const uint32_t n_spans, uint32_t* __restrict__ tile_rel,
                                                             uint32_t* __restrict__ tile_cnt,
                                                             uint4* __restrict__ tile_ck,
-                                                            uint32_t* __restrict__ tile_bits,
                                                             uint32_t* __restrict__ span_count,
                                                             uint32_t* __restrict__ span_caps) {
     const uint32_t lane = threadIdx.x & 31;
@@ -344,15 +413,11 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, co
         uint32_t n = 0;
         if (t0 < t1) {
             if (S.stage_max) {
-                if (S.gbs_mode)
-                    n = count_span<NCAP, true, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, tile_bits, acc);
-                else
-                    n = count_span<NCAP, false, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, tile_bits, acc);
+                if (S.gbs_mode) n = count_span<NCAP, true, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+                else n = count_span<NCAP, false, true>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
             } else {
-                if (S.gbs_mode)
-                    n = count_span<NCAP, true, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, tile_bits, acc);
-                else
-                    n = count_span<NCAP, false, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, tile_bits, acc);
+                if (S.gbs_mode) n = count_span<NCAP, true, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
+                else n = count_span<NCAP, false, false>(S, G, s, t0, t1, lane, tile_rel, tile_cnt, tile_ck, acc);
             }
         }
         if (lane == 0) span_count[s] = n;
@@ -364,52 +429,55 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, co
     }
 }
 
-template <int MODE, int NCAP, bool GBS, bool STMAX>
+template <int MODE, int NCAP, bool GBS, bool STMAX, bool BULK>
 __device__ __forceinline__ void write_tile(const DevSpace& S, const TileGeom& G, Walker& W, uint32_t t, uint64_t pos,
-                                           uint32_t lane, const uint32_t* bits, uint64_t out, const Cols& cols,
-                                           uint64_t capacity) {
+                                           uint32_t lane, uint64_t out, const Cols& cols, uint64_t capacity,
+                                           BulkStager<MODE == 2 ? 8 : 1>* bs) {
     CapAcc<NCAP> none;
-    uint32_t* b = const_cast<uint32_t*>(bits);
     if (G.ragged(t))
-        run_tile<MODE, NCAP, true, GBS, STMAX>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, b, out, cols,
-                                               capacity, false);
+        run_tile<MODE, NCAP, true, GBS, STMAX, BULK>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
+                                                     capacity, false, bs);
     else
-        run_tile<MODE, NCAP, false, GBS, STMAX>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, b, out, cols,
-                                                capacity, false);
+        run_tile<MODE, NCAP, false, GBS, STMAX, BULK>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
+                                                      capacity, false, bs);
 }
 
-// write pass: one tile per warp, tiles in grid order (at any moment the grid
-// writes one compact window of the output columns)
-template <int MODE, int NCAP>
-__global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+// write pass: tiles in grid-stride order (at any moment the grid writes one
+// compact window of the output columns)
+template <int MODE, int NCAP, bool BULK>
+__global__ void __launch_bounds__(kThreads, BULK ? 2 : 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                             const uint4* __restrict__ tile_ck,
                                                             const uint32_t* __restrict__ tile_rel,
                                                             const uint32_t* __restrict__ tile_cnt,
-                                                            const uint32_t* __restrict__ tile_bits,
                                                             const uint64_t* __restrict__ span_off, const Cols cols,
                                                             const uint64_t capacity) {
+    constexpr int NC = MODE == 2 ? 8 : 1;
+    extern __shared__ uint64_t s_ring[];  // BULK: kWarpsPerBlock x NC x kRing
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
     const TileGeom G = geom(lo, hi);
+    BulkStager<NC> bs;
+    bs.ring = s_ring + (BULK ? wid * NC * kRing : 0);
     for (uint32_t t = blockIdx.x * kWarpsPerBlock + wid; t < G.n_tiles; t += n_warps) {
         if (__ldg(tile_cnt + t) == 0) continue;  // no survivor: nothing to write
         const uint64_t ts = G.start(t);
         const uint64_t pos = ts + lane;
         const uint4 ck = __ldg(tile_ck + t);
         const uint64_t out = __ldg(span_off + ck.w) + __ldg(tile_rel + t);
-        const uint32_t* bits = tile_bits + (size_t)t * kTileRounds;
         Walker W;
-        // a lane past the end of the range is parked on the last index (its
-        // ballot bits are clear)
+        // a lane past the end of the range is parked on the last index: it
+        // takes part in the ballots with inactive positions
         W.restore(S, ck, pos < hi ? lane : (uint32_t)(hi - 1 - ts));
+        bs.sent = out;
         if (S.stage_max) {
-            if (S.gbs_mode) write_tile<MODE, NCAP, true, true>(S, G, W, t, pos, lane, bits, out, cols, capacity);
-            else write_tile<MODE, NCAP, false, true>(S, G, W, t, pos, lane, bits, out, cols, capacity);
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, true, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
+            else write_tile<MODE, NCAP, false, true, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
         } else {
-            if (S.gbs_mode) write_tile<MODE, NCAP, true, false>(S, G, W, t, pos, lane, bits, out, cols, capacity);
-            else write_tile<MODE, NCAP, false, false>(S, G, W, t, pos, lane, bits, out, cols, capacity);
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, false, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
+            else write_tile<MODE, NCAP, false, false, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
         }
     }
+    if (BULK && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // global writes done
 }
 
 // one block: exclusive scan of the span counts into u64 offsets starting at
@@ -587,18 +655,23 @@ void* count_kernel_for(uint32_t n_cap) {
     }
 }
 
-template <int MODE>
+template <int MODE, bool BULK>
 void* write_kernel_for(uint32_t n_cap) {
     switch (ncap_stride_(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1>);
-        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2>);
-        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4>);
-        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8>);
+        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1, BULK>);
+        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2, BULK>);
+        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4, BULK>);
+        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8, BULK>);
     }
 }
 
-void* write_fn(me_out_mode mode, uint32_t n_cap) {
-    return mode == ME_OUT_FULL ? write_kernel_for<2>(n_cap) : write_kernel_for<1>(n_cap);
+void* write_fn(me_out_mode mode, uint32_t n_cap, bool bulk) {
+    if (mode == ME_OUT_FULL) return bulk ? write_kernel_for<2, true>(n_cap) : write_kernel_for<2, false>(n_cap);
+    return bulk ? write_kernel_for<1, true>(n_cap) : write_kernel_for<1, false>(n_cap);
+}
+
+size_t write_smem(me_out_mode mode, bool bulk) {
+    return bulk ? (size_t)kWarpsPerBlock * (mode == ME_OUT_FULL ? 8 : 1) * kRing * 8 : 0;
 }
 
 }  // namespace
@@ -610,19 +683,21 @@ uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
     return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
 }
 
-int sweep_blocks_per_sm(int pass, uint32_t n_cap) {
-    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX, n_cap);
+int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool bulk) {
+    const me_out_mode mode = pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX;
+    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(mode, n_cap, bulk);
+    const size_t smem = pass == 0 ? 0 : write_smem(mode, bulk);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* tile_rel, uint32_t* tile_cnt, uint4* tile_ck, uint32_t* tile_bits,
-                         uint32_t* span_count, uint32_t* span_caps, cudaStream_t st) {
-    void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,        (void*)&n_spans,
-                    (void*)&tile_rel, (void*)&tile_cnt, (void*)&tile_ck,   (void*)&tile_bits,
-                    (void*)&span_count, (void*)&span_caps};
+                         uint32_t* tile_rel, uint32_t* tile_cnt, uint4* tile_ck, uint32_t* span_count,
+                         uint32_t* span_caps, cudaStream_t st) {
+    void* args[] = {(void*)&S,       (void*)&lo,         (void*)&hi,       (void*)&n_spans, (void*)&tile_rel,
+                    (void*)&tile_cnt, (void*)&tile_ck, (void*)&span_count, (void*)&span_caps};
     return cudaLaunchKernel(count_kernel_for(S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
@@ -634,11 +709,14 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 }
 
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
-                         const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint32_t* tile_bits,
-                         const uint64_t* span_off, me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st) {
-    void* args[] = {(void*)&S,        (void*)&lo,        (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
-                    (void*)&tile_cnt, (void*)&tile_bits, (void*)&span_off, (void*)&cols,    (void*)&capacity};
-    return cudaLaunchKernel(write_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
+                         const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
+                         me_out_mode mode, bool bulk, Cols cols, uint64_t capacity, cudaStream_t st) {
+    void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
+                    (void*)&tile_cnt, (void*)&span_off, (void*)&cols, (void*)&capacity};
+    void* fn = write_fn(mode, S.n_cap, bulk);
+    const size_t smem = write_smem(mode, bulk);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaLaunchKernel(fn, dim3(n_blocks), dim3(kThreads), args, smem, st);
 }
 
 cudaError_t launch_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,

@@ -1,0 +1,25 @@
+"""One FULL sweep call of bench.py's launch configuration (C5, one 2^28-config
+chunk), for ncu: prints the chunk's survivors so the profiled write kernel's
+DRAM traffic can be set against its algorithmic bytes (survivors x 64 B)."""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+import me_inputs as mi  # noqa: E402
+import paper_2411_06465_b200 as me  # noqa: E402
+
+CHUNK = 1 << 28
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+sp = mi.config("C5")
+stream = torch.cuda.Stream()
+plan = me.Plan(sp, device=0, stream=stream.cuda_stream)
+cols = [torch.empty(CHUNK + 64, dtype=torch.int64, device="cuda") for _ in range(8)]
+with torch.cuda.stream(stream):
+    r = plan.sweep(k * CHUNK, (k + 1) * CHUNK, mode=me.ME_OUT_FULL, out_cols=cols)
+    n = r.counts()[0]
+    ms = r.timing()
+print(json.dumps({"chunk": k, "begin": k * CHUNK, "end": (k + 1) * CHUNK, "survivors": n,
+                  "algorithmic_write_bytes": n * 64, "timing_ms": ms}))
