@@ -108,6 +108,7 @@ struct me_plan {
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
     uint32_t bulk = 0;                      // write pass through shared memory + bulk copies (ME_WRITE_BULK=1)
     uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
+    uint32_t serial = 0;                    // 1 = count pass on the caller's stream too (ME_SERIAL)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
     // of sub-range i (on the caller's stream).
@@ -232,6 +233,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
     if (const char* e = getenv("ME_WRITE_BULK")) P->bulk = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_SERIAL")) P->serial = (uint32_t)atoi(e);
     const int occ_c = sweep_blocks_per_sm(0, D.n_cap, false), occ_w = sweep_blocks_per_sm(2, D.n_cap, P->bulk != 0);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
@@ -374,7 +376,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     // stream, which waits only for the tables and for the write pass that last
     // used the scratch set, so the count of sub-range i+1 runs while the
     // caller's stream still writes the columns of sub-range i.
-    cudaStream_t cs = P->cstream;
+    cudaStream_t cs = P->serial ? st : P->cstream;
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
