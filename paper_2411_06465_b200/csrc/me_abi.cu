@@ -106,7 +106,7 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t bulk = 0;                      // write pass through shared memory + bulk copies (ME_WRITE_BULK=1)
+    uint32_t comb = 1;                      // write combining into aligned 32-row windows (ME_WRITE_COMB)
     uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
     uint32_t serial = 0;                    // 1 = count pass on the caller's stream too (ME_SERIAL)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
@@ -231,10 +231,10 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     P->max_spans = (uint32_t)P->sms * 96;
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
-    if (const char* e = getenv("ME_WRITE_BULK")) P->bulk = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_WRITE_COMB")) P->comb = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_SERIAL")) P->serial = (uint32_t)atoi(e);
-    const int occ_c = sweep_blocks_per_sm(0, D.n_cap, false), occ_w = sweep_blocks_per_sm(2, D.n_cap, P->bulk != 0);
+    const int occ_c = sweep_blocks_per_sm(0, D.n_cap, false), occ_w = sweep_blocks_per_sm(2, D.n_cap, P->comb != 0);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
     P->write_bps = (uint32_t)(occ_w > 2 ? 2 : occ_w);
@@ -380,7 +380,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
-    bool bulk = false;
+    bool comb = false;
     auto pipeline = [&](uint64_t* stats, bool write, Cols cols, uint64_t capacity) -> int {
         if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
         for (uint64_t lo = b; lo < e; lo += kMaxSub) {
@@ -413,7 +413,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             cudaEventRecord(tev[3], st);
             if (write) {
                 ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_rel, sc.tile_cnt,
-                                  sc.span_off, o->mode, bulk, cols, capacity, st);
+                                  sc.span_off, o->mode, comb, cols, capacity, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "write kernel");
             }
             cudaEventRecord(tev[4], st);
@@ -448,10 +448,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
     }
-    // bulk copies need 16-byte aligned columns
-    bulk = P->bulk != 0;
-    for (int j = 0; j < nc; j++)
-        if (((uintptr_t)cols.c[j]) & 15u) bulk = false;
+    comb = P->comb != 0;
     if ((rc = pipeline(R->stats, nc != 0, cols, R->capacity))) return fail(rc);
     R->ran_count = len != 0;
     R->ran_write = nc && len;

@@ -190,60 +190,38 @@ struct CapAcc {
     }
 };
 
-// Bulk (TMA) staging of a warp's survivor columns for the write pass.  The
-// lanes put their rows into a per-warp shared-memory ring (kRing rows per
-// column, ring slot = row mod kRing, so a row's shared and global addresses
-// have the same 16-byte phase); whenever >= kSend rows are pending, one lane
-// hands them to the bulk-copy engine (cp.async.bulk shared -> global, one copy
-// per column and ring segment) -- full, contiguous transfers instead of the
-// 8-byte lane stores, whose unaligned ~200-byte runs cap the store rate at
-// ~4.1 TB/s on B200 (scripts/storebench.cu).  Single rows at odd ends go out
-// as plain stores (bulk copies move multiples of 16 bytes).
-constexpr uint32_t kRing = 128, kSend = 64;
-
-__device__ __forceinline__ void bulk_s2g(void* g, const void* sm, uint32_t bytes) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sm);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "r"(bytes)
-                 : "memory");
-}
-
+// Write combining (COMB): the rows of a warp's survivors are staged in a
+// 64-row shared-memory ring per column (slot = row mod 64) and leave it in
+// windows of 32 rows aligned to 32 (256-byte aligned, full-warp column
+// stores), whatever the survivor density of a round; only the first and the
+// last window of a tile are partial.  Measured store patterns:
+// scripts/storebench.cu.
 template <int NC>
-struct BulkStager {
-    uint64_t* ring;  // NC x kRing rows of this warp
-    uint64_t sent;   // first row not yet handed out
-    __device__ __forceinline__ void put(uint64_t row, int c, uint64_t v) { ring[c * kRing + (row & (kRing - 1))] = v; }
-    // hand rows [sent, upto) out; rows >= capacity are dropped
-    __device__ __forceinline__ void send(const Cols& cols, uint64_t upto, uint64_t capacity, uint32_t lane) {
-        uint64_t hi = upto < capacity ? upto : capacity;
-        if (sent < hi) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // lanes' STS -> async proxy
-            __syncwarp();
-            if (lane == 0) {
-                uint64_t lo = sent;
-                if (lo & 1) {
+struct Combiner {
+    uint64_t* buf;  // NC x 64 rows of this warp
+    uint64_t wb;    // first row of the open window (multiple of 32)
+    uint64_t row0;  // first row of the tile (rows below belong to another tile)
+    __device__ __forceinline__ void start(uint64_t out0) {
+        row0 = out0;
+        wb = out0 & ~31ull;
+    }
+    __device__ __forceinline__ void put(uint64_t row, int c, uint64_t v) { buf[c * 64 + (row & 63u)] = v; }
+    // store the open window's rows [wb, lim) (rows >= row0 and < capacity)
+    __device__ __forceinline__ void flush(const Cols& cols, uint64_t capacity, uint32_t lane, uint64_t lim) {
+        const uint64_t row = wb + lane;
+        if (row >= row0 && row < lim && row < capacity) {
 #pragma unroll
-                    for (int c = 0; c < NC; c++) cols.c[c][lo] = ring[c * kRing + (lo & (kRing - 1))];
-                    lo++;
-                }
-                if ((hi - lo) & 1) {
-                    hi--;
-#pragma unroll
-                    for (int c = 0; c < NC; c++) cols.c[c][hi] = ring[c * kRing + (hi & (kRing - 1))];
-                }
-                while (lo < hi) {
-                    const uint64_t wrap = (lo | (kRing - 1)) + 1;
-                    const uint64_t e = hi < wrap ? hi : wrap;
-#pragma unroll
-                    for (int c = 0; c < NC; c++)
-                        bulk_s2g(cols.c[c] + lo, ring + c * kRing + (lo & (kRing - 1)), (uint32_t)(e - lo) * 8u);
-                    lo = e;
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // ring slots reusable
-            }
-            __syncwarp();
+            for (int c = 0; c < NC; c++) cols.c[c][row] = buf[c * 64 + (row & 63u)];
         }
-        sent = upto;
+    }
+    // after a round whose rows end at `end`: emit every completed window
+    __device__ __forceinline__ void round_done(const Cols& cols, uint64_t capacity, uint32_t lane, uint64_t end) {
+        if (end >= wb + 32) {
+            __syncwarp();
+            flush(cols, capacity, lane, wb + 32);
+            wb += 32;
+            __syncwarp();  // the window's slots are free again
+        }
     }
 };
 
@@ -259,11 +237,11 @@ struct BulkStager {
 // B200, scripts/storebench.cu and DESIGN.md §6: shared-memory staging into
 // aligned full-line stores lifts the store pattern itself from ~4.1 to ~5.7
 // TB/s but costs more issue slots than it saves in this kernel.)
-template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX, bool BULK = false>
+template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX, bool COMB = false>
 __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
                                              uint64_t hi, uint32_t rounds, uint32_t lane, CapAcc<NCAP>& acc,
                                              uint64_t out, const Cols& cols, uint64_t capacity,
-                                             bool advance_out, BulkStager<MODE == 2 ? 8 : 1>* bs = nullptr) {
+                                             bool advance_out, Combiner<MODE == 2 ? 8 : 1>* cb = nullptr) {
     constexpr int NC = MODE == 2 ? 8 : 1;
     constexpr bool PREFETCH = MODE != 0;  // the write pass hides the pair load behind a round
     const uint32_t pstep = 32u >> S.lg_rcdo;
@@ -299,7 +277,7 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
             const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
             if (mask) {
                 const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
-                if (BULK || o < capacity) {
+                if (COMB || o < capacity) {
                     uint64_t v[NC];
                     v[0] = pos | ((uint64_t)mask << 56);
                     if (MODE == 2) {
@@ -312,9 +290,9 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
                         v[6] = (uint64_t)u * (STMAX && last ? W.L.hcL : W.L.hc);
                         v[7] = total;
                     }
-                    if (BULK) {
+                    if (COMB) {
 #pragma unroll
-                        for (int c = 0; c < NC; c++) bs->put(o, c, v[c]);
+                        for (int c = 0; c < NC; c++) cb->put(o, c, v[c]);
                     } else {
 #pragma unroll
                         for (int c = 0; c < NC; c++) cols.c[c][o] = v[c];
@@ -322,7 +300,7 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
                 }
             }
             out += __popc(ballot);
-            if (BULK && out - bs->sent >= kSend) bs->send(cols, out, capacity, lane);
+            if (COMB) cb->round_done(cols, capacity, lane, out);
         }
         if (more && (!RAGGED || pos + 32 < hi)) {
             if (in_row) {
@@ -335,7 +313,11 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
             }
         }
     }
-    if (BULK) bs->send(cols, out, capacity, lane);
+    if (COMB) {  // the tile's last, partial window
+        __syncwarp();
+        cb->flush(cols, capacity, lane, out);
+        __syncwarp();
+    }
     return cnt;
 }
 
@@ -429,35 +411,35 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, co
     }
 }
 
-template <int MODE, int NCAP, bool GBS, bool STMAX, bool BULK>
+template <int MODE, int NCAP, bool GBS, bool STMAX, bool COMB>
 __device__ __forceinline__ void write_tile(const DevSpace& S, const TileGeom& G, Walker& W, uint32_t t, uint64_t pos,
                                            uint32_t lane, uint64_t out, const Cols& cols, uint64_t capacity,
-                                           BulkStager<MODE == 2 ? 8 : 1>* bs) {
+                                           Combiner<MODE == 2 ? 8 : 1>* cb) {
     CapAcc<NCAP> none;
     if (G.ragged(t))
-        run_tile<MODE, NCAP, true, GBS, STMAX, BULK>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
-                                                     capacity, false, bs);
+        run_tile<MODE, NCAP, true, GBS, STMAX, COMB>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
+                                                     capacity, false, cb);
     else
-        run_tile<MODE, NCAP, false, GBS, STMAX, BULK>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
-                                                      capacity, false, bs);
+        run_tile<MODE, NCAP, false, GBS, STMAX, COMB>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
+                                                      capacity, false, cb);
 }
 
 // write pass: tiles in grid-stride order (at any moment the grid writes one
 // compact window of the output columns)
-template <int MODE, int NCAP, bool BULK>
-__global__ void __launch_bounds__(kThreads, BULK ? 2 : 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+template <int MODE, int NCAP, bool COMB>
+__global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                             const uint4* __restrict__ tile_ck,
                                                             const uint32_t* __restrict__ tile_rel,
                                                             const uint32_t* __restrict__ tile_cnt,
                                                             const uint64_t* __restrict__ span_off, const Cols cols,
                                                             const uint64_t capacity) {
     constexpr int NC = MODE == 2 ? 8 : 1;
-    extern __shared__ uint64_t s_ring[];  // BULK: kWarpsPerBlock x NC x kRing
+    __shared__ uint64_t s_comb[COMB ? kWarpsPerBlock * NC * 64 : 1];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
     const TileGeom G = geom(lo, hi);
-    BulkStager<NC> bs;
-    bs.ring = s_ring + (BULK ? wid * NC * kRing : 0);
+    Combiner<NC> cb;
+    cb.buf = s_comb + (COMB ? wid * NC * 64 : 0);
     for (uint32_t t = blockIdx.x * kWarpsPerBlock + wid; t < G.n_tiles; t += n_warps) {
         if (__ldg(tile_cnt + t) == 0) continue;  // no survivor: nothing to write
         const uint64_t ts = G.start(t);
@@ -468,16 +450,15 @@ __global__ void __launch_bounds__(kThreads, BULK ? 2 : 3) write_kernel(const Dev
         // a lane past the end of the range is parked on the last index: it
         // takes part in the ballots with inactive positions
         W.restore(S, ck, pos < hi ? lane : (uint32_t)(hi - 1 - ts));
-        bs.sent = out;
+        cb.start(out);
         if (S.stage_max) {
-            if (S.gbs_mode) write_tile<MODE, NCAP, true, true, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
-            else write_tile<MODE, NCAP, false, true, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, true, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
+            else write_tile<MODE, NCAP, false, true, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
         } else {
-            if (S.gbs_mode) write_tile<MODE, NCAP, true, false, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
-            else write_tile<MODE, NCAP, false, false, BULK>(S, G, W, t, pos, lane, out, cols, capacity, &bs);
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, false, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
+            else write_tile<MODE, NCAP, false, false, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
         }
     }
-    if (BULK && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // global writes done
 }
 
 // one block: exclusive scan of the span counts into u64 offsets starting at
@@ -655,24 +636,22 @@ void* count_kernel_for(uint32_t n_cap) {
     }
 }
 
-template <int MODE, bool BULK>
+template <int MODE, bool COMB>
 void* write_kernel_for(uint32_t n_cap) {
     switch (ncap_stride_(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1, BULK>);
-        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2, BULK>);
-        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4, BULK>);
-        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8, BULK>);
+        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1, COMB>);
+        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2, COMB>);
+        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4, COMB>);
+        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8, COMB>);
     }
 }
 
-void* write_fn(me_out_mode mode, uint32_t n_cap, bool bulk) {
-    if (mode == ME_OUT_FULL) return bulk ? write_kernel_for<2, true>(n_cap) : write_kernel_for<2, false>(n_cap);
-    return bulk ? write_kernel_for<1, true>(n_cap) : write_kernel_for<1, false>(n_cap);
+void* write_fn(me_out_mode mode, uint32_t n_cap, bool comb) {
+    if (mode == ME_OUT_FULL) return comb ? write_kernel_for<2, true>(n_cap) : write_kernel_for<2, false>(n_cap);
+    return comb ? write_kernel_for<1, true>(n_cap) : write_kernel_for<1, false>(n_cap);
 }
 
-size_t write_smem(me_out_mode mode, bool bulk) {
-    return bulk ? (size_t)kWarpsPerBlock * (mode == ME_OUT_FULL ? 8 : 1) * kRing * 8 : 0;
-}
+size_t write_smem(me_out_mode, bool) { return 0; }
 
 }  // namespace
 
@@ -683,10 +662,10 @@ uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
     return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
 }
 
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool bulk) {
+int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool comb) {
     const me_out_mode mode = pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX;
-    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(mode, n_cap, bulk);
-    const size_t smem = pass == 0 ? 0 : write_smem(mode, bulk);
+    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(mode, n_cap, comb);
+    const size_t smem = pass == 0 ? 0 : write_smem(mode, comb);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess) return 1;
@@ -710,11 +689,11 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, bool bulk, Cols cols, uint64_t capacity, cudaStream_t st) {
+                         me_out_mode mode, bool comb, Cols cols, uint64_t capacity, cudaStream_t st) {
     void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
                     (void*)&tile_cnt, (void*)&span_off, (void*)&cols, (void*)&capacity};
-    void* fn = write_fn(mode, S.n_cap, bulk);
-    const size_t smem = write_smem(mode, bulk);
+    void* fn = write_fn(mode, S.n_cap, comb);
+    const size_t smem = write_smem(mode, comb);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return cudaLaunchKernel(fn, dim3(n_blocks), dim3(kThreads), args, smem, st);
 }

@@ -205,7 +205,7 @@ uint32_t ncap_stride(uint32_t n_cap);
 // tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
 uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
 // resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool bulk);
+int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool comb);
 // count pass over [lo, hi) cut into n_spans spans of whole tiles: per tile its
 // walker checkpoint {seg, j, r, span} and the rank of its first survivor in the
 // span; per span its survivor count and per-capacity counts
@@ -216,11 +216,10 @@ cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st);
 // write pass over [lo, hi): survivors of tile t stored from row
-// span_off[span(t)] + tile_rel[t]; bulk = shared-memory staging + bulk copies
-// (every column pointer 16-byte aligned)
+// span_off[span(t)] + tile_rel[t]; comb = write combining in aligned 32-row windows
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, bool bulk, Cols cols, uint64_t capacity, cudaStream_t st);
+                         me_out_mode mode, bool comb, Cols cols, uint64_t capacity, cudaStream_t st);
 // NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
 // (rank key of DESIGN.md §9); best_key / best_index initialised to ~0
 cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint64_t n_rows, uint32_t cap,
