@@ -291,6 +291,21 @@ def main():
             roof["traffic"] = t["dram_bytes_read"] + t["dram_bytes_write"]
             roof["traffic_note"] = (f"ncu DRAM bytes of the write kernel of C5 chunk {t['chunk']} "
                                     f"(algorithmic {t['algorithmic_write_bytes']} B for that launch)")
+        # integer-issue roofline of the count pass (the INT path): warp
+        # instructions per round of 32 configs from the committed ncu capture,
+        # times the configs of the step, over the count kernels' event time
+        if ncu.exists() and count_ms > 0:
+            t = json.loads(ncu.read_text())
+            ipr = t.get("instr_per_config_count")
+            if ipr:
+                clock = peaks.get("sm_max_mhz", 1965.0) * 1e6
+                issue_peak = 148 * 4 * clock
+                ach = (job_e - job_b) * args.steps / 32 * ipr / (count_ms / 1e3)
+                line_issue = {"bound": "alu", "kernel": "count_kernel<4> (count pass)",
+                              "achieved": ach, "peak": issue_peak, "unit": "warp-instr/s", "frac": ach / issue_peak,
+                              "instr_per_round_ncu": ipr,
+                              "peak_source": "148 SMs x 4 SMSPs x 1 warp-instr/cycle x sm_max_mhz"}
+                roof["count_pass_issue"] = line_issue
         mb = ROOT / "profiles" / "r1_v4" / "microbench.json"
         if mb.exists():
             w = json.loads(mb.read_text())["write_only_gbs"]

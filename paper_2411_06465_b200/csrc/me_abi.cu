@@ -106,9 +106,9 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t comb = 1;                      // write combining into aligned 32-row windows (ME_WRITE_COMB)
+    uint32_t comb = 0;                      // write combining into aligned 32-row windows (ME_WRITE_COMB=1)
     uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
-    uint32_t serial = 0;                    // 1 = count pass on the caller's stream too (ME_SERIAL)
+    uint32_t serial = 1;                    // count pass on the caller's stream (ME_SERIAL=0: own stream, overlapped)
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
     // of sub-range i (on the caller's stream).
