@@ -277,43 +277,44 @@ def main():
     n_launch = len(timings)
     survivors_local_per_step = n_local // args.steps
     peaks, peak_src = measured_peaks()
+    ncu = ROOT / "profiles" / "ncu_write_traffic.json"
+    ncu_t = json.loads(ncu.read_text()) if ncu.exists() else {}
+    # integer-issue roofline of the count pass (the INT path): warp
+    # instructions per round of 32 configs from the committed ncu capture,
+    # times this rank's configs of the timed steps, over the count kernels'
+    # CUDA-event time (serial passes, so the event time is the kernel's own)
+    issue = None
+    ipr = ncu_t.get("instr_per_config_count")
+    if ipr and count_ms > 0:
+        clock = peaks.get("sm_max_mhz", 1965.0) * 1e6
+        issue_peak = 148 * 4 * clock
+        ach = (job_e - job_b) // world * args.steps / 32 * ipr / (count_ms / 1e3)
+        issue = {"bound": "alu", "kernel": "count_kernel<4> (count pass)", "achieved": ach, "peak": issue_peak,
+                 "unit": "warp-instr/s", "frac": ach / issue_peak, "traffic": 0,
+                 "instr_per_round_ncu": ipr,
+                 "peak_source": "148 SMs x 4 SMSPs x 1 warp-instr/cycle x sm_max_mhz (MEASURED_PEAKS.json)"}
     if mode != me.ME_OUT_COUNT:
         bytes_write = survivors_local_per_step * 8 * ncols * args.steps
         achieved = bytes_write / (write_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"sweep_kernel<{2 if ncols == 8 else 1},4> (write pass)",
+        roof = {"bound": "hbm", "kernel": f"write_kernel<{2 if ncols == 8 else 1},4> (write pass)",
                 "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "traffic": None, "peak_source": f"{peak_src} hbm_gbs (copy)",
                 "algorithmic_bytes_per_launch": bytes_write / max(1, n_launch),
                 "avg_launch_ms": write_ms / max(1, n_launch)}
-        ncu = ROOT / "profiles" / "ncu_write_traffic.json"
-        if ncu.exists():  # one ncu --set full capture of one chunk (scripts/profile_chunk.py)
-            t = json.loads(ncu.read_text())
-            roof["traffic"] = t["dram_bytes_read"] + t["dram_bytes_write"]
-            roof["traffic_note"] = (f"ncu DRAM bytes of the write kernel of C5 chunk {t['chunk']} "
-                                    f"(algorithmic {t['algorithmic_write_bytes']} B for that launch)")
-        # integer-issue roofline of the count pass (the INT path): warp
-        # instructions per round of 32 configs from the committed ncu capture,
-        # times the configs of the step, over the count kernels' event time
-        if ncu.exists() and count_ms > 0:
-            t = json.loads(ncu.read_text())
-            ipr = t.get("instr_per_config_count")
-            if ipr:
-                clock = peaks.get("sm_max_mhz", 1965.0) * 1e6
-                issue_peak = 148 * 4 * clock
-                ach = (job_e - job_b) * args.steps / 32 * ipr / (count_ms / 1e3)
-                line_issue = {"bound": "alu", "kernel": "count_kernel<4> (count pass)",
-                              "achieved": ach, "peak": issue_peak, "unit": "warp-instr/s", "frac": ach / issue_peak,
-                              "instr_per_round_ncu": ipr,
-                              "peak_source": "148 SMs x 4 SMSPs x 1 warp-instr/cycle x sm_max_mhz"}
-                roof["count_pass_issue"] = line_issue
+        if ncu_t:  # one ncu --set full capture of one chunk (scripts/profile_chunk.py)
+            roof["traffic"] = ncu_t["dram_bytes_read"] + ncu_t["dram_bytes_write"]
+            roof["traffic_note"] = (f"ncu DRAM bytes of the write kernel of C5 chunk {ncu_t['chunk']} "
+                                    f"(algorithmic {ncu_t['algorithmic_write_bytes']} B for that launch)")
         mb = ROOT / "profiles" / "r1_v4" / "microbench.json"
         if mb.exists():
             w = json.loads(mb.read_text())["write_only_gbs"]
             roof["write_only_peak_gbs"] = w
             roof["frac_of_write_only"] = achieved / w
+        if issue:
+            roof["count_pass_issue"] = issue
     else:
-        roof = {"bound": "alu", "kernel": "sweep_kernel<0,4> (count pass)", "achieved": None, "peak": None,
-                "unit": "warp-instr/s", "frac": None, "traffic": None}
+        roof = issue or {"bound": "alu", "kernel": "count_kernel<4> (count pass)", "achieved": None, "peak": None,
+                         "unit": "warp-instr/s", "frac": None, "traffic": 0}
     line = {
         "metric": "estimator configs/sec", "value": value, "unit": "configs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
