@@ -53,6 +53,7 @@ class Space:
     thr_num: int = 4
     thr_den: int = 5
     stage_max: int = 0  # 1 = NEXT-1: feasibility of the largest pipeline stage
+    zero_stage: int = 0  # NEXT-4: 2 / 3 = gradients / also weights sharded with the optimizer
     name: str = ""
 
     @property

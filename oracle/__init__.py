@@ -44,7 +44,7 @@ class Model(ctypes.Structure):
 class Cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in ("d", "t", "p", "c", "b", "s", "gbs", "L0")] + [
         ("rc", ctypes.c_uint8), ("dopt", ctypes.c_uint8), ("uneven", ctypes.c_uint8),
-        ("pad_", ctypes.c_uint8)]
+        ("zero", ctypes.c_uint8)]
 
 
 class Breakdown(ctypes.Structure):
@@ -69,7 +69,7 @@ class SpaceC(ctypes.Structure):
                 ("uneven", ctypes.c_uint8), ("stage_max", ctypes.c_uint8),
                 ("gbs", ctypes.c_uint32), ("max_t", ctypes.c_uint32), ("max_c", ctypes.c_uint32),
                 ("max_p", ctypes.c_uint32), ("thr_num", ctypes.c_uint32),
-                ("thr_den", ctypes.c_uint32)]
+                ("thr_den", ctypes.c_uint32), ("zero_stage", ctypes.c_uint32)]
 
 
 _lib = None
@@ -135,8 +135,8 @@ def activation_per_layer(shape, s, b):
     return _scalar(lib().or_activation_per_layer, shape, s, b)
 
 
-def make_cfg(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0) -> Cfg:
-    return Cfg(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, 0)
+def make_cfg(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0, zero=0) -> Cfg:
+    return Cfg(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, zero)
 
 
 def first_stage_layers(shape, **cfg):
@@ -201,7 +201,7 @@ class _SpaceHolder:
         self.c = SpaceC(self.models, len(sp.models), self.world, len(sp.world), self.caps, len(cb),
                         sp.gpus_per_node, self.mbs, len(sp.mbs), self.seq, len(sp.seq),
                         sp.rc_mask, sp.do_mask, sp.uneven, getattr(sp, "stage_max", 0), sp.gbs, sp.max_t, sp.max_c,
-                        sp.max_p, sp.thr_num, sp.thr_den)
+                        sp.max_p, sp.thr_num, sp.thr_den, getattr(sp, "zero_stage", 0))
 
 
 def space_size(sp) -> int:

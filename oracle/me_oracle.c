@@ -210,6 +210,7 @@ static int cfg_check(const or_model* m, const or_cfg* c) {
     int st = model_ok(m);
     if (st) return st;
     if (!c || !c->d || !c->t || !c->p || !c->c || !c->b || !c->s) return OR_EINVAL;
+    if (c->zero > 3) return OR_EINVAL;
     /* R10: t | k (then t | a because k | a), t | v, t | h_ffn */
     if (m->k % c->t || m->v % c->t || m->f % c->t) return OR_EDIV;
     /* Eq.17: c splits the sequence */
@@ -224,6 +225,27 @@ static int cfg_check(const or_model* m, const or_cfg* c) {
 /* ------------------------------------------------------------------ */
 /* Eq.18 with its parts                                                */
 /* ------------------------------------------------------------------ */
+
+/* Model-state bytes of a stage holding psi parameters: the ledger of
+ * P:192-199 (weight BF16 2 B, gradient FP32 4 B, Adam master / momentum /
+ * variance FP32 4 + 4 + 4 B).  Distributed optimizer (Eq.5 / Eq.10): the
+ * 12-byte optimizer states are divided among the d*c ranks -- the largest rank
+ * holds ceil(psi / (d c)) whole parameters (R8); gradients and weights stay
+ * replicated (R9).  Off: Eq.4, 18 B per parameter (R21).  NEXT-4 extension
+ * (ZeRO): zero = 2 also divides the gradients, zero = 3 also
+ * the weights, with the same ceil rule. */
+static void model_state_bytes(rat psi, const or_cfg* c, rat* params, rat* grads, rat* optim) {
+    *params = rmul(RI(2), psi);
+    *grads = rmul(RI(4), psi);
+    *optim = rmul(RI(12), psi);
+    if (c->dopt) {
+        rat share = rdiv(psi, RI((i128)c->d * c->c)); /* Psi_s / (d c) */
+        i128 ceil_share = (share.n + share.d - 1) / share.d;
+        *optim = rmul(RI(12), RI(ceil_share));
+        if (c->zero >= 2) *grads = rmul(RI(4), RI(ceil_share));
+        if (c->zero >= 3) *params = rmul(RI(2), RI(ceil_share));
+    }
+}
 int or_estimate(const or_model* m, const or_cfg* c, or_breakdown* out) {
     int st = cfg_check(m, c);
     if (st) return st;
@@ -245,17 +267,8 @@ int or_estimate(const or_model* m, const or_cfg* c, or_breakdown* out) {
      * is off (R21) */
     rat psi = psi_stage0(m, c->t, c->p, L0);
     uint64_t psi_s = to_u64(psi, &bad);
-    rat params = rmul(RI(2), psi);
-    rat grads = rmul(RI(4), psi);
-    rat optim;
-    if (c->dopt) {
-        rat share = rdiv(psi, RI((i128)c->d * c->c)); /* Psi_s / (d c) */
-        /* R8: the largest d*c rank holds ceil(Psi_s/(d c)) whole parameters */
-        i128 ceil_share = (share.n + share.d - 1) / share.d;
-        optim = rmul(RI(12), RI(ceil_share));
-    } else {
-        optim = rmul(RI(12), psi);
-    }
+    rat params, grads, optim;
+    model_state_bytes(psi, c, &params, &grads, &optim);
 
     /* activations: Eq.17, generalised per DESIGN.md §3:
      *   sbh/(tc) * ( (12 + 4k/a + 8h_ffn/h) n_inf L0 + 8 n_inf + delta_{p,1} 4(1 + v/h) )
@@ -341,13 +354,8 @@ int or_estimate_stage(const or_model* m, const or_cfg* c, uint32_t i, or_breakdo
     if (first && last) psi = radd(radd(rdiv(rmul(RI(2), rmul(h, v)), T), h), layer_part); /* Eq.6 */
     else if (first) psi = radd(rdiv(rmul(h, v), T), layer_part);   /* Eq.7 */
     else if (last) psi = radd(radd(rdiv(rmul(h, v), T), h), layer_part); /* Eq.9 */
-    rat params = rmul(RI(2), psi), grads = rmul(RI(4), psi), optim;
-    if (c->dopt) {
-        rat share = rdiv(psi, RI((i128)c->d * c->c));
-        optim = rmul(RI(12), RI((share.n + share.d - 1) / share.d)); /* R8 */
-    } else {
-        optim = rmul(RI(12), psi);
-    }
+    rat params, grads, optim;
+    model_state_bytes(psi, c, &params, &grads, &optim);
     rat sbh_tc = R((i128)c->s * c->b * m->h, (i128)c->t * c->c);
     rat br = eq12_bracket(m);
     rat layers = c->rc ? rmul(sbh_tc, radd(RI((i128)2 * n_i * Li), br))
@@ -455,7 +463,7 @@ static int space_ok(const or_space* sp) {
         !sp->n_mbs || !sp->seq || !sp->n_seq)
         return OR_EINVAL;
     if (sp->n_caps > 8 || (sp->n_caps && !sp->cap_bytes)) return OR_EINVAL;
-    if (!(sp->rc_mask & 3) || !(sp->do_mask & 3)) return OR_EINVAL;
+    if (!(sp->rc_mask & 3) || !(sp->do_mask & 3) || sp->zero_stage > 3) return OR_EINVAL;
     if (!sp->thr_num || !sp->thr_den || sp->thr_num > 1024 || sp->thr_den > 1024) return OR_EINVAL;
     for (uint32_t i = 0; i < sp->n_models; i++)
         if (model_ok(&sp->models[i])) return OR_EINVAL;
@@ -569,6 +577,7 @@ static void walk(walk_t* w) {
                                     c.b = b; c.s = s; c.gbs = sp->gbs; c.L0 = 0;
                                     c.rc = (uint8_t)rc; c.dopt = (uint8_t)dopt;
                                     c.uneven = sp->uneven;
+                                    c.zero = (uint8_t)sp->zero_stage;
                                     if (w->decode_only) {
                                         w->dec_model = mi;
                                         w->dec_world = sp->world[ni];
@@ -653,6 +662,7 @@ int or_points(const or_space* sp, const uint64_t* points, uint64_t n, or_breakdo
                                     c.b = b; c.s = s; c.gbs = sp->gbs;
                                     c.rc = (uint8_t)rc; c.dopt = (uint8_t)dopt;
                                     c.uneven = sp->uneven;
+                                    c.zero = (uint8_t)sp->zero_stage;
                                     or_breakdown r;
                                     st = sp->stage_max ? or_estimate_max(m, &c, &r, NULL)
                                                        : or_estimate(m, &c, &r);

@@ -48,7 +48,9 @@ typedef struct {
     uint8_t rc;       /* 1 = full recompute (R20, not in the paper) */
     uint8_t dopt;     /* 1 = distributed optimizer (Eq.5/10), 0 = Eq.4 */
     uint8_t uneven;   /* 1 = allow p not dividing L (R19) */
-    uint8_t pad_;
+    uint8_t zero;     /* NEXT-4 (extension): with dopt, 0/1 = optimizer states
+                         sharded over d*c (the paper, ZeRO stage 1); 2 = also the
+                         FP32 gradients; 3 = also the BF16 weights (ZeRO-2/3) */
 } or_cfg;
 
 /* Eq.18 split into the ledger of P:192-199 and the three activation groups. */
@@ -68,6 +70,7 @@ typedef struct {
                                                     stage_max: 1 = largest pipeline stage (NEXT-1) */
     uint32_t gbs, max_t, max_c, max_p;           /* 0 = unlimited */
     uint32_t thr_num, thr_den;                   /* feasible <=> total*den <= cap*num */
+    uint32_t zero_stage;                         /* or_cfg.zero of every configuration */
 } or_space;
 
 /* Eq.1, Eq.2, Eq.3 */

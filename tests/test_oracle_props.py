@@ -234,3 +234,37 @@ def test_points_match_sweep(oracle_mod):
     r2, m2 = oracle_mod.points(sp, pick[::-1])
     assert (r2[::-1] == rows[::97]).all()
     assert (m2[::-1] == (idx[::97] >> np.uint64(56))).all()
+
+
+def test_zero_stages(oracle_mod):
+    """NEXT-4 byte policies: ZeRO stage 1 (the paper's distributed optimizer),
+    2 (+ FP32 gradients) and 3 (+ BF16 weights) sharded over d*c.  Pins: the
+    ZeRO per-device model-state formulas (P:53, P:188 cite ZeRO) with this
+    ledger's FP32 gradients -- stage 1: (2 + 4) Psi + 12 Psi / N_d, stage 2:
+    2 Psi + (4 + 12) Psi / N_d, stage 3: (2 + 4 + 12) Psi / N_d -- exact when
+    N_d = d c divides Psi, the largest contiguous shard otherwise; stage 1 is
+    the paper's estimate; N_d = 1 reduces every stage to Eq.4."""
+    o = oracle_mod
+    for shape in (M8, M70, (16, 24, 4, 4, 2, 32)):
+        for d, t, p, c in ((1, 1, 1, 1), (8, 1, 1, 1), (4, 2, 2, 2), (3, 1, 2, 1), (5, 2, 1, 1)):
+            kw = dict(d=d, t=t, p=p, c=c, b=1, s=16)
+            base = o.estimate(shape, **kw)
+            psi = base["params"] // 2
+            nd = d * c
+            share = -(-psi // nd)
+            assert o.estimate(shape, zero=1, **kw) == base
+            z2 = o.estimate(shape, zero=2, **kw)
+            z3 = o.estimate(shape, zero=3, **kw)
+            assert (z2["params"], z2["grads"], z2["optim"]) == (2 * psi, 4 * share, 12 * share)
+            assert (z3["params"], z3["grads"], z3["optim"]) == (2 * share, 4 * share, 12 * share)
+            if psi % nd == 0:
+                assert 18 * psi == (z3["params"] + z3["grads"] + z3["optim"]) * nd
+                assert z2["params"] + z2["grads"] + z2["optim"] == 2 * psi + 16 * psi // nd
+            for z in (z2, z3):  # activations untouched
+                assert (z["act_layers"], z["act_embed"], z["act_head"]) == \
+                    (base["act_layers"], base["act_embed"], base["act_head"])
+            if nd == 1:
+                assert z2 == base and z3 == base
+            # without the distributed optimizer the stage is irrelevant (Eq.4)
+            off = o.estimate(shape, dopt=0, **kw)
+            assert o.estimate(shape, dopt=0, zero=3, **kw) == off
