@@ -63,12 +63,16 @@ typedef struct {
  *                      (= L when p = 1)
  *  recompute           1 = full activation recompute (R20, extension)
  *  dist_opt            1 = distributed optimizer, 12 B/param sharded over d*c
- *                      (Eq.5, Eq.10; ceil rule R8); 0 = Eq.4 (18 B/param) */
+ *                      (Eq.5, Eq.10; ceil rule R8); 0 = Eq.4 (18 B/param)
+ *  zero_stage          see the field (ME_EINVAL above 3) */
 typedef struct {
     uint32_t dp, tp, pp, cp, mbs, seq;
     uint32_t gbs;
     uint32_t first_stage_layers;
-    uint8_t recompute, dist_opt, allow_uneven_pp, _pad;
+    uint8_t recompute, dist_opt, allow_uneven_pp;
+    uint8_t zero_stage; /* NEXT-4, with dist_opt: 0/1 = optimizer states sharded
+                           over d*c (the paper); 2 = also the FP32 gradients;
+                           3 = also the BF16 weights (ZeRO-2/3, extension) */
 } me_parallel;
 
 /* Stage-0 per-GPU bytes (Eq.18 split by the ledger of P:192-199):
@@ -113,6 +117,7 @@ typedef struct {
     uint32_t n_seq;
     uint8_t recompute_mask, dist_opt_mask, allow_uneven_pp, stage_policy;
     uint32_t gbs, max_tp, max_cp, max_pp;
+    uint32_t zero_stage; /* me_parallel.zero_stage of every configuration (0..3) */
 } me_cfg_range;
 
 /* Output modes of a sweep:

@@ -32,8 +32,8 @@ def version() -> str:
     return lib().me_version().decode()
 
 
-def _parallel(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0) -> me_parallel:
-    return me_parallel(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, 0)
+def _parallel(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0, zero=0) -> me_parallel:
+    return me_parallel(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, zero)
 
 
 def me_estimate(shape, **cfg) -> Dict[str, int]:
@@ -89,7 +89,7 @@ class _SpaceC:
         self.cl = me_cluster(self.world, len(sp.world), self.caps, len(cb), sp.gpus_per_node)
         self.cr = me_cfg_range(self.mbs, len(sp.mbs), self.seq, len(sp.seq), sp.rc_mask, sp.do_mask, sp.uneven,
                                getattr(sp, "stage_max", 0),
-                               sp.gbs, sp.max_t, sp.max_c, sp.max_p)
+                               sp.gbs, sp.max_t, sp.max_c, sp.max_p, getattr(sp, "zero_stage", 0))
         self.thr = me_threshold(sp.thr_num, sp.thr_den)
         self.n_cap = len(cb)
 

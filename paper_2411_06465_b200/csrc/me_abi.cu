@@ -220,6 +220,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.n_cap = (uint32_t)H.caps.size();
     D.gbs_mode = H.gbs ? 1u : 0u;
     D.stage_max = H.stage_max ? 1u : 0u;
+    D.zero_stage = H.zero_stage;
     for (int q = 0; q < 8; q++) D.thr[q] = 0;
     D.thr_max = 0;
     for (size_t q = 0; q < H.caps.size(); q++) {

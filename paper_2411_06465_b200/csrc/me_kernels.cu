@@ -48,7 +48,7 @@ struct LaneRow {
     uint64_t ms;        // params + grads + optim for this lane's do
     uint64_t a, b;      // per-token activation bytes = n_inf * a + b (this lane's rc)
     uint64_t kp;        // p * a + b (paper mode: n_inf = p)
-    uint64_t psi;       // Psi_s
+    uint64_t par, gra;  // weight / gradient bytes for this lane's do (and the ZeRO stage)
     uint64_t optim;     // optimizer bytes for this lane's do
     uint64_t lam, mu;   // per-token layer bytes = n_inf * lam + mu
     uint64_t e8, hc;    // per-token embedding bytes = n_inf * e8; head bytes = hc
@@ -56,20 +56,22 @@ struct LaneRow {
     // NEXT-1 (stage_max): the last pipeline stage (p >= 2), one microbatch in
     // flight: total = msL + u * kL, layers = u * layL, head = u * hcL
     bool two;
-    uint64_t msL, kL, psiL, optimL, layL, hcL;
+    uint64_t msL, kL, parL, graL, optimL, layL, hcL;
 };
 
 __device__ __forceinline__ void make_lane_row(const DevModel& M, uint32_t t, uint32_t c, uint32_t p, uint32_t d,
-                                              uint32_t rc, uint32_t dopt, bool stage_max, LaneRow& L) {
+                                              uint32_t rc, uint32_t dopt, bool stage_max, uint32_t zero,
+                                              LaneRow& L) {
     RowCoef R;
     const uint32_t L0 = p == 1 ? M.layers : div_u32(M.layers + p - 1, p);
-    make_row(M, t, c, p, d, L0, R);
+    make_row(M, t, c, p, d, L0, zero, R);
     L.two = stage_max && p >= 2;
     if (L.two) {
         // the last stage holds floor((L - L0) / (p - 1)) layers
         const uint32_t Ll = (M.layers - L0) / (p - 1);
-        const TermsT<uint64_t> T = stage_terms<uint64_t>(M, t, c, d, false, true, Ll, 1u, 1u, rc, dopt);
-        L.psiL = T.params >> 1;
+        const TermsT<uint64_t> T = stage_terms<uint64_t>(M, t, c, d, false, true, Ll, 1u, 1u, rc, dopt, zero);
+        L.parL = T.params;
+        L.graL = T.grads;
         L.optimL = T.optim;
         L.msL = T.params + T.grads + T.optim;
         L.layL = T.layers;
@@ -80,7 +82,8 @@ __device__ __forceinline__ void make_lane_row(const DevModel& M, uint32_t t, uin
     L.a = (rc ? R.lam1 : R.lam0) + R.e8;
     L.b = rc ? R.bt + R.hc : R.hc;
     L.kp = (uint64_t)p * L.a + L.b;
-    L.psi = R.psi;
+    L.par = dopt ? R.par1 : 2ull * R.psi;
+    L.gra = dopt ? R.gra1 : 4ull * R.psi;
     L.optim = dopt ? R.optim1 : 12ull * R.psi;
     L.lam = rc ? R.lam1 : R.lam0;
     L.mu = rc ? R.bt : 0ull;
@@ -113,7 +116,7 @@ struct Walker {
         const uint2 b = __ldg(reinterpret_cast<const uint2*>(S.tuples + tid) + 2);  // w pair_off
         w = b.x;
         pp = reinterpret_cast<const uint2*>(S.pairs) + b.y + (r >> S.lg_rcdo);
-        make_lane_row(M, a.x, a.y, a.z, a.w, rc, dopt, S.stage_max != 0, L);
+        make_lane_row(M, a.x, a.y, a.z, a.w, rc, dopt, S.stage_max != 0, S.zero_stage, L);
     }
 
     __device__ __forceinline__ void set_digits(const DevSpace& S) {
@@ -281,9 +284,8 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
                     uint64_t v[NC];
                     v[0] = pos | ((uint64_t)mask << 56);
                     if (MODE == 2) {
-                        const uint64_t psi = STMAX && last ? W.L.psiL : W.L.psi;
-                        v[1] = 2ull * psi;
-                        v[2] = 4ull * psi;
+                        v[1] = STMAX && last ? W.L.parL : W.L.par;
+                        v[2] = STMAX && last ? W.L.graL : W.L.gra;
                         v[3] = STMAX && last ? W.L.optimL : W.L.optim;
                         v[4] = (uint64_t)u * (STMAX && last ? W.L.layL : (uint64_t)n_inf * W.L.lam + W.L.mu);
                         v[5] = STMAX && last ? 0ull : (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
@@ -523,7 +525,7 @@ __device__ int estimate_one(const me_model& Min, const me_parallel& P, me_breakd
     if (!M.hidden || !M.ffn_hidden || !M.layers || !M.heads || !M.kv_heads || !M.vocab)
         return ME_EINVAL;
     if (M.heads % M.kv_heads || M.hidden % M.heads) return ME_EINVAL;
-    if (!P.dp || !P.tp || !P.pp || !P.cp || !P.mbs || !P.seq) return ME_EINVAL;
+    if (!P.dp || !P.tp || !P.pp || !P.cp || !P.mbs || !P.seq || P.zero_stage > 3) return ME_EINVAL;
     const uint32_t t = P.tp, c = P.cp, p = P.pp, d = P.dp, L = M.layers;
     if (M.kv_heads % t || M.vocab % t || M.ffn_hidden % t) return ME_EDIV;  // R10
     if (P.seq % c) return ME_EDIV;
@@ -544,12 +546,12 @@ __device__ int estimate_one(const me_model& Min, const me_parallel& P, me_breakd
     // come from the same u64 code the sweep runs
     const DevModel DM = dev_model(M);
     RowCoefT<unsigned __int128> W;
-    make_row(DM, t, c, p, d, L0, W);
+    make_row(DM, t, c, p, d, L0, (uint32_t)P.zero_stage, W);
     const TermsT<unsigned __int128> T2 = config_terms(W, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u);
     const unsigned __int128 lim = (unsigned __int128)1 << 63;
     if (W.psi >= lim || W.ms0 >= lim || T2.total >= lim) return ME_EOVERFLOW;
     RowCoef R;
-    make_row(DM, t, c, p, d, L0, R);
+    make_row(DM, t, c, p, d, L0, (uint32_t)P.zero_stage, R);
     const TermsT<uint64_t> T = config_terms(R, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u);
     out.params = T.params;
     out.grads = T.grads;
@@ -583,9 +585,10 @@ __device__ int estimate_stage_one(const me_model& M, const me_parallel& P, uint3
         const uint32_t n_i = (uint32_t)((uint64_t)(p - i) < m ? (uint64_t)(p - i) : m);
         const uint32_t rc = P.recompute ? 1u : 0u, dopt = P.dist_opt ? 1u : 0u;
         const TermsT<unsigned __int128> W = stage_terms<unsigned __int128>(DM, t, c, d, i == 0, i == p - 1, Li, n_i,
-                                                                           u, rc, dopt);
+                                                                           u, rc, dopt, P.zero_stage);
         if (W.total >= lim) return ME_EOVERFLOW;
-        const TermsT<uint64_t> T = stage_terms<uint64_t>(DM, t, c, d, i == 0, i == p - 1, Li, n_i, u, rc, dopt);
+        const TermsT<uint64_t> T = stage_terms<uint64_t>(DM, t, c, d, i == 0, i == p - 1, Li, n_i, u, rc, dopt,
+                                                         P.zero_stage);
         if (!have || T.total > out.total) {
             out = me_breakdown{T.params, T.grads, T.optim, T.layers, T.embed, T.head, T.total};
             which = i;

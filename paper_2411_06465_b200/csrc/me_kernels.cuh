@@ -37,6 +37,7 @@ struct DevSpace {
     uint32_t n_cap;
     uint32_t gbs_mode;            // 1 = a global batch bounds the in-flight microbatches (R17)
     uint32_t stage_max;           // 1 = feasibility of the largest pipeline stage (NEXT-1)
+    uint32_t zero_stage;          // 2 / 3 = gradients / also weights sharded with the optimizer (NEXT-4)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
     uint64_t thr_max;             // the largest threshold: survivor <=> total <= thr_max
 };
@@ -47,6 +48,8 @@ template <typename U>
 struct RowCoefT {
     U psi;        // Psi_s, Eq.6 (p = 1) / Eq.7 (p > 1) with L/p -> L0
     U optim1;     // 12 ceil(Psi_s / (d c))   (Eq.10 + reading R8)
+    U par1, gra1; // weight / gradient bytes with the distributed optimizer: 2 Psi_s / 4 Psi_s
+                  // (R9), or 2 / 4 ceil(Psi_s / (d c)) at ZeRO stage 3 / >= 2 (NEXT-4)
     U ms0, ms1;   // model-state bytes with the distributed optimizer off / on
     U lam0;       // L0 * B_t                 (rc = 0 layer bytes per token per mb)
     U lam1;       // 2 ht L0                  (rc = 1: kept layer inputs, R20)
@@ -72,7 +75,7 @@ __device__ __forceinline__ uint32_t div_u32(uint32_t x, uint32_t d) {
 // (t | k | a | h, t | v, t | h_ffn) except the optimizer ceil (R8).
 template <typename U>
 __device__ __forceinline__ void make_row(const DevModel& M, uint32_t t, uint32_t c, uint32_t p,
-                                         uint32_t d, uint32_t L0, RowCoefT<U>& R) {
+                                         uint32_t d, uint32_t L0, uint32_t zero, RowCoefT<U>& R) {
     const uint32_t h = M.hidden;
     const uint32_t hd = M.head_dim;
     uint32_t ht, kt, vt, ft;
@@ -102,8 +105,10 @@ __device__ __forceinline__ void make_row(const DevModel& M, uint32_t t, uint32_t
         share = (R.psi + dc - 1) / dc;
     }
     R.optim1 = (U)12 * share;
+    R.par1 = zero >= 3 ? (U)2 * share : (U)2 * R.psi;
+    R.gra1 = zero >= 2 ? (U)4 * share : (U)4 * R.psi;
     R.ms0 = (U)18 * R.psi;
-    R.ms1 = (U)6 * R.psi + R.optim1;
+    R.ms1 = R.par1 + R.gra1 + R.optim1;
     R.bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft;
     R.lam0 = (U)L0 * R.bt;
     R.lam1 = (U)2 * ht * L0;
@@ -125,7 +130,7 @@ struct TermsT {
 template <typename U>
 __device__ __forceinline__ TermsT<U> stage_terms(const DevModel& M, uint32_t t, uint32_t c, uint32_t d, bool first,
                                                  bool last, uint32_t Li, uint32_t n_i, uint32_t u, uint32_t rc,
-                                                 uint32_t dopt) {
+                                                 uint32_t dopt, uint32_t zero) {
     const uint32_t h = M.hidden, hd = M.head_dim;
     const uint32_t ht = div_u32(h, t), kt = div_u32(M.kv_heads, t), vt = div_u32(M.vocab, t),
                    ft = div_u32(M.ffn_hidden, t);
@@ -136,8 +141,8 @@ __device__ __forceinline__ TermsT<U> stage_terms(const DevModel& M, uint32_t t, 
     const U share = (psi + dc - 1) / dc;
     const U bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft;
     TermsT<U> T;
-    T.params = (U)2 * psi;
-    T.grads = (U)4 * psi;
+    T.params = dopt && zero >= 3 ? (U)2 * share : (U)2 * psi;
+    T.grads = dopt && zero >= 2 ? (U)4 * share : (U)4 * psi;
     T.optim = dopt ? (U)12 * share : (U)12 * psi;
     T.layers = (U)u * (rc ? (U)2 * ht * n_i * Li + bt : (U)n_i * Li * bt);
     T.embed = first ? (U)u * ((U)8 * ht * n_i) : (U)0;
@@ -163,8 +168,8 @@ __device__ __forceinline__ TermsT<U> config_terms_no_total(const RowCoefT<U>& R,
                                                            uint32_t rc, uint32_t dopt) {
     const uint32_t n_inf = min(R.p, m);
     TermsT<U> T;
-    T.params = (U)2 * R.psi;
-    T.grads = (U)4 * R.psi;
+    T.params = dopt ? R.par1 : (U)2 * R.psi;
+    T.grads = dopt ? R.gra1 : (U)4 * R.psi;
     T.optim = dopt ? R.optim1 : (U)12 * R.psi;
     T.layers = (U)u * (rc ? ((U)n_inf * R.lam1 + R.bt) : (U)n_inf * R.lam0);
     T.embed = (U)u * ((U)n_inf * R.e8);
@@ -180,8 +185,8 @@ __device__ __forceinline__ TermsT<U> config_terms(const RowCoefT<U>& R, uint32_t
                                                   uint32_t rc, uint32_t dopt) {
     const uint32_t n_inf = min(R.p, m);
     TermsT<U> T;
-    T.params = (U)2 * R.psi;
-    T.grads = (U)4 * R.psi;
+    T.params = dopt ? R.par1 : (U)2 * R.psi;
+    T.grads = dopt ? R.gra1 : (U)4 * R.psi;
     T.optim = dopt ? R.optim1 : (U)12 * R.psi;
     T.layers = (U)u * (rc ? ((U)n_inf * R.lam1 + R.bt) : (U)n_inf * R.lam0);
     T.embed = (U)u * ((U)n_inf * R.e8);

@@ -39,6 +39,8 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
     uneven = cr->allow_uneven_pp ? 1 : 0;
     if (cr->stage_policy > 1) return fail(detail, ME_EINVAL, "stage_policy must be 0 or 1");
     stage_max = cr->stage_policy;
+    if (cr->zero_stage > 3) return fail(detail, ME_EINVAL, "zero_stage must be 0..3");
+    zero_stage = (uint8_t)cr->zero_stage;
 
     for (size_t i = 0; i < models.size(); i++) {
         const me_model& m = models[i];
@@ -228,6 +230,7 @@ int HostSpace::decode(uint64_t index, uint32_t* model_id, uint32_t* world_size,
     c.recompute = (uint8_t)((rcdo_rc >> sel) & 1);
     c.dist_opt = (uint8_t)((rcdo_do >> sel) & 1);
     c.allow_uneven_pp = uneven;
+    c.zero_stage = zero_stage;
     if (model_id) *model_id = mdl;
     if (world_size) *world_size = world[n];
     if (out) *out = c;

@@ -52,7 +52,7 @@ class HostSpace {
     std::vector<uint32_t> world, mbs, seq;
     std::vector<uint64_t> caps;
     uint32_t gpus_per_node = 0, gbs = 0, max_t = 0, max_c = 0, max_p = 0;
-    uint8_t rc_mask = 0, do_mask = 0, uneven = 0, stage_max = 0;
+    uint8_t rc_mask = 0, do_mask = 0, uneven = 0, stage_max = 0, zero_stage = 0;
     // (rc, do) digits of the innermost axes
     uint32_t n_rcdo = 0, lg_rcdo = 0, rcdo_rc = 0, rcdo_do = 0;
 

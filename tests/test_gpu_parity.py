@@ -286,3 +286,36 @@ def test_sweep_stage_max(me, oracle_mod, name, mode):
         import dataclasses
         r0 = me.Plan(dataclasses.replace(sp, stage_max=0)).sweep(mode=me.ME_OUT_COUNT)
         assert r0.counts()[0] != res.counts()[0]
+
+
+# ---------------------------------------------------------------- NEXT-4: ZeRO stages
+def test_estimate_zero_stages(me, oracle_mod):
+    rng = np.random.default_rng(29)
+    shapes = mi.random_models(10, seed=31) + [mi.PRESETS["llama3.1-70b"]]
+    caps = [40 << 30, 80 << 30]
+    for shape in shapes:
+        cfgs = random_cfgs(rng, shape, 60)
+        for cfg in cfgs:
+            cfg["zero"] = int(rng.integers(0, 4))
+        rows, mask, status = me.me_estimate_batch([shape], None, cfgs, caps_bytes=caps)
+        for i, cfg in enumerate(cfgs):
+            st = oracle_mod.estimate_status(shape, **cfg)
+            assert status[i] == st, (shape, cfg)
+            if st == 0:
+                e = oracle_mod.estimate(shape, **cfg)
+                assert rows[i].tolist() == [e[k] for k in oracle_mod.TERMS], (shape, cfg)
+                assert mask[i] == oracle_mod.cap_mask(e["total"], caps)
+                if cfg["p"] > 1:
+                    for stg in (0, cfg["p"] - 1):
+                        got, _ = me.me_estimate_stage(shape, stg, **cfg)
+                        assert got == oracle_mod.estimate_stage(shape, stg, **cfg)
+
+
+@pytest.mark.parametrize("zero", [2, 3])
+@pytest.mark.parametrize("stage_max", [0, 1])
+def test_sweep_zero_stages(me, oracle_mod, zero, stage_max):
+    sp = mi.Space(models=mi.random_models(12, seed=37) + [mi.PRESETS["llama3.1-8b"]], world=[16, 24, 128],
+                  caps_gb=[40, 80, 192], mbs=[1, 2, 4], seq=[4096, 16384], uneven=1, zero_stage=zero,
+                  stage_max=stage_max)
+    res = me.Plan(sp).sweep(mode=me.ME_OUT_FULL)
+    assert_same(me, res, *oracle_rows(oracle_mod, sp), me.ME_OUT_FULL)
