@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--mode", default="full", choices=["full", "index", "count"])
+    ap.add_argument("--mode", default="full", choices=["records", "full", "index", "count"])
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -193,8 +193,10 @@ def main():
     dev = local
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    mode = {"full": me.ME_OUT_FULL, "index": me.ME_OUT_INDEX, "count": me.ME_OUT_COUNT}[args.mode]
-    ncols = {me.ME_OUT_FULL: 8, me.ME_OUT_INDEX: 1, me.ME_OUT_COUNT: 0}[mode]
+    mode = {"records": me.ME_OUT_RECORDS, "full": me.ME_OUT_FULL, "index": me.ME_OUT_INDEX,
+            "count": me.ME_OUT_COUNT}[args.mode]
+    # u64 words written per survivor (FULL: 8 columns, RECORDS: one 64-byte row)
+    ncols = {me.ME_OUT_RECORDS: 8, me.ME_OUT_FULL: 8, me.ME_OUT_INDEX: 1, me.ME_OUT_COUNT: 0}[mode]
 
     sp = mi.config(args.workload)
     stream = torch.cuda.Stream(device=dev)
@@ -210,7 +212,7 @@ def main():
         calls.append((s, e))
         s = e
     comm = me.Comm(dev) if world > 1 else None
-    ring = [[torch.empty(CHUNK + 64, dtype=torch.int64, device=dev) for _ in range(ncols)] for _ in range(2)]
+    ring = [out_buffers(torch, me, mode, CHUNK + 64, device=dev) for _ in range(2)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(collect=None):
@@ -296,7 +298,7 @@ def main():
     if mode != me.ME_OUT_COUNT:
         bytes_write = survivors_local_per_step * 8 * ncols * args.steps
         achieved = bytes_write / (write_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"write_kernel<{2 if ncols == 8 else 1},4> (write pass)",
+        roof = {"bound": "hbm", "kernel": f"write_kernel<{int(mode)},4> (write pass)",
                 "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "traffic": None, "peak_source": f"{peak_src} hbm_gbs (copy)",
                 "algorithmic_bytes_per_launch": bytes_write / max(1, n_launch),
@@ -354,14 +356,26 @@ def main():
     return 0
 
 
+def out_buffers(torch, me, mode, rows, **kw):
+    """Output buffers of `rows` survivors: 8 columns (FULL; one allocation cut
+    into adjacent slices), 1 column (INDEX), one array of 64-byte records
+    (RECORDS) or none (COUNT)."""
+    if mode == me.ME_OUT_COUNT:
+        return []
+    if mode == me.ME_OUT_INDEX:
+        return [torch.empty(rows, dtype=torch.int64, **kw)]
+    flat = torch.empty(8 * rows, dtype=torch.int64, **kw)
+    return [flat] if mode == me.ME_OUT_RECORDS else list(flat.view(8, rows).unbind(0))
+
+
 def e2e_run(me, sp, dev, world, comm, calls, mode, ncols, steps, stream):
     """End to end through the C ABI: host description in, host columns out."""
     import ctypes
 
     import torch
     HOST_ROWS = 1 << 26
-    host = [torch.empty(HOST_ROWS, dtype=torch.int64, pin_memory=True) for _ in range(ncols)]
-    ring = [torch.empty(CHUNK + 64, dtype=torch.int64, device=dev) for _ in range(ncols)]
+    host = out_buffers(torch, me, mode, HOST_ROWS, pin_memory=True)
+    ring = out_buffers(torch, me, mode, CHUNK + 64, device=dev)
     h2d = d2h = 0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -372,7 +386,7 @@ def e2e_run(me, sp, dev, world, comm, calls, mode, ncols, steps, stream):
             r = plan.sweep(b, e, mode=mode, out_cols=ring if ncols else None, comm=comm)
             lo, gl, off = r.counts()
             if ncols:
-                arr = (ctypes.c_void_p * 8)(*([h.data_ptr() for h in host] + [None] * (8 - ncols)))
+                arr = (ctypes.c_void_p * 8)(*([h.data_ptr() for h in host] + [None] * (8 - len(host))))
                 for first in range(0, lo, HOST_ROWS):
                     n = min(HOST_ROWS, lo - first)
                     me.check(me.lib().me_result_copy_to_host(r.h, first, n, arr), "me_result_copy_to_host")

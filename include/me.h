@@ -121,11 +121,20 @@ typedef struct {
 } me_cfg_range;
 
 /* Output modes of a sweep:
- *  COUNT  survivor counts only (total and per capacity)
- *  INDEX  one u64 column: flat index | (capacity mask << 56)
- *  FULL   eight u64 columns (structure of arrays): index|mask, params, grads,
- *         optim, act_layers, act_embed, act_head, total */
-typedef enum { ME_OUT_COUNT = 0, ME_OUT_INDEX = 1, ME_OUT_FULL = 2 } me_out_mode;
+ *  COUNT    survivor counts only (total and per capacity)
+ *  INDEX    one u64 column: flat index | (capacity mask << 56)
+ *  FULL     eight u64 columns (structure of arrays): index|mask, params, grads,
+ *           optim, act_layers, act_embed, act_head, total
+ *  RECORDS  the same eight values per survivor as one 64-byte me_record row
+ *           (array of structures): column 0 only, 8 u64 words per row.  The
+ *           fastest FULL-content mode (one contiguous run of whole records per
+ *           warp round instead of eight short column runs). */
+typedef enum { ME_OUT_COUNT = 0, ME_OUT_INDEX = 1, ME_OUT_FULL = 2, ME_OUT_RECORDS = 3 } me_out_mode;
+
+typedef struct {
+    uint64_t index_mask; /* flat index | (capacity mask << 56) */
+    uint64_t params, grads, optim, act_layers, act_embed, act_head, total;
+} me_record;
 
 enum { ME_STAGE_FIRST = 0, ME_STAGE_MAX = 1 };
 #define ME_STAGE_ARGMAX 0xFFFFFFFFu
@@ -156,7 +165,9 @@ typedef struct {
                               columns in global order (NCCL broadcasts over NVLink) */
     uint32_t _pad;
     /* Optional caller-owned output columns: device pointers, ME_N_COLS of
-     * them for FULL, 1 for INDEX (NULL = the library allocates exactly, which
+     * them for FULL, 1 for INDEX, 1 for RECORDS (out_capacity rows of 64 B,
+     * 8-byte aligned; 32-byte alignment gives whole-sector stores)
+     * (NULL = the library allocates exactly, which
      * synchronises the host once).  With caller columns the call is fully
      * asynchronous: survivors beyond out_capacity are counted but not written
      * and me_result_status() then returns ME_ERANGE. */
@@ -231,11 +242,11 @@ int me_result_counts(me_result* r, uint64_t* local, uint64_t* global, uint64_t* 
 /* per-capacity survivor counts (n_cap entries), global when comm is set */
 int me_result_cap_counts(me_result* r, uint64_t* per_cap);
 /* device pointers of the output columns (NULL entries for COUNT mode / unused
- * columns).  With comm+gather these are the gathered global columns, else this
+ * columns; RECORDS: cols[0] = the me_record array).  With comm+gather these are the gathered global columns, else this
  * rank's.  n_rows = rows visible in those columns. */
 int me_result_columns(me_result* r, uint64_t** cols /* ME_N_COLS */, uint64_t* n_rows);
 /* copy rows [first, first+n) of the visible columns to host arrays; cols_host[j]
- * receives column j and may be NULL.  ME_ERANGE if out of bounds. */
+ * receives column j and may be NULL (RECORDS: cols_host[0] receives n records).  ME_ERANGE if out of bounds. */
 int me_result_copy_to_host(me_result* r, uint64_t first, uint64_t n, uint64_t* const* cols_host);
 /* ME_OK, or ME_ERANGE when caller columns overflowed.  Waits. */
 int me_result_status(me_result* r);

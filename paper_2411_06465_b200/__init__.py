@@ -18,7 +18,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import _abi
-from ._abi import (ME_N_COLS, ME_OUT_COUNT, ME_OUT_FULL, ME_OUT_INDEX, MEError, check, lib, me_breakdown,
+from ._abi import (ME_N_COLS, ME_OUT_COUNT, ME_OUT_FULL, ME_OUT_INDEX, ME_OUT_RECORDS, MEError, check, lib, me_breakdown,
                    me_cfg_range, me_cluster, me_model, me_model_range, me_parallel, me_sweep_opts, me_threshold)
 
 lib()  # fail at import time when libme.so is absent
@@ -180,20 +180,22 @@ class Result:
         return list(a)
 
     def columns(self):
-        """Device columns as torch int64 tensors (u64 bit patterns), or None."""
+        """Device columns as torch int64 tensors (u64 bit patterns), or None;
+        RECORDS: column 0 is an (n, 8) tensor of me_record rows."""
         ptrs = (ctypes.c_void_p * ME_N_COLS)()
         n = ctypes.c_uint64()
         check(lib().me_result_columns(self.h, ptrs, ctypes.byref(n)), "me_result_columns")
+        wd = 8 if self.mode == ME_OUT_RECORDS else 1
         out = []
         for j in range(ME_N_COLS):
             p = ptrs[j]
             if not p:
                 out.append(None)
                 continue
-            t = self.plan.alloc.tensor(p, n.value) if self.plan.alloc else None
+            t = self.plan.alloc.tensor(p, n.value * wd) if self.plan.alloc else None
             if t is None and self.user_cols is not None:
-                t = self.user_cols[j][:n.value]
-            out.append(t)
+                t = self.user_cols[j].reshape(-1)[:n.value * wd]
+            out.append(t.view(-1, 8) if wd == 8 and t is not None else t)
         return out, n.value
 
     def to_host(self, first: int = 0, n: Optional[int] = None) -> Dict[str, np.ndarray]:
@@ -202,6 +204,11 @@ class Result:
         check(lib().me_result_columns(self.h, ptrs, ctypes.byref(rows)), "me_result_columns")
         if n is None:
             n = rows.value - first
+        if self.mode == ME_OUT_RECORDS:  # one (n, 8) array of records, returned as its columns
+            rec = np.zeros((n, 8), dtype=np.uint64)
+            hp = (ctypes.c_void_p * ME_N_COLS)(*([rec.ctypes.data] + [None] * (ME_N_COLS - 1)))
+            check(lib().me_result_copy_to_host(self.h, first, n, hp), "me_result_copy_to_host")
+            return dict(zip(COLUMNS, (rec[:, j] for j in range(8))))
         ncol = 8 if self.mode == ME_OUT_FULL else (1 if self.mode == ME_OUT_INDEX else 0)
         arrays = [np.zeros(n, dtype=np.uint64) for _ in range(ncol)]
         hp = (ctypes.c_void_p * ME_N_COLS)(*([a.ctypes.data for a in arrays] + [None] * (ME_N_COLS - ncol)))
@@ -276,13 +283,14 @@ class Plan:
     def sweep(self, begin: int = 0, end: int = 0, mode: int = ME_OUT_FULL, out_cols=None, comm: Optional[Comm] = None,
               gather: bool = False) -> Result:
         """me_plan_sweep.  out_cols: optional list of torch int64 device tensors
-        (8 for FULL, 1 for INDEX) of equal length = capacity."""
+        (8 for FULL, 1 for INDEX) of equal length = capacity; RECORDS: one
+        tensor of 8 * capacity elements."""
         cols_arr = None
         cap = 0
         if out_cols is not None:
             cols_arr = (ctypes.c_void_p * ME_N_COLS)(*([t.data_ptr() for t in out_cols] +
                                                        [None] * (ME_N_COLS - len(out_cols))))
-            cap = min(t.numel() for t in out_cols)
+            cap = min(t.numel() for t in out_cols) // (8 if mode == ME_OUT_RECORDS else 1)
         o = me_sweep_opts(begin, end, mode, self.device, self.stream, _abi.me_alloc_fn(), _abi.me_free_fn(), None,
                           comm.h if comm else None, 1 if gather else 0, 0, cols_arr, cap)
         h = ctypes.c_void_p()

@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libme.so"
 
 ME_OK, ME_EINVAL, ME_EDIV, ME_EOVERFLOW, ME_ENOMEM, ME_ECUDA, ME_ENCCL, ME_ERANGE = range(8)
-ME_OUT_COUNT, ME_OUT_INDEX, ME_OUT_FULL = 0, 1, 2
+ME_OUT_COUNT, ME_OUT_INDEX, ME_OUT_FULL, ME_OUT_RECORDS = 0, 1, 2, 3
 ME_N_COLS = 8
 
 u8, u32, u64 = ctypes.c_uint8, ctypes.c_uint32, ctypes.c_uint64

@@ -221,12 +221,17 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.gbs_mode = H.gbs ? 1u : 0u;
     D.stage_max = H.stage_max ? 1u : 0u;
     D.zero_stage = H.zero_stage;
-    for (int q = 0; q < 8; q++) D.thr[q] = 0;
+    for (int q = 0; q < 8; q++) D.thr[q] = 0, D.thr1[q] = 1, D.cslot[q] = (uint32_t)q;
     D.thr_max = 0;
+    uint32_t q_max = 0;
     for (size_t q = 0; q < H.caps.size(); q++) {
         D.thr[q] = (uint64_t)(((unsigned __int128)H.caps[q] * thr.num) / thr.den);
-        if (q == 0 || D.thr[q] > D.thr_max) D.thr_max = D.thr[q];
+        D.thr1[q] = (D.thr[q] < (1ull << 62) ? D.thr[q] : (1ull << 62)) + 1;
+        if (q == 0 || D.thr[q] > D.thr_max) D.thr_max = D.thr[q], q_max = (uint32_t)q;
     }
+    D.cslot[0] = q_max;  // swap slots 0 and q_max for the count pass
+    D.cslot[q_max] = 0;
+    for (int k = 0; k < 8; k++) D.thr1c[k] = D.thr1[D.cslot[k]];
     // launch shape: spans = 96 per SM (divisible by every grid of 1..4
     // resident 8-warp blocks per SM, so the grid-stride over spans is even)
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
@@ -235,7 +240,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_WRITE_COMB")) P->comb = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_SERIAL")) P->serial = (uint32_t)atoi(e);
-    const int occ_c = sweep_blocks_per_sm(0, D.n_cap, false), occ_w = sweep_blocks_per_sm(2, D.n_cap, P->comb != 0);
+    const int occ_c = sweep_blocks_per_sm(0, D.n_cap, 0), occ_w = sweep_blocks_per_sm(2, D.n_cap, (int)P->comb);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
     P->write_bps = (uint32_t)(occ_w > 2 ? 2 : occ_w);
@@ -330,13 +335,17 @@ static void result_release(me_result* R) {
     delete R;
 }
 
-static int n_cols_of(me_out_mode m) { return m == ME_OUT_FULL ? ME_N_COLS : (m == ME_OUT_INDEX ? 1 : 0); }
+static int n_cols_of(me_out_mode m) {
+    return m == ME_OUT_FULL ? ME_N_COLS : (m == ME_OUT_INDEX || m == ME_OUT_RECORDS ? 1 : 0);
+}
+// u64 words per row of each output column (RECORDS: one column of 8-word rows)
+static uint64_t words_of(me_out_mode m) { return m == ME_OUT_RECORDS ? ME_N_COLS : 1; }
 
 static int resolve(me_result* R);
 
 static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_result** out) {
     if (!P || !o || !out) return err(ME_EINVAL, "null argument");
-    if (o->mode != ME_OUT_COUNT && o->mode != ME_OUT_INDEX && o->mode != ME_OUT_FULL)
+    if (o->mode != ME_OUT_COUNT && o->mode != ME_OUT_INDEX && o->mode != ME_OUT_FULL && o->mode != ME_OUT_RECORDS)
         return err(ME_EINVAL, "bad output mode");
     DeviceGuard g(P->device);
     cudaStream_t st = (cudaStream_t)o->stream;
@@ -381,7 +390,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
-    bool comb = false;
+    int comb = 0;
     auto pipeline = [&](uint64_t* stats, bool write, Cols cols, uint64_t capacity) -> int {
         if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
         for (uint64_t lo = b; lo < e; lo += kMaxSub) {
@@ -440,7 +449,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 return fail(cuda_err(cudaGetLastError(), "count readback"));
             R->own_cols = true;
             for (int j = 0; j < nc; j++) {
-                R->cols[j] = (uint64_t*)R->A.get(cnt * 8);
+                R->cols[j] = (uint64_t*)R->A.get(cnt * 8 * words_of(o->mode));
                 if (!R->cols[j]) return fail(err(ME_ENOMEM, "result column allocation"));
             }
             R->capacity = cnt;
@@ -449,7 +458,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
     }
-    comb = P->comb != 0;
+    comb = (int)P->comb;
     if ((rc = pipeline(R->stats, nc != 0, cols, R->capacity))) return fail(rc);
     R->ran_count = len != 0;
     R->ran_write = nc && len;
@@ -473,7 +482,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             }
             R->g_rows = off[o->comm->nranks];
             for (int j = 0; j < nc; j++) {
-                R->gcols[j] = (uint64_t*)R->A.get(R->g_rows * 8);
+                R->gcols[j] = (uint64_t*)R->A.get(R->g_rows * 8 * words_of(o->mode));
                 if (!R->gcols[j]) return fail(err(ME_ENOMEM, "gathered column allocation"));
             }
             if (R->capacity < R->local) return fail(err(ME_ERANGE, "caller columns overflowed; cannot gather"));
@@ -481,8 +490,9 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             for (int j = 0; j < nc; j++)
                 for (int r = 0; r < o->comm->nranks; r++) {
                     if (!cnt[r]) continue;
+                    const uint64_t wd = words_of(o->mode);
                     nr = ncclBroadcast(r == o->comm->rank ? (const void*)R->cols[j] : nullptr,
-                                       R->gcols[j] + off[r], cnt[r], ncclUint64, r, o->comm->nccl, st);
+                                       R->gcols[j] + off[r] * wd, cnt[r] * wd, ncclUint64, r, o->comm->nccl, st);
                     if (nr != ncclSuccess) break;
                 }
             ncclResult_t ng = ncclGroupEnd();
@@ -592,7 +602,8 @@ extern "C" int me_result_copy_to_host(me_result* R, uint64_t first, uint64_t n, 
     for (int j = 0; j < ME_N_COLS; j++) {
         if (!cols_host[j]) continue;
         if (!cols[j]) return err(ME_EINVAL, "column not produced in this mode");
-        CU(cudaMemcpyAsync(cols_host[j], cols[j] + first, n * 8, cudaMemcpyDeviceToHost, R->stream));
+        const uint64_t wd = words_of(R->mode);
+        CU(cudaMemcpyAsync(cols_host[j], cols[j] + first * wd, n * 8 * wd, cudaMemcpyDeviceToHost, R->stream));
     }
     CU(cudaStreamSynchronize(R->stream));
     return ME_OK;
@@ -622,7 +633,7 @@ extern "C" void me_result_free(me_result* R) { result_release(R); }
 extern "C" int me_result_rank(me_result* R, uint32_t cap, uint64_t* best_index) {
     if (!R || !best_index) return err(ME_EINVAL, "null argument");
     if (cap >= R->n_cap) return err(ME_EINVAL, "capacity index out of range");
-    if (R->mode == ME_OUT_COUNT) return err(ME_EINVAL, "ranking needs an INDEX or FULL result");
+    if (R->mode == ME_OUT_COUNT) return err(ME_EINVAL, "ranking needs an INDEX, FULL or RECORDS result");
     if (R->comm && !R->gather) return err(ME_EINVAL, "ranking a sharded result needs gather = 1");
     uint64_t* cols[ME_N_COLS];
     uint64_t rows = 0;
@@ -636,7 +647,7 @@ extern "C" int me_result_rank(me_result* R, uint32_t cap, uint64_t* best_index) 
     cudaError_t ce = cudaMalloc(&didx, n_seg * 8);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(dkey, 0xFF, n_seg * 8, R->stream);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(didx, 0xFF, n_seg * 8, R->stream);
-    if (ce == cudaSuccess) ce = launch_rank(P->ds, cols[0], rows, cap, dkey, didx, R->stream);
+    if (ce == cudaSuccess) ce = launch_rank(P->ds, cols[0], (uint32_t)words_of(R->mode), rows, cap, dkey, didx, R->stream);
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(best_index, didx, n_seg * 8, cudaMemcpyDeviceToHost, R->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(R->stream);
     cudaFree(dkey);

@@ -42,21 +42,23 @@ __device__ __forceinline__ uint32_t upper_bound_u64(const uint64_t* __restrict__
 // Per-lane row coefficients.  Lanes advance by 32 and every row length is a
 // multiple of the (rc, do) digit count (1, 2 or 4), so a lane's (rc, do) digits
 // never change along its walk: the rc / do selections of RowCoef are made once
-// per row, leaving per config only
-//   total = ms + u * (n_inf * a + b)          (n_inf = p in paper mode).
+// per row.  The sweep evaluates the complement of the total,
+//   ~total = ~ms + u * (-(n_inf * a + b))      (mod 2^64; n_inf = p in paper mode)
+// so each capacity test is one carry chain (le_carry below).
 struct LaneRow {
-    uint64_t ms;        // params + grads + optim for this lane's do
-    uint64_t a, b;      // per-token activation bytes = n_inf * a + b (this lane's rc)
-    uint64_t kp;        // p * a + b (paper mode: n_inf = p)
+    uint64_t nms;       // ~(params + grads + optim) for this lane's do
+    uint64_t na, nb;    // -a, -b: per-token activation bytes = n_inf * a + b (this lane's rc)
+    uint64_t nkp;       // -(p * a + b) (paper mode: n_inf = p)
     uint64_t par, gra;  // weight / gradient bytes for this lane's do (and the ZeRO stage)
     uint64_t optim;     // optimizer bytes for this lane's do
     uint64_t lam, mu;   // per-token layer bytes = n_inf * lam + mu
     uint64_t e8, hc;    // per-token embedding bytes = n_inf * e8; head bytes = hc
+    uint64_t lay, emb;  // paper mode: p * lam + mu, p * e8
     uint32_t p;
     // NEXT-1 (stage_max): the last pipeline stage (p >= 2), one microbatch in
     // flight: total = msL + u * kL, layers = u * layL, head = u * hcL
     bool two;
-    uint64_t msL, kL, parL, graL, optimL, layL, hcL;
+    uint64_t nmsL, nkL, parL, graL, optimL, layL, hcL;
 };
 
 __device__ __forceinline__ void make_lane_row(const DevModel& M, uint32_t t, uint32_t c, uint32_t p, uint32_t d,
@@ -73,15 +75,17 @@ __device__ __forceinline__ void make_lane_row(const DevModel& M, uint32_t t, uin
         L.parL = T.params;
         L.graL = T.grads;
         L.optimL = T.optim;
-        L.msL = T.params + T.grads + T.optim;
+        L.nmsL = ~(T.params + T.grads + T.optim);
         L.layL = T.layers;
         L.hcL = T.head;
-        L.kL = T.layers + T.head;
+        L.nkL = 0ull - (T.layers + T.head);
     }
-    L.ms = dopt ? R.ms1 : R.ms0;
-    L.a = (rc ? R.lam1 : R.lam0) + R.e8;
-    L.b = rc ? R.bt + R.hc : R.hc;
-    L.kp = (uint64_t)p * L.a + L.b;
+    const uint64_t a = (rc ? R.lam1 : R.lam0) + R.e8;
+    const uint64_t b = rc ? R.bt + R.hc : R.hc;
+    L.nms = ~(dopt ? R.ms1 : R.ms0);
+    L.na = 0ull - a;
+    L.nb = 0ull - b;
+    L.nkp = 0ull - ((uint64_t)p * a + b);
     L.par = dopt ? R.par1 : 2ull * R.psi;
     L.gra = dopt ? R.gra1 : 4ull * R.psi;
     L.optim = dopt ? R.optim1 : 12ull * R.psi;
@@ -89,6 +93,8 @@ __device__ __forceinline__ void make_lane_row(const DevModel& M, uint32_t t, uin
     L.mu = rc ? R.bt : 0ull;
     L.e8 = R.e8;
     L.hc = R.hc;
+    L.lay = (uint64_t)p * L.lam + L.mu;
+    L.emb = (uint64_t)p * R.e8;
     L.p = p;
 }
 
@@ -175,11 +181,35 @@ struct Walker {
     }
 };
 
+// total <= thr  <=>  the 64-bit sum thr1 + ntot carries out, with thr1 = thr + 1
+// and ntot = ~total = 2^64 - 1 - total.  Two chained 32-bit adds produce the
+// carry; le_count returns acc + carry, le_shift 2 * acc + carry (a capacity
+// mask is built from the last slot down).
+__device__ __forceinline__ uint32_t le_count(uint32_t acc, uint64_t ntot, uint64_t thr1) {
+    asm("{\n\t.reg .u32 t;\n\t"
+        "add.cc.u32 t, %1, %2;\n\t"
+        "addc.cc.u32 t, %3, %4;\n\t"
+        "addc.u32 %0, %0, 0;\n\t}"
+        : "+r"(acc)
+        : "r"((uint32_t)ntot), "r"((uint32_t)thr1), "r"((uint32_t)(ntot >> 32)), "r"((uint32_t)(thr1 >> 32)));
+    return acc;
+}
+__device__ __forceinline__ uint32_t le_shift(uint32_t acc, uint64_t ntot, uint64_t thr1) {
+    asm("{\n\t.reg .u32 t;\n\t"
+        "add.cc.u32 t, %1, %2;\n\t"
+        "addc.cc.u32 t, %3, %4;\n\t"
+        "addc.u32 %0, %0, %0;\n\t}"
+        : "+r"(acc)
+        : "r"((uint32_t)ntot), "r"((uint32_t)thr1), "r"((uint32_t)(ntot >> 32)), "r"((uint32_t)(thr1 >> 32)));
+    return acc;
+}
+
+// capacity mask of a config from ntot = ~total: bit q = (total <= thr_q)
 template <int NCAP>
-__device__ __forceinline__ uint32_t cap_mask(const DevSpace& S, uint64_t total) {
+__device__ __forceinline__ uint32_t cap_mask(const DevSpace& S, uint64_t ntot) {
     uint32_t mask = 0;
 #pragma unroll
-    for (int q = 0; q < NCAP; q++) mask |= (total <= S.thr[q] ? 1u : 0u) << q;
+    for (int q = NCAP - 1; q >= 0; q--) mask = le_shift(mask, ntot, S.thr1[q]);
     return mask;
 }
 
@@ -241,14 +271,13 @@ struct Combiner {
 // aligned full-line stores lifts the store pattern itself from ~4.1 to ~5.7
 // TB/s but costs more issue slots than it saves in this kernel.)
 template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX, bool COMB = false>
-__device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
+__device__ __forceinline__ void run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
                                              uint64_t hi, uint32_t rounds, uint32_t lane, CapAcc<NCAP>& acc,
                                              uint64_t out, const Cols& cols, uint64_t capacity,
-                                             bool advance_out, Combiner<MODE == 2 ? 8 : 1>* cb = nullptr) {
-    constexpr int NC = MODE == 2 ? 8 : 1;
+                                             bool advance_out, Combiner<MODE >= 2 ? 8 : 1>* cb = nullptr) {
+    constexpr int NC = MODE >= 2 ? 8 : 1;
     constexpr bool PREFETCH = MODE != 0;  // the write pass hides the pair load behind a round
     const uint32_t pstep = 32u >> S.lg_rcdo;
-    uint32_t cnt = 0;
     uint2 pr = __ldg(W.pp);
     for (uint32_t it = 0; it < rounds; it++, pos += 32) {
         const bool more = (it + 1 < rounds) || advance_out;
@@ -258,41 +287,51 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
 
         const uint32_t u = pr.x;
         const uint32_t n_inf = GBS ? min(W.L.p, pr.y) : W.L.p;
-        const uint64_t K = GBS ? (uint64_t)n_inf * W.L.a + W.L.b : W.L.kp;
-        uint64_t total = W.L.ms + (uint64_t)u * K;
+        const uint64_t nK = GBS ? (uint64_t)n_inf * W.L.na + W.L.nb : W.L.nkp;
+        uint64_t ntot = W.L.nms + (uint64_t)u * nK;  // ~total
         bool last = false;
         if (STMAX && W.L.two) {
-            const uint64_t tl = W.L.msL + (uint64_t)u * W.L.kL;
-            last = tl > total;
-            total = last ? tl : total;
+            const uint64_t ntl = W.L.nmsL + (uint64_t)u * W.L.nkL;
+            last = ntl < ntot;  // the last stage's total is larger
+            ntot = last ? ntl : ntot;
         }
         const bool act = !RAGGED || (pos >= lo && pos < hi);
         if (MODE == 0) {
-            // counts only: survivors (total <= the largest threshold) and
-            // survivors per capacity
+            // counts only: survivors per capacity in count-slot order (slot 0
+            // = the largest threshold: its count is the survivor count)
             if (act) {
-                cnt += total <= S.thr_max ? 1u : 0u;
 #pragma unroll
-                for (int q = 0; q < NCAP; q++) acc.capc[q] += total <= S.thr[q] ? 1u : 0u;
+                for (int q = 0; q < NCAP; q++) acc.capc[q] = le_count(acc.capc[q], ntot, S.thr1c[q]);
             }
         } else {
-            const uint32_t mask = act ? cap_mask<NCAP>(S, total) : 0u;
+            const uint32_t mask = act ? cap_mask<NCAP>(S, ntot) : 0u;
             const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
             if (mask) {
                 const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
                 if (COMB || o < capacity) {
                     uint64_t v[NC];
                     v[0] = pos | ((uint64_t)mask << 56);
-                    if (MODE == 2) {
+                    if (MODE >= 2) {
                         v[1] = STMAX && last ? W.L.parL : W.L.par;
                         v[2] = STMAX && last ? W.L.graL : W.L.gra;
                         v[3] = STMAX && last ? W.L.optimL : W.L.optim;
-                        v[4] = (uint64_t)u * (STMAX && last ? W.L.layL : (uint64_t)n_inf * W.L.lam + W.L.mu);
-                        v[5] = STMAX && last ? 0ull : (uint64_t)u * ((uint64_t)n_inf * W.L.e8);
+                        const uint64_t lay = GBS ? (uint64_t)n_inf * W.L.lam + W.L.mu : W.L.lay;
+                        const uint64_t emb = GBS ? (uint64_t)n_inf * W.L.e8 : W.L.emb;
+                        v[4] = (uint64_t)u * (STMAX && last ? W.L.layL : lay);
+                        v[5] = STMAX && last ? 0ull : (uint64_t)u * emb;
                         v[6] = (uint64_t)u * (STMAX && last ? W.L.hcL : W.L.hc);
-                        v[7] = total;
+                        v[7] = ~ntot;
                     }
-                    if (COMB) {
+                    if (MODE == 3) {
+                        // records (array of structures): one 64-byte row, two 32-byte stores
+                        uint64_t* q = cols.c[0] + o * 8;
+                        asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(q), "l"(v[0]), "l"(v[1]),
+                                     "l"(v[2]), "l"(v[3])
+                                     : "memory");
+                        asm volatile("st.global.v4.u64 [%0+32], {%1, %2, %3, %4};" ::"l"(q), "l"(v[4]), "l"(v[5]),
+                                     "l"(v[6]), "l"(v[7])
+                                     : "memory");
+                    } else if (COMB) {
 #pragma unroll
                         for (int c = 0; c < NC; c++) cb->put(o, c, v[c]);
                     } else {
@@ -320,7 +359,6 @@ __device__ __forceinline__ uint32_t run_tile(const DevSpace& S, Walker& W, uint6
         cb->flush(cols, capacity, lane, out);
         __syncwarp();
     }
-    return cnt;
 }
 
 struct TileGeom {
@@ -358,7 +396,7 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
     // park it on the last index (its own positions stay inactive)
     const uint64_t p0 = G.start(t0) + lane;
     W.seek(S, p0 < G.hi ? p0 : G.hi - 1);
-    uint32_t run = 0;
+    uint32_t run = 0, prev = 0;
     for (uint32_t t = t0; t < t1; t++) {
         const uint64_t ts = G.start(t);
         if (lane == 0) {  // lane 0 is at the tile's first index
@@ -366,14 +404,16 @@ __device__ __forceinline__ uint32_t count_span(const DevSpace& S, const TileGeom
             tile_rel[t] = run;
         }
         const bool last = t + 1 == t1;
-        uint32_t cnt;
         if (G.ragged(t))
-            cnt = run_tile<0, NCAP, true, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{},
+            run_tile<0, NCAP, true, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0, Cols{},
                                                       0, !last);
         else
-            cnt = run_tile<0, NCAP, false, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
+            run_tile<0, NCAP, false, GBS, STMAX>(S, W, ts + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
                                                        Cols{}, 0, !last);
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        // survivors = this tile's increase of the lane counter of count slot 0
+        const uint32_t cur = acc.capc[0];
+        const uint32_t cnt = __reduce_add_sync(0xffffffffu, cur - prev);
+        prev = cur;
         if (lane == 0) tile_cnt[t] = cnt;
         run += cnt;
     }
@@ -408,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, co
 #pragma unroll
         for (int q = 0; q < NCAP; q++) {
             const uint32_t c = __reduce_add_sync(0xffffffffu, acc.capc[q]);
-            if (lane == 0) span_caps[(size_t)s * NCAP + q] = c;
+            if (lane == 0) span_caps[(size_t)s * NCAP + S.cslot[q]] = c;
         }
     }
 }
@@ -416,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, co
 template <int MODE, int NCAP, bool GBS, bool STMAX, bool COMB>
 __device__ __forceinline__ void write_tile(const DevSpace& S, const TileGeom& G, Walker& W, uint32_t t, uint64_t pos,
                                            uint32_t lane, uint64_t out, const Cols& cols, uint64_t capacity,
-                                           Combiner<MODE == 2 ? 8 : 1>* cb) {
+                                           Combiner<MODE >= 2 ? 8 : 1>* cb) {
     CapAcc<NCAP> none;
     if (G.ragged(t))
         run_tile<MODE, NCAP, true, GBS, STMAX, COMB>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
@@ -429,13 +469,13 @@ __device__ __forceinline__ void write_tile(const DevSpace& S, const TileGeom& G,
 // write pass: tiles in grid-stride order (at any moment the grid writes one
 // compact window of the output columns)
 template <int MODE, int NCAP, bool COMB>
-__global__ void __launch_bounds__(kThreads, 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
+__global__ void __launch_bounds__(kThreads, MODE == 3 ? 2 : 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                             const uint4* __restrict__ tile_ck,
                                                             const uint32_t* __restrict__ tile_rel,
                                                             const uint32_t* __restrict__ tile_cnt,
                                                             const uint64_t* __restrict__ span_off, const Cols cols,
                                                             const uint64_t capacity) {
-    constexpr int NC = MODE == 2 ? 8 : 1;
+    constexpr int NC = MODE >= 2 ? 8 : 1;
     __shared__ uint64_t s_comb[COMB ? kWarpsPerBlock * NC * 64 : 1];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
@@ -649,12 +689,15 @@ void* write_kernel_for(uint32_t n_cap) {
     }
 }
 
-void* write_fn(me_out_mode mode, uint32_t n_cap, bool comb) {
+// wvar: 0 plain column stores, 1 write combining (FULL / INDEX)
+void* write_fn(me_out_mode mode, uint32_t n_cap, int wvar) {
+    if (mode == ME_OUT_RECORDS) return write_kernel_for<3, false>(n_cap);
+    const bool comb = wvar == 1;
     if (mode == ME_OUT_FULL) return comb ? write_kernel_for<2, true>(n_cap) : write_kernel_for<2, false>(n_cap);
     return comb ? write_kernel_for<1, true>(n_cap) : write_kernel_for<1, false>(n_cap);
 }
 
-size_t write_smem(me_out_mode, bool) { return 0; }
+size_t write_smem(me_out_mode, int) { return 0; }
 
 }  // namespace
 
@@ -665,10 +708,11 @@ uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
     return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
 }
 
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool comb) {
-    const me_out_mode mode = pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX;
-    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(mode, n_cap, comb);
-    const size_t smem = pass == 0 ? 0 : write_smem(mode, comb);
+// pass 0 count, 1 INDEX write, 2 FULL write, 3 RECORDS write
+int sweep_blocks_per_sm(int pass, uint32_t n_cap, int wvar) {
+    const me_out_mode mode = pass == 3 ? ME_OUT_RECORDS : (pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX);
+    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(mode, n_cap, wvar);
+    const size_t smem = pass == 0 ? 0 : write_smem(mode, wvar);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess) return 1;
@@ -692,11 +736,11 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, bool comb, Cols cols, uint64_t capacity, cudaStream_t st) {
+                         me_out_mode mode, int wvar, Cols cols, uint64_t capacity, cudaStream_t st) {
     void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
                     (void*)&tile_cnt, (void*)&span_off, (void*)&cols, (void*)&capacity};
-    void* fn = write_fn(mode, S.n_cap, comb);
-    const size_t smem = write_smem(mode, comb);
+    void* fn = write_fn(mode, S.n_cap, wvar);
+    const size_t smem = write_smem(mode, wvar);
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return cudaLaunchKernel(fn, dim3(n_blocks), dim3(kThreads), args, smem, st);
 }

@@ -40,6 +40,13 @@ struct DevSpace {
     uint32_t zero_stage;          // 2 / 3 = gradients / also weights sharded with the optimizer (NEXT-4)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
     uint64_t thr_max;             // the largest threshold: survivor <=> total <= thr_max
+    // thr_j + 1 with thr_j clamped to 2^62 (every total is < 2^58): the sweep
+    // tests total <= thr_j as the carry out of (thr_j + 1) + ~total
+    uint64_t thr1[8];
+    // count pass order of the slots: slot 0 holds thr_max (its counter is the
+    // survivor count), count slot k is capacity cslot[k]
+    uint64_t thr1c[8];
+    uint32_t cslot[8];
 };
 
 // Per (model, tuple) coefficients: every estimator term of a config in this
@@ -210,7 +217,7 @@ uint32_t ncap_stride(uint32_t n_cap);
 // tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
 uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
 // resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, bool comb);
+int sweep_blocks_per_sm(int pass, uint32_t n_cap, int wvar);
 // count pass over [lo, hi) cut into n_spans spans of whole tiles: per tile its
 // walker checkpoint {seg, j, r, span} and the rank of its first survivor in the
 // span; per span its survivor count and per-capacity counts
@@ -224,10 +231,11 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 // span_off[span(t)] + tile_rel[t]; comb = write combining in aligned 32-row windows
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, bool comb, Cols cols, uint64_t capacity, cudaStream_t st);
+                         me_out_mode mode, int wvar, Cols cols, uint64_t capacity, cudaStream_t st);
 // NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
-// (rank key of DESIGN.md §9); best_key / best_index initialised to ~0
-cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint64_t n_rows, uint32_t cap,
+// (rank key of DESIGN.md §9); best_key / best_index initialised to ~0.
+// stride = u64 words between rows of the index column (8 for RECORDS)
+cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint32_t stride, uint64_t n_rows, uint32_t cap,
                         uint64_t* best_key, uint64_t* best_index, cudaStream_t st);
 // one configuration, one stage or (stage = 0xFFFFFFFF) the largest stage (NEXT-1)
 cudaError_t launch_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,

@@ -48,10 +48,10 @@ __device__ __forceinline__ bool rank_key(const DevSpace& S, uint64_t index, uint
     return true;
 }
 
-__global__ void rank_min_key(const DevSpace S, const uint64_t* __restrict__ col, uint64_t n, uint32_t cap,
-                             unsigned long long* __restrict__ best_key) {
+__global__ void rank_min_key(const DevSpace S, const uint64_t* __restrict__ col, uint32_t stride, uint64_t n,
+                             uint32_t cap, unsigned long long* __restrict__ best_key) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t v = col[i];
+        const uint64_t v = col[i * stride];
         if (!((v >> (56 + cap)) & 1u)) continue;  // not feasible for capacity `cap`
         uint32_t seg;
         uint64_t key;
@@ -60,11 +60,11 @@ __global__ void rank_min_key(const DevSpace S, const uint64_t* __restrict__ col,
     }
 }
 
-__global__ void rank_min_index(const DevSpace S, const uint64_t* __restrict__ col, uint64_t n, uint32_t cap,
-                               const unsigned long long* __restrict__ best_key,
+__global__ void rank_min_index(const DevSpace S, const uint64_t* __restrict__ col, uint32_t stride, uint64_t n,
+                               uint32_t cap, const unsigned long long* __restrict__ best_key,
                                unsigned long long* __restrict__ best_index) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t v = col[i];
+        const uint64_t v = col[i * stride];
         if (!((v >> (56 + cap)) & 1u)) continue;
         uint32_t seg;
         uint64_t key;
@@ -76,13 +76,14 @@ __global__ void rank_min_index(const DevSpace S, const uint64_t* __restrict__ co
 
 }  // namespace
 
-cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint64_t n_rows, uint32_t cap,
+cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint32_t stride, uint64_t n_rows, uint32_t cap,
                         uint64_t* best_key, uint64_t* best_index, cudaStream_t st) {
     if (!n_rows) return cudaSuccess;
     uint64_t blocks = (n_rows + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
-    rank_min_key<<<(unsigned)blocks, 256, 0, st>>>(S, index_col, n_rows, cap, (unsigned long long*)best_key);
-    rank_min_index<<<(unsigned)blocks, 256, 0, st>>>(S, index_col, n_rows, cap, (const unsigned long long*)best_key,
+    rank_min_key<<<(unsigned)blocks, 256, 0, st>>>(S, index_col, stride, n_rows, cap, (unsigned long long*)best_key);
+    rank_min_index<<<(unsigned)blocks, 256, 0, st>>>(S, index_col, stride, n_rows, cap,
+                                                     (const unsigned long long*)best_key,
                                                      (unsigned long long*)best_index);
     return cudaGetLastError();
 }

@@ -32,9 +32,9 @@ def main():
     for sp in spaces:
         plan = me.Plan(sp, device=local)
         idx, rows, n, caps = oracle.sweep(sp, threads=4) if rank == 0 else (None, None, None, None)
-        for begin, end in ((0, 0), (7, plan.size - 3)):
-            # gathered FULL result on every rank
-            r = plan.sweep(begin, end, mode=me.ME_OUT_FULL, comm=comm, gather=True)
+        for k, (begin, end) in enumerate(((0, 0), (7, plan.size - 3))):
+            # gathered FULL / RECORDS result on every rank
+            r = plan.sweep(begin, end, mode=(me.ME_OUT_FULL, me.ME_OUT_RECORDS)[k], comm=comm, gather=True)
             lo, gl, off = r.counts()
             got = r.to_host()
             # sharded INDEX result: local rows + global offset

@@ -66,7 +66,7 @@ def ref_rank(oracle_mod, sp, cap):
 
 
 @pytest.mark.parametrize("name", ["C1", "C3", "rand"])
-@pytest.mark.parametrize("mode", [1, 2], ids=["index", "full"])
+@pytest.mark.parametrize("mode", [1, 2, 3], ids=["index", "full", "records"])
 def test_rank_matches_reference(me, oracle_mod, name, mode):
     if name == "rand":
         sp = mi.Space(models=mi.random_models(4, seed=41), world=[16, 24, 64], caps_gb=[40, 80, 192],

@@ -37,7 +37,7 @@ def assert_same(me, res, idx, rows, n, caps, mode):
         return
     got = res.to_host()
     assert np.array_equal(got["index_mask"], idx)
-    if mode == me.ME_OUT_FULL:
+    if mode in (me.ME_OUT_FULL, me.ME_OUT_RECORDS):
         for j, k in enumerate(me.TERMS):
             assert np.array_equal(got[k], rows[:, j]), k
 
@@ -144,7 +144,7 @@ def small_spaces():
 
 
 @pytest.mark.parametrize("name,sp", list(small_spaces()), ids=[n for n, _ in small_spaces()])
-@pytest.mark.parametrize("mode", [0, 1, 2], ids=["count", "index", "full"])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3], ids=["count", "index", "full", "records"])
 def test_sweep_small_spaces(me, oracle_mod, name, sp, mode):
     plan = me.Plan(sp)
     assert plan.size == oracle_mod.space_size(sp)
@@ -159,11 +159,12 @@ def test_sweep_subranges(me, oracle_mod):
     rng = np.random.default_rng(3)
     ranges = [(0, 1), (5, 5), (31, 33), (1000, 1031), (plan.size - 1, plan.size), (0, 0)]
     ranges += [tuple(sorted(int(x) for x in rng.integers(0, plan.size, 2))) for _ in range(6)]
-    for b, e in ranges:
-        res = plan.sweep(b, e, mode=me.ME_OUT_FULL)
+    for i, (b, e) in enumerate(ranges):
+        mode = (me.ME_OUT_FULL, me.ME_OUT_RECORDS)[i & 1]
+        res = plan.sweep(b, e, mode=mode)
         if (b, e) == (0, 0):
             e = plan.size
-        assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), me.ME_OUT_FULL)
+        assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), mode)
 
 
 def test_caller_columns_and_overflow(me, oracle_mod):
@@ -176,6 +177,17 @@ def test_caller_columns_and_overflow(me, oracle_mod):
     assert res.status() == 0
     assert_same(me, res, idx, rows, n, caps, me.ME_OUT_FULL)
     assert (cols[0][n:] == -1).all()
+    rec = torch.full(((n + 3) * 8,), -1, dtype=torch.int64, device="cuda")
+    res = plan.sweep(mode=me.ME_OUT_RECORDS, out_cols=[rec])
+    assert res.status() == 0
+    assert_same(me, res, idx, rows, n, caps, me.ME_OUT_RECORDS)
+    assert (rec[n * 8:] == -1).all()
+    small_rec = torch.full(((n // 3) * 8 + 8,), -1, dtype=torch.int64, device="cuda")
+    res = plan.sweep(mode=me.ME_OUT_RECORDS, out_cols=[small_rec[:(n // 3) * 8]])
+    assert res.status() == 7  # ME_ERANGE: rows past the capacity are not written
+    assert (small_rec[(n // 3) * 8:] == -1).all()
+    got = small_rec[:(n // 3) * 8].view(-1, 8).cpu().numpy().view(np.uint64)
+    assert np.array_equal(got[:, 0], idx[: n // 3])
     small = [torch.zeros(n // 2, dtype=torch.int64, device="cuda")]
     res = plan.sweep(mode=me.ME_OUT_INDEX, out_cols=small)
     assert res.status() == 7  # ME_ERANGE
@@ -193,8 +205,8 @@ def test_random_model_grid(me, oracle_mod):
     assert_same(me, res, *oracle_rows(oracle_mod, sp, threads=16), me.ME_OUT_FULL)
 
 
-@pytest.mark.parametrize("name", ["C4", "C5"])
-def test_full_size_sampled(me, oracle_mod, name):
+@pytest.mark.parametrize("name,mode", [("C4", 2), ("C5", 2), ("C5", 3)], ids=["C4-full", "C5-full", "C5-records"])
+def test_full_size_sampled(me, oracle_mod, name, mode):
     """BASELINE.json configs[3]/[4] at full size, in bench.py's launch
     configuration (chunks of bench.CHUNK): windows compared record by record
     with the oracle, sampled rows of whole chunks recomputed one by one, and
@@ -210,15 +222,20 @@ def test_full_size_sampled(me, oracle_mod, name):
     wins = [(0, 20_000), (plan.size - 20_000, plan.size)]
     wins += [(s, s + 20_000) for s in (int(x) for x in rng.integers(0, plan.size - 20_000, 4))]
     for b, e in wins:
-        res = plan.sweep(b, e, mode=me.ME_OUT_FULL)
-        assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), me.ME_OUT_FULL)
+        res = plan.sweep(b, e, mode=mode)
+        assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), mode)
     # whole bench chunks: sampled rows and ordering properties
     chunk = bench.CHUNK
-    cols = [torch.empty(chunk, dtype=torch.int64, device="cuda") for _ in range(8)]
+    if mode == me.ME_OUT_RECORDS:
+        rec = torch.empty(chunk * 8, dtype=torch.int64, device="cuda")
+        out_cols = [rec]
+        cols = [rec.view(chunk, 8)[:, j] for j in range(8)]
+    else:
+        cols = out_cols = [torch.empty(chunk, dtype=torch.int64, device="cuda") for _ in range(8)]
     starts = [0, (plan.size // chunk // 2) * chunk, (plan.size - 1) // chunk * chunk]
     for s in starts:
         e = min(plan.size, s + chunk)
-        res = plan.sweep(s, e, mode=me.ME_OUT_FULL, out_cols=cols)
+        res = plan.sweep(s, e, mode=mode, out_cols=out_cols)
         assert res.status() == 0
         n = res.counts()[0]
         assert 0 < n <= e - s
@@ -264,7 +281,7 @@ def test_estimate_stage_matches_oracle(me, oracle_mod):
         me.me_estimate_stage(mi.PRESETS["llama3.1-8b"], 4, d=1, t=1, p=4, c=1, b=1, s=8192)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2], ids=["count", "index", "full"])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3], ids=["count", "index", "full", "records"])
 @pytest.mark.parametrize("name", ["C3u", "gbs", "rand"])
 def test_sweep_stage_max(me, oracle_mod, name, mode):
     """NEXT-1 sweeps: feasibility of the largest pipeline stage."""
