@@ -119,8 +119,13 @@ struct me_plan {
         uint32_t* span_count = nullptr;
         uint64_t* span_off = nullptr;
         uint32_t* span_caps = nullptr;
+        uint64_t* ustate = nullptr;     // fused pipeline: look-back state per block unit
         cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
     } scratch[2];
+    uint32_t fused = 1;                 // 1 = fused single-pass kernel (ME_FUSED=0: count/scan/write passes)
+    uint32_t span_tiles = 16;           // fused: tiles per warp span (ME_SPAN_TILES)
+    uint32_t max_units = 0;
+    int fused_bps[4] = {0, 0, 0, 0};    // co-resident blocks per SM of the fused kernel per output mode
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // count + scan passes
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
@@ -240,6 +245,11 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_WRITE_COMB")) P->comb = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_SERIAL")) P->serial = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_FUSED")) P->fused = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_SPAN_TILES")) P->span_tiles = (uint32_t)atoi(e);
+    if (P->span_tiles < 1) P->span_tiles = 1;
+    P->max_units = (P->max_tiles + P->span_tiles * kWarpsPerBlock - 1) / (P->span_tiles * kWarpsPerBlock) + 1;
+    for (int m = 0; m < 4; m++) P->fused_bps[m] = fused_blocks_per_sm((me_out_mode)m, D.n_cap);
     const int occ_c = sweep_blocks_per_sm(0, D.n_cap, 0), occ_w = sweep_blocks_per_sm(2, D.n_cap, (int)P->comb);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
@@ -257,12 +267,15 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         sc.span_count = (uint32_t*)P->A.get((size_t)P->max_spans * 4);
         sc.span_off = (uint64_t*)P->A.get((size_t)P->max_spans * 8);
         sc.span_caps = (uint32_t*)P->A.get((size_t)P->max_spans * 8 * 4);
+        sc.ustate = (uint64_t*)P->A.get((size_t)P->max_units * 8);
+        P->owned.push_back(sc.ustate);
         P->owned.push_back(sc.tile_rel);
         P->owned.push_back(sc.tile_ck);
         P->owned.push_back(sc.span_count);
         P->owned.push_back(sc.span_off);
         P->owned.push_back(sc.span_caps);
-        if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps) {
+        if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps ||
+            !sc.ustate) {
             me_plan_free(P);
             return err(ME_ENOMEM, "scratch allocation");
         }
@@ -386,7 +399,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     // stream, which waits only for the tables and for the write pass that last
     // used the scratch set, so the count of sub-range i+1 runs while the
     // caller's stream still writes the columns of sub-range i.
-    cudaStream_t cs = P->serial ? st : P->cstream;
+    cudaStream_t cs = P->serial || P->fused ? st : P->cstream;
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
@@ -411,6 +424,26 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 R->tev.push_back(x);
             }
             cudaStreamWaitEvent(cs, sc.free_ev, 0);
+            if (P->fused) {
+                // one kernel: count + look-back + write (timing: the kernel
+                // is the write pass, or the count pass when nothing is written)
+                const me_out_mode fm = write ? o->mode : ME_OUT_COUNT;
+                const uint32_t units =
+                    (n_tiles + P->span_tiles * kWarpsPerBlock - 1) / (P->span_tiles * kWarpsPerBlock);
+                cudaError_t ce = cudaMemsetAsync(sc.ustate, 0, (size_t)units * 8, st);
+                if (ce != cudaSuccess) return cuda_err(ce, "memset");
+                cudaEventRecord(tev[0], st);
+                if (write)
+                    for (int k = 1; k < 4; k++) cudaEventRecord(tev[k], st);
+                ce = launch_fused(P->ds, lo, hi, P->span_tiles, (uint32_t)(P->sms * P->fused_bps[fm]), sc.tile_ck,
+                                  sc.ustate, stats, fm, cols, capacity, st);
+                if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
+                if (!write)
+                    for (int k = 1; k < 4; k++) cudaEventRecord(tev[k], st);
+                cudaEventRecord(tev[4], st);
+                cudaEventRecord(sc.free_ev, st);
+                continue;
+            }
             cudaEventRecord(tev[0], cs);
             cudaError_t ce = launch_count(P->ds, lo, hi, n_spans, grid(P->count_bps, n_spans), sc.tile_rel,
                                           sc.tile_cnt, sc.tile_ck, sc.span_count, sc.span_caps, cs);

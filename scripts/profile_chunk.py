@@ -1,4 +1,4 @@
-"""One FULL sweep call of bench.py's launch configuration (C5, one 2^28-config
+"""One RECORDS (or FULL: second argument "full") sweep call of bench.py's launch configuration (C5, one 2^28-config
 chunk), for ncu: prints the chunk's survivors so the profiled write kernel's
 DRAM traffic can be set against its algorithmic bytes (survivors x 64 B)."""
 import json
@@ -13,13 +13,17 @@ import paper_2411_06465_b200 as me  # noqa: E402
 
 CHUNK = 1 << 28
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+mode = me.ME_OUT_FULL if len(sys.argv) > 2 and sys.argv[2] == "full" else me.ME_OUT_RECORDS
 sp = mi.config("C5")
 stream = torch.cuda.Stream()
 plan = me.Plan(sp, device=0, stream=stream.cuda_stream)
-cols = [torch.empty(CHUNK + 64, dtype=torch.int64, device="cuda") for _ in range(8)]
+if mode == me.ME_OUT_FULL:
+    cols = [torch.empty(CHUNK + 64, dtype=torch.int64, device="cuda") for _ in range(8)]
+else:
+    cols = [torch.empty(8 * (CHUNK + 64), dtype=torch.int64, device="cuda")]
 with torch.cuda.stream(stream):
-    r = plan.sweep(k * CHUNK, (k + 1) * CHUNK, mode=me.ME_OUT_FULL, out_cols=cols)
+    r = plan.sweep(k * CHUNK, (k + 1) * CHUNK, mode=mode, out_cols=cols)
     n = r.counts()[0]
     ms = r.timing()
-print(json.dumps({"chunk": k, "begin": k * CHUNK, "end": (k + 1) * CHUNK, "survivors": n,
+print(json.dumps({"chunk": k, "mode": int(mode), "begin": k * CHUNK, "end": (k + 1) * CHUNK, "survivors": n,
                   "algorithmic_write_bytes": n * 64, "timing_ms": ms}))
