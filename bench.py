@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--mode", default="full", choices=["records", "full", "index", "count"])
+    ap.add_argument("--mode", default="records", choices=["records", "full", "index", "count"])
     ap.add_argument("--workload", default=WORKLOAD)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -279,41 +279,54 @@ def main():
     n_launch = len(timings)
     survivors_local_per_step = n_local // args.steps
     peaks, peak_src = measured_peaks()
-    ncu = ROOT / "profiles" / "ncu_write_traffic.json"
-    ncu_t = json.loads(ncu.read_text()) if ncu.exists() else {}
-    # integer-issue roofline of the count pass (the INT path): warp
-    # instructions per round of 32 configs from the committed ncu capture,
-    # times this rank's configs of the timed steps, over the count kernels'
-    # CUDA-event time (serial passes, so the event time is the kernel's own)
+    # per-kernel ncu summary of one C5 chunk (scripts/gpu_prof.sh +
+    # scripts/ncu_summary.py): DRAM traffic and warp instructions per round
+    ncu = ROOT / "profiles" / "ncu_chunk40.json"
+    ncu_k = json.loads(ncu.read_text()).get("kernels", {}) if ncu.exists() else {}
+    ncu_c = json.loads(ncu.read_text()) if ncu.exists() else {}
+
+    def ncu_kernel(prefix):
+        return next((v for k, v in ncu_k.items() if k.startswith(prefix)), None)
+
+    # integer-issue roofline of the pass that evaluates every config (the
+    # stage kernel K1; COUNT mode: the count kernel): warp instructions per
+    # round of 32 configs from the ncu capture x this rank's rounds, over the
+    # pass's CUDA-event time (with overlapped passes that time includes
+    # sharing the SMs with the previous sub-range's expand kernel)
     issue = None
-    ipr = ncu_t.get("instr_per_config_count")
+    kname = "count_kernel" if mode == me.ME_OUT_COUNT else "stage_kernel"
+    kk = ncu_kernel(kname)
+    ipr = kk and kk.get("warp_instr_per_round")
     if ipr and count_ms > 0:
         clock = peaks.get("sm_max_mhz", 1965.0) * 1e6
         issue_peak = 148 * 4 * clock
         ach = (job_e - job_b) // world * args.steps / 32 * ipr / (count_ms / 1e3)
-        issue = {"bound": "alu", "kernel": "count_kernel<4> (count pass)", "achieved": ach, "peak": issue_peak,
-                 "unit": "warp-instr/s", "frac": ach / issue_peak, "traffic": 0,
+        issue = {"bound": "alu", "kernel": f"{kname} (evaluates every config)", "achieved": ach,
+                 "peak": issue_peak, "unit": "warp-instr/s", "frac": ach / issue_peak, "traffic": 0,
                  "instr_per_round_ncu": ipr,
                  "peak_source": "148 SMs x 4 SMSPs x 1 warp-instr/cycle x sm_max_mhz (MEASURED_PEAKS.json)"}
     if mode != me.ME_OUT_COUNT:
         bytes_write = survivors_local_per_step * 8 * ncols * args.steps
         achieved = bytes_write / (write_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"write_kernel<{int(mode)},4> (write pass)",
+        roof = {"bound": "hbm", "kernel": f"expand_kernel<{int(mode)},4> (writes every survivor row)",
                 "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "traffic": None, "peak_source": f"{peak_src} hbm_gbs (copy)",
                 "algorithmic_bytes_per_launch": bytes_write / max(1, n_launch),
                 "avg_launch_ms": write_ms / max(1, n_launch)}
-        if ncu_t:  # one ncu --set full capture of one chunk (scripts/profile_chunk.py)
-            roof["traffic"] = ncu_t["dram_bytes_read"] + ncu_t["dram_bytes_write"]
-            roof["traffic_note"] = (f"ncu DRAM bytes of the write kernel of C5 chunk {ncu_t['chunk']} "
-                                    f"(algorithmic {ncu_t['algorithmic_write_bytes']} B for that launch)")
+        ek = ncu_kernel("expand_kernel")
+        if ek:
+            roof["traffic"] = ek["dram_bytes_read"] + ek["dram_bytes_write"]
+            roof["traffic_note"] = (f"ncu DRAM bytes (read {ek['dram_bytes_read']:.4g} + write "
+                                    f"{ek['dram_bytes_write']:.4g}) of the expand kernel of C5 chunk "
+                                    f"{ncu_c['chunk']}, algorithmic {ncu_c['algorithmic_write_bytes']} B for that "
+                                    "launch; the reads are the 8-byte survivor descriptors and the row table")
         mb = ROOT / "profiles" / "r1_v4" / "microbench.json"
         if mb.exists():
             w = json.loads(mb.read_text())["write_only_gbs"]
             roof["write_only_peak_gbs"] = w
             roof["frac_of_write_only"] = achieved / w
         if issue:
-            roof["count_pass_issue"] = issue
+            roof["stage_pass_issue"] = issue
     else:
         roof = issue or {"bound": "alu", "kernel": "count_kernel<4> (count pass)", "achieved": None, "peak": None,
                          "unit": "warp-instr/s", "frac": None, "traffic": 0}
@@ -330,7 +343,8 @@ def main():
         "kernel_ms_per_step": {"count": count_ms / args.steps, "scan": scan_ms / args.steps,
                                "write": write_ms / args.steps},
         "roofline": roof,
-        "gpu_launches": 3 * n_launch if mode != me.ME_OUT_COUNT else 2 * n_launch,
+        # per sub-range: row, stage, scan, expand kernels (COUNT: count, scan)
+        "gpu_launches": 4 * n_launch if mode != me.ME_OUT_COUNT else 2 * n_launch,
         "clocks": clocks.summary(),
     }
 

@@ -108,7 +108,11 @@ struct me_plan {
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
     uint32_t comb = 0;                      // write combining into aligned 32-row windows (ME_WRITE_COMB=1)
     uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
-    uint32_t serial = 1;                    // count pass on the caller's stream (ME_SERIAL=0: own stream, overlapped)
+    // count pass on the caller's stream (1) or on the plan's own stream,
+    // overlapping the write pass of the previous sub-range (0; ME_SERIAL).
+    // Default: overlapped for the row-table pipeline (its K1 is issue bound,
+    // its K3 memory bound), serial for the others.
+    int serial = -1;
     // Two scratch sets, alternated by successive sub-ranges, so that the count
     // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
     // of sub-range i (on the caller's stream).
@@ -120,11 +124,26 @@ struct me_plan {
         uint64_t* span_off = nullptr;
         uint32_t* span_caps = nullptr;
         uint64_t* ustate = nullptr;     // fused pipeline: look-back state per block unit
+        // row-table pipeline (pipe 2)
+        RowEnt* rows = nullptr;         // the sub-range's rows
+        StEnt* st = nullptr;            // their last-stage terms per digit (stage_max)
+        uint2* rck = nullptr;           // span checkpoints {row, offset}
+        uint64_t* desc = nullptr;       // survivor descriptors, span_len slots per span
+        uint32_t* rcount = nullptr;     // survivors per span
+        uint64_t* roff = nullptr;       // output row of each span's first survivor
         cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
     } scratch[2];
+    // write-mode pipeline: 2 = row table + descriptors (K0 rows, K1 stage,
+    // scan, K3 expand; default), 1 = fused single-pass kernel, 0 = count /
+    // scan / write passes (ME_PIPE).  COUNT mode always uses the count pass.
+    uint32_t pipe = 2;
+    uint32_t rspan_tiles = 16;          // pipe 2: tiles per K1 span (ME_ROWS_SPAN)
+    uint32_t max_rspans = 0, max_rows = 0;
+    int expand_bps[4] = {0, 0, 0, 0};   // co-resident K3 blocks per SM per output mode
     uint32_t fused = 1;                 // 1 = fused single-pass kernel (ME_FUSED=0: count/scan/write passes)
     uint32_t span_tiles = 16;           // fused: tiles per warp span (ME_SPAN_TILES)
     uint32_t max_units = 0;
+    int fused_minb = 2;                 // fused kernel register budget: 2 or 3 blocks per SM (ME_FUSED_MINB)
     int fused_bps[4] = {0, 0, 0, 0};    // co-resident blocks per SM of the fused kernel per output mode
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // count + scan passes
@@ -192,13 +211,14 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     std::vector<DevModel> dmodels;
     for (const me_model& m : H.models) dmodels.push_back(dev_model(m));
     uint32_t *dcls, *dlo, *dlt;
-    uint64_t *dsp, *dlp;
+    uint64_t *dsp, *dlp, *dsr;
     DevTuple* dtu;
     DevPair* dpr;
     uint32_t* dpb;
     if ((st = upload(P->A, dmodels, &dm)) || (P->owned.push_back(dm), false) ||
         (st = upload(P->A, H.model_class, &dcls)) || (P->owned.push_back(dcls), false) ||
         (st = upload(P->A, H.seg_prefix, &dsp)) || (P->owned.push_back(dsp), false) ||
+        (st = upload(P->A, H.seg_row, &dsr)) || (P->owned.push_back(dsr), false) ||
         (st = upload(P->A, H.list_off, &dlo)) || (P->owned.push_back(dlo), false) ||
         (st = upload(P->A, H.list_tuple, &dlt)) || (P->owned.push_back(dlt), false) ||
         (st = upload(P->A, H.list_prefix, &dlp)) || (P->owned.push_back(dlp), false) ||
@@ -211,6 +231,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.models = dm;
     D.model_class = dcls;
     D.seg_prefix = dsp;
+    D.seg_row = dsr;
     D.list_off = dlo;
     D.list_tuple = dlt;
     D.list_prefix = dlp;
@@ -244,12 +265,26 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
     if (const char* e = getenv("ME_WRITE_COMB")) P->comb = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
-    if (const char* e = getenv("ME_SERIAL")) P->serial = (uint32_t)atoi(e);
-    if (const char* e = getenv("ME_FUSED")) P->fused = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
+    if (const char* e = getenv("ME_FUSED")) P->pipe = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_PIPE")) P->pipe = (uint32_t)atoi(e);
+    P->fused = P->pipe == 1;
+    if (P->serial < 0) P->serial = P->pipe == 2 ? 0 : 1;
+    if (const char* e = getenv("ME_ROWS_SPAN")) P->rspan_tiles = (uint32_t)atoi(e);
+    if (P->rspan_tiles < 1) P->rspan_tiles = 1;
+    {
+        const uint64_t eff = H.total + 64 < kMaxSub ? H.total + 64 : kMaxSub;
+        const uint32_t eff_tiles = n_tiles_of(31, 31 + eff) + 1;
+        P->max_rspans = (eff_tiles + P->rspan_tiles - 1) / P->rspan_tiles + 1;
+        P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
+        if (P->max_rows < 1) P->max_rows = 1;
+    }
+    for (int m = 1; m < 4; m++) P->expand_bps[m] = expand_blocks_per_sm((me_out_mode)m, D.n_cap);
     if (const char* e = getenv("ME_SPAN_TILES")) P->span_tiles = (uint32_t)atoi(e);
     if (P->span_tiles < 1) P->span_tiles = 1;
     P->max_units = (P->max_tiles + P->span_tiles * kWarpsPerBlock - 1) / (P->span_tiles * kWarpsPerBlock) + 1;
-    for (int m = 0; m < 4; m++) P->fused_bps[m] = fused_blocks_per_sm((me_out_mode)m, D.n_cap);
+    if (const char* e = getenv("ME_FUSED_MINB")) P->fused_minb = atoi(e);
+    for (int m = 0; m < 4; m++) P->fused_bps[m] = fused_blocks_per_sm((me_out_mode)m, D.n_cap, P->fused_minb);
     const int occ_c = sweep_blocks_per_sm(0, D.n_cap, 0), occ_w = sweep_blocks_per_sm(2, D.n_cap, (int)P->comb);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
@@ -274,8 +309,25 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         P->owned.push_back(sc.span_count);
         P->owned.push_back(sc.span_off);
         P->owned.push_back(sc.span_caps);
+        bool rows_ok = true;
+        if (P->pipe == 2) {
+            const size_t span_len = (size_t)P->rspan_tiles * kTile;
+            sc.rows = (RowEnt*)P->A.get((size_t)P->max_rows * sizeof(RowEnt));
+            sc.rck = (uint2*)P->A.get((size_t)P->max_rspans * 8);
+            sc.desc = (uint64_t*)P->A.get((size_t)P->max_rspans * span_len * 8);
+            sc.rcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
+            sc.roff = (uint64_t*)P->A.get((size_t)P->max_rspans * 8);
+            for (void* x : {(void*)sc.rows, (void*)sc.rck, (void*)sc.desc, (void*)sc.rcount, (void*)sc.roff})
+                P->owned.push_back(x);
+            rows_ok = sc.rows && sc.rck && sc.desc && sc.rcount && sc.roff;
+            if (H.stage_max) {
+                sc.st = (StEnt*)P->A.get((size_t)P->max_rows * H.n_rcdo * sizeof(StEnt));
+                P->owned.push_back(sc.st);
+                rows_ok = rows_ok && sc.st;
+            }
+        }
         if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps ||
-            !sc.ustate) {
+            !sc.ustate || !rows_ok) {
             me_plan_free(P);
             return err(ME_ENOMEM, "scratch allocation");
         }
@@ -311,6 +363,7 @@ extern "C" int me_plan_table_bytes(const me_plan* plan, uint64_t* bytes) {
     if (!plan || !bytes) return err(ME_EINVAL, "null argument");
     const HostSpace& H = plan->hs;
     *bytes = H.models.size() * sizeof(me_model) + H.model_class.size() * 4 + H.seg_prefix.size() * 8 +
+             H.seg_row.size() * 8 +
              H.list_off.size() * 4 + H.list_tuple.size() * 4 + H.list_prefix.size() * 8 +
              H.tuples.size() * sizeof(DevTuple) + H.pairs.size() * sizeof(DevPair);
     return ME_OK;
@@ -406,8 +459,22 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     int comb = 0;
     auto pipeline = [&](uint64_t* stats, bool write, Cols cols, uint64_t capacity) -> int {
         if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
-        for (uint64_t lo = b; lo < e; lo += kMaxSub) {
-            const uint64_t hi = e - lo < kMaxSub ? e : lo + kMaxSub;
+        const bool rows_pipe = P->pipe == 2 && write;
+        for (uint64_t lo = b, hi = b; lo < e; lo = hi) {
+            hi = e - lo < kMaxSub ? e : lo + kMaxSub;
+            uint64_t g0 = 0;
+            uint32_t n_rows = 0;
+            if (rows_pipe) {
+                // the sub-range also holds at most max_rows rows (the rows
+                // covering [lo & ~31, lo) are < 32 and max_rows >= 1: hi > lo)
+                const HostSpace& H = P->hs;
+                g0 = H.row_of(lo & ~31ull);
+                if (H.row_of(hi - 1) + 1 - g0 > P->max_rows) {
+                    const uint64_t cut = H.row_start(g0 + P->max_rows);
+                    if (cut > lo) hi = cut;
+                }
+                n_rows = (uint32_t)(H.row_of(hi - 1) + 1 - g0);
+            }
             me_plan::Scratch& sc = P->scratch[P->turn++ & 1];
             const uint32_t n_tiles = n_tiles_of(lo, hi);
             const uint32_t n_spans = n_tiles < P->max_spans ? n_tiles : P->max_spans;
@@ -424,6 +491,27 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 R->tev.push_back(x);
             }
             cudaStreamWaitEvent(cs, sc.free_ev, 0);
+            if (rows_pipe) {
+                // K0 rows + K1 stage + scan on the count stream, K3 on the caller's
+                const uint32_t n_rsp = (n_tiles + P->rspan_tiles - 1) / P->rspan_tiles;
+                cudaEventRecord(tev[0], cs);
+                cudaError_t ce = launch_rows(P->ds, g0, n_rows, lo, hi, P->rspan_tiles, sc.rows, sc.st, sc.rck, cs);
+                if (ce == cudaSuccess)
+                    ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, sc.rcount, cs);
+                if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
+                cudaEventRecord(tev[1], cs);
+                ce = launch_scan(sc.rcount, nullptr, n_rsp, 0, sc.roff, stats, cs);
+                if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
+                cudaEventRecord(tev[2], cs);
+                cudaStreamWaitEvent(st, tev[2], 0);
+                cudaEventRecord(tev[3], st);
+                ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, sc.rcount, sc.roff, o->mode,
+                                   cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[o->mode]), st);
+                if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
+                cudaEventRecord(tev[4], st);
+                cudaEventRecord(sc.free_ev, st);
+                continue;
+            }
             if (P->fused) {
                 // one kernel: count + look-back + write (timing: the kernel
                 // is the write pass, or the count pass when nothing is written)
@@ -435,7 +523,8 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 cudaEventRecord(tev[0], st);
                 if (write)
                     for (int k = 1; k < 4; k++) cudaEventRecord(tev[k], st);
-                ce = launch_fused(P->ds, lo, hi, P->span_tiles, (uint32_t)(P->sms * P->fused_bps[fm]), sc.tile_ck,
+                ce = launch_fused(P->ds, lo, hi, P->span_tiles, (uint32_t)(P->sms * P->fused_bps[fm]), P->fused_minb,
+                                  sc.tile_ck,
                                   sc.ustate, stats, fm, cols, capacity, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
                 if (!write)

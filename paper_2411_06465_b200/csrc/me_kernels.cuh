@@ -26,6 +26,7 @@ struct DevSpace {
     const DevModel* models;
     const uint32_t* model_class;
     const uint64_t* seg_prefix;   // n_seg + 1
+    const uint64_t* seg_row;      // n_seg + 1: rows before each segment
     const uint32_t* list_off;     // n_class * n_world + 1
     const uint32_t* list_tuple;
     const uint64_t* list_prefix;
@@ -202,6 +203,25 @@ __device__ __forceinline__ TermsT<U> config_terms(const RowCoefT<U>& R, uint32_t
     return T;
 }
 
+// ---- row-table pipeline (me_rows.cu) --------------------------------------
+// One row of the sub-range table (128 B): the row's RowCoef, first index and
+// pair offset; uint4-loadable prefix {w, pair_off, p, two}.
+struct __align__(16) RowEnt {
+    uint32_t w, pair_off, p, two;  // two: NEXT-1 last stage may decide (stage_max and p >= 2)
+    uint64_t ms0, ms1;
+    uint64_t lam0, lam1;
+    uint64_t e8, bt;
+    uint64_t hc, psi;
+    uint64_t par1, gra1;
+    uint64_t optim1, rs;           // rs = flat index of the row's first config
+    uint64_t _pad[2];
+};
+// NEXT-1: last-stage terms of one row for one (rc, do) digit (64 B)
+struct __align__(16) StEnt {
+    uint64_t msL, kL, parL, graL, optimL, layL, hcL, _pad;
+};
+constexpr uint32_t kMaxRows = 1u << 21;  // rows of one sub-range (descriptor row field: 24 bits)
+
 // ---- launch wrappers (me_kernels.cu) ------------------------------------
 struct Cols {
     uint64_t* c[ME_N_COLS];
@@ -237,10 +257,24 @@ cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n
 // state = (units) u64 zeroed, stats[0] = rows before lo on entry; adds this
 // range's survivors to stats[0] and stats[1 + j].  n_blocks must not exceed
 // the co-resident grid (fused_blocks_per_sm x SMs).
-int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
+// (minb = the register budget variant: 2 or 3 resident blocks per SM)
+int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb);
 cudaError_t launch_fused(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t span_tiles, uint32_t n_blocks,
-                         uint4* span_ck, uint64_t* state, uint64_t* stats, me_out_mode mode, Cols cols,
+                         int minb, uint4* span_ck, uint64_t* state, uint64_t* stats, me_out_mode mode, Cols cols,
                          uint64_t capacity, cudaStream_t st);
+// row-table pipeline (me_rows.cu): K0 rows [g0, g0 + n_rows) of the range
+// [lo, hi) + span checkpoints, K1 survivors -> descriptors + span counts, K3
+// descriptors -> output rows (and stats[1 + j] per capacity)
+int expand_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
+cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_t lo, uint64_t hi,
+                        uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck, cudaStream_t stream);
+cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
+                         uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t* span_count,
+                         cudaStream_t stream);
+cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
+                          uint32_t span_tiles, const uint64_t* desc, const uint32_t* span_count,
+                          const uint64_t* span_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
+                          uint32_t n_blocks, cudaStream_t stream);
 // NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
 // (rank key of DESIGN.md §9); best_key / best_index initialised to ~0.
 // stride = u64 words between rows of the index column (8 for RECORDS)

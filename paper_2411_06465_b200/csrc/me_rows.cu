@@ -1,0 +1,569 @@
+// me_rows.cu -- the row-table sweep pipeline (sm_100a), DESIGN.md §6.
+//
+// A row is a run of configurations sharing (model, N, t, c, p, d): every
+// estimator term of its configs is an affine function of the pair's tokens
+// per microbatch u (and in-flight count), with coefficients fixed per row
+// (RowCoef).  Per sub-range of the flat index space:
+//
+//  K0 row_kernel      one thread per row of the sub-range: its coefficients,
+//                     first index and pair offset (RowEnt), the last-stage
+//                     terms per (rc, do) digit when the largest stage decides
+//                     (StEnt), and the walker checkpoint of every span that
+//                     starts inside it;
+//  K1 stage_kernel    one warp per span of whole tiles: walks the span with
+//                     the row table (a row change is one 80-byte load, not a
+//                     re-derivation), tests every config against the
+//                     capacities and appends one 8-byte descriptor
+//                     {position in row, local row, capacity mask} per
+//                     survivor to the span's slice of a descriptor buffer;
+//                     stores the span's survivor count;
+//  scan               span counts -> output offsets (scan_kernel);
+//  K3 expand_kernel   warps take spans in grid-stride order and turn 32
+//                     descriptors at a time into output rows: every lane
+//                     produces one survivor, so the stores of a warp cover
+//                     32 consecutive rows (records: 2 KB contiguous), and the
+//                     per-capacity counts come from ballots of the masks.
+//
+// K1 evaluates every configuration once (no second walk in the write pass);
+// K3 touches survivors only.  Counts per capacity are exact: K3 sees every
+// survivor once.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "me_kernels.cuh"
+
+namespace me {
+
+namespace {
+
+__device__ __forceinline__ uint32_t upper_bound_u64(const uint64_t* __restrict__ a, uint32_t n, uint64_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// total <= thr  <=>  thr1 + ~total carries out of 64 bits (thr1 = thr + 1)
+__device__ __forceinline__ uint32_t le_shift(uint32_t acc, uint64_t ntot, uint64_t thr1) {
+    asm("{\n\t.reg .u32 t;\n\t"
+        "add.cc.u32 t, %1, %2;\n\t"
+        "addc.cc.u32 t, %3, %4;\n\t"
+        "addc.u32 %0, %0, %0;\n\t}"
+        : "+r"(acc)
+        : "r"((uint32_t)ntot), "r"((uint32_t)thr1), "r"((uint32_t)(ntot >> 32)), "r"((uint32_t)(thr1 >> 32)));
+    return acc;
+}
+
+template <int NCAP>
+__device__ __forceinline__ uint32_t cap_mask_n(const DevSpace& S, uint64_t ntot) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int q = NCAP - 1; q >= 0; q--) mask = le_shift(mask, ntot, S.thr1[q]);
+    return mask;
+}
+
+// lane-constant selections of a row's coefficients for the lane's (rc, do)
+struct LaneCoef {
+    uint64_t nms;        // ~model-state bytes
+    uint64_t na, nb;     // -(per-token activation bytes) = -(n_inf a + b)
+    uint64_t nkp;        // -(p a + b)
+    uint32_t p;
+    bool two;            // NEXT-1: the last stage may decide
+    uint64_t nmsL, nkL;  // ~msL, -kL of the last stage
+};
+
+__device__ __forceinline__ void lane_coef(const uint4 h, const ulonglong2 ms, const ulonglong2 lam,
+                                          const ulonglong2 e8bt, const uint64_t hc, uint32_t rc, uint32_t dopt,
+                                          LaneCoef& C) {
+    const uint32_t p = h.z;
+    const uint64_t a = (rc ? lam.y : lam.x) + e8bt.x;
+    const uint64_t b = rc ? e8bt.y + hc : hc;
+    C.nms = ~(dopt ? ms.y : ms.x);
+    C.na = 0ull - a;
+    C.nb = 0ull - b;
+    C.nkp = 0ull - ((uint64_t)p * a + b);
+    C.p = p;
+}
+
+// Table walker: lane position = (row k of the sub-range table, offset r).
+struct TWalker {
+    uint32_t k, r, w;
+    const uint2* pp;
+    uint32_t rc, dopt, sel;
+    LaneCoef C;
+
+    __device__ __forceinline__ void set_row(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                            const StEnt* __restrict__ st) {
+        const uint4* e = reinterpret_cast<const uint4*>(rows + k);
+        const uint4 h = __ldg(e);
+        const uint4 v1 = __ldg(e + 1), v2 = __ldg(e + 2), v3 = __ldg(e + 3), v4 = __ldg(e + 4);
+        w = h.x;
+        pp = reinterpret_cast<const uint2*>(S.pairs) + h.y + (r >> S.lg_rcdo);
+        const ulonglong2 ms = make_ulonglong2(((uint64_t)v1.y << 32) | v1.x, ((uint64_t)v1.w << 32) | v1.z);
+        const ulonglong2 lam = make_ulonglong2(((uint64_t)v2.y << 32) | v2.x, ((uint64_t)v2.w << 32) | v2.z);
+        const ulonglong2 eb = make_ulonglong2(((uint64_t)v3.y << 32) | v3.x, ((uint64_t)v3.w << 32) | v3.z);
+        const uint64_t hc = ((uint64_t)v4.y << 32) | v4.x;
+        lane_coef(h, ms, lam, eb, hc, rc, dopt, C);
+        C.two = h.w != 0;
+        if (S.stage_max && C.two) {
+            const StEnt& x = st[(size_t)k << S.lg_rcdo | sel];
+            C.nmsL = ~__ldg(&x.msL);
+            C.nkL = 0ull - __ldg(&x.kL);
+        }
+    }
+
+    __device__ __forceinline__ void restore(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                            const StEnt* __restrict__ st, uint2 ck, uint32_t lane) {
+        k = ck.x;
+        r = ck.y + lane;
+        sel = r & ((1u << S.lg_rcdo) - 1u);  // constant along the walk: row lengths are multiples of n_rcdo
+        rc = (S.rcdo_rc >> sel) & 1u;
+        dopt = (S.rcdo_do >> sel) & 1u;
+        set_row(S, rows, st);
+        while (r >= w) {
+            r -= w;
+            ++k;
+            set_row(S, rows, st);
+        }
+    }
+
+    __device__ __forceinline__ void advance32(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                              const StEnt* __restrict__ st, uint32_t pstep) {
+        r += 32;
+        if (r < w) {
+            pp += pstep;
+        } else {
+            do {
+                r -= w;
+                ++k;
+                set_row(S, rows, st);
+            } while (r >= w);
+        }
+    }
+};
+
+// ---------------------------------------------------------------- K0
+__global__ void row_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows, const uint64_t base,
+                           const uint64_t hi, const uint32_t span_len, const uint32_t n_spans,
+                           RowEnt* __restrict__ rows, StEnt* __restrict__ st, uint2* __restrict__ span_ck) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_rows; k += gridDim.x * blockDim.x) {
+        const uint64_t g = g0 + k;
+        const uint32_t s = upper_bound_u64(S.seg_row, S.n_seg + 1, g) - 1;
+        const uint32_t m = s / S.n_world, n = s - m * S.n_world;
+        const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(S.models + m));
+        const uint4 m1 = __ldg(reinterpret_cast<const uint4*>(S.models + m) + 1);
+        const DevModel M{m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, 0u};
+        const uint32_t cls = __ldg(S.model_class + m);
+        const uint32_t j = __ldg(S.list_off + cls * S.n_world + n) + (uint32_t)(g - __ldg(S.seg_row + s));
+        const DevTuple tu = S.tuples[__ldg(S.list_tuple + j)];
+        const uint64_t rs = __ldg(S.seg_prefix + s) + __ldg(S.list_prefix + j);
+        const uint32_t L0 = tu.p == 1 ? M.layers : div_u32(M.layers + tu.p - 1, tu.p);
+        RowCoef R;
+        make_row(M, tu.t, tu.c, tu.p, tu.d, L0, S.zero_stage, R);
+        const bool two = S.stage_max && tu.p >= 2;
+        RowEnt e;
+        e.w = tu.w;
+        e.pair_off = tu.pair_off;
+        e.p = tu.p;
+        e.two = two ? 1u : 0u;
+        e.ms0 = R.ms0;
+        e.ms1 = R.ms1;
+        e.lam0 = R.lam0;
+        e.lam1 = R.lam1;
+        e.e8 = R.e8;
+        e.bt = R.bt;
+        e.hc = R.hc;
+        e.psi = R.psi;
+        e.par1 = R.par1;
+        e.gra1 = R.gra1;
+        e.optim1 = R.optim1;
+        e.rs = rs;
+        rows[k] = e;
+        if (two) {
+            // the last stage holds floor((L - L0) / (p - 1)) layers, one microbatch
+            const uint32_t Ll = (M.layers - L0) / (tu.p - 1);
+            for (uint32_t sel = 0; sel < (1u << S.lg_rcdo); sel++) {
+                const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+                const TermsT<uint64_t> T =
+                    stage_terms<uint64_t>(M, tu.t, tu.c, tu.d, false, true, Ll, 1u, 1u, rc, dopt, S.zero_stage);
+                StEnt x;
+                x.msL = T.params + T.grads + T.optim;
+                x.kL = T.layers + T.head;
+                x.parL = T.params;
+                x.graL = T.grads;
+                x.optimL = T.optim;
+                x.layL = T.layers;
+                x.hcL = T.head;
+                x._pad = 0;
+                st[(size_t)k << S.lg_rcdo | sel] = x;
+            }
+        }
+        // checkpoints of the spans starting inside this row
+        const uint64_t lo_r = rs > base ? rs : base;
+        const uint64_t hi_r = rs + tu.w < hi ? rs + tu.w : hi;
+        if (lo_r < hi_r) {
+            uint64_t sp = (lo_r - base + span_len - 1) / span_len;
+            for (; sp < n_spans; sp++) {
+                const uint64_t ps = base + sp * span_len;
+                if (ps >= hi_r) break;
+                span_ck[sp] = make_uint2(k, (uint32_t)(ps - rs));
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K1
+// Descriptor of a survivor: bits 0..31 position in its row, 32..55 row of
+// the sub-range table, 56..63 capacity mask.
+template <int NCAP, bool GBS, bool STMAX, bool RAGGED>
+__device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                           const StEnt* __restrict__ st, uint32_t rounds, uint32_t lo_rel,
+                                           uint32_t hi_rel, uint2 ck, uint64_t* __restrict__ desc,
+                                           uint32_t* __restrict__ count_out, uint32_t lane) {
+    // positions relative to the span start; RAGGED: the span is cut by the
+    // range [lo, hi) = [lo_rel, hi_rel) (first / last span), a lane past the
+    // end is parked on the last index and never advances
+    TWalker W;
+    W.restore(S, rows, st, ck, !RAGGED || lane < hi_rel ? lane : hi_rel - 1);
+    const uint32_t pstep = 32u >> S.lg_rcdo;
+    uint32_t cnt = 0;
+    uint32_t rel = lane;
+    uint2 pr = __ldg(W.pp);
+    for (uint32_t it = 0; it < rounds; it++, rel += 32) {
+        const bool more = it + 1 < rounds;
+        const bool in_row = W.r + 32 < W.w;
+        uint2 prn = pr;
+        if (in_row && more) prn = __ldg(W.pp + pstep);  // next round's pair, issued early
+        const uint32_t u = pr.x;
+        const uint32_t n_inf = GBS ? min(W.C.p, pr.y) : W.C.p;
+        const uint64_t nK = GBS ? (uint64_t)n_inf * W.C.na + W.C.nb : W.C.nkp;
+        uint64_t ntot = W.C.nms + (uint64_t)u * nK;  // ~total
+        if (STMAX && W.C.two) {
+            const uint64_t ntl = W.C.nmsL + (uint64_t)u * W.C.nkL;
+            ntot = ntl < ntot ? ntl : ntot;
+        }
+        uint32_t mask = cap_mask_n<NCAP>(S, ntot);
+        if (RAGGED && (rel < lo_rel || rel >= hi_rel)) mask = 0;
+        const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
+        if (mask) {
+            const uint32_t hi_word = W.k | (mask << 24);
+            desc[cnt + __popc(ballot & ((1u << lane) - 1u))] = ((uint64_t)hi_word << 32) | W.r;
+        }
+        cnt += __popc(ballot);
+        if (more && (!RAGGED || rel + 32 < hi_rel)) {
+            if (in_row) {
+                W.r += 32;
+                W.pp += pstep;
+                pr = prn;
+            } else {
+                W.advance32(S, rows, st, pstep);
+                pr = __ldg(W.pp);
+            }
+        }
+    }
+    if (lane == 0) *count_out = cnt;
+}
+
+template <int NCAP>
+__global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
+                                                            const StEnt* __restrict__ st, const uint64_t lo,
+                                                            const uint64_t hi, const uint32_t span_tiles,
+                                                            const uint32_t n_spans, const uint2* __restrict__ span_ck,
+                                                            uint64_t* __restrict__ desc,
+                                                            uint32_t* __restrict__ span_count) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t sp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (sp >= n_spans) return;
+    const uint64_t base = lo & ~31ull;
+    const uint32_t n_tiles = (uint32_t)((hi - base + kTile - 1) / kTile);
+    const uint32_t t0 = sp * span_tiles;
+    const uint32_t t1 = min(n_tiles, t0 + span_tiles);
+    const uint64_t s0 = base + (uint64_t)t0 * kTile;
+    const uint64_t e = min(base + (uint64_t)t1 * kTile, hi);
+    const uint32_t rounds = (uint32_t)((e - s0 + 31) / 32);
+    const uint32_t lo_rel = lo > s0 ? (uint32_t)(lo - s0) : 0u, hi_rel = (uint32_t)(e - s0);
+    const bool ragged = lo_rel != 0 || (hi_rel & 31u) != 0;
+    const uint2 ck = __ldg(span_ck + sp);
+    uint64_t* d = desc + (size_t)sp * span_tiles * kTile;
+    uint32_t* c = span_count + sp;
+#define ME_STAGE(GBS, STMAX)                                                                           \
+    (ragged ? stage_span<NCAP, GBS, STMAX, true>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane) \
+            : stage_span<NCAP, GBS, STMAX, false>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane))
+    if (S.stage_max) {
+        if (S.gbs_mode) ME_STAGE(true, true);
+        else ME_STAGE(false, true);
+    } else {
+        if (S.gbs_mode) ME_STAGE(true, false);
+        else ME_STAGE(false, false);
+    }
+#undef ME_STAGE
+}
+
+// ---------------------------------------------------------------- K3
+// (no "memory" clobber: the kernel never reads what it stores, so the
+// loads of later survivors may be scheduled ahead of these stores)
+__device__ __forceinline__ void store_record(uint64_t* q, const uint64_t (&v)[8]) {
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(q), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3]));
+    asm volatile("st.global.v4.u64 [%0+32], {%1, %2, %3, %4};" ::"l"(q), "l"(v[4]), "l"(v[5]), "l"(v[6]), "l"(v[7]));
+}
+
+// per-lane capacity counters: 16-bit fields, capacities 4j .. 4j + 3 in word j
+// (the mask bits spread to bit 16 i by one multiply)
+template <int NCAP>
+struct CapPack {
+    uint64_t w[(NCAP + 3) / 4];
+    __device__ __forceinline__ CapPack() {
+#pragma unroll
+        for (int j = 0; j < (NCAP + 3) / 4; j++) w[j] = 0;
+    }
+    __device__ __forceinline__ void add(uint32_t mask) {
+#pragma unroll
+        for (int j = 0; j < (NCAP + 3) / 4; j++)
+            w[j] += ((uint64_t)((mask >> (4 * j)) & 0xFu) * 0x0000200040008001ull) & 0x0001000100010001ull;
+    }
+    // move the fields into u32 counters (call before a field can reach 2^16)
+    __device__ __forceinline__ void flush(uint32_t (&capc)[NCAP]) {
+#pragma unroll
+        for (int q = 0; q < NCAP; q++) capc[q] += (uint32_t)(w[q / 4] >> (16 * (q % 4))) & 0xFFFFu;
+#pragma unroll
+        for (int j = 0; j < (NCAP + 3) / 4; j++) w[j] = 0;
+    }
+};
+
+// one survivor: its output values from the descriptor (MODE 1: index|mask only)
+// A survivor's row data, loaded in one batch (6 x 16 B of its RowEnt) so that
+// the loads of several survivors are in flight together.
+struct RowLoad {
+    uint4 h;               // w, pair_off, p, two
+    ulonglong2 lam, e8bt;  // lam0, lam1 / e8, bt
+    ulonglong2 hcpsi, pg;  // hc, psi / par1, gra1
+    ulonglong2 optrs;      // optim1, rs
+};
+
+__device__ __forceinline__ ulonglong2 ldg_u2(const void* p) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+    return make_ulonglong2(((uint64_t)x.y << 32) | x.x, ((uint64_t)x.w << 32) | x.z);
+}
+
+__device__ __forceinline__ void load_row(const RowEnt* __restrict__ e, RowLoad& L) {
+    L.h = __ldg(reinterpret_cast<const uint4*>(e));
+    L.lam = ldg_u2(&e->lam0);
+    L.e8bt = ldg_u2(&e->e8);
+    L.hcpsi = ldg_u2(&e->hc);
+    L.pg = ldg_u2(&e->par1);
+    L.optrs = ldg_u2(&e->optim1);
+}
+
+// one survivor's output values from its descriptor, row data and pair
+// (MODE 1: index|mask only)
+template <int MODE, bool GBS, bool STMAX>
+__device__ __forceinline__ void expand_vals(const DevSpace& S, const StEnt* __restrict__ st, uint64_t dsc,
+                                            const RowLoad& L, uint2 pr, uint64_t (&v)[8]) {
+    const uint32_t r = (uint32_t)dsc, k = (uint32_t)(dsc >> 32) & 0xFFFFFFu;
+    const uint32_t mask = (uint32_t)(dsc >> 56);
+    v[0] = (L.optrs.y + r) | ((uint64_t)mask << 56);
+    if (MODE == 1) return;
+    const uint32_t sel = r & ((1u << S.lg_rcdo) - 1u);
+    const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+    const uint32_t u = pr.x, p = L.h.z;
+    const uint32_t n_inf = GBS ? min(p, pr.y) : p;
+    const uint64_t psi = L.hcpsi.y;
+    const uint64_t lam = rc ? L.lam.y : L.lam.x;
+    const uint64_t mu = rc ? L.e8bt.y : 0ull;
+    v[1] = dopt ? L.pg.x : 2ull * psi;
+    v[2] = dopt ? L.pg.y : 4ull * psi;
+    v[3] = dopt ? L.optrs.x : 12ull * psi;
+    v[4] = (uint64_t)u * ((uint64_t)n_inf * lam + mu);
+    v[5] = (uint64_t)u * ((uint64_t)n_inf * L.e8bt.x);
+    v[6] = (uint64_t)u * L.hcpsi.x;
+    v[7] = v[1] + v[2] + v[3] + v[4] + v[5] + v[6];
+    if (STMAX && L.h.w) {
+        const StEnt& x = st[(size_t)k << S.lg_rcdo | sel];
+        const uint64_t tl = __ldg(&x.msL) + (uint64_t)u * __ldg(&x.kL);
+        if (tl > v[7]) {  // the last stage decides (ties: stage 0)
+            v[1] = __ldg(&x.parL);
+            v[2] = __ldg(&x.graL);
+            v[3] = __ldg(&x.optimL);
+            v[4] = (uint64_t)u * __ldg(&x.layL);
+            v[5] = 0;
+            v[6] = (uint64_t)u * __ldg(&x.hcL);
+            v[7] = tl;
+        }
+    }
+}
+
+// U survivors per lane per iteration, in phases (descriptors, rows, pairs,
+// values + stores) so that each phase's loads are in flight together: the
+// kernel is bound by load latency otherwise
+template <int MODE, int NCAP, bool GBS, bool STMAX, int U>
+__device__ __forceinline__ void expand_spans(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                             const StEnt* __restrict__ st, uint32_t span_len, uint32_t n_spans,
+                                             const uint64_t* __restrict__ desc,
+                                             const uint32_t* __restrict__ span_count,
+                                             const uint64_t* __restrict__ span_off, const Cols& cols,
+                                             uint64_t capacity, uint32_t (&capc)[NCAP]) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
+    const uint2* pairs = reinterpret_cast<const uint2*>(S.pairs);
+    for (uint32_t sp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); sp < n_spans; sp += n_warps) {
+        const uint32_t n = __ldg(span_count + sp);
+        if (!n) continue;
+        const uint64_t off = __ldg(span_off + sp);
+        const uint64_t* d = desc + (size_t)sp * span_len;
+        CapPack<NCAP> pk;  // <= span_len / 32 survivors per lane per span: fits 16 bits
+        for (uint32_t i0 = 0; i0 < n; i0 += 32 * U) {
+            uint64_t dsc[U];
+#pragma unroll
+            for (int j = 0; j < U; j++) {
+                const uint32_t i = i0 + 32 * j + lane;
+                dsc[j] = i < n ? __ldg(d + i) : 0ull;  // mask 0: no survivor (row 0, offset 0)
+            }
+            RowLoad L[U];
+#pragma unroll
+            for (int j = 0; j < U; j++) {
+                if (MODE == 1) L[j].optrs.y = __ldg(&rows[(uint32_t)(dsc[j] >> 32) & 0xFFFFFFu].rs);
+                else load_row(rows + ((uint32_t)(dsc[j] >> 32) & 0xFFFFFFu), L[j]);
+            }
+            uint2 pr[U];
+#pragma unroll
+            for (int j = 0; j < U; j++)
+                pr[j] = MODE == 1 ? make_uint2(0, 0) : __ldg(pairs + L[j].h.y + ((uint32_t)dsc[j] >> S.lg_rcdo));
+#pragma unroll
+            for (int j = 0; j < U; j++) {
+                const uint32_t mask = (uint32_t)(dsc[j] >> 56);
+                pk.add(mask);
+                uint64_t v[8];
+                expand_vals<MODE, GBS, STMAX>(S, st, dsc[j], L[j], pr[j], v);
+                const uint64_t o = off + i0 + 32 * j + lane;
+                if (mask && o < capacity) {
+                    if (MODE == 3) {
+                        store_record(cols.c[0] + o * 8, v);
+                    } else if (MODE == 2) {
+#pragma unroll
+                        for (int c = 0; c < 8; c++) cols.c[c][o] = v[c];
+                    } else {
+                        cols.c[0][o] = v[0];
+                    }
+                }
+            }
+        }
+        pk.flush(capc);
+    }
+}
+
+// stats[1 + j] += survivors for capacity j (one atomic per block and capacity)
+template <int MODE, int NCAP, int U>
+__global__ void __launch_bounds__(kThreads, 2) expand_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
+                                                             const StEnt* __restrict__ st, const uint32_t span_len,
+                                                             const uint32_t n_spans, const uint64_t* __restrict__ desc,
+                                                             const uint32_t* __restrict__ span_count,
+                                                             const uint64_t* __restrict__ span_off, const Cols cols,
+                                                             const uint64_t capacity, uint64_t* __restrict__ stats) {
+    __shared__ uint32_t s_cap[NCAP];
+    if (threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t capc[NCAP];
+#pragma unroll
+    for (int q = 0; q < NCAP; q++) capc[q] = 0;
+#define ME_EXPAND(GBS, STMAX)                                                                              \
+    expand_spans<MODE, NCAP, GBS, STMAX, U>(S, rows, st, span_len, n_spans, desc, span_count, span_off, cols, \
+                                            capacity, capc)
+    if (S.stage_max) {
+        if (S.gbs_mode) ME_EXPAND(true, true);
+        else ME_EXPAND(false, true);
+    } else {
+        if (S.gbs_mode) ME_EXPAND(true, false);
+        else ME_EXPAND(false, false);
+    }
+#undef ME_EXPAND
+#pragma unroll
+    for (int q = 0; q < NCAP; q++) {
+        const uint32_t c = __reduce_add_sync(0xffffffffu, capc[q]);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cap + q, c);
+    }
+    __syncthreads();
+    if (threadIdx.x < NCAP && s_cap[threadIdx.x])
+        atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
+}
+
+uint32_t ncap_pad(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
+
+template <int MODE, int U>
+void* expand_fn_(uint32_t n_cap) {
+    switch (ncap_pad(n_cap)) {
+        case 1: return reinterpret_cast<void*>(&expand_kernel<MODE, 1, U>);
+        case 2: return reinterpret_cast<void*>(&expand_kernel<MODE, 2, U>);
+        case 4: return reinterpret_cast<void*>(&expand_kernel<MODE, 4, U>);
+        default: return reinterpret_cast<void*>(&expand_kernel<MODE, 8, U>);
+    }
+}
+// u: survivors per lane per iteration (2 or 4; ME_EXPAND_U)
+template <int U>
+void* expand_fn_u(me_out_mode mode, uint32_t n_cap) {
+    return mode == ME_OUT_RECORDS ? expand_fn_<3, U>(n_cap)
+                                  : mode == ME_OUT_FULL ? expand_fn_<2, U>(n_cap) : expand_fn_<1, U>(n_cap);
+}
+int g_expand_u = 2;
+void* expand_fn(me_out_mode mode, uint32_t n_cap) {
+    return g_expand_u >= 4 ? expand_fn_u<4>(mode, n_cap) : expand_fn_u<2>(mode, n_cap);
+}
+void* stage_fn(uint32_t n_cap) {
+    switch (ncap_pad(n_cap)) {
+        case 1: return reinterpret_cast<void*>(&stage_kernel<1>);
+        case 2: return reinterpret_cast<void*>(&stage_kernel<2>);
+        case 4: return reinterpret_cast<void*>(&stage_kernel<4>);
+        default: return reinterpret_cast<void*>(&stage_kernel<8>);
+    }
+}
+
+}  // namespace
+
+int expand_blocks_per_sm(me_out_mode mode, uint32_t n_cap) {
+    if (const char* e = getenv("ME_EXPAND_U")) g_expand_u = atoi(e);
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, expand_fn(mode, n_cap), kThreads, 0) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_t lo, uint64_t hi,
+                        uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck, cudaStream_t stream) {
+    const uint64_t base = lo & ~31ull;
+    const uint32_t n_tiles = n_tiles_of(lo, hi);
+    const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
+    const uint32_t blocks = (n_rows + 255) / 256;
+    row_kernel<<<blocks ? blocks : 1, 256, 0, stream>>>(S, g0, n_rows, base, hi, span_tiles * kTile, n_spans, rows,
+                                                        st, span_ck);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
+                         uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t* span_count,
+                         cudaStream_t stream) {
+    const uint32_t n_tiles = n_tiles_of(lo, hi);
+    const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
+    void* args[] = {(void*)&S,       (void*)&rows,    (void*)&st,   (void*)&lo,        (void*)&hi,
+                    (void*)&span_tiles, (void*)&n_spans, (void*)&span_ck, (void*)&desc, (void*)&span_count};
+    return cudaLaunchKernel(stage_fn(S.n_cap), dim3((n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock),
+                            dim3(kThreads), args, 0, stream);
+}
+
+cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
+                          uint32_t span_tiles, const uint64_t* desc, const uint32_t* span_count,
+                          const uint64_t* span_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
+                          uint32_t n_blocks, cudaStream_t stream) {
+    const uint32_t n_tiles = n_tiles_of(lo, hi);
+    const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
+    const uint32_t span_len = span_tiles * kTile;
+    const uint32_t need = (n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (n_blocks > need) n_blocks = need ? need : 1;
+    void* args[] = {(void*)&S,          (void*)&rows,     (void*)&st,   (void*)&span_len, (void*)&n_spans,
+                    (void*)&desc,       (void*)&span_count, (void*)&span_off, (void*)&cols, (void*)&capacity,
+                    (void*)&stats};
+    return cudaLaunchKernel(expand_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, stream);
+}
+
+}  // namespace me

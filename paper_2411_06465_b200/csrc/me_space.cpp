@@ -194,9 +194,38 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
         }
     seg_prefix[models.size() * nW] = acc;
     total = acc;
+    // rows (= (model, N, tuple) runs of configs) before each segment
+    seg_row.resize(models.size() * nW + 1);
+    uint64_t rows = 0;
+    for (size_t i = 0; i < models.size(); i++)
+        for (uint32_t n = 0; n < nW; n++) {
+            seg_row[i * nW + n] = rows;
+            const size_t ln = (size_t)model_class[i] * nW + n;
+            rows += list_off[ln + 1] - list_off[ln];
+        }
+    seg_row[models.size() * nW] = rows;
+    total_rows = rows;
     if (for_sweep && total >= Limits::index)
         return fail(detail, ME_EOVERFLOW, "space has >= 2^56 configurations");
     return ME_OK;
+}
+
+uint64_t HostSpace::row_of(uint64_t index) const {
+    const uint32_t nW = (uint32_t)world.size();
+    const size_t seg = std::upper_bound(seg_prefix.begin(), seg_prefix.end(), index) - seg_prefix.begin() - 1;
+    const uint64_t within = index - seg_prefix[seg];
+    const size_t ln = (size_t)model_class[seg / nW] * nW + seg % nW;
+    const size_t j = std::upper_bound(list_prefix.begin() + list_off[ln], list_prefix.begin() + list_off[ln + 1],
+                                      within) - list_prefix.begin() - 1;
+    return seg_row[seg] + (j - list_off[ln]);
+}
+
+uint64_t HostSpace::row_start(uint64_t g) const {
+    if (g >= total_rows) return total;
+    const uint32_t nW = (uint32_t)world.size();
+    const size_t seg = std::upper_bound(seg_row.begin(), seg_row.end(), g) - seg_row.begin() - 1;
+    const size_t ln = (size_t)model_class[seg / nW] * nW + seg % nW;
+    return seg_prefix[seg] + list_prefix[list_off[ln] + (g - seg_row[seg])];
 }
 
 int HostSpace::decode(uint64_t index, uint32_t* model_id, uint32_t* world_size,

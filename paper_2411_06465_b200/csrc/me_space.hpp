@@ -46,6 +46,10 @@ class HostSpace {
     int build(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
               bool for_sweep, std::string* detail);
     int decode(uint64_t index, uint32_t* model_id, uint32_t* world, me_parallel* out) const;
+    // global row (model, N, tuple run) holding flat index `index` (< total)
+    uint64_t row_of(uint64_t index) const;
+    // flat index of the first config of global row g (total for g >= total_rows)
+    uint64_t row_start(uint64_t g) const;
 
     // inputs (copied)
     std::vector<me_model> models;
@@ -68,7 +72,8 @@ class HostSpace {
     std::vector<uint64_t> list_prefix;  // segment-local exclusive prefix of w
     std::vector<uint64_t> class_seg;    // size of the segment of (class, n)
     std::vector<uint64_t> seg_prefix;   // n_models * n_world + 1
-    uint64_t total = 0;
+    std::vector<uint64_t> seg_row;      // n_models * n_world + 1: rows before each segment
+    uint64_t total = 0, total_rows = 0;
 };
 
 }  // namespace me
