@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -130,7 +131,8 @@ struct me_plan {
         uint2* rck = nullptr;           // span checkpoints {row, offset}
         uint64_t* desc = nullptr;       // survivor descriptors, span_len slots per span
         uint32_t* rcount = nullptr;     // survivors per span
-        uint64_t* roff = nullptr;       // output row of each span's first survivor
+        uint32_t* rbcount = nullptr;    // survivors per stage-kernel block (kWarpsPerBlock spans)
+        uint64_t* roff = nullptr;       // output row of each block's first survivor
         cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
     } scratch[2];
     // write-mode pipeline: 2 = row table + descriptors (K0 rows, K1 stage,
@@ -240,6 +242,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.pair_b = dpb;
     D.n_seg = (uint32_t)(H.seg_prefix.size() - 1);
     D.n_world = (uint32_t)H.world.size();
+    D.n_pairs = (uint32_t)H.pairs.size();
     D.lg_rcdo = H.lg_rcdo;
     D.rcdo_rc = H.rcdo_rc;
     D.rcdo_do = H.rcdo_do;
@@ -280,6 +283,8 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         if (P->max_rows < 1) P->max_rows = 1;
     }
     for (int m = 1; m < 4; m++) P->expand_bps[m] = expand_blocks_per_sm((me_out_mode)m, D.n_cap);
+    if (const char* e = getenv("ME_EXPAND_BPS"))  // K3 grid: fewer blocks leave room for the overlapped K1
+        for (int m = 1; m < 4; m++) P->expand_bps[m] = std::min(P->expand_bps[m], std::max(1, atoi(e)));
     if (const char* e = getenv("ME_SPAN_TILES")) P->span_tiles = (uint32_t)atoi(e);
     if (P->span_tiles < 1) P->span_tiles = 1;
     P->max_units = (P->max_tiles + P->span_tiles * kWarpsPerBlock - 1) / (P->span_tiles * kWarpsPerBlock) + 1;
@@ -317,9 +322,11 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
             sc.desc = (uint64_t*)P->A.get((size_t)P->max_rspans * span_len * 8);
             sc.rcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
             sc.roff = (uint64_t*)P->A.get((size_t)P->max_rspans * 8);
-            for (void* x : {(void*)sc.rows, (void*)sc.rck, (void*)sc.desc, (void*)sc.rcount, (void*)sc.roff})
+            sc.rbcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
+            for (void* x : {(void*)sc.rows, (void*)sc.rck, (void*)sc.desc, (void*)sc.rcount, (void*)sc.roff,
+                            (void*)sc.rbcount})
                 P->owned.push_back(x);
-            rows_ok = sc.rows && sc.rck && sc.desc && sc.rcount && sc.roff;
+            rows_ok = sc.rows && sc.rck && sc.desc && sc.rcount && sc.roff && sc.rbcount;
             if (H.stage_max) {
                 sc.st = (StEnt*)P->A.get((size_t)P->max_rows * H.n_rcdo * sizeof(StEnt));
                 P->owned.push_back(sc.st);
@@ -497,10 +504,12 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 cudaEventRecord(tev[0], cs);
                 cudaError_t ce = launch_rows(P->ds, g0, n_rows, lo, hi, P->rspan_tiles, sc.rows, sc.st, sc.rck, cs);
                 if (ce == cudaSuccess)
-                    ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, sc.rcount, cs);
+                    ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, sc.rcount,
+                                      sc.rbcount, cs);
                 if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
                 cudaEventRecord(tev[1], cs);
-                ce = launch_scan(sc.rcount, nullptr, n_rsp, 0, sc.roff, stats, cs);
+                ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kWarpsPerBlock - 1) / kWarpsPerBlock, 0, sc.roff, stats,
+                                 cs);
                 if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
                 cudaEventRecord(tev[2], cs);
                 cudaStreamWaitEvent(st, tev[2], 0);

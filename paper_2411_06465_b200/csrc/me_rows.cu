@@ -269,15 +269,40 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
 }
 
 template <int NCAP>
+__device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                          const StEnt* __restrict__ st, uint64_t lo, uint64_t hi, uint32_t span_tiles,
+                                          uint32_t sp, const uint2* __restrict__ span_ck, uint64_t* __restrict__ desc,
+                                          uint32_t* __restrict__ span_count, uint32_t lane);
+
+template <int NCAP>
 __global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
                                                             const StEnt* __restrict__ st, const uint64_t lo,
                                                             const uint64_t hi, const uint32_t span_tiles,
                                                             const uint32_t n_spans, const uint2* __restrict__ span_ck,
                                                             uint64_t* __restrict__ desc,
-                                                            uint32_t* __restrict__ span_count) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t sp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (sp >= n_spans) return;
+                                                            uint32_t* __restrict__ span_count,
+                                                            uint32_t* __restrict__ block_count) {
+    __shared__ uint32_t s_cnt[kWarpsPerBlock];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t sp = blockIdx.x * kWarpsPerBlock + wid;
+    if (sp < n_spans) stage_one<NCAP>(S, rows, st, lo, hi, span_tiles, sp, span_ck, desc, span_count, lane);
+    // the block's survivors (the scan runs over blocks; the expand kernel
+    // adds the counts of the earlier spans of its block)
+    if (lane == 0) s_cnt[wid] = sp < n_spans ? span_count[sp] : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < kWarpsPerBlock; w++) t += s_cnt[w];
+        block_count[blockIdx.x] = t;
+    }
+}
+
+template <int NCAP>
+__device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                          const StEnt* __restrict__ st, uint64_t lo, uint64_t hi, uint32_t span_tiles,
+                                          uint32_t sp, const uint2* __restrict__ span_ck, uint64_t* __restrict__ desc,
+                                          uint32_t* __restrict__ span_count, uint32_t lane) {
     const uint64_t base = lo & ~31ull;
     const uint32_t n_tiles = (uint32_t)((hi - base + kTile - 1) / kTile);
     const uint32_t t0 = sp * span_tiles;
@@ -349,13 +374,29 @@ __device__ __forceinline__ ulonglong2 ldg_u2(const void* p) {
     return make_ulonglong2(((uint64_t)x.y << 32) | x.x, ((uint64_t)x.w << 32) | x.z);
 }
 
+__device__ __forceinline__ ulonglong2 ld_u2(const void* p) {
+    const uint4 x = *reinterpret_cast<const uint4*>(p);
+    return make_ulonglong2(((uint64_t)x.y << 32) | x.x, ((uint64_t)x.w << 32) | x.z);
+}
+
+// SMEM: e points into the warp's shared-memory copy of the span's rows
+template <bool SMEM>
 __device__ __forceinline__ void load_row(const RowEnt* __restrict__ e, RowLoad& L) {
-    L.h = __ldg(reinterpret_cast<const uint4*>(e));
-    L.lam = ldg_u2(&e->lam0);
-    L.e8bt = ldg_u2(&e->e8);
-    L.hcpsi = ldg_u2(&e->hc);
-    L.pg = ldg_u2(&e->par1);
-    L.optrs = ldg_u2(&e->optim1);
+    if (SMEM) {
+        L.h = *reinterpret_cast<const uint4*>(e);
+        L.lam = ld_u2(&e->lam0);
+        L.e8bt = ld_u2(&e->e8);
+        L.hcpsi = ld_u2(&e->hc);
+        L.pg = ld_u2(&e->par1);
+        L.optrs = ld_u2(&e->optim1);
+    } else {
+        L.h = __ldg(reinterpret_cast<const uint4*>(e));
+        L.lam = ldg_u2(&e->lam0);
+        L.e8bt = ldg_u2(&e->e8);
+        L.hcpsi = ldg_u2(&e->hc);
+        L.pg = ldg_u2(&e->par1);
+        L.optrs = ldg_u2(&e->optim1);
+    }
 }
 
 // one survivor's output values from its descriptor, row data and pair
@@ -396,60 +437,93 @@ __device__ __forceinline__ void expand_vals(const DevSpace& S, const StEnt* __re
     }
 }
 
-// U survivors per lane per iteration, in phases (descriptors, rows, pairs,
-// values + stores) so that each phase's loads are in flight together: the
-// kernel is bound by load latency otherwise
+// Shared memory of the expand kernel: the pairs pool (when it fits) and, per
+// warp, a copy of the rows its current span refers to (when they fit):
+// the survivors' row and pair reads then cost no global-memory round trip.
+constexpr uint32_t kSmemPairs = 2048;  // 16 KB
+constexpr uint32_t kSmemRows = 24;     // per warp: 3 KB (C5: a 16-tile span touches <= 23 rows)
+
+// the survivors [0, n) of one span, U per lane per iteration, in phases
+// (descriptors, rows, pairs, values + stores) so that each phase's loads are
+// in flight together.  SMEM: rows from the warp's shared copy (row k at
+// srow[k - k0]); pairs: shared or global (pairs).
+template <int MODE, int NCAP, bool GBS, bool STMAX, int U, bool SMEM>
+__device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                            const RowEnt* srow, uint32_t k0, const uint2* pairs,
+                                            const StEnt* __restrict__ st, const uint64_t* __restrict__ d, uint32_t n,
+                                            uint64_t off, const Cols& cols, uint64_t capacity, CapPack<NCAP>& pk,
+                                            uint32_t lane) {
+    for (uint32_t i0 = 0; i0 < n; i0 += 32 * U) {
+        uint64_t dsc[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const uint32_t i = i0 + 32 * j + lane;
+            dsc[j] = i < n ? __ldg(d + i) : ((uint64_t)k0 << 32);  // mask 0: no survivor (row k0, offset 0)
+        }
+        RowLoad L[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const uint32_t k = (uint32_t)(dsc[j] >> 32) & 0xFFFFFFu;
+            const RowEnt* e = SMEM ? srow + (k - k0) : rows + k;
+            if (MODE == 1) L[j].optrs.y = SMEM ? e->rs : __ldg(&e->rs);
+            else load_row<SMEM>(e, L[j]);
+        }
+        uint2 pr[U];
+#pragma unroll
+        for (int j = 0; j < U; j++) pr[j] = MODE == 1 ? make_uint2(0, 0) : pairs[L[j].h.y + ((uint32_t)dsc[j] >> S.lg_rcdo)];
+#pragma unroll
+        for (int j = 0; j < U; j++) {
+            const uint32_t mask = (uint32_t)(dsc[j] >> 56);
+            pk.add(mask);
+            uint64_t v[8];
+            expand_vals<MODE, GBS, STMAX>(S, st, dsc[j], L[j], pr[j], v);
+            const uint64_t o = off + i0 + 32 * j + lane;
+            if (mask && o < capacity) {
+                if (MODE == 3) {
+                    store_record(cols.c[0] + o * 8, v);
+                } else if (MODE == 2) {
+#pragma unroll
+                    for (int c = 0; c < 8; c++) cols.c[c][o] = v[c];
+                } else {
+                    cols.c[0][o] = v[0];
+                }
+            }
+        }
+    }
+}
+
 template <int MODE, int NCAP, bool GBS, bool STMAX, int U>
 __device__ __forceinline__ void expand_spans(const DevSpace& S, const RowEnt* __restrict__ rows,
                                              const StEnt* __restrict__ st, uint32_t span_len, uint32_t n_spans,
                                              const uint64_t* __restrict__ desc,
                                              const uint32_t* __restrict__ span_count,
-                                             const uint64_t* __restrict__ span_off, const Cols& cols,
-                                             uint64_t capacity, uint32_t (&capc)[NCAP]) {
+                                             const uint64_t* __restrict__ block_off, const Cols& cols,
+                                             uint64_t capacity, const uint2* pairs, RowEnt* srow,
+                                             uint32_t (&capc)[NCAP]) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
-    const uint2* pairs = reinterpret_cast<const uint2*>(S.pairs);
     for (uint32_t sp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); sp < n_spans; sp += n_warps) {
         const uint32_t n = __ldg(span_count + sp);
         if (!n) continue;
-        const uint64_t off = __ldg(span_off + sp);
+        // output row of the span: its block's offset + the earlier spans of the block
+        uint64_t off = __ldg(block_off + sp / kWarpsPerBlock);
+        for (uint32_t q = sp & ~(kWarpsPerBlock - 1u); q < sp; q++) off += __ldg(span_count + q);
         const uint64_t* d = desc + (size_t)sp * span_len;
+        // rows of the span: from its first and last survivor (index order)
+        const uint32_t k0 = (uint32_t)(__ldg(d) >> 32) & 0xFFFFFFu;
+        const uint32_t k1 = (uint32_t)(__ldg(d + n - 1) >> 32) & 0xFFFFFFu;
         CapPack<NCAP> pk;  // <= span_len / 32 survivors per lane per span: fits 16 bits
-        for (uint32_t i0 = 0; i0 < n; i0 += 32 * U) {
-            uint64_t dsc[U];
-#pragma unroll
-            for (int j = 0; j < U; j++) {
-                const uint32_t i = i0 + 32 * j + lane;
-                dsc[j] = i < n ? __ldg(d + i) : 0ull;  // mask 0: no survivor (row 0, offset 0)
-            }
-            RowLoad L[U];
-#pragma unroll
-            for (int j = 0; j < U; j++) {
-                if (MODE == 1) L[j].optrs.y = __ldg(&rows[(uint32_t)(dsc[j] >> 32) & 0xFFFFFFu].rs);
-                else load_row(rows + ((uint32_t)(dsc[j] >> 32) & 0xFFFFFFu), L[j]);
-            }
-            uint2 pr[U];
-#pragma unroll
-            for (int j = 0; j < U; j++)
-                pr[j] = MODE == 1 ? make_uint2(0, 0) : __ldg(pairs + L[j].h.y + ((uint32_t)dsc[j] >> S.lg_rcdo));
-#pragma unroll
-            for (int j = 0; j < U; j++) {
-                const uint32_t mask = (uint32_t)(dsc[j] >> 56);
-                pk.add(mask);
-                uint64_t v[8];
-                expand_vals<MODE, GBS, STMAX>(S, st, dsc[j], L[j], pr[j], v);
-                const uint64_t o = off + i0 + 32 * j + lane;
-                if (mask && o < capacity) {
-                    if (MODE == 3) {
-                        store_record(cols.c[0] + o * 8, v);
-                    } else if (MODE == 2) {
-#pragma unroll
-                        for (int c = 0; c < 8; c++) cols.c[c][o] = v[c];
-                    } else {
-                        cols.c[0][o] = v[0];
-                    }
-                }
-            }
+        if (k1 - k0 < kSmemRows) {
+            __syncwarp();  // the previous span's readers are done with srow
+            const uint4* src = reinterpret_cast<const uint4*>(rows + k0);
+            uint4* dst = reinterpret_cast<uint4*>(srow);
+            for (uint32_t c = lane; c < (k1 - k0 + 1) * (sizeof(RowEnt) / 16); c += 32) dst[c] = __ldg(src + c);
+            __syncwarp();
+            expand_span<MODE, NCAP, GBS, STMAX, U, true>(S, rows, srow, k0, pairs, st, d, n, off, cols, capacity, pk,
+                                                         lane);
+        } else {
+            expand_span<MODE, NCAP, GBS, STMAX, U, false>(S, rows, srow, k0, pairs, st, d, n, off, cols, capacity,
+                                                          pk, lane);
         }
         pk.flush(capc);
     }
@@ -461,17 +535,25 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const DevSpace S, c
                                                              const StEnt* __restrict__ st, const uint32_t span_len,
                                                              const uint32_t n_spans, const uint64_t* __restrict__ desc,
                                                              const uint32_t* __restrict__ span_count,
-                                                             const uint64_t* __restrict__ span_off, const Cols cols,
+                                                             const uint64_t* __restrict__ block_off, const Cols cols,
                                                              const uint64_t capacity, uint64_t* __restrict__ stats) {
     __shared__ uint32_t s_cap[NCAP];
+    __shared__ uint2 s_pairs[kSmemPairs];
+    __shared__ __align__(16) RowEnt s_rows[kWarpsPerBlock][kSmemRows];
     if (threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
+    const bool pairs_smem = S.n_pairs <= kSmemPairs;
+    if (pairs_smem)
+        for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x)
+            s_pairs[i] = __ldg(reinterpret_cast<const uint2*>(S.pairs) + i);
     __syncthreads();
+    const uint2* pairs = pairs_smem ? s_pairs : reinterpret_cast<const uint2*>(S.pairs);
+    RowEnt* srow = s_rows[threadIdx.x >> 5];
     uint32_t capc[NCAP];
 #pragma unroll
     for (int q = 0; q < NCAP; q++) capc[q] = 0;
 #define ME_EXPAND(GBS, STMAX)                                                                              \
-    expand_spans<MODE, NCAP, GBS, STMAX, U>(S, rows, st, span_len, n_spans, desc, span_count, span_off, cols, \
-                                            capacity, capc)
+    expand_spans<MODE, NCAP, GBS, STMAX, U>(S, rows, st, span_len, n_spans, desc, span_count, block_off, cols, \
+                                            capacity, pairs, srow, capc)
     if (S.stage_max) {
         if (S.gbs_mode) ME_EXPAND(true, true);
         else ME_EXPAND(false, true);
@@ -542,18 +624,19 @@ cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_
 
 cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
                          uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t* span_count,
-                         cudaStream_t stream) {
+                         uint32_t* block_count, cudaStream_t stream) {
     const uint32_t n_tiles = n_tiles_of(lo, hi);
     const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
-    void* args[] = {(void*)&S,       (void*)&rows,    (void*)&st,   (void*)&lo,        (void*)&hi,
-                    (void*)&span_tiles, (void*)&n_spans, (void*)&span_ck, (void*)&desc, (void*)&span_count};
+    void* args[] = {(void*)&S,          (void*)&rows,    (void*)&st,      (void*)&lo,   (void*)&hi,
+                    (void*)&span_tiles, (void*)&n_spans, (void*)&span_ck, (void*)&desc, (void*)&span_count,
+                    (void*)&block_count};
     return cudaLaunchKernel(stage_fn(S.n_cap), dim3((n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock),
                             dim3(kThreads), args, 0, stream);
 }
 
 cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
                           uint32_t span_tiles, const uint64_t* desc, const uint32_t* span_count,
-                          const uint64_t* span_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
+                          const uint64_t* block_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
                           uint32_t n_blocks, cudaStream_t stream) {
     const uint32_t n_tiles = n_tiles_of(lo, hi);
     const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
@@ -561,7 +644,7 @@ cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st
     const uint32_t need = (n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (n_blocks > need) n_blocks = need ? need : 1;
     void* args[] = {(void*)&S,          (void*)&rows,     (void*)&st,   (void*)&span_len, (void*)&n_spans,
-                    (void*)&desc,       (void*)&span_count, (void*)&span_off, (void*)&cols, (void*)&capacity,
+                    (void*)&desc,       (void*)&span_count, (void*)&block_off, (void*)&cols, (void*)&capacity,
                     (void*)&stats};
     return cudaLaunchKernel(expand_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, stream);
 }
