@@ -133,6 +133,7 @@ struct me_plan {
         uint32_t* rcount = nullptr;     // survivors per span
         uint32_t* rbcount = nullptr;    // survivors per stage-kernel block (kWarpsPerBlock spans)
         uint64_t* roff = nullptr;       // output row of each block's first survivor
+        uint32_t* rnext = nullptr;      // expand kernel: next span to take
         cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
     } scratch[2];
     // write-mode pipeline: 2 = row table + descriptors (K0 rows, K1 stage,
@@ -323,10 +324,11 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
             sc.rcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
             sc.roff = (uint64_t*)P->A.get((size_t)P->max_rspans * 8);
             sc.rbcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
+            sc.rnext = (uint32_t*)P->A.get(256);
             for (void* x : {(void*)sc.rows, (void*)sc.rck, (void*)sc.desc, (void*)sc.rcount, (void*)sc.roff,
-                            (void*)sc.rbcount})
+                            (void*)sc.rbcount, (void*)sc.rnext})
                 P->owned.push_back(x);
-            rows_ok = sc.rows && sc.rck && sc.desc && sc.rcount && sc.roff && sc.rbcount;
+            rows_ok = sc.rows && sc.rck && sc.desc && sc.rcount && sc.roff && sc.rbcount && sc.rnext;
             if (H.stage_max) {
                 sc.st = (StEnt*)P->A.get((size_t)P->max_rows * H.n_rcdo * sizeof(StEnt));
                 P->owned.push_back(sc.st);
@@ -505,7 +507,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 cudaError_t ce = launch_rows(P->ds, g0, n_rows, lo, hi, P->rspan_tiles, sc.rows, sc.st, sc.rck, cs);
                 if (ce == cudaSuccess)
                     ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, sc.rcount,
-                                      sc.rbcount, cs);
+                                      sc.rbcount, o->mode, cs);
                 if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
                 cudaEventRecord(tev[1], cs);
                 ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kWarpsPerBlock - 1) / kWarpsPerBlock, 0, sc.roff, stats,
@@ -515,7 +517,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 cudaStreamWaitEvent(st, tev[2], 0);
                 cudaEventRecord(tev[3], st);
                 ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, sc.rcount, sc.roff, o->mode,
-                                   cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[o->mode]), st);
+                                   cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[o->mode]), sc.rnext, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
                 cudaEventRecord(tev[4], st);
                 cudaEventRecord(sc.free_ev, st);

@@ -219,7 +219,11 @@ __global__ void row_kernel(const DevSpace S, const uint64_t g0, const uint32_t n
 // ---------------------------------------------------------------- K1
 // Descriptor of a survivor: bits 0..31 position in its row, 32..55 row of
 // the sub-range table, 56..63 capacity mask.
-template <int NCAP, bool GBS, bool STMAX, bool RAGGED>
+// MASK: the descriptor carries the capacity mask (INDEX output, whose expand
+// pass computes no totals); otherwise only the survivor test (total <= the
+// largest threshold: one carry chain) is made here and the expand kernel
+// derives the mask from the total it computes anyway.
+template <int NCAP, bool GBS, bool STMAX, bool RAGGED, bool MASK>
 __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __restrict__ rows,
                                            const StEnt* __restrict__ st, uint32_t rounds, uint32_t lo_rel,
                                            uint32_t hi_rel, uint2 ck, uint64_t* __restrict__ desc,
@@ -246,11 +250,11 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
             const uint64_t ntl = W.C.nmsL + (uint64_t)u * W.C.nkL;
             ntot = ntl < ntot ? ntl : ntot;
         }
-        uint32_t mask = cap_mask_n<NCAP>(S, ntot);
+        uint32_t mask = MASK ? cap_mask_n<NCAP>(S, ntot) : le_shift(0u, ntot, S.thr1c[0]);
         if (RAGGED && (rel < lo_rel || rel >= hi_rel)) mask = 0;
         const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
         if (mask) {
-            const uint32_t hi_word = W.k | (mask << 24);
+            const uint32_t hi_word = MASK ? W.k | (mask << 24) : W.k;
             desc[cnt + __popc(ballot & ((1u << lane) - 1u))] = ((uint64_t)hi_word << 32) | W.r;
         }
         cnt += __popc(ballot);
@@ -268,13 +272,13 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
     if (lane == 0) *count_out = cnt;
 }
 
-template <int NCAP>
+template <int NCAP, bool MASK>
 __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __restrict__ rows,
                                           const StEnt* __restrict__ st, uint64_t lo, uint64_t hi, uint32_t span_tiles,
                                           uint32_t sp, const uint2* __restrict__ span_ck, uint64_t* __restrict__ desc,
                                           uint32_t* __restrict__ span_count, uint32_t lane);
 
-template <int NCAP>
+template <int NCAP, bool MASK>
 __global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
                                                             const StEnt* __restrict__ st, const uint64_t lo,
                                                             const uint64_t hi, const uint32_t span_tiles,
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, co
     __shared__ uint32_t s_cnt[kWarpsPerBlock];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t sp = blockIdx.x * kWarpsPerBlock + wid;
-    if (sp < n_spans) stage_one<NCAP>(S, rows, st, lo, hi, span_tiles, sp, span_ck, desc, span_count, lane);
+    if (sp < n_spans) stage_one<NCAP, MASK>(S, rows, st, lo, hi, span_tiles, sp, span_ck, desc, span_count, lane);
     // the block's survivors (the scan runs over blocks; the expand kernel
     // adds the counts of the earlier spans of its block)
     if (lane == 0) s_cnt[wid] = sp < n_spans ? span_count[sp] : 0u;
@@ -298,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, co
     }
 }
 
-template <int NCAP>
+template <int NCAP, bool MASK>
 __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __restrict__ rows,
                                           const StEnt* __restrict__ st, uint64_t lo, uint64_t hi, uint32_t span_tiles,
                                           uint32_t sp, const uint2* __restrict__ span_ck, uint64_t* __restrict__ desc,
@@ -316,8 +320,8 @@ __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __res
     uint64_t* d = desc + (size_t)sp * span_tiles * kTile;
     uint32_t* c = span_count + sp;
 #define ME_STAGE(GBS, STMAX)                                                                           \
-    (ragged ? stage_span<NCAP, GBS, STMAX, true>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane) \
-            : stage_span<NCAP, GBS, STMAX, false>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane))
+    (ragged ? stage_span<NCAP, GBS, STMAX, true, MASK>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane) \
+            : stage_span<NCAP, GBS, STMAX, false, MASK>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane))
     if (S.stage_max) {
         if (S.gbs_mode) ME_STAGE(true, true);
         else ME_STAGE(false, true);
@@ -401,13 +405,14 @@ __device__ __forceinline__ void load_row(const RowEnt* __restrict__ e, RowLoad& 
 
 // one survivor's output values from its descriptor, row data and pair
 // (MODE 1: index|mask only)
-template <int MODE, bool GBS, bool STMAX>
+template <int MODE, int NCAP, bool GBS, bool STMAX>
 __device__ __forceinline__ void expand_vals(const DevSpace& S, const StEnt* __restrict__ st, uint64_t dsc,
                                             const RowLoad& L, uint2 pr, uint64_t (&v)[8]) {
     const uint32_t r = (uint32_t)dsc, k = (uint32_t)(dsc >> 32) & 0xFFFFFFu;
-    const uint32_t mask = (uint32_t)(dsc >> 56);
-    v[0] = (L.optrs.y + r) | ((uint64_t)mask << 56);
-    if (MODE == 1) return;
+    if (MODE == 1) {  // INDEX: the stage kernel stored the capacity mask
+        v[0] = (L.optrs.y + r) | ((dsc >> 56) << 56);
+        return;
+    }
     const uint32_t sel = r & ((1u << S.lg_rcdo) - 1u);
     const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
     const uint32_t u = pr.x, p = L.h.z;
@@ -435,6 +440,7 @@ __device__ __forceinline__ void expand_vals(const DevSpace& S, const StEnt* __re
             v[7] = tl;
         }
     }
+    v[0] = (L.optrs.y + r) | ((uint64_t)cap_mask_n<NCAP>(S, ~v[7]) << 56);
 }
 
 // Shared memory of the expand kernel: the pairs pool (when it fits) and, per
@@ -458,7 +464,7 @@ __device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __r
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const uint32_t i = i0 + 32 * j + lane;
-            dsc[j] = i < n ? __ldg(d + i) : ((uint64_t)k0 << 32);  // mask 0: no survivor (row k0, offset 0)
+            dsc[j] = i < n ? __ldg(d + i) : ((uint64_t)k0 << 32);  // past the end: row k0, offset 0 (not stored)
         }
         RowLoad L[U];
 #pragma unroll
@@ -473,12 +479,12 @@ __device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __r
         for (int j = 0; j < U; j++) pr[j] = MODE == 1 ? make_uint2(0, 0) : pairs[L[j].h.y + ((uint32_t)dsc[j] >> S.lg_rcdo)];
 #pragma unroll
         for (int j = 0; j < U; j++) {
-            const uint32_t mask = (uint32_t)(dsc[j] >> 56);
-            pk.add(mask);
+            const bool valid = i0 + 32 * j + lane < n;
             uint64_t v[8];
-            expand_vals<MODE, GBS, STMAX>(S, st, dsc[j], L[j], pr[j], v);
+            expand_vals<MODE, NCAP, GBS, STMAX>(S, st, dsc[j], L[j], pr[j], v);
+            pk.add(valid ? (uint32_t)(v[0] >> 56) : 0u);
             const uint64_t o = off + i0 + 32 * j + lane;
-            if (mask && o < capacity) {
+            if (valid && o < capacity) {
                 if (MODE == 3) {
                     store_record(cols.c[0] + o * 8, v);
                 } else if (MODE == 2) {
@@ -499,10 +505,15 @@ __device__ __forceinline__ void expand_spans(const DevSpace& S, const RowEnt* __
                                              const uint32_t* __restrict__ span_count,
                                              const uint64_t* __restrict__ block_off, const Cols& cols,
                                              uint64_t capacity, const uint2* pairs, RowEnt* srow,
-                                             uint32_t (&capc)[NCAP]) {
+                                             uint32_t* next_span, uint32_t (&capc)[NCAP]) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
-    for (uint32_t sp = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); sp < n_spans; sp += n_warps) {
+    // spans are taken in order from a counter (the survivors per span vary:
+    // a static assignment leaves a long tail)
+    uint32_t sp = 0;
+    while (true) {
+        if (lane == 0) sp = atomicAdd(next_span, 1u);
+        sp = __shfl_sync(0xffffffffu, sp, 0);
+        if (sp >= n_spans) break;
         const uint32_t n = __ldg(span_count + sp);
         if (!n) continue;
         // output row of the span: its block's offset + the earlier spans of the block
@@ -536,7 +547,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const DevSpace S, c
                                                              const uint32_t n_spans, const uint64_t* __restrict__ desc,
                                                              const uint32_t* __restrict__ span_count,
                                                              const uint64_t* __restrict__ block_off, const Cols cols,
-                                                             const uint64_t capacity, uint64_t* __restrict__ stats) {
+                                                             const uint64_t capacity, uint64_t* __restrict__ stats,
+                                                             uint32_t* __restrict__ next_span) {
     __shared__ uint32_t s_cap[NCAP];
     __shared__ uint2 s_pairs[kSmemPairs];
     __shared__ __align__(16) RowEnt s_rows[kWarpsPerBlock][kSmemRows];
@@ -553,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const DevSpace S, c
     for (int q = 0; q < NCAP; q++) capc[q] = 0;
 #define ME_EXPAND(GBS, STMAX)                                                                              \
     expand_spans<MODE, NCAP, GBS, STMAX, U>(S, rows, st, span_len, n_spans, desc, span_count, block_off, cols, \
-                                            capacity, pairs, srow, capc)
+                                            capacity, pairs, srow, next_span, capc)
     if (S.stage_max) {
         if (S.gbs_mode) ME_EXPAND(true, true);
         else ME_EXPAND(false, true);
@@ -593,14 +605,16 @@ int g_expand_u = 2;
 void* expand_fn(me_out_mode mode, uint32_t n_cap) {
     return g_expand_u >= 4 ? expand_fn_u<4>(mode, n_cap) : expand_fn_u<2>(mode, n_cap);
 }
-void* stage_fn(uint32_t n_cap) {
+template <bool MASK>
+void* stage_fn_(uint32_t n_cap) {
     switch (ncap_pad(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&stage_kernel<1>);
-        case 2: return reinterpret_cast<void*>(&stage_kernel<2>);
-        case 4: return reinterpret_cast<void*>(&stage_kernel<4>);
-        default: return reinterpret_cast<void*>(&stage_kernel<8>);
+        case 1: return reinterpret_cast<void*>(&stage_kernel<1, MASK>);
+        case 2: return reinterpret_cast<void*>(&stage_kernel<2, MASK>);
+        case 4: return reinterpret_cast<void*>(&stage_kernel<4, MASK>);
+        default: return reinterpret_cast<void*>(&stage_kernel<8, MASK>);
     }
 }
+void* stage_fn(uint32_t n_cap, bool mask) { return mask ? stage_fn_<true>(n_cap) : stage_fn_<false>(n_cap); }
 
 }  // namespace
 
@@ -624,20 +638,20 @@ cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_
 
 cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
                          uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t* span_count,
-                         uint32_t* block_count, cudaStream_t stream) {
+                         uint32_t* block_count, me_out_mode mode, cudaStream_t stream) {
     const uint32_t n_tiles = n_tiles_of(lo, hi);
     const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
     void* args[] = {(void*)&S,          (void*)&rows,    (void*)&st,      (void*)&lo,   (void*)&hi,
                     (void*)&span_tiles, (void*)&n_spans, (void*)&span_ck, (void*)&desc, (void*)&span_count,
                     (void*)&block_count};
-    return cudaLaunchKernel(stage_fn(S.n_cap), dim3((n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock),
+    return cudaLaunchKernel(stage_fn(S.n_cap, mode == ME_OUT_INDEX), dim3((n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock),
                             dim3(kThreads), args, 0, stream);
 }
 
 cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
                           uint32_t span_tiles, const uint64_t* desc, const uint32_t* span_count,
                           const uint64_t* block_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
-                          uint32_t n_blocks, cudaStream_t stream) {
+                          uint32_t n_blocks, uint32_t* next_span, cudaStream_t stream) {
     const uint32_t n_tiles = n_tiles_of(lo, hi);
     const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
     const uint32_t span_len = span_tiles * kTile;
@@ -645,7 +659,9 @@ cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st
     if (n_blocks > need) n_blocks = need ? need : 1;
     void* args[] = {(void*)&S,          (void*)&rows,     (void*)&st,   (void*)&span_len, (void*)&n_spans,
                     (void*)&desc,       (void*)&span_count, (void*)&block_off, (void*)&cols, (void*)&capacity,
-                    (void*)&stats};
+                    (void*)&stats,      (void*)&next_span};
+    cudaError_t ce = cudaMemsetAsync(next_span, 0, 4, stream);
+    if (ce != cudaSuccess) return ce;
     return cudaLaunchKernel(expand_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, stream);
 }
 
