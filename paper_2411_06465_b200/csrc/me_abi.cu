@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -142,6 +143,7 @@ struct me_plan {
     uint32_t pipe = 2;
     uint32_t rspan_tiles = 16;          // pipe 2: tiles per K1 span (ME_ROWS_SPAN)
     uint32_t max_rspans = 0, max_rows = 0;
+    uint32_t d32 = 0;                   // 32-bit survivor descriptors (no span touches > 255 rows)
     int expand_bps[4] = {0, 0, 0, 0};   // co-resident K3 blocks per SM per output mode
     uint32_t fused = 1;                 // 1 = fused single-pass kernel (ME_FUSED=0: count/scan/write passes)
     uint32_t span_tiles = 16;           // fused: tiles per warp span (ME_SPAN_TILES)
@@ -282,6 +284,12 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         P->max_rspans = (eff_tiles + P->rspan_tiles - 1) / P->rspan_tiles + 1;
         P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
         if (P->max_rows < 1) P->max_rows = 1;
+        // a span of L positions touches at most ceil(L / min_w) + 1 rows
+        uint64_t min_w = UINT64_MAX;
+        for (uint32_t t : H.list_tuple) min_w = std::min<uint64_t>(min_w, H.tuples[t].w);
+        const uint64_t L = (uint64_t)P->rspan_tiles * kTile;
+        P->d32 = L <= 65536 && min_w != UINT64_MAX && (L + min_w - 1) / min_w + 1 <= 256 ? 1u : 0u;
+        if (const char* e = getenv("ME_DESC64")) P->d32 = atoi(e) ? 0u : P->d32;
     }
     for (int m = 1; m < 4; m++) P->expand_bps[m] = expand_blocks_per_sm((me_out_mode)m, D.n_cap);
     if (const char* e = getenv("ME_EXPAND_BPS"))  // K3 grid: fewer blocks leave room for the overlapped K1
@@ -506,8 +514,8 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 cudaEventRecord(tev[0], cs);
                 cudaError_t ce = launch_rows(P->ds, g0, n_rows, lo, hi, P->rspan_tiles, sc.rows, sc.st, sc.rck, cs);
                 if (ce == cudaSuccess)
-                    ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, sc.rcount,
-                                      sc.rbcount, o->mode, cs);
+                    ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, P->d32,
+                                      sc.rcount, sc.rbcount, o->mode, cs);
                 if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
                 cudaEventRecord(tev[1], cs);
                 ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kWarpsPerBlock - 1) / kWarpsPerBlock, 0, sc.roff, stats,
@@ -516,8 +524,9 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 cudaEventRecord(tev[2], cs);
                 cudaStreamWaitEvent(st, tev[2], 0);
                 cudaEventRecord(tev[3], st);
-                ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, sc.rcount, sc.roff, o->mode,
-                                   cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[o->mode]), sc.rnext, st);
+                ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, P->d32, sc.rck, sc.rcount,
+                                   sc.roff, o->mode, cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[o->mode]),
+                                   sc.rnext, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
                 cudaEventRecord(tev[4], st);
                 cudaEventRecord(sc.free_ev, st);

@@ -270,11 +270,11 @@ int expand_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
 cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_t lo, uint64_t hi,
                         uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck, cudaStream_t stream);
 cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
-                         uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t* span_count,
+                         uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t d32, uint32_t* span_count,
                          uint32_t* block_count, me_out_mode mode, cudaStream_t stream);
 cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
-                          uint32_t span_tiles, const uint64_t* desc, const uint32_t* span_count,
-                          const uint64_t* block_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
+                          uint32_t span_tiles, const uint64_t* desc, uint32_t d32, const uint2* span_ck,
+                          const uint32_t* span_count, const uint64_t* block_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
                           uint32_t n_blocks, uint32_t* next_span, cudaStream_t stream);
 // NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
 // (rank key of DESIGN.md §9); best_key / best_index initialised to ~0.

@@ -217,8 +217,12 @@ __global__ void row_kernel(const DevSpace S, const uint64_t g0, const uint32_t n
 }
 
 // ---------------------------------------------------------------- K1
-// Descriptor of a survivor: bits 0..31 position in its row, 32..55 row of
-// the sub-range table, 56..63 capacity mask.
+// Descriptor of a survivor, two formats (the plan picks D32 when no span can
+// touch more than 255 rows):
+//  D64  bits 0..31 position in its row, 32..55 row of the sub-range table,
+//       56..63 capacity mask;
+//  D32  bits 0..15 position in the span, 16..23 row - the span's first row,
+//       24..31 capacity mask.
 // MASK: the descriptor carries the capacity mask (INDEX output, whose expand
 // pass computes no totals); otherwise only the survivor test (total <= the
 // largest threshold: one carry chain) is made here and the expand kernel
@@ -226,7 +230,7 @@ __global__ void row_kernel(const DevSpace S, const uint64_t g0, const uint32_t n
 template <int NCAP, bool GBS, bool STMAX, bool RAGGED, bool MASK>
 __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __restrict__ rows,
                                            const StEnt* __restrict__ st, uint32_t rounds, uint32_t lo_rel,
-                                           uint32_t hi_rel, uint2 ck, uint64_t* __restrict__ desc,
+                                           uint32_t hi_rel, uint2 ck, uint64_t* __restrict__ desc, bool d32,
                                            uint32_t* __restrict__ count_out, uint32_t lane) {
     // positions relative to the span start; RAGGED: the span is cut by the
     // range [lo, hi) = [lo_rel, hi_rel) (first / last span), a lane past the
@@ -254,8 +258,10 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
         if (RAGGED && (rel < lo_rel || rel >= hi_rel)) mask = 0;
         const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
         if (mask) {
-            const uint32_t hi_word = MASK ? W.k | (mask << 24) : W.k;
-            desc[cnt + __popc(ballot & ((1u << lane) - 1u))] = ((uint64_t)hi_word << 32) | W.r;
+            const uint32_t m = MASK ? mask << 24 : 0u;
+            const uint32_t at = cnt + __popc(ballot & ((1u << lane) - 1u));
+            if (d32) reinterpret_cast<uint32_t*>(desc)[at] = rel | ((W.k - ck.x) << 16) | m;
+            else desc[at] = ((uint64_t)(W.k | m) << 32) | W.r;
         }
         cnt += __popc(ballot);
         if (more && (!RAGGED || rel + 32 < hi_rel)) {
@@ -276,20 +282,21 @@ template <int NCAP, bool MASK>
 __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __restrict__ rows,
                                           const StEnt* __restrict__ st, uint64_t lo, uint64_t hi, uint32_t span_tiles,
                                           uint32_t sp, const uint2* __restrict__ span_ck, uint64_t* __restrict__ desc,
-                                          uint32_t* __restrict__ span_count, uint32_t lane);
+                                          bool d32, uint32_t* __restrict__ span_count, uint32_t lane);
 
 template <int NCAP, bool MASK>
 __global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
                                                             const StEnt* __restrict__ st, const uint64_t lo,
                                                             const uint64_t hi, const uint32_t span_tiles,
                                                             const uint32_t n_spans, const uint2* __restrict__ span_ck,
-                                                            uint64_t* __restrict__ desc,
+                                                            uint64_t* __restrict__ desc, const uint32_t d32,
                                                             uint32_t* __restrict__ span_count,
                                                             uint32_t* __restrict__ block_count) {
     __shared__ uint32_t s_cnt[kWarpsPerBlock];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t sp = blockIdx.x * kWarpsPerBlock + wid;
-    if (sp < n_spans) stage_one<NCAP, MASK>(S, rows, st, lo, hi, span_tiles, sp, span_ck, desc, span_count, lane);
+    if (sp < n_spans)
+        stage_one<NCAP, MASK>(S, rows, st, lo, hi, span_tiles, sp, span_ck, desc, d32 != 0, span_count, lane);
     // the block's survivors (the scan runs over blocks; the expand kernel
     // adds the counts of the earlier spans of its block)
     if (lane == 0) s_cnt[wid] = sp < n_spans ? span_count[sp] : 0u;
@@ -306,7 +313,7 @@ template <int NCAP, bool MASK>
 __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __restrict__ rows,
                                           const StEnt* __restrict__ st, uint64_t lo, uint64_t hi, uint32_t span_tiles,
                                           uint32_t sp, const uint2* __restrict__ span_ck, uint64_t* __restrict__ desc,
-                                          uint32_t* __restrict__ span_count, uint32_t lane) {
+                                          bool d32, uint32_t* __restrict__ span_count, uint32_t lane) {
     const uint64_t base = lo & ~31ull;
     const uint32_t n_tiles = (uint32_t)((hi - base + kTile - 1) / kTile);
     const uint32_t t0 = sp * span_tiles;
@@ -317,11 +324,13 @@ __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __res
     const uint32_t lo_rel = lo > s0 ? (uint32_t)(lo - s0) : 0u, hi_rel = (uint32_t)(e - s0);
     const bool ragged = lo_rel != 0 || (hi_rel & 31u) != 0;
     const uint2 ck = __ldg(span_ck + sp);
-    uint64_t* d = desc + (size_t)sp * span_tiles * kTile;
+    // the span's slice: span_len slots of the descriptor format
+    uint64_t* d = d32 ? reinterpret_cast<uint64_t*>(reinterpret_cast<uint32_t*>(desc) + (size_t)sp * span_tiles * kTile)
+                      : desc + (size_t)sp * span_tiles * kTile;
     uint32_t* c = span_count + sp;
 #define ME_STAGE(GBS, STMAX)                                                                           \
-    (ragged ? stage_span<NCAP, GBS, STMAX, true, MASK>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane) \
-            : stage_span<NCAP, GBS, STMAX, false, MASK>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, c, lane))
+    (ragged ? stage_span<NCAP, GBS, STMAX, true, MASK>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, d32, c, lane) \
+            : stage_span<NCAP, GBS, STMAX, false, MASK>(S, rows, st, rounds, lo_rel, hi_rel, ck, d, d32, c, lane))
     if (S.stage_max) {
         if (S.gbs_mode) ME_STAGE(true, true);
         else ME_STAGE(false, true);
@@ -405,12 +414,14 @@ __device__ __forceinline__ void load_row(const RowEnt* __restrict__ e, RowLoad& 
 
 // one survivor's output values from its descriptor, row data and pair
 // (MODE 1: index|mask only)
+// (k, r) = row and position in it, idx = flat index, dmask = the mask the
+// stage kernel stored (INDEX only)
 template <int MODE, int NCAP, bool GBS, bool STMAX>
-__device__ __forceinline__ void expand_vals(const DevSpace& S, const StEnt* __restrict__ st, uint64_t dsc,
-                                            const RowLoad& L, uint2 pr, uint64_t (&v)[8]) {
-    const uint32_t r = (uint32_t)dsc, k = (uint32_t)(dsc >> 32) & 0xFFFFFFu;
-    if (MODE == 1) {  // INDEX: the stage kernel stored the capacity mask
-        v[0] = (L.optrs.y + r) | ((dsc >> 56) << 56);
+__device__ __forceinline__ void expand_vals(const DevSpace& S, const StEnt* __restrict__ st, uint32_t k, uint32_t r,
+                                            uint64_t idx, uint32_t dmask, const RowLoad& L, uint2 pr,
+                                            uint64_t (&v)[8]) {
+    if (MODE == 1) {
+        v[0] = idx | ((uint64_t)dmask << 56);
         return;
     }
     const uint32_t sel = r & ((1u << S.lg_rcdo) - 1u);
@@ -440,7 +451,7 @@ __device__ __forceinline__ void expand_vals(const DevSpace& S, const StEnt* __re
             v[7] = tl;
         }
     }
-    v[0] = (L.optrs.y + r) | ((uint64_t)cap_mask_n<NCAP>(S, ~v[7]) << 56);
+    v[0] = idx | ((uint64_t)cap_mask_n<NCAP>(S, ~v[7]) << 56);
 }
 
 // Shared memory of the expand kernel: the pairs pool (when it fits) and, per
@@ -453,35 +464,51 @@ constexpr uint32_t kSmemRows = 24;     // per warp: 3 KB (C5: a 16-tile span tou
 // (descriptors, rows, pairs, values + stores) so that each phase's loads are
 // in flight together.  SMEM: rows from the warp's shared copy (row k at
 // srow[k - k0]); pairs: shared or global (pairs).
-template <int MODE, int NCAP, bool GBS, bool STMAX, int U, bool SMEM>
+template <int MODE, int NCAP, bool GBS, bool STMAX, int U, bool SMEM, bool D32>
 __device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __restrict__ rows,
-                                            const RowEnt* srow, uint32_t k0, const uint2* pairs,
-                                            const StEnt* __restrict__ st, const uint64_t* __restrict__ d, uint32_t n,
-                                            uint64_t off, const Cols& cols, uint64_t capacity, CapPack<NCAP>& pk,
-                                            uint32_t lane) {
+                                            const RowEnt* srow, uint32_t k0, uint32_t kspan, uint64_t s0,
+                                            const uint2* pairs, const StEnt* __restrict__ st,
+                                            const void* __restrict__ dv, uint32_t n, uint64_t off, const Cols& cols,
+                                            uint64_t capacity, CapPack<NCAP>& pk, uint32_t lane) {
     for (uint32_t i0 = 0; i0 < n; i0 += 32 * U) {
-        uint64_t dsc[U];
+        // descriptors -> (row, position in row or index, stored mask); past the end: row k0
+        uint32_t k[U], r[U], dm[U];
+        uint64_t idx[U];
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const uint32_t i = i0 + 32 * j + lane;
-            dsc[j] = i < n ? __ldg(d + i) : ((uint64_t)k0 << 32);  // past the end: row k0, offset 0 (not stored)
+            if (D32) {
+                const uint32_t x = i < n ? __ldg(reinterpret_cast<const uint32_t*>(dv) + i) : 0u;
+                k[j] = i < n ? kspan + ((x >> 16) & 0xFFu) : k0;
+                idx[j] = s0 + (x & 0xFFFFu);
+                dm[j] = x >> 24;
+            } else {
+                const uint64_t x = i < n ? __ldg(reinterpret_cast<const uint64_t*>(dv) + i) : ((uint64_t)k0 << 32);
+                k[j] = (uint32_t)(x >> 32) & 0xFFFFFFu;
+                r[j] = (uint32_t)x;
+                dm[j] = (uint32_t)(x >> 56);
+            }
         }
         RowLoad L[U];
+        const bool need_rs = MODE != 1 || !D32;
 #pragma unroll
         for (int j = 0; j < U; j++) {
-            const uint32_t k = (uint32_t)(dsc[j] >> 32) & 0xFFFFFFu;
-            const RowEnt* e = SMEM ? srow + (k - k0) : rows + k;
-            if (MODE == 1) L[j].optrs.y = SMEM ? e->rs : __ldg(&e->rs);
-            else load_row<SMEM>(e, L[j]);
+            const RowEnt* e = SMEM ? srow + (k[j] - k0) : rows + k[j];
+            if (MODE != 1) load_row<SMEM>(e, L[j]);
+            else if (need_rs) L[j].optrs.y = SMEM ? e->rs : __ldg(&e->rs);
         }
         uint2 pr[U];
 #pragma unroll
-        for (int j = 0; j < U; j++) pr[j] = MODE == 1 ? make_uint2(0, 0) : pairs[L[j].h.y + ((uint32_t)dsc[j] >> S.lg_rcdo)];
+        for (int j = 0; j < U; j++) {
+            if (D32) r[j] = MODE != 1 && i0 + 32 * j + lane < n ? (uint32_t)(idx[j] - L[j].optrs.y) : 0u;
+            else idx[j] = L[j].optrs.y + r[j];
+            pr[j] = MODE == 1 ? make_uint2(0, 0) : pairs[L[j].h.y + (r[j] >> S.lg_rcdo)];
+        }
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const bool valid = i0 + 32 * j + lane < n;
             uint64_t v[8];
-            expand_vals<MODE, NCAP, GBS, STMAX>(S, st, dsc[j], L[j], pr[j], v);
+            expand_vals<MODE, NCAP, GBS, STMAX>(S, st, k[j], r[j], idx[j], dm[j], L[j], pr[j], v);
             pk.add(valid ? (uint32_t)(v[0] >> 56) : 0u);
             const uint64_t o = off + i0 + 32 * j + lane;
             if (valid && o < capacity) {
@@ -501,7 +528,8 @@ __device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __r
 template <int MODE, int NCAP, bool GBS, bool STMAX, int U>
 __device__ __forceinline__ void expand_spans(const DevSpace& S, const RowEnt* __restrict__ rows,
                                              const StEnt* __restrict__ st, uint32_t span_len, uint32_t n_spans,
-                                             const uint64_t* __restrict__ desc,
+                                             const uint64_t* __restrict__ desc, bool d32,
+                                             const uint2* __restrict__ span_ck, uint64_t base,
                                              const uint32_t* __restrict__ span_count,
                                              const uint64_t* __restrict__ block_off, const Cols& cols,
                                              uint64_t capacity, const uint2* pairs, RowEnt* srow,
@@ -519,23 +547,40 @@ __device__ __forceinline__ void expand_spans(const DevSpace& S, const RowEnt* __
         // output row of the span: its block's offset + the earlier spans of the block
         uint64_t off = __ldg(block_off + sp / kWarpsPerBlock);
         for (uint32_t q = sp & ~(kWarpsPerBlock - 1u); q < sp; q++) off += __ldg(span_count + q);
-        const uint64_t* d = desc + (size_t)sp * span_len;
         // rows of the span: from its first and last survivor (index order)
-        const uint32_t k0 = (uint32_t)(__ldg(d) >> 32) & 0xFFFFFFu;
-        const uint32_t k1 = (uint32_t)(__ldg(d + n - 1) >> 32) & 0xFFFFFFu;
+        const uint2 ck = __ldg(span_ck + sp);
+        const uint64_t s0 = base + (uint64_t)sp * span_len;
+        const void* dv;
+        uint32_t k0, k1;
+        if (d32) {
+            const uint32_t* d = reinterpret_cast<const uint32_t*>(desc) + (size_t)sp * span_len;
+            k0 = ck.x + ((__ldg(d) >> 16) & 0xFFu);
+            k1 = ck.x + ((__ldg(d + n - 1) >> 16) & 0xFFu);
+            dv = d;
+        } else {
+            const uint64_t* d = desc + (size_t)sp * span_len;
+            k0 = (uint32_t)(__ldg(d) >> 32) & 0xFFFFFFu;
+            k1 = (uint32_t)(__ldg(d + n - 1) >> 32) & 0xFFFFFFu;
+            dv = d;
+        }
         CapPack<NCAP> pk;  // <= span_len / 32 survivors per lane per span: fits 16 bits
-        if (k1 - k0 < kSmemRows) {
+#define ME_SPAN(SM, D)                                                                                           \
+    expand_span<MODE, NCAP, GBS, STMAX, U, SM, D>(S, rows, srow, k0, ck.x, s0, pairs, st, dv, n, off, cols, capacity, \
+                                                  pk, lane)
+        const bool smem = k1 - k0 < kSmemRows && !(MODE == 1 && d32);
+        if (smem) {
             __syncwarp();  // the previous span's readers are done with srow
             const uint4* src = reinterpret_cast<const uint4*>(rows + k0);
             uint4* dst = reinterpret_cast<uint4*>(srow);
             for (uint32_t c = lane; c < (k1 - k0 + 1) * (sizeof(RowEnt) / 16); c += 32) dst[c] = __ldg(src + c);
             __syncwarp();
-            expand_span<MODE, NCAP, GBS, STMAX, U, true>(S, rows, srow, k0, pairs, st, d, n, off, cols, capacity, pk,
-                                                         lane);
+            if (d32) ME_SPAN(true, true);
+            else ME_SPAN(true, false);
         } else {
-            expand_span<MODE, NCAP, GBS, STMAX, U, false>(S, rows, srow, k0, pairs, st, d, n, off, cols, capacity,
-                                                          pk, lane);
+            if (d32) ME_SPAN(false, true);
+            else ME_SPAN(false, false);
         }
+#undef ME_SPAN
         pk.flush(capc);
     }
 }
@@ -545,6 +590,8 @@ template <int MODE, int NCAP, int U>
 __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
                                                              const StEnt* __restrict__ st, const uint32_t span_len,
                                                              const uint32_t n_spans, const uint64_t* __restrict__ desc,
+                                                             const uint32_t d32, const uint2* __restrict__ span_ck,
+                                                             const uint64_t base,
                                                              const uint32_t* __restrict__ span_count,
                                                              const uint64_t* __restrict__ block_off, const Cols cols,
                                                              const uint64_t capacity, uint64_t* __restrict__ stats,
@@ -564,8 +611,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const DevSpace S, c
 #pragma unroll
     for (int q = 0; q < NCAP; q++) capc[q] = 0;
 #define ME_EXPAND(GBS, STMAX)                                                                              \
-    expand_spans<MODE, NCAP, GBS, STMAX, U>(S, rows, st, span_len, n_spans, desc, span_count, block_off, cols, \
-                                            capacity, pairs, srow, next_span, capc)
+    expand_spans<MODE, NCAP, GBS, STMAX, U>(S, rows, st, span_len, n_spans, desc, d32 != 0, span_ck, base,      \
+                                            span_count, block_off, cols, capacity, pairs, srow, next_span, capc)
     if (S.stage_max) {
         if (S.gbs_mode) ME_EXPAND(true, true);
         else ME_EXPAND(false, true);
@@ -637,19 +684,20 @@ cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_
 }
 
 cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
-                         uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t* span_count,
+                         uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t d32, uint32_t* span_count,
                          uint32_t* block_count, me_out_mode mode, cudaStream_t stream) {
     const uint32_t n_tiles = n_tiles_of(lo, hi);
     const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
     void* args[] = {(void*)&S,          (void*)&rows,    (void*)&st,      (void*)&lo,   (void*)&hi,
-                    (void*)&span_tiles, (void*)&n_spans, (void*)&span_ck, (void*)&desc, (void*)&span_count,
-                    (void*)&block_count};
+                    (void*)&span_tiles, (void*)&n_spans, (void*)&span_ck, (void*)&desc, (void*)&d32,
+                    (void*)&span_count, (void*)&block_count};
     return cudaLaunchKernel(stage_fn(S.n_cap, mode == ME_OUT_INDEX), dim3((n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock),
                             dim3(kThreads), args, 0, stream);
 }
 
 cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
-                          uint32_t span_tiles, const uint64_t* desc, const uint32_t* span_count,
+                          uint32_t span_tiles, const uint64_t* desc, uint32_t d32, const uint2* span_ck,
+                          const uint32_t* span_count,
                           const uint64_t* block_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
                           uint32_t n_blocks, uint32_t* next_span, cudaStream_t stream) {
     const uint32_t n_tiles = n_tiles_of(lo, hi);
@@ -657,9 +705,10 @@ cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st
     const uint32_t span_len = span_tiles * kTile;
     const uint32_t need = (n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (n_blocks > need) n_blocks = need ? need : 1;
-    void* args[] = {(void*)&S,          (void*)&rows,     (void*)&st,   (void*)&span_len, (void*)&n_spans,
-                    (void*)&desc,       (void*)&span_count, (void*)&block_off, (void*)&cols, (void*)&capacity,
-                    (void*)&stats,      (void*)&next_span};
+    const uint64_t base = lo & ~31ull;
+    void* args[] = {(void*)&S,    (void*)&rows,    (void*)&st,   (void*)&span_len,   (void*)&n_spans,
+                    (void*)&desc, (void*)&d32,     (void*)&span_ck, (void*)&base,   (void*)&span_count,
+                    (void*)&block_off, (void*)&cols, (void*)&capacity, (void*)&stats, (void*)&next_span};
     cudaError_t ce = cudaMemsetAsync(next_span, 0, 4, stream);
     if (ce != cudaSuccess) return ce;
     return cudaLaunchKernel(expand_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, stream);

@@ -336,3 +336,25 @@ def test_sweep_zero_stages(me, oracle_mod, zero, stage_max):
                   stage_max=stage_max)
     res = me.Plan(sp).sweep(mode=me.ME_OUT_FULL)
     assert_same(me, res, *oracle_rows(oracle_mod, sp), me.ME_OUT_FULL)
+
+
+@pytest.mark.parametrize("env", [{"ME_PIPE": "0"}, {"ME_PIPE": "1"}, {"ME_DESC64": "1"}, {"ME_SERIAL": "1"},
+                                 {"ME_EXPAND_U": "4"}],
+                         ids=["pipe0", "pipe1", "desc64", "serial", "u4"])
+def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
+    """The selectable pipelines and kernel variants (read at plan creation)
+    give the same rows: count/scan/write passes, the fused single pass, the
+    row-table pipeline with 64-bit descriptors, serial streams, 4 survivors
+    per lane in the expand kernel."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    spaces = [mi.config("C3", uneven=1),
+              mi.Space(models=mi.random_models(12, seed=5), world=[24, 64, 96], caps_gb=[40, 80, 192],
+                       mbs=[1, 2, 4], seq=[4096, 8192], uneven=1, gbs=768)]
+    for sp in spaces:
+        plan = me.Plan(sp)
+        ref = oracle_rows(oracle_mod, sp)
+        for mode in (me.ME_OUT_INDEX, me.ME_OUT_FULL, me.ME_OUT_RECORDS):
+            res = plan.sweep(mode=mode)
+            assert res.status() == 0
+            assert_same(me, res, *ref, mode)
