@@ -95,6 +95,8 @@ struct me_comm {
 // ---------------------------------------------------------------------------
 // plan
 // ---------------------------------------------------------------------------
+constexpr uint32_t kMaxSets = 4;
+
 struct me_plan {
     HostSpace hs;
     DevSpace ds{};
@@ -108,7 +110,6 @@ struct me_plan {
     int sms = 148;
     uint32_t max_spans = 0, max_tiles = 0;
     uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t comb = 0;                      // write combining into aligned 32-row windows (ME_WRITE_COMB=1)
     uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
     // count pass on the caller's stream (1) or on the plan's own stream,
     // overlapping the write pass of the previous sub-range (0; ME_SERIAL).
@@ -136,7 +137,8 @@ struct me_plan {
         uint64_t* roff = nullptr;       // output row of each block's first survivor
         uint32_t* rnext = nullptr;      // expand kernel: next span to take
         cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
-    } scratch[2];
+    } scratch[kMaxSets];
+    uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
     // write-mode pipeline: 2 = row table + descriptors (K0 rows, K1 stage,
     // scan, K3 expand; default), 1 = fused single-pass kernel, 0 = count /
     // scan / write passes (ME_PIPE).  COUNT mode always uses the count pass.
@@ -269,7 +271,6 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     P->max_spans = (uint32_t)P->sms * 96;
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
-    if (const char* e = getenv("ME_WRITE_COMB")) P->comb = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
     if (const char* e = getenv("ME_FUSED")) P->pipe = (uint32_t)atoi(e);
@@ -291,15 +292,19 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         P->d32 = L <= 65536 && min_w != UINT64_MAX && (L + min_w - 1) / min_w + 1 <= 256 ? 1u : 0u;
         if (const char* e = getenv("ME_DESC64")) P->d32 = atoi(e) ? 0u : P->d32;
     }
-    for (int m = 1; m < 4; m++) P->expand_bps[m] = expand_blocks_per_sm((me_out_mode)m, D.n_cap);
-    if (const char* e = getenv("ME_EXPAND_BPS"))  // K3 grid: fewer blocks leave room for the overlapped K1
-        for (int m = 1; m < 4; m++) P->expand_bps[m] = std::min(P->expand_bps[m], std::max(1, atoi(e)));
+    // K3 grid: 2 blocks per SM saturate HBM and leave registers for the
+    // overlapped K1 of the next sub-range (measured: 3 per SM, all the
+    // registers, is 7% slower on C5; 1 per SM cannot keep HBM busy)
+    int ebps = 2;
+    if (const char* e = getenv("ME_EXPAND_BPS")) ebps = std::max(1, atoi(e));
+    for (int m = 1; m < 4; m++)
+        P->expand_bps[m] = std::min(expand_blocks_per_sm((me_out_mode)m, D.n_cap), ebps);
     if (const char* e = getenv("ME_SPAN_TILES")) P->span_tiles = (uint32_t)atoi(e);
     if (P->span_tiles < 1) P->span_tiles = 1;
     P->max_units = (P->max_tiles + P->span_tiles * kWarpsPerBlock - 1) / (P->span_tiles * kWarpsPerBlock) + 1;
     if (const char* e = getenv("ME_FUSED_MINB")) P->fused_minb = atoi(e);
     for (int m = 0; m < 4; m++) P->fused_bps[m] = fused_blocks_per_sm((me_out_mode)m, D.n_cap, P->fused_minb);
-    const int occ_c = sweep_blocks_per_sm(0, D.n_cap, 0), occ_w = sweep_blocks_per_sm(2, D.n_cap, (int)P->comb);
+    const int occ_c = sweep_blocks_per_sm(0, D.n_cap), occ_w = sweep_blocks_per_sm(2, D.n_cap);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
     P->write_bps = (uint32_t)(occ_w > 2 ? 2 : occ_w);
@@ -308,7 +313,9 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_COUNT_BPS")) P->count_bps = (uint32_t)atoi(e);
     if (P->write_bps < 1) P->write_bps = 1;
     if (P->count_bps < 1) P->count_bps = 1;
-    for (auto& sc : P->scratch) {
+    if (const char* e = getenv("ME_SETS")) P->n_sets = (uint32_t)std::min(std::max(atoi(e), 2), (int)kMaxSets);
+    for (uint32_t si = 0; si < P->n_sets; si++) {
+        me_plan::Scratch& sc = P->scratch[si];
         sc.tile_rel = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
         sc.tile_cnt = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
         P->owned.push_back(sc.tile_cnt);
@@ -473,7 +480,6 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
-    int comb = 0;
     auto pipeline = [&](uint64_t* stats, bool write, Cols cols, uint64_t capacity) -> int {
         if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
         const bool rows_pipe = P->pipe == 2 && write;
@@ -492,7 +498,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 }
                 n_rows = (uint32_t)(H.row_of(hi - 1) + 1 - g0);
             }
-            me_plan::Scratch& sc = P->scratch[P->turn++ & 1];
+            me_plan::Scratch& sc = P->scratch[P->turn++ % P->n_sets];
             const uint32_t n_tiles = n_tiles_of(lo, hi);
             const uint32_t n_spans = n_tiles < P->max_spans ? n_tiles : P->max_spans;
             // grid_mode 0: persistent grids of bps resident blocks per SM;
@@ -565,7 +571,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             cudaEventRecord(tev[3], st);
             if (write) {
                 ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_rel, sc.tile_cnt,
-                                  sc.span_off, o->mode, comb, cols, capacity, st);
+                                  sc.span_off, o->mode, cols, capacity, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "write kernel");
             }
             cudaEventRecord(tev[4], st);
@@ -600,7 +606,6 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
     }
-    comb = (int)P->comb;
     if ((rc = pipeline(R->stats, nc != 0, cols, R->capacity))) return fail(rc);
     R->ran_count = len != 0;
     R->ran_write = nc && len;

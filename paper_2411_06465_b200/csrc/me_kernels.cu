@@ -235,41 +235,6 @@ struct CapAcc {
     }
 };
 
-// Write combining (COMB): the rows of a warp's survivors are staged in a
-// 64-row shared-memory ring per column (slot = row mod 64) and leave it in
-// windows of 32 rows aligned to 32 (256-byte aligned, full-warp column
-// stores), whatever the survivor density of a round; only the first and the
-// last window of a tile are partial.  Measured store patterns:
-// scripts/storebench.cu.
-template <int NC>
-struct Combiner {
-    uint64_t* buf;  // NC x 64 rows of this warp
-    uint64_t wb;    // first row of the open window (multiple of 32)
-    uint64_t row0;  // first row of the tile (rows below belong to another tile)
-    __device__ __forceinline__ void start(uint64_t out0) {
-        row0 = out0;
-        wb = out0 & ~31ull;
-    }
-    __device__ __forceinline__ void put(uint64_t row, int c, uint64_t v) { buf[c * 64 + (row & 63u)] = v; }
-    // store the open window's rows [wb, lim) (rows >= row0 and < capacity)
-    __device__ __forceinline__ void flush(const Cols& cols, uint64_t capacity, uint32_t lane, uint64_t lim) {
-        const uint64_t row = wb + lane;
-        if (row >= row0 && row < lim && row < capacity) {
-#pragma unroll
-            for (int c = 0; c < NC; c++) cols.c[c][row] = buf[c * 64 + (row & 63u)];
-        }
-    }
-    // after a round whose rows end at `end`: emit every completed window
-    __device__ __forceinline__ void round_done(const Cols& cols, uint64_t capacity, uint32_t lane, uint64_t end) {
-        if (end >= wb + 32) {
-            __syncwarp();
-            flush(cols, capacity, lane, wb + 32);
-            wb += 32;
-            __syncwarp();  // the window's slots are free again
-        }
-    }
-};
-
 // Evaluate one tile's rounds starting at the walker's position (lane's index
 // = pos).  RAGGED: the tile is cut by lo/hi (first or last tile of a range).
 // GBS: a global batch bounds the in-flight microbatches (R17).  STMAX: the
@@ -283,11 +248,10 @@ struct Combiner {
 // B200, scripts/storebench.cu and DESIGN.md §6: shared-memory staging into
 // aligned full-line stores lifts the store pattern itself from ~4.1 to ~5.7
 // TB/s but costs more issue slots than it saves in this kernel.)
-template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX, bool COMB = false>
+template <int MODE, int NCAP, bool RAGGED, bool GBS, bool STMAX>
 __device__ __forceinline__ uint64_t run_tile(const DevSpace& S, Walker& W, uint64_t pos, uint64_t lo,
                                              uint64_t hi, uint32_t rounds, uint32_t lane, CapAcc<NCAP>& acc,
-                                             uint64_t out, const Cols& cols, uint64_t capacity,
-                                             bool advance_out, Combiner<MODE >= 2 ? 8 : 1>* cb = nullptr) {
+                                             uint64_t out, const Cols& cols, uint64_t capacity, bool advance_out) {
     constexpr int NC = MODE >= 2 ? 8 : 1;
     constexpr bool PREFETCH = MODE != 0;  // the write pass hides the pair load behind a round
     const uint32_t pstep = 32u >> S.lg_rcdo;
@@ -321,7 +285,7 @@ __device__ __forceinline__ uint64_t run_tile(const DevSpace& S, Walker& W, uint6
             const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
             if (mask) {
                 const uint64_t o = out + __popc(ballot & ((1u << lane) - 1u));
-                if (COMB || o < capacity) {
+                if (o < capacity) {
                     uint64_t v[NC];
                     v[0] = pos | ((uint64_t)mask << 56);
                     if (MODE >= 2) {
@@ -344,9 +308,6 @@ __device__ __forceinline__ uint64_t run_tile(const DevSpace& S, Walker& W, uint6
                         asm volatile("st.global.v4.u64 [%0+32], {%1, %2, %3, %4};" ::"l"(q), "l"(v[4]), "l"(v[5]),
                                      "l"(v[6]), "l"(v[7])
                                      : "memory");
-                    } else if (COMB) {
-#pragma unroll
-                        for (int c = 0; c < NC; c++) cb->put(o, c, v[c]);
                     } else {
 #pragma unroll
                         for (int c = 0; c < NC; c++) cols.c[c][o] = v[c];
@@ -354,7 +315,6 @@ __device__ __forceinline__ uint64_t run_tile(const DevSpace& S, Walker& W, uint6
                 }
             }
             out += __popc(ballot);
-            if (COMB) cb->round_done(cols, capacity, lane, out);
         }
         if (more && (!RAGGED || pos + 32 < hi)) {
             if (in_row) {
@@ -366,11 +326,6 @@ __device__ __forceinline__ uint64_t run_tile(const DevSpace& S, Walker& W, uint6
                 pr = __ldg(W.pp);
             }
         }
-    }
-    if (COMB) {  // the tile's last, partial window
-        __syncwarp();
-        cb->flush(cols, capacity, lane, out);
-        __syncwarp();
     }
     return out;
 }
@@ -467,35 +422,30 @@ __global__ void __launch_bounds__(kThreads, 3) count_kernel(const DevSpace S, co
     }
 }
 
-template <int MODE, int NCAP, bool GBS, bool STMAX, bool COMB>
+template <int MODE, int NCAP, bool GBS, bool STMAX>
 __device__ __forceinline__ void write_tile(const DevSpace& S, const TileGeom& G, Walker& W, uint32_t t, uint64_t pos,
-                                           uint32_t lane, uint64_t out, const Cols& cols, uint64_t capacity,
-                                           Combiner<MODE >= 2 ? 8 : 1>* cb) {
+                                           uint32_t lane, uint64_t out, const Cols& cols, uint64_t capacity) {
     CapAcc<NCAP> none;
     if (G.ragged(t))
-        run_tile<MODE, NCAP, true, GBS, STMAX, COMB>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols,
-                                                     capacity, false, cb);
+        run_tile<MODE, NCAP, true, GBS, STMAX>(S, W, pos, G.lo, G.hi, G.rounds(t), lane, none, out, cols, capacity,
+                                               false);
     else
-        run_tile<MODE, NCAP, false, GBS, STMAX, COMB>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols,
-                                                      capacity, false, cb);
+        run_tile<MODE, NCAP, false, GBS, STMAX>(S, W, pos, G.lo, G.hi, kTileRounds, lane, none, out, cols, capacity,
+                                                false);
 }
 
 // write pass: tiles in grid-stride order (at any moment the grid writes one
 // compact window of the output columns)
-template <int MODE, int NCAP, bool COMB>
+template <int MODE, int NCAP>
 __global__ void __launch_bounds__(kThreads, MODE == 3 ? 2 : 3) write_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
                                                             const uint4* __restrict__ tile_ck,
                                                             const uint32_t* __restrict__ tile_rel,
                                                             const uint32_t* __restrict__ tile_cnt,
                                                             const uint64_t* __restrict__ span_off, const Cols cols,
                                                             const uint64_t capacity) {
-    constexpr int NC = MODE >= 2 ? 8 : 1;
-    __shared__ uint64_t s_comb[COMB ? kWarpsPerBlock * NC * 64 : 1];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t n_warps = gridDim.x * kWarpsPerBlock;
     const TileGeom G = geom(lo, hi);
-    Combiner<NC> cb;
-    cb.buf = s_comb + (COMB ? wid * NC * 64 : 0);
     for (uint32_t t = blockIdx.x * kWarpsPerBlock + wid; t < G.n_tiles; t += n_warps) {
         if (__ldg(tile_cnt + t) == 0) continue;  // no survivor: nothing to write
         const uint64_t ts = G.start(t);
@@ -506,13 +456,12 @@ __global__ void __launch_bounds__(kThreads, MODE == 3 ? 2 : 3) write_kernel(cons
         // a lane past the end of the range is parked on the last index: it
         // takes part in the ballots with inactive positions
         W.restore(S, ck, pos < hi ? lane : (uint32_t)(hi - 1 - ts));
-        cb.start(out);
         if (S.stage_max) {
-            if (S.gbs_mode) write_tile<MODE, NCAP, true, true, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
-            else write_tile<MODE, NCAP, false, true, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, true>(S, G, W, t, pos, lane, out, cols, capacity);
+            else write_tile<MODE, NCAP, false, true>(S, G, W, t, pos, lane, out, cols, capacity);
         } else {
-            if (S.gbs_mode) write_tile<MODE, NCAP, true, false, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
-            else write_tile<MODE, NCAP, false, false, COMB>(S, G, W, t, pos, lane, out, cols, capacity, &cb);
+            if (S.gbs_mode) write_tile<MODE, NCAP, true, false>(S, G, W, t, pos, lane, out, cols, capacity);
+            else write_tile<MODE, NCAP, false, false>(S, G, W, t, pos, lane, out, cols, capacity);
         }
     }
 }
@@ -916,25 +865,21 @@ void* count_kernel_for(uint32_t n_cap) {
     }
 }
 
-template <int MODE, bool COMB>
+template <int MODE>
 void* write_kernel_for(uint32_t n_cap) {
     switch (ncap_stride_(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1, COMB>);
-        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2, COMB>);
-        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4, COMB>);
-        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8, COMB>);
+        case 1: return reinterpret_cast<void*>(&write_kernel<MODE, 1>);
+        case 2: return reinterpret_cast<void*>(&write_kernel<MODE, 2>);
+        case 4: return reinterpret_cast<void*>(&write_kernel<MODE, 4>);
+        default: return reinterpret_cast<void*>(&write_kernel<MODE, 8>);
     }
 }
 
-// wvar: 0 plain column stores, 1 write combining (FULL / INDEX)
-void* write_fn(me_out_mode mode, uint32_t n_cap, int wvar) {
-    if (mode == ME_OUT_RECORDS) return write_kernel_for<3, false>(n_cap);
-    const bool comb = wvar == 1;
-    if (mode == ME_OUT_FULL) return comb ? write_kernel_for<2, true>(n_cap) : write_kernel_for<2, false>(n_cap);
-    return comb ? write_kernel_for<1, true>(n_cap) : write_kernel_for<1, false>(n_cap);
+void* write_fn(me_out_mode mode, uint32_t n_cap) {
+    if (mode == ME_OUT_RECORDS) return write_kernel_for<3>(n_cap);
+    return mode == ME_OUT_FULL ? write_kernel_for<2>(n_cap) : write_kernel_for<1>(n_cap);
 }
 
-size_t write_smem(me_out_mode, int) { return 0; }
 
 }  // namespace
 
@@ -970,13 +915,11 @@ void* fused_fn(me_out_mode mode, uint32_t n_cap, int minb) {
 }
 
 // pass 0 count, 1 INDEX write, 2 FULL write, 3 RECORDS write
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, int wvar) {
+int sweep_blocks_per_sm(int pass, uint32_t n_cap) {
     const me_out_mode mode = pass == 3 ? ME_OUT_RECORDS : (pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX);
-    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(mode, n_cap, wvar);
-    const size_t smem = pass == 0 ? 0 : write_smem(mode, wvar);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* fn = pass == 0 ? count_kernel_for(n_cap) : write_fn(mode, n_cap);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 
@@ -997,13 +940,10 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, int wvar, Cols cols, uint64_t capacity, cudaStream_t st) {
+                         me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st) {
     void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
                     (void*)&tile_cnt, (void*)&span_off, (void*)&cols, (void*)&capacity};
-    void* fn = write_fn(mode, S.n_cap, wvar);
-    const size_t smem = write_smem(mode, wvar);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return cudaLaunchKernel(fn, dim3(n_blocks), dim3(kThreads), args, smem, st);
+    return cudaLaunchKernel(write_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
 int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb) {

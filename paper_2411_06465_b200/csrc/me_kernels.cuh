@@ -215,7 +215,9 @@ struct __align__(16) RowEnt {
     uint64_t hc, psi;
     uint64_t par1, gra1;
     uint64_t optim1, rs;           // rs = flat index of the row's first config
-    uint64_t _pad[2];
+    // survivor bound per (rc, do) digit: total <= thr_max  <=>  u <= umax
+    // (paper mode; with the largest stage when stage_max); unused with gbs
+    uint32_t umax[4];
 };
 // NEXT-1: last-stage terms of one row for one (rc, do) digit (64 B)
 struct __align__(16) StEnt {
@@ -238,7 +240,7 @@ uint32_t ncap_stride(uint32_t n_cap);
 // tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
 uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
 // resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
-int sweep_blocks_per_sm(int pass, uint32_t n_cap, int wvar);
+int sweep_blocks_per_sm(int pass, uint32_t n_cap);
 // count pass over [lo, hi) cut into n_spans spans of whole tiles: per tile its
 // walker checkpoint {seg, j, r, span} and the rank of its first survivor in the
 // span; per span its survivor count and per-capacity counts
@@ -249,10 +251,10 @@ cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st);
 // write pass over [lo, hi): survivors of tile t stored from row
-// span_off[span(t)] + tile_rel[t]; comb = write combining in aligned 32-row windows
+// span_off[span(t)] + tile_rel[t]
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, int wvar, Cols cols, uint64_t capacity, cudaStream_t st);
+                         me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st);
 // fused single-pass sweep of [lo, hi) (count + decoupled look-back + write;
 // me_kernels.cu): span_ck = (spans) uint4 scratch for the span checkpoints,
 // state = (units) u64 zeroed, stats[0] = rows before lo on entry; adds this

@@ -74,6 +74,7 @@ struct LaneCoef {
     uint32_t p;
     bool two;            // NEXT-1: the last stage may decide
     uint64_t nmsL, nkL;  // ~msL, -kL of the last stage
+    uint32_t umax;       // FAST walker: survivor <=> u <= umax
 };
 
 __device__ __forceinline__ void lane_coef(const uint4 h, const ulonglong2 ms, const ulonglong2 lam,
@@ -90,6 +91,9 @@ __device__ __forceinline__ void lane_coef(const uint4 h, const ulonglong2 ms, co
 }
 
 // Table walker: lane position = (row k of the sub-range table, offset r).
+// FAST: the survivor test is u <= umax (paper mode, no mask): a row change
+// loads 32 bytes instead of 80.
+template <bool FAST>
 struct TWalker {
     uint32_t k, r, w;
     const uint2* pp;
@@ -100,9 +104,14 @@ struct TWalker {
                                             const StEnt* __restrict__ st) {
         const uint4* e = reinterpret_cast<const uint4*>(rows + k);
         const uint4 h = __ldg(e);
-        const uint4 v1 = __ldg(e + 1), v2 = __ldg(e + 2), v3 = __ldg(e + 3), v4 = __ldg(e + 4);
         w = h.x;
         pp = reinterpret_cast<const uint2*>(S.pairs) + h.y + (r >> S.lg_rcdo);
+        if (FAST) {
+            const uint4 um = __ldg(e + 7);
+            C.umax = sel == 0 ? um.x : sel == 1 ? um.y : sel == 2 ? um.z : um.w;
+            return;
+        }
+        const uint4 v1 = __ldg(e + 1), v2 = __ldg(e + 2), v3 = __ldg(e + 3), v4 = __ldg(e + 4);
         const ulonglong2 ms = make_ulonglong2(((uint64_t)v1.y << 32) | v1.x, ((uint64_t)v1.w << 32) | v1.z);
         const ulonglong2 lam = make_ulonglong2(((uint64_t)v2.y << 32) | v2.x, ((uint64_t)v2.w << 32) | v2.z);
         const ulonglong2 eb = make_ulonglong2(((uint64_t)v3.y << 32) | v3.x, ((uint64_t)v3.w << 32) | v3.z);
@@ -182,6 +191,26 @@ __global__ void row_kernel(const DevSpace S, const uint64_t g0, const uint32_t n
         e.gra1 = R.gra1;
         e.optim1 = R.optim1;
         e.rs = rs;
+        // survivor bound per digit: total = ms + u K <= thr_max  <=>  u <= (thr_max - ms) / K
+        // (u >= 1: a bound of 0 admits nothing); the last stage's bound too when it may decide
+        const uint32_t Ll = two ? (M.layers - L0) / (tu.p - 1) : 0u;
+        for (uint32_t sel = 0; sel < 4; sel++) {
+            uint64_t U = 0;
+            if (sel < (1u << S.lg_rcdo)) {
+                const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+                const uint64_t ms = dopt ? R.ms1 : R.ms0;
+                const uint64_t K = (uint64_t)tu.p * ((rc ? R.lam1 : R.lam0) + R.e8) + (rc ? R.bt + R.hc : R.hc);
+                U = ms > S.thr_max ? 0ull : (S.thr_max - ms) / K;
+                if (two) {
+                    const TermsT<uint64_t> T =
+                        stage_terms<uint64_t>(M, tu.t, tu.c, tu.d, false, true, Ll, 1u, 1u, rc, dopt, S.zero_stage);
+                    const uint64_t msL = T.params + T.grads + T.optim, kL = T.layers + T.head;
+                    const uint64_t UL = msL > S.thr_max ? 0ull : (S.thr_max - msL) / kL;
+                    U = U < UL ? U : UL;
+                }
+            }
+            e.umax[sel] = U > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)U;
+        }
         rows[k] = e;
         if (two) {
             // the last stage holds floor((L - L0) / (p - 1)) layers, one microbatch
@@ -235,7 +264,8 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
     // positions relative to the span start; RAGGED: the span is cut by the
     // range [lo, hi) = [lo_rel, hi_rel) (first / last span), a lane past the
     // end is parked on the last index and never advances
-    TWalker W;
+    constexpr bool FAST = !GBS && !MASK;
+    TWalker<FAST> W;
     W.restore(S, rows, st, ck, !RAGGED || lane < hi_rel ? lane : hi_rel - 1);
     const uint32_t pstep = 32u >> S.lg_rcdo;
     uint32_t cnt = 0;
@@ -247,14 +277,19 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
         uint2 prn = pr;
         if (in_row && more) prn = __ldg(W.pp + pstep);  // next round's pair, issued early
         const uint32_t u = pr.x;
-        const uint32_t n_inf = GBS ? min(W.C.p, pr.y) : W.C.p;
-        const uint64_t nK = GBS ? (uint64_t)n_inf * W.C.na + W.C.nb : W.C.nkp;
-        uint64_t ntot = W.C.nms + (uint64_t)u * nK;  // ~total
-        if (STMAX && W.C.two) {
-            const uint64_t ntl = W.C.nmsL + (uint64_t)u * W.C.nkL;
-            ntot = ntl < ntot ? ntl : ntot;
+        uint32_t mask;
+        if (FAST) {
+            mask = u <= W.C.umax ? 1u : 0u;
+        } else {
+            const uint32_t n_inf = GBS ? min(W.C.p, pr.y) : W.C.p;
+            const uint64_t nK = GBS ? (uint64_t)n_inf * W.C.na + W.C.nb : W.C.nkp;
+            uint64_t ntot = W.C.nms + (uint64_t)u * nK;  // ~total
+            if (STMAX && W.C.two) {
+                const uint64_t ntl = W.C.nmsL + (uint64_t)u * W.C.nkL;
+                ntot = ntl < ntot ? ntl : ntot;
+            }
+            mask = MASK ? cap_mask_n<NCAP>(S, ntot) : le_shift(0u, ntot, S.thr1c[0]);
         }
-        uint32_t mask = MASK ? cap_mask_n<NCAP>(S, ntot) : le_shift(0u, ntot, S.thr1c[0]);
         if (RAGGED && (rel < lo_rel || rel >= hi_rel)) mask = 0;
         const uint32_t ballot = __ballot_sync(0xffffffffu, mask != 0);
         if (mask) {
@@ -489,26 +524,54 @@ __device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __r
                 dm[j] = (uint32_t)(x >> 56);
             }
         }
-        RowLoad L[U];
-        const bool need_rs = MODE != 1 || !D32;
+        if (SMEM) {
+            // rows and pairs in shared memory: the U descriptor loads are the
+            // only global round trip
 #pragma unroll
-        for (int j = 0; j < U; j++) {
-            const RowEnt* e = SMEM ? srow + (k[j] - k0) : rows + k[j];
-            if (MODE != 1) load_row<SMEM>(e, L[j]);
-            else if (need_rs) L[j].optrs.y = SMEM ? e->rs : __ldg(&e->rs);
-        }
-        uint2 pr[U];
+            for (int j = 0; j < U; j++) {
+                const bool valid = i0 + 32 * j + lane < n;
+                RowLoad Lj;
+                const RowEnt* e = srow + (k[j] - k0);
+                if (MODE != 1) load_row<true>(e, Lj);
+                else if (!D32) Lj.optrs.y = e->rs;
+                uint32_t rj = r[j];
+                uint64_t ij = idx[j];
+                if (D32) rj = MODE != 1 && valid ? (uint32_t)(ij - Lj.optrs.y) : 0u;
+                else ij = Lj.optrs.y + rj;
+                const uint2 pj = MODE == 1 ? make_uint2(0, 0) : pairs[Lj.h.y + (rj >> S.lg_rcdo)];
+                uint64_t v[8];
+                expand_vals<MODE, NCAP, GBS, STMAX>(S, st, k[j], rj, ij, dm[j], Lj, pj, v);
+                pk.add(valid ? (uint32_t)(v[0] >> 56) : 0u);
+                const uint64_t o = off + i0 + 32 * j + lane;
+                if (valid && o < capacity) {
+                    if (MODE == 3) {
+                        store_record(cols.c[0] + o * 8, v);
+                    } else if (MODE == 2) {
 #pragma unroll
-        for (int j = 0; j < U; j++) {
-            if (D32) r[j] = MODE != 1 && i0 + 32 * j + lane < n ? (uint32_t)(idx[j] - L[j].optrs.y) : 0u;
-            else idx[j] = L[j].optrs.y + r[j];
-            pr[j] = MODE == 1 ? make_uint2(0, 0) : pairs[L[j].h.y + (r[j] >> S.lg_rcdo)];
+                        for (int c = 0; c < 8; c++) cols.c[c][o] = v[c];
+                    } else {
+                        cols.c[0][o] = v[0];
+                    }
+                }
+            }
+            continue;
         }
+        // rows from global memory (the span's rows do not fit the shared
+        // copy): one survivor at a time, descriptors already loaded
 #pragma unroll
         for (int j = 0; j < U; j++) {
             const bool valid = i0 + 32 * j + lane < n;
+            RowLoad Lj;
+            const RowEnt* e = rows + k[j];
+            if (MODE != 1) load_row<false>(e, Lj);
+            else if (!D32) Lj.optrs.y = __ldg(&e->rs);
+            uint32_t rj = r[j];
+            uint64_t ij = idx[j];
+            if (D32) rj = MODE != 1 && valid ? (uint32_t)(ij - Lj.optrs.y) : 0u;
+            else ij = Lj.optrs.y + rj;
+            const uint2 pj = MODE == 1 ? make_uint2(0, 0) : pairs[Lj.h.y + (rj >> S.lg_rcdo)];
             uint64_t v[8];
-            expand_vals<MODE, NCAP, GBS, STMAX>(S, st, k[j], r[j], idx[j], dm[j], L[j], pr[j], v);
+            expand_vals<MODE, NCAP, GBS, STMAX>(S, st, k[j], rj, ij, dm[j], Lj, pj, v);
             pk.add(valid ? (uint32_t)(v[0] >> 56) : 0u);
             const uint64_t o = off + i0 + 32 * j + lane;
             if (valid && o < capacity) {
