@@ -554,8 +554,7 @@ __device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __r
                     }
                 }
             }
-            continue;
-        }
+        } else {
         // rows from global memory (the span's rows do not fit the shared
         // copy): one survivor at a time, descriptors already loaded
 #pragma unroll
@@ -584,6 +583,7 @@ __device__ __forceinline__ void expand_span(const DevSpace& S, const RowEnt* __r
                     cols.c[0][o] = v[0];
                 }
             }
+        }
         }
     }
 }
