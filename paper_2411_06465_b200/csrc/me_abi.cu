@@ -486,7 +486,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         for (uint64_t lo = b, hi = b; lo < e; lo = hi) {
             hi = e - lo < kMaxSub ? e : lo + kMaxSub;
             uint64_t g0 = 0;
-            uint32_t n_rows = 0;
+            uint32_t n_rows = 0, seg_lo = 0, n_seg_sub = 0;
             if (rows_pipe) {
                 // the sub-range also holds at most max_rows rows (the rows
                 // covering [lo & ~31, lo) are < 32 and max_rows >= 1: hi > lo)
@@ -497,6 +497,12 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                     if (cut > lo) hi = cut;
                 }
                 n_rows = (uint32_t)(H.row_of(hi - 1) + 1 - g0);
+                // segments of rows g0 and g0 + n_rows - 1 (K0 searches only between them)
+                const auto seg_of = [&](uint64_t g) {
+                    return (uint32_t)(std::upper_bound(H.seg_row.begin(), H.seg_row.end(), g) - H.seg_row.begin() - 1);
+                };
+                seg_lo = seg_of(g0);
+                n_seg_sub = seg_of(g0 + n_rows - 1) - seg_lo + 2;
             }
             me_plan::Scratch& sc = P->scratch[P->turn++ % P->n_sets];
             const uint32_t n_tiles = n_tiles_of(lo, hi);
@@ -518,7 +524,8 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                 // K0 rows + K1 stage + scan on the count stream, K3 on the caller's
                 const uint32_t n_rsp = (n_tiles + P->rspan_tiles - 1) / P->rspan_tiles;
                 cudaEventRecord(tev[0], cs);
-                cudaError_t ce = launch_rows(P->ds, g0, n_rows, lo, hi, P->rspan_tiles, sc.rows, sc.st, sc.rck, cs);
+                cudaError_t ce = launch_rows(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, P->rspan_tiles, sc.rows, sc.st,
+                                                sc.rck, cs);
                 if (ce == cudaSuccess)
                     ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, P->d32,
                                       sc.rcount, sc.rbcount, o->mode, cs);

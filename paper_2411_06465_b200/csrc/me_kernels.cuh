@@ -269,8 +269,9 @@ cudaError_t launch_fused(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t s
 // [lo, hi) + span checkpoints, K1 survivors -> descriptors + span counts, K3
 // descriptors -> output rows (and stats[1 + j] per capacity)
 int expand_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
-cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_t lo, uint64_t hi,
-                        uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck, cudaStream_t stream);
+cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
+                        uint64_t lo, uint64_t hi, uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck,
+                        cudaStream_t stream);
 cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
                          uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t d32, uint32_t* span_count,
                          uint32_t* block_count, me_out_mode mode, cudaStream_t stream);

@@ -156,12 +156,15 @@ struct TWalker {
 };
 
 // ---------------------------------------------------------------- K0
-__global__ void row_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows, const uint64_t base,
-                           const uint64_t hi, const uint32_t span_len, const uint32_t n_spans,
-                           RowEnt* __restrict__ rows, StEnt* __restrict__ st, uint2* __restrict__ span_ck) {
+// seg_lo, n_seg_sub: the segments holding rows [g0, g0 + n_rows) are
+// seg_lo .. seg_lo + n_seg_sub - 2 (the binary search covers only them)
+__global__ void row_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows, const uint32_t seg_lo,
+                           const uint32_t n_seg_sub, const uint64_t base, const uint64_t hi, const uint32_t span_len,
+                           const uint32_t n_spans, RowEnt* __restrict__ rows, StEnt* __restrict__ st,
+                           uint2* __restrict__ span_ck) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_rows; k += gridDim.x * blockDim.x) {
         const uint64_t g = g0 + k;
-        const uint32_t s = upper_bound_u64(S.seg_row, S.n_seg + 1, g) - 1;
+        const uint32_t s = seg_lo + upper_bound_u64(S.seg_row + seg_lo, n_seg_sub, g) - 1;
         const uint32_t m = s / S.n_world, n = s - m * S.n_world;
         const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(S.models + m));
         const uint4 m1 = __ldg(reinterpret_cast<const uint4*>(S.models + m) + 1);
@@ -735,14 +738,15 @@ int expand_blocks_per_sm(me_out_mode mode, uint32_t n_cap) {
     return nb > 0 ? nb : 1;
 }
 
-cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint64_t lo, uint64_t hi,
-                        uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck, cudaStream_t stream) {
+cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
+                        uint64_t lo, uint64_t hi, uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck,
+                        cudaStream_t stream) {
     const uint64_t base = lo & ~31ull;
     const uint32_t n_tiles = n_tiles_of(lo, hi);
     const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
     const uint32_t blocks = (n_rows + 255) / 256;
-    row_kernel<<<blocks ? blocks : 1, 256, 0, stream>>>(S, g0, n_rows, base, hi, span_tiles * kTile, n_spans, rows,
-                                                        st, span_ck);
+    row_kernel<<<blocks ? blocks : 1, 256, 0, stream>>>(S, g0, n_rows, seg_lo, n_seg_sub, base, hi,
+                                                        span_tiles * kTile, n_spans, rows, st, span_ck);
     return cudaGetLastError();
 }
 
