@@ -126,7 +126,6 @@ struct me_plan {
         uint32_t* span_count = nullptr;
         uint64_t* span_off = nullptr;
         uint32_t* span_caps = nullptr;
-        uint64_t* ustate = nullptr;     // fused pipeline: look-back state per block unit
         // row-table pipeline (pipe 2)
         RowEnt* rows = nullptr;         // the sub-range's rows
         StEnt* st = nullptr;            // their last-stage terms per digit (stage_max)
@@ -140,18 +139,13 @@ struct me_plan {
     } scratch[kMaxSets];
     uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
     // write-mode pipeline: 2 = row table + descriptors (K0 rows, K1 stage,
-    // scan, K3 expand; default), 1 = fused single-pass kernel, 0 = count /
-    // scan / write passes (ME_PIPE).  COUNT mode always uses the count pass.
+    // scan, K3 expand; default), 0 = count / scan / write passes (ME_PIPE).
+    // COUNT mode always uses the count pass.
     uint32_t pipe = 2;
     uint32_t rspan_tiles = 16;          // pipe 2: tiles per K1 span (ME_ROWS_SPAN)
     uint32_t max_rspans = 0, max_rows = 0;
     uint32_t d32 = 0;                   // 32-bit survivor descriptors (no span touches > 255 rows)
     int expand_bps[4] = {0, 0, 0, 0};   // co-resident K3 blocks per SM per output mode
-    uint32_t fused = 1;                 // 1 = fused single-pass kernel (ME_FUSED=0: count/scan/write passes)
-    uint32_t span_tiles = 16;           // fused: tiles per warp span (ME_SPAN_TILES)
-    uint32_t max_units = 0;
-    int fused_minb = 2;                 // fused kernel register budget: 2 or 3 blocks per SM (ME_FUSED_MINB)
-    int fused_bps[4] = {0, 0, 0, 0};    // co-resident blocks per SM of the fused kernel per output mode
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // count + scan passes
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
@@ -273,9 +267,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
     if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
-    if (const char* e = getenv("ME_FUSED")) P->pipe = (uint32_t)atoi(e);
-    if (const char* e = getenv("ME_PIPE")) P->pipe = (uint32_t)atoi(e);
-    P->fused = P->pipe == 1;
+    if (const char* e = getenv("ME_PIPE")) P->pipe = atoi(e) == 0 ? 0u : 2u;
     if (P->serial < 0) P->serial = P->pipe == 2 ? 0 : 1;
     if (const char* e = getenv("ME_ROWS_SPAN")) P->rspan_tiles = (uint32_t)atoi(e);
     if (P->rspan_tiles < 1) P->rspan_tiles = 1;
@@ -284,6 +276,9 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         const uint32_t eff_tiles = n_tiles_of(31, 31 + eff) + 1;
         P->max_rspans = (eff_tiles + P->rspan_tiles - 1) / P->rspan_tiles + 1;
         P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
+        // (tests: a small cap exercises the cutting of sub-ranges by rows; >= 64
+        // so that the < 32 rows before a sub-range's first index always fit)
+        if (const char* e = getenv("ME_MAX_ROWS")) P->max_rows = std::min(P->max_rows, (uint32_t)std::max(64, atoi(e)));
         if (P->max_rows < 1) P->max_rows = 1;
         // a span of L positions touches at most ceil(L / min_w) + 1 rows
         uint64_t min_w = UINT64_MAX;
@@ -299,11 +294,6 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_EXPAND_BPS")) ebps = std::max(1, atoi(e));
     for (int m = 1; m < 4; m++)
         P->expand_bps[m] = std::min(expand_blocks_per_sm((me_out_mode)m, D.n_cap), ebps);
-    if (const char* e = getenv("ME_SPAN_TILES")) P->span_tiles = (uint32_t)atoi(e);
-    if (P->span_tiles < 1) P->span_tiles = 1;
-    P->max_units = (P->max_tiles + P->span_tiles * kWarpsPerBlock - 1) / (P->span_tiles * kWarpsPerBlock) + 1;
-    if (const char* e = getenv("ME_FUSED_MINB")) P->fused_minb = atoi(e);
-    for (int m = 0; m < 4; m++) P->fused_bps[m] = fused_blocks_per_sm((me_out_mode)m, D.n_cap, P->fused_minb);
     const int occ_c = sweep_blocks_per_sm(0, D.n_cap), occ_w = sweep_blocks_per_sm(2, D.n_cap);
     // both passes resident at once: the write pass (memory/latency bound) and
     // the count pass of the next sub-range (issue bound) share every SM
@@ -323,8 +313,6 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         sc.span_count = (uint32_t*)P->A.get((size_t)P->max_spans * 4);
         sc.span_off = (uint64_t*)P->A.get((size_t)P->max_spans * 8);
         sc.span_caps = (uint32_t*)P->A.get((size_t)P->max_spans * 8 * 4);
-        sc.ustate = (uint64_t*)P->A.get((size_t)P->max_units * 8);
-        P->owned.push_back(sc.ustate);
         P->owned.push_back(sc.tile_rel);
         P->owned.push_back(sc.tile_ck);
         P->owned.push_back(sc.span_count);
@@ -351,7 +339,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
             }
         }
         if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps ||
-            !sc.ustate || !rows_ok) {
+            !rows_ok) {
             me_plan_free(P);
             return err(ME_ENOMEM, "scratch allocation");
         }
@@ -476,7 +464,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     // stream, which waits only for the tables and for the write pass that last
     // used the scratch set, so the count of sub-range i+1 runs while the
     // caller's stream still writes the columns of sub-range i.
-    cudaStream_t cs = P->serial || P->fused ? st : P->cstream;
+    cudaStream_t cs = P->serial ? st : P->cstream;
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
@@ -541,27 +529,6 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                                    sc.roff, o->mode, cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[o->mode]),
                                    sc.rnext, st);
                 if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
-                cudaEventRecord(tev[4], st);
-                cudaEventRecord(sc.free_ev, st);
-                continue;
-            }
-            if (P->fused) {
-                // one kernel: count + look-back + write (timing: the kernel
-                // is the write pass, or the count pass when nothing is written)
-                const me_out_mode fm = write ? o->mode : ME_OUT_COUNT;
-                const uint32_t units =
-                    (n_tiles + P->span_tiles * kWarpsPerBlock - 1) / (P->span_tiles * kWarpsPerBlock);
-                cudaError_t ce = cudaMemsetAsync(sc.ustate, 0, (size_t)units * 8, st);
-                if (ce != cudaSuccess) return cuda_err(ce, "memset");
-                cudaEventRecord(tev[0], st);
-                if (write)
-                    for (int k = 1; k < 4; k++) cudaEventRecord(tev[k], st);
-                ce = launch_fused(P->ds, lo, hi, P->span_tiles, (uint32_t)(P->sms * P->fused_bps[fm]), P->fused_minb,
-                                  sc.tile_ck,
-                                  sc.ustate, stats, fm, cols, capacity, st);
-                if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
-                if (!write)
-                    for (int k = 1; k < 4; k++) cudaEventRecord(tev[k], st);
                 cudaEventRecord(tev[4], st);
                 cudaEventRecord(sc.free_ev, st);
                 continue;

@@ -158,18 +158,6 @@ struct Walker {
         set_row(S);
     }
 
-    // walker state {seg, j, r} of absolute index pos, without entering the row
-    __device__ __forceinline__ static uint4 locate(const DevSpace& S, uint64_t pos) {
-        const uint32_t s = upper_bound_u64(S.seg_prefix, S.n_seg + 1, pos) - 1;
-        const uint32_t m = s / S.n_world, n = s - m * S.n_world;
-        const uint32_t cls = __ldg(S.model_class + m);
-        const uint32_t j0 = __ldg(S.list_off + cls * S.n_world + n);
-        const uint32_t j1 = __ldg(S.list_off + cls * S.n_world + n + 1);
-        const uint64_t within = pos - __ldg(S.seg_prefix + s);
-        const uint32_t j = j0 + upper_bound_u64(S.list_prefix + j0, j1 - j0, within) - 1;
-        return make_uint4(s, j, (uint32_t)(within - __ldg(S.list_prefix + j)), 0u);
-    }
-
     // position on checkpoint (state of index x) + lane
     __device__ __forceinline__ void restore(const DevSpace& S, uint4 ck, uint32_t lane) {
         enter_segment(S, ck.x);
@@ -466,229 +454,6 @@ __global__ void __launch_bounds__(kThreads, MODE == 3 ? 2 : 3) write_kernel(cons
     }
 }
 
-// ---------------------------------------------------------------------------
-// Fused single-pass sweep: count, decoupled look-back, write.
-//
-// The sub-range's tiles are cut into spans of `span_tiles` tiles; a block
-// unit is kWarpsPerBlock consecutive spans (one per warp).  Blocks take units
-// in grid-stride order (a co-resident grid: cooperative launch).  Per unit:
-//  1. every warp walks its span counting survivors (per capacity, per lane);
-//  2. warp 0 publishes the unit's aggregate, looks back over the states of
-//     earlier units (32 at a time: aggregates are summed until an inclusive
-//     prefix is found), publishes the unit's inclusive prefix;
-//  3. every warp re-walks its span from the walker state saved in step 1 and
-//     stores its survivors from its row offset on.
-// Unit u waits only on units < u, which are owned by resident blocks that
-// take their units in increasing order, so the chain always completes.
-// state[u]: 0 = not ready, (v << 2) | 1 = aggregate v, (v << 2) | 2 =
-// inclusive prefix v (output rows before unit u + 1: the survivors of the
-// earlier sub-ranges and of units 0..u).
-
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// warp 0: exclusive prefix of unit u (u > 0; its aggregate agg already
-// published): sum the aggregates of the units before it back to the nearest
-// inclusive prefix, 32 units per step; publishes u's inclusive prefix
-__device__ __forceinline__ uint64_t look_back(uint64_t* __restrict__ state, uint32_t u, uint64_t agg,
-                                              uint32_t lane) {
-    uint64_t excl = 0;
-    int64_t j = (int64_t)u - 1;
-    while (true) {
-        const int64_t idx = j - (int64_t)lane;
-        uint64_t v = idx >= 0 ? ld_relaxed(state + idx) : 2ull;  // before unit 0: prefix 0
-        while (__any_sync(0xffffffffu, (v & 3u) == 0)) {
-            if ((v & 3u) == 0) v = ld_relaxed(state + idx);
-        }
-        const uint32_t pm = __ballot_sync(0xffffffffu, (v & 3u) == 2);
-        // lanes up to and including the nearest inclusive prefix contribute
-        const uint32_t upto = pm ? (__ffs(pm) - 1) : 31u;
-        uint64_t x = lane <= upto ? (v >> 2) : 0ull;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        excl += x;
-        if (pm) break;
-        j -= 32;
-    }
-    if (lane == 0) st_relaxed(state + u, ((excl + agg) << 2) | 2u);
-    return excl;
-}
-
-template <int MODE, int NCAP, bool GBS, bool STMAX>
-__device__ __forceinline__ uint32_t fused_count(const DevSpace& S, const TileGeom& G, uint32_t span_tiles,
-                                                uint32_t n_spans, const uint4* __restrict__ span_ck, uint32_t u,
-                                                uint32_t lane, uint32_t wid, CapAcc<NCAP>& acc) {
-    const uint32_t sp = u * kWarpsPerBlock + wid;
-    const uint32_t t0 = sp < n_spans ? sp * span_tiles : G.n_tiles;
-    const uint32_t t1 = min(G.n_tiles, t0 + span_tiles);
-    if (t0 >= t1) return 0;
-    // from the span's checkpoint; a lane past the end of the range is parked
-    // on the last index (its positions stay inactive)
-    Walker W;
-    const uint64_t p0 = G.start(t0) + lane;
-    W.restore(S, __ldg(span_ck + sp), p0 < G.hi ? lane : (uint32_t)(G.hi - 1 - G.start(t0)));
-    const uint32_t before = acc.capc[0];
-    for (uint32_t t = t0; t < t1; t++) {
-        const bool more = t + 1 < t1;
-        if (G.ragged(t))
-            run_tile<0, NCAP, true, GBS, STMAX>(S, W, G.start(t) + lane, G.lo, G.hi, G.rounds(t), lane, acc, 0,
-                                                Cols{}, 0, more);
-        else
-            run_tile<0, NCAP, false, GBS, STMAX>(S, W, G.start(t) + lane, G.lo, G.hi, kTileRounds, lane, acc, 0,
-                                                 Cols{}, 0, more);
-    }
-    return __reduce_add_sync(0xffffffffu, acc.capc[0] - before);
-}
-
-template <int MODE, int NCAP, bool GBS, bool STMAX>
-__device__ __forceinline__ void fused_write(const DevSpace& S, const TileGeom& G, uint32_t span_tiles,
-                                            uint32_t n_spans, const uint4* __restrict__ span_ck, uint32_t u,
-                                            uint32_t lane, uint32_t wid, uint64_t out, const Cols& cols,
-                                            uint64_t capacity) {
-    const uint32_t sp = u * kWarpsPerBlock + wid;
-    const uint32_t t0 = sp * span_tiles;
-    const uint32_t t1 = min(G.n_tiles, t0 + span_tiles);
-    Walker W;
-    const uint64_t p0 = G.start(t0) + lane;
-    W.restore(S, __ldg(span_ck + sp), p0 < G.hi ? lane : (uint32_t)(G.hi - 1 - G.start(t0)));
-    CapAcc<NCAP> none;
-    for (uint32_t t = t0; t < t1; t++) {
-        const bool more = t + 1 < t1;
-        if (G.ragged(t))
-            out = run_tile<MODE, NCAP, true, GBS, STMAX>(S, W, G.start(t) + lane, G.lo, G.hi, G.rounds(t), lane, none,
-                                                         out, cols, capacity, more);
-        else
-            out = run_tile<MODE, NCAP, false, GBS, STMAX>(S, W, G.start(t) + lane, G.lo, G.hi, kTileRounds, lane,
-                                                          none, out, cols, capacity, more);
-    }
-}
-
-// Units of a block in order u_0 < u_1 < ...; the look-back of u_k runs after
-// the count of u_{k+1}, when the units before u_k have long published, so it
-// rarely waits.  Shared: s_cnt[parity][warp] survivors of a warp's span,
-// s_out[parity][warp] its first output row.
-template <int MODE, int NCAP, bool GBS, bool STMAX>
-__device__ __forceinline__ void fused_units(const DevSpace& S, const TileGeom& G, uint32_t span_tiles,
-                                            uint32_t n_spans, uint32_t n_units, const uint4* __restrict__ span_ck,
-                                            uint64_t* __restrict__ state, uint64_t* __restrict__ stats,
-                                            const Cols& cols, uint64_t capacity, uint32_t (*s_cnt)[kWarpsPerBlock],
-                                            uint64_t (*s_out)[kWarpsPerBlock], CapAcc<NCAP>& acc) {
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t u = blockIdx.x;
-    if (u >= n_units) return;  // block-uniform
-    if (MODE == 0) {
-        for (; u < n_units; u += gridDim.x) fused_count<MODE, NCAP, GBS, STMAX>(S, G, span_tiles, n_spans, span_ck, u,
-                                                                                  lane, wid, acc);
-        return;
-    }
-    uint32_t n = fused_count<MODE, NCAP, GBS, STMAX>(S, G, span_tiles, n_spans, span_ck, u, lane, wid, acc);
-    if (lane == 0) s_cnt[0][wid] = n;
-    __syncthreads();
-    uint64_t base0 = 0;  // warp 0 of the block holding unit 0: rows before this range
-    if (wid == 0) {
-        const uint32_t c = lane < kWarpsPerBlock ? s_cnt[0][lane] : 0u;
-        const uint64_t agg = __reduce_add_sync(0xffffffffu, c);
-        if (lane == 0) {
-            if (u == 0) {
-                // the chain starts at stats[0], read before the publish that
-                // every other unit (and so every add to stats[0] at the end
-                // of this kernel) waits for: prefixes are global row offsets
-                base0 = ld_relaxed(stats);
-                __threadfence();
-                st_relaxed(state, ((base0 + agg) << 2) | 2u);
-            } else {
-                st_relaxed(state + u, (agg << 2) | 1u);
-            }
-        }
-    }
-    for (uint32_t k = 0;; k++) {
-        const uint32_t un = u + gridDim.x;
-        const bool has_next = un < n_units;
-        if (has_next) {
-            n = fused_count<MODE, NCAP, GBS, STMAX>(S, G, span_tiles, n_spans, span_ck, un, lane, wid, acc);
-            if (lane == 0) s_cnt[(k + 1) & 1][wid] = n;
-        }
-        __syncthreads();
-        if (wid == 0) {
-            if (has_next) {
-                const uint32_t c = lane < kWarpsPerBlock ? s_cnt[(k + 1) & 1][lane] : 0u;
-                const uint64_t agg = __reduce_add_sync(0xffffffffu, c);
-                if (lane == 0) st_relaxed(state + un, (agg << 2) | 1u);
-            }
-            const uint32_t c = lane < kWarpsPerBlock ? s_cnt[k & 1][lane] : 0u;
-            const uint64_t agg = __reduce_add_sync(0xffffffffu, c);
-            const uint64_t excl = u == 0 ? __shfl_sync(0xffffffffu, base0, 0) : look_back(state, u, agg, lane);
-            // exclusive prefix over the block's warps
-            uint32_t x = c;
-#pragma unroll
-            for (int o = 1; o < kWarpsPerBlock; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if ((int)lane >= o) x += y;
-            }
-            if (lane < kWarpsPerBlock) s_out[k & 1][lane] = excl + (x - c);
-        }
-        __syncthreads();
-        if (s_cnt[k & 1][wid])
-            fused_write<MODE, NCAP, GBS, STMAX>(S, G, span_tiles, n_spans, span_ck, u, lane, wid, s_out[k & 1][wid],
-                                                cols, capacity);
-        if (!has_next) break;
-        u = un;
-    }
-}
-
-// stats: [0] survivors of the earlier sub-ranges (read by unit 0 before any
-// block can add to it: every non-zero add below follows unit 0's publish),
-// [1 + j] survivors for capacity j; both accumulated at the end by atomics.
-// walker checkpoint {seg, j, r} of the first index of every span (one thread
-// per span: two binary searches) for the fused kernel
-__global__ void span_ck_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi, const uint32_t span_tiles,
-                               const uint32_t n_spans, uint4* __restrict__ span_ck) {
-    const TileGeom G = geom(lo, hi);
-    for (uint32_t sp = blockIdx.x * blockDim.x + threadIdx.x; sp < n_spans; sp += gridDim.x * blockDim.x)
-        span_ck[sp] = Walker::locate(S, G.start(sp * span_tiles));
-}
-
-template <int MODE, int NCAP, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) fused_kernel(const DevSpace S, const uint64_t lo, const uint64_t hi,
-                                                            const uint32_t span_tiles, const uint32_t n_spans,
-                                                            const uint32_t n_units,
-                                                            const uint4* __restrict__ span_ck,
-                                                            uint64_t* __restrict__ state,
-                                                            uint64_t* __restrict__ stats, const Cols cols,
-                                                            const uint64_t capacity) {
-    __shared__ uint32_t s_cnt[2][kWarpsPerBlock];
-    __shared__ uint64_t s_out[2][kWarpsPerBlock];
-    const uint32_t lane = threadIdx.x & 31;
-    const TileGeom G = geom(lo, hi);
-    CapAcc<NCAP> acc;
-#define ME_FUSED_UNITS(GBS, STMAX)                                                                          \
-    fused_units<MODE, NCAP, GBS, STMAX>(S, G, span_tiles, n_spans, n_units, span_ck, state, stats, cols, capacity, \
-                                        s_cnt, s_out, acc)
-    if (S.stage_max) {
-        if (S.gbs_mode) ME_FUSED_UNITS(true, true);
-        else ME_FUSED_UNITS(false, true);
-    } else {
-        if (S.gbs_mode) ME_FUSED_UNITS(true, false);
-        else ME_FUSED_UNITS(false, false);
-    }
-#undef ME_FUSED_UNITS
-    __threadfence();
-#pragma unroll
-    for (int q = 0; q < NCAP; q++) {
-        const uint32_t c = __reduce_add_sync(0xffffffffu, acc.capc[q]);
-        if (lane == 0 && c) {
-            atomicAdd((unsigned long long*)(stats + 1 + S.cslot[q]), (unsigned long long)c);
-            if (q == 0) atomicAdd((unsigned long long*)stats, (unsigned long long)c);
-        }
-    }
-}
-
 // one block: exclusive scan of the span counts into u64 offsets starting at
 // the running total stats[0]; stats[0] and stats[1 + q] accumulate the totals
 // of this sub-range
@@ -890,30 +655,6 @@ uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
     return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
 }
 
-template <int MODE, int MINB>
-void* fused_kernel_for(uint32_t n_cap) {
-    switch (ncap_stride_(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&fused_kernel<MODE, 1, MINB>);
-        case 2: return reinterpret_cast<void*>(&fused_kernel<MODE, 2, MINB>);
-        case 4: return reinterpret_cast<void*>(&fused_kernel<MODE, 4, MINB>);
-        default: return reinterpret_cast<void*>(&fused_kernel<MODE, 8, MINB>);
-    }
-}
-
-// minb: the kernel's minimum resident blocks per SM (register budget): 2 or 3
-template <int MINB>
-void* fused_fn_(me_out_mode mode, uint32_t n_cap) {
-    switch (mode) {
-        case ME_OUT_COUNT: return fused_kernel_for<0, MINB>(n_cap);
-        case ME_OUT_INDEX: return fused_kernel_for<1, MINB>(n_cap);
-        case ME_OUT_FULL: return fused_kernel_for<2, MINB>(n_cap);
-        default: return fused_kernel_for<3, MINB>(n_cap);
-    }
-}
-void* fused_fn(me_out_mode mode, uint32_t n_cap, int minb) {
-    return minb >= 3 ? fused_fn_<3>(mode, n_cap) : fused_fn_<2>(mode, n_cap);
-}
-
 // pass 0 count, 1 INDEX write, 2 FULL write, 3 RECORDS write
 int sweep_blocks_per_sm(int pass, uint32_t n_cap) {
     const me_out_mode mode = pass == 3 ? ME_OUT_RECORDS : (pass == 2 ? ME_OUT_FULL : ME_OUT_INDEX);
@@ -944,28 +685,6 @@ cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n
     void* args[] = {(void*)&S,        (void*)&lo,       (void*)&hi,       (void*)&tile_ck, (void*)&tile_rel,
                     (void*)&tile_cnt, (void*)&span_off, (void*)&cols, (void*)&capacity};
     return cudaLaunchKernel(write_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, 0, st);
-}
-
-int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb) {
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fused_fn(mode, n_cap, minb), kThreads, 0) != cudaSuccess)
-        return 1;
-    return nb > 0 ? nb : 1;
-}
-
-cudaError_t launch_fused(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t span_tiles, uint32_t n_blocks,
-                         int minb, uint4* span_ck, uint64_t* state, uint64_t* stats, me_out_mode mode, Cols cols,
-                         uint64_t capacity, cudaStream_t st) {
-    const uint32_t n_tiles = n_tiles_of(lo, hi);
-    const uint32_t n_spans = (n_tiles + span_tiles - 1) / span_tiles;
-    const uint32_t n_units = (n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    if (n_blocks > n_units) n_blocks = n_units ? n_units : 1;
-    span_ck_kernel<<<(n_spans + 255) / 256, 256, 0, st>>>(S, lo, hi, span_tiles, n_spans, span_ck);
-    void* args[] = {(void*)&S,       (void*)&lo,      (void*)&hi,      (void*)&span_tiles, (void*)&n_spans,
-                    (void*)&n_units, (void*)&span_ck, (void*)&state, (void*)&stats,      (void*)&cols,
-                    (void*)&capacity};
-    // cooperative: the look-back chain needs every block resident
-    return cudaLaunchCooperativeKernel(fused_fn(mode, S.n_cap, minb), dim3(n_blocks), dim3(kThreads), args, 0, st);
 }
 
 cudaError_t launch_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,

@@ -255,16 +255,6 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
                          const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
                          me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st);
-// fused single-pass sweep of [lo, hi) (count + decoupled look-back + write;
-// me_kernels.cu): span_ck = (spans) uint4 scratch for the span checkpoints,
-// state = (units) u64 zeroed, stats[0] = rows before lo on entry; adds this
-// range's survivors to stats[0] and stats[1 + j].  n_blocks must not exceed
-// the co-resident grid (fused_blocks_per_sm x SMs).
-// (minb = the register budget variant: 2 or 3 resident blocks per SM)
-int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb);
-cudaError_t launch_fused(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t span_tiles, uint32_t n_blocks,
-                         int minb, uint4* span_ck, uint64_t* state, uint64_t* stats, me_out_mode mode, Cols cols,
-                         uint64_t capacity, cudaStream_t st);
 // row-table pipeline (me_rows.cu): K0 rows [g0, g0 + n_rows) of the range
 // [lo, hi) + span checkpoints, K1 survivors -> descriptors + span counts, K3
 // descriptors -> output rows (and stats[1 + j] per capacity)

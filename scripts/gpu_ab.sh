@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 if [ -z "$NOTEST" ]; then
 timeout 1500 python -m pytest tests -m gpu -q -x --timeout 1200 ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 fi
-for v in ${VARIANTS:-"ME_FUSED=1"}; do
+for v in ${VARIANTS:-"ME_PIPE=2"}; do
   for m in ${MODES:-records}; do
   env $(echo $v | tr , " ") timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --mode $m > gpurun_out/bench_ab.log 2>&1
   echo "$v $m :: $(python3 -c "
