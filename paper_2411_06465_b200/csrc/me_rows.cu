@@ -273,6 +273,7 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
     const uint32_t pstep = 32u >> S.lg_rcdo;
     uint32_t cnt = 0;
     uint32_t rel = lane;
+    uint32_t dk16 = (W.k - ck.x) << 16;  // D32: row - span's first row, in place
     uint2 pr = __ldg(W.pp);
     for (uint32_t it = 0; it < rounds; it++, rel += 32) {
         const bool more = it + 1 < rounds;
@@ -298,7 +299,7 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
         if (mask) {
             const uint32_t m = MASK ? mask << 24 : 0u;
             const uint32_t at = cnt + __popc(ballot & ((1u << lane) - 1u));
-            if (d32) reinterpret_cast<uint32_t*>(desc)[at] = rel | ((W.k - ck.x) << 16) | m;
+            if (d32) reinterpret_cast<uint32_t*>(desc)[at] = rel | dk16 | m;
             else desc[at] = ((uint64_t)(W.k | m) << 32) | W.r;
         }
         cnt += __popc(ballot);
@@ -310,6 +311,7 @@ __device__ __forceinline__ void stage_span(const DevSpace& S, const RowEnt* __re
             } else {
                 W.advance32(S, rows, st, pstep);
                 pr = __ldg(W.pp);
+                dk16 = (W.k - ck.x) << 16;
             }
         }
     }
