@@ -1,4 +1,5 @@
 """NEXT-3 (safety-rule validation) and NEXT-2 (colouring) on the GPU path."""
+import numpy as np
 import pytest
 
 import me_inputs as mi
@@ -99,3 +100,26 @@ def test_rank_picks_paper_choice(me):
     res = me.Plan(sp100).sweep(mode=me.ME_OUT_INDEX)
     mid, N, cfg = me.me_decode(sp100, int(res.rank(0)[0]))
     assert (cfg["t"], cfg["c"], cfg["p"], cfg["b"]) == (4, 1, 1, 2), cfg
+
+
+def test_three_class_colouring_sweep(me, oracle_mod):
+    """NEXT-2 3-class colouring of a sweep (green <= 80 %, yellow <= 100 %,
+    red > 100 % of C; caption P:420): capacities {C, 5C/4} at the 4/5 rule
+    give bit 0 = green and bit 1 = green or yellow, exactly (5C/4 * 4/5 = C
+    for C a multiple of 4 bytes).  Checked row by row against the totals."""
+    C = 40 << 30
+    sp = mi.Space(models=[mi.PRESETS["llama3.1-8b"], mi.PRESETS["llama2-13b"]], world=[64, 256],
+                  caps_gb=[40, 50], mbs=[1, 2, 4, 8], seq=[4096, 8192, 16384], gbs=1024)
+    res = me.Plan(sp).sweep(mode=me.ME_OUT_RECORDS)
+    got = res.to_host()
+    mask = got["index_mask"] >> np.uint64(56)
+    total = got["total"]
+    assert len(total) > 0
+    green = total * np.uint64(5) <= np.uint64(C * 4)
+    yellow_or_green = total <= np.uint64(C)
+    assert np.array_equal((mask & np.uint64(1)) == 1, green)
+    assert np.array_equal((mask >> np.uint64(1) & np.uint64(1)) == 1, yellow_or_green)
+    # the survivors are exactly the oracle's (any bit set: total <= C)
+    idx, rows, n, caps = oracle_mod.sweep(sp)
+    assert np.array_equal(got["index_mask"], idx)
+    assert caps[0] == int(green.sum()) and caps[1] == n
