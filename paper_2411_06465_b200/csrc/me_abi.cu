@@ -132,7 +132,7 @@ struct me_plan {
         uint2* rck = nullptr;           // span checkpoints {row, offset}
         uint64_t* desc = nullptr;       // survivor descriptors, span_len slots per span
         uint32_t* rcount = nullptr;     // survivors per span
-        uint32_t* rbcount = nullptr;    // survivors per stage-kernel block (kWarpsPerBlock spans)
+        uint32_t* rbcount = nullptr;    // survivors per stage-kernel block (kStageWarps spans)
         uint64_t* roff = nullptr;       // output row of each block's first survivor
         uint32_t* rnext = nullptr;      // expand kernel: next span to take
         cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
@@ -519,7 +519,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
                                       sc.rcount, sc.rbcount, o->mode, cs);
                 if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
                 cudaEventRecord(tev[1], cs);
-                ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kWarpsPerBlock - 1) / kWarpsPerBlock, 0, sc.roff, stats,
+                ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kStageWarps - 1) / kStageWarps, 0, sc.roff, stats,
                                  cs);
                 if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
                 cudaEventRecord(tev[2], cs);

@@ -224,6 +224,11 @@ struct __align__(16) StEnt {
     uint64_t msL, kL, parL, graL, optimL, layL, hcL, _pad;
 };
 constexpr uint32_t kMaxRows = 1u << 21;  // rows of one sub-range (descriptor row field: 24 bits)
+// warps (spans) per stage-kernel block; the scan runs over these blocks
+#ifndef ME_STAGE_WARPS
+#define ME_STAGE_WARPS 4
+#endif
+constexpr uint32_t kStageWarps = ME_STAGE_WARPS;
 
 // ---- launch wrappers (me_kernels.cu) ------------------------------------
 struct Cols {

@@ -325,16 +325,16 @@ __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __res
                                           bool d32, uint32_t* __restrict__ span_count, uint32_t lane);
 
 template <int NCAP, bool MASK>
-__global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
+__global__ void __launch_bounds__(kStageWarps * 32, 24 / kStageWarps) stage_kernel(const DevSpace S, const RowEnt* __restrict__ rows,
                                                             const StEnt* __restrict__ st, const uint64_t lo,
                                                             const uint64_t hi, const uint32_t span_tiles,
                                                             const uint32_t n_spans, const uint2* __restrict__ span_ck,
                                                             uint64_t* __restrict__ desc, const uint32_t d32,
                                                             uint32_t* __restrict__ span_count,
                                                             uint32_t* __restrict__ block_count) {
-    __shared__ uint32_t s_cnt[kWarpsPerBlock];
+    __shared__ uint32_t s_cnt[kStageWarps];
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t sp = blockIdx.x * kWarpsPerBlock + wid;
+    const uint32_t sp = blockIdx.x * kStageWarps + wid;
     if (sp < n_spans)
         stage_one<NCAP, MASK>(S, rows, st, lo, hi, span_tiles, sp, span_ck, desc, d32 != 0, span_count, lane);
     // the block's survivors (the scan runs over blocks; the expand kernel
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 3) stage_kernel(const DevSpace S, co
     if (threadIdx.x == 0) {
         uint32_t t = 0;
 #pragma unroll
-        for (int w = 0; w < kWarpsPerBlock; w++) t += s_cnt[w];
+        for (int w = 0; w < kStageWarps; w++) t += s_cnt[w];
         block_count[blockIdx.x] = t;
     }
 }
@@ -613,8 +613,8 @@ __device__ __forceinline__ void expand_spans(const DevSpace& S, const RowEnt* __
         const uint32_t n = __ldg(span_count + sp);
         if (!n) continue;
         // output row of the span: its block's offset + the earlier spans of the block
-        uint64_t off = __ldg(block_off + sp / kWarpsPerBlock);
-        for (uint32_t q = sp & ~(kWarpsPerBlock - 1u); q < sp; q++) off += __ldg(span_count + q);
+        uint64_t off = __ldg(block_off + sp / kStageWarps);
+        for (uint32_t q = sp & ~(kStageWarps - 1u); q < sp; q++) off += __ldg(span_count + q);
         // rows of the span: from its first and last survivor (index order)
         const uint2 ck = __ldg(span_ck + sp);
         const uint64_t s0 = base + (uint64_t)sp * span_len;
@@ -760,8 +760,8 @@ cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st,
     void* args[] = {(void*)&S,          (void*)&rows,    (void*)&st,      (void*)&lo,   (void*)&hi,
                     (void*)&span_tiles, (void*)&n_spans, (void*)&span_ck, (void*)&desc, (void*)&d32,
                     (void*)&span_count, (void*)&block_count};
-    return cudaLaunchKernel(stage_fn(S.n_cap, mode == ME_OUT_INDEX), dim3((n_spans + kWarpsPerBlock - 1) / kWarpsPerBlock),
-                            dim3(kThreads), args, 0, stream);
+    return cudaLaunchKernel(stage_fn(S.n_cap, mode == ME_OUT_INDEX), dim3((n_spans + kStageWarps - 1) / kStageWarps),
+                            dim3(kStageWarps * 32), args, 0, stream);
 }
 
 cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
