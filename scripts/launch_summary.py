@@ -15,7 +15,7 @@ for r in data:
         v = float(r[vi].replace(",", ""))
     except ValueError:
         continue
-    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[ui], 1.0)
+    scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "ms": 1.0, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[ui], 1.0)
     name = r[ki].split("(")[0].replace("void ", "").replace("me::<unnamed>::", "")[:60]
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1
