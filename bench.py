@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--partition", default="cyclic", choices=["cyclic", "even"],
+                    help="N>1: cyclic = rank r sweeps calls r, r+N, ... of CHUNK configs on its own and the "
+                         "per-call counts are joined by one allgather per step; even = every call covers "
+                         "N*CHUNK configs split evenly over the ranks by the library (one join per call)")
     return ap.parse_args()
 
 
@@ -212,15 +216,41 @@ def main():
         calls.append((s, e))
         s = e
     comm = me.Comm(dev) if world > 1 else None
+    calls_even = calls
+    cyclic = world > 1 and args.partition == "cyclic"
+    if cyclic:
+        # whole CHUNK-config calls dealt round-robin: neighbouring chunks have
+        # similar survivor density, so every rank writes about as many rows,
+        # and no rank waits for the others until the step's single join
+        all_calls = [(b, min(job_e, b + CHUNK)) for b in range(job_b, job_e, CHUNK)]
+        calls = all_calls[rank::world]
+        per_rank = -(-len(all_calls) // world)
+    sweep_comm = None if cyclic else comm
+
+    def join(results):
+        """a8 for the cyclic partition: allgather of every call's survivor
+        count; global offset of call q = survivors of calls 0..q-1."""
+        cnt = torch.zeros(per_rank, dtype=torch.int64, device=dev)
+        for i, r in enumerate(results):
+            cnt[i] = r.counts()[0]
+        g = torch.empty(world * per_rank, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(g, cnt)
+        by_call = g.view(world, per_rank).t().reshape(-1)[:len(all_calls)]  # call q = rank q%N, slot q//N
+        return torch.cumsum(by_call, 0) - by_call, int(by_call.sum())
+
     ring = [out_buffers(torch, me, mode, CHUNK + 64, device=dev) for _ in range(2)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(collect=None):
         out = []
         for q, (b, e) in enumerate(calls):
-            r = plan.sweep(b, e, mode=mode, out_cols=ring[q & 1] if ncols else None, comm=comm)
+            r = plan.sweep(b, e, mode=mode, out_cols=ring[q & 1] if ncols else None, comm=sweep_comm)
             out.append(r)
+        if cyclic:
+            joined.append(join(out)[1])
         return out
+
+    joined = []
 
     def drain(results, timings=None):
         n_local = n_global = 0
@@ -265,6 +295,8 @@ def main():
         lo, gl = drain(res, timings)
         n_local += lo
         n_global += gl
+    if cyclic:
+        n_global = sum(joined[-args.steps:])
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -338,7 +370,8 @@ def main():
         "config": {"workload": args.workload, "space_configs": total, "configs_per_gpu_per_step": (job_e - job_b) // world,
                    "per_step": "all of C5 (strong scaling)", "mode": args.mode, "chunk_configs_per_rank": CHUNK,
                    "caps_gib": sp.caps_gb, "threshold": "4/5", "l2": "flushed (256 MiB write) before every step; "
-                   "outputs (GBs per step) also exceed L2", "parallelism": f"index-space partition x{world}"},
+                   "outputs (GBs per step) also exceed L2", "parallelism": f"index-space partition x{world}"
+                   + (f", {args.partition} calls of {CHUNK} configs" if world > 1 else "")},
         "feasible_per_step": n_global // args.steps,
         "kernel_ms_per_step": {"count": count_ms / args.steps, "scan": scan_ms / args.steps,
                                "write": write_ms / args.steps},
@@ -351,7 +384,7 @@ def main():
     # e2e: the public API with host buffers -- plan creation (host tables +
     # H2D) and a D2H of every survivor column inside the timed region
     if not args.no_e2e:
-        e2e_ms, h2d, d2h = e2e_run(me, sp, dev, world, comm, calls, mode, ncols, args.e2e_steps, stream)
+        e2e_ms, h2d, d2h = e2e_run(me, sp, dev, world, comm, calls_even, mode, ncols, args.e2e_steps, stream)
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -382,7 +415,7 @@ def out_buffers(torch, me, mode, rows, **kw):
     return [flat] if mode == me.ME_OUT_RECORDS else list(flat.view(8, rows).unbind(0))
 
 
-def e2e_run(me, sp, dev, world, comm, calls, mode, ncols, steps, stream):
+def e2e_run(me, sp, dev, world, comm, calls_even, mode, ncols, steps, stream):
     """End to end through the C ABI: host description in, host columns out."""
     import ctypes
 
