@@ -190,6 +190,7 @@ def main():
 
     import me_inputs as mi
     import paper_2411_06465_b200 as me
+    from paper_2411_06465_b200.cyclic import cyclic_calls, cyclic_join, n_calls
 
     rank, world, local = dist_env()
     assert world == args.gpus or world == 1, "launch N>1 with torchrun"
@@ -222,21 +223,13 @@ def main():
         # whole CHUNK-config calls dealt round-robin: neighbouring chunks have
         # similar survivor density, so every rank writes about as many rows,
         # and no rank waits for the others until the step's single join
-        all_calls = [(b, min(job_e, b + CHUNK)) for b in range(job_b, job_e, CHUNK)]
-        calls = all_calls[rank::world]
-        per_rank = -(-len(all_calls) // world)
+        calls = cyclic_calls(job_b, job_e, CHUNK, rank, world)
+        calls_total = n_calls(job_b, job_e, CHUNK)
     sweep_comm = None if cyclic else comm
 
     def join(results):
-        """a8 for the cyclic partition: allgather of every call's survivor
-        count; global offset of call q = survivors of calls 0..q-1."""
-        cnt = torch.zeros(per_rank, dtype=torch.int64, device=dev)
-        for i, r in enumerate(results):
-            cnt[i] = r.counts()[0]
-        g = torch.empty(world * per_rank, dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(g, cnt)
-        by_call = g.view(world, per_rank).t().reshape(-1)[:len(all_calls)]  # call q = rank q%N, slot q//N
-        return torch.cumsum(by_call, 0) - by_call, int(by_call.sum())
+        """a8 for the cyclic partition: one allgather of every call's count"""
+        return cyclic_join([r.counts()[0] for r in results], calls_total, world, device=dev)
 
     ring = [out_buffers(torch, me, mode, CHUNK + 64, device=dev) for _ in range(2)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -247,7 +240,7 @@ def main():
             r = plan.sweep(b, e, mode=mode, out_cols=ring[q & 1] if ncols else None, comm=sweep_comm)
             out.append(r)
         if cyclic:
-            joined.append(join(out)[1])
+            joined.append(join(out)[2])
         return out
 
     joined = []

@@ -91,3 +91,63 @@ def test_bench_units_partition_space():
     ranges = [bench.unit_range(total, u) for u in range(bench.UNITS)]
     assert ranges[0][0] == 0 and ranges[-1][1] == total
     assert all(ranges[i][1] == ranges[i + 1][0] for i in range(bench.UNITS - 1))
+
+
+def cyclic_worker(rank, world, port, space_name, chunk, q):
+    """bench.py's default N>1 partition: rank r sweeps calls r, r+N, ... alone
+    (here with the oracle), cyclic_join allgathers the per-call counts."""
+    import oracle
+    from paper_2411_06465_b200.cyclic import cyclic_calls, cyclic_join, n_calls
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sp = mi.config(space_name)
+        total = oracle.space_size(sp)
+        for (b, e) in ((0, total), (5, total - 3)):
+            mine = cyclic_calls(b, e, chunk, rank, world)
+            idx = [oracle.sweep(sp, cb, ce)[0].tolist() for cb, ce in mine]
+            off, cnt, glob = cyclic_join([len(x) for x in idx], n_calls(b, e, chunk), world)
+            parts = [None] * world
+            dist.all_gather_object(parts, (mine, idx))
+            if rank == 0:
+                ref_idx, _, ref_n, _ = oracle.sweep(sp, b, e)
+                nq = n_calls(b, e, chunk)
+                calls = [parts[q % world][0][q // world] for q in range(nq)]
+                got = [parts[q % world][1][q // world] for q in range(nq)]
+                cat = [x for g in got for x in g]
+                ok = (cat == [int(x) for x in ref_idx] and glob == ref_n
+                      and calls[0][0] == b and calls[-1][1] == e
+                      and all(calls[i][1] == calls[i + 1][0] for i in range(nq - 1))
+                      and cnt.tolist() == [len(g) for g in got]
+                      and off.tolist() == [sum(len(g) for g in got[:i]) for i in range(nq)])
+                q.put((b, e, ok))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("chunk", [7, 64])
+def test_two_rank_cyclic_partition_and_join(chunk):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=cyclic_worker, args=(r, 2, port, "C1", chunk, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    results = [q.get(timeout=5) for _ in range(2)]
+    assert all(ok for _, _, ok in results), results
+
+
+def test_cyclic_calls_cover_range():
+    from paper_2411_06465_b200.cyclic import cyclic_calls, n_calls
+    for b, e, chunk, world in ((0, 100, 7, 3), (5, 6, 4, 4), (3, 3, 2, 2), (0, 1 << 36, 1 << 28, 8)):
+        calls = sorted(c for r in range(world) for c in cyclic_calls(b, e, chunk, r, world))
+        assert len(calls) == n_calls(b, e, chunk)
+        if calls:
+            assert calls[0][0] == b and calls[-1][1] == e
+            assert all(calls[i][1] == calls[i + 1][0] for i in range(len(calls) - 1))
+    with pytest.raises(ValueError):
+        cyclic_calls(0, 10, 0, 0, 1)
