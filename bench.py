@@ -408,7 +408,7 @@ def out_buffers(torch, me, mode, rows, **kw):
     return [flat] if mode == me.ME_OUT_RECORDS else list(flat.view(8, rows).unbind(0))
 
 
-def e2e_run(me, sp, dev, world, comm, calls_even, mode, ncols, steps, stream):
+def e2e_run(me, sp, dev, world, comm, calls, mode, ncols, steps, stream):
     """End to end through the C ABI: host description in, host columns out."""
     import ctypes
 
