@@ -84,7 +84,10 @@ typedef struct {
 } me_breakdown;
 
 /* feasible for capacity j <=> total <= floor(cap_j * num / den); the paper's
- * rule is num/den = 4/5.  1 <= num, den <= 1024. */
+ * rule is num/den = 4/5 ("at or below 80%": a total equal
+ * to the threshold is feasible).  1 <= num, den <= 1024.  Thresholds are
+ * computed exactly in 128 bits and clamped to 2^63 (every total is below 2^63,
+ * so the clamp never changes a verdict). */
 typedef struct {
     uint32_t num, den;
 } me_threshold;
@@ -257,6 +260,22 @@ int me_result_wait(me_result* r);
 int me_result_timing(me_result* r, float* ms4);
 void me_result_free(me_result* r);
 
+/* Order-dependent digest of a result's rows, for verifying a whole result (or
+ * a sharded one) against an independent enumeration without moving its rows.
+ * Not part of the method.  For the row at position j (0-based, in the result's
+ * ascending index order) with values r = (index|mask, params, grads, optim,
+ * act_layers, act_embed, act_head, total):
+ *   digest[0] = sum_j mix(r_0 + C) * M^j                       (mod 2^64)
+ *   digest[1] = sum_j g(r) * M^j,  g: h <- C; h <- mix(h ^ r_k), k = 0..7
+ * mix = the splitmix64 finaliser (x ^= x >> 30; x *= 0xBF58476D1CE4E5B9;
+ * x ^= x >> 27; x *= 0x94D049BB133111EB; x ^= x >> 31), C = 0x9E3779B97F4A7C15,
+ * M = 0xD1B54A32D192ED03.  digest[1] = 0 for INDEX results.  A comm result
+ * without gather: COLLECTIVE (every rank calls it), the digest of the global
+ * result (rank shards merged in rank order: D = sum_r M^offset_r D_r).
+ * ME_EINVAL for COUNT results, ME_ERANGE if caller columns overflowed.
+ * Synchronous. */
+int me_result_digest(me_result* r, uint64_t digest[2]);
+
 /* NEXT-2 planner (the search heuristics of P:552-593): for every
  * (model, N) segment of the plan (n_models * n_world entries, model-major),
  * the flat index of the best row of an INDEX or FULL result that is feasible
@@ -285,6 +304,9 @@ int me_comm_unique_id(uint8_t id[128]);
 int me_comm_init(const uint8_t id[128], int rank, int nranks, int device, me_comm** out);
 int me_comm_rank(const me_comm* c, int* rank, int* nranks);
 void me_comm_destroy(me_comm* c);
+/* ME_ENCCL when the communicator recorded an asynchronous error
+ * (ncclCommGetAsyncError), else ME_OK. */
+int me_comm_check(me_comm* c);
 
 const char* me_strerror(int status);
 const char* me_last_error_detail(void);

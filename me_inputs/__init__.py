@@ -12,7 +12,7 @@ from __future__ import annotations
 import csv
 import dataclasses
 from pathlib import Path
-from typing import List, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -55,9 +55,12 @@ class Space:
     stage_max: int = 0  # 1 = NEXT-1: feasibility of the largest pipeline stage
     zero_stage: int = 0  # NEXT-4: 2 / 3 = gradients / also weights sharded with the optimizer
     name: str = ""
+    caps_bytes: Optional[List[int]] = None  # capacities given in bytes (overrides caps_gb)
 
     @property
     def cap_bytes(self) -> List[int]:
+        if self.caps_bytes is not None:
+            return list(self.caps_bytes)
         return [g * GIB for g in self.caps_gb]
 
     def with_models(self, models) -> "Space":

@@ -100,6 +100,8 @@ def lib():
         _lib.or_stage_layers.restype = ctypes.c_uint32
         _lib.or_estimate_stage.argtypes = [P(Model), P(Cfg), ctypes.c_uint32, P(Breakdown)]
         _lib.or_estimate_max.argtypes = [P(Model), P(Cfg), P(Breakdown), _u32p]
+        _lib.or_digest.argtypes = [P(SpaceC), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                   _u64p]
     return _lib
 
 
@@ -247,7 +249,7 @@ def sweep(sp, begin=0, end=0, rows=True, threads=None, max_rows=None):
     if st:
         raise OracleError(st, "sweep")
     n = count.value
-    caps = [cc[i] for i in range(len(sp.caps_gb))]
+    caps = [cc[i] for i in range(len(sp.cap_bytes))]
     if rows:
         return idx[:n].copy(), rw[:n].copy(), n, caps
     return None, None, n, caps
@@ -268,6 +270,51 @@ def points(sp, indices):
     inv = np.empty_like(order)
     inv[order] = np.arange(len(order))
     return rows[inv], masks[inv]
+
+
+DIGEST_WORDS = 11  # count, 8 per-capacity counts, index digest, record digest
+
+
+def digest(sp, begin=0, end=0, chunk=1 << 28, threads=None):
+    """Per chunk of [begin, end): (count, cap_counts[8], index digest, record
+    digest) as a uint64 array (n_chunks, 11); the digest definition is in
+    me_oracle.h (or_digest).  Test infrastructure for whole-chunk parity."""
+    h = _SpaceHolder(sp)
+    end = end or space_size(sp)
+    n_chunks = max(0, -(-(end - begin) // chunk))
+    out = np.zeros((max(1, n_chunks), DIGEST_WORDS), dtype=np.uint64)
+    st = lib().or_digest(ctypes.byref(h.c), begin, end, chunk, threads or default_threads(),
+                         out.ctypes.data_as(_u64p))
+    if st:
+        raise OracleError(st, "digest")
+    return out[:n_chunks]
+
+
+def digest_of_rows(idx_mask, rows):
+    """The same digest from explicit survivor rows (numpy, for the pins)."""
+    C, M = 0x9E3779B97F4A7C15, 0xD1B54A32D192ED03
+    W = (1 << 64) - 1
+
+    def mix(x):
+        x ^= x >> 30
+        x = (x * 0xBF58476D1CE4E5B9) & W
+        x ^= x >> 27
+        x = (x * 0x94D049BB133111EB) & W
+        x ^= x >> 31
+        return x
+
+    di = dr = 0
+    pw = 1
+    for j in range(len(idx_mask)):
+        r = [int(idx_mask[j])] + [int(x) for x in rows[j]]
+        gi = mix((r[0] + C) & W)
+        gr = C
+        for v in r:
+            gr = mix(gr ^ v)
+        di = (di + gi * pw) & W
+        dr = (dr + gr * pw) & W
+        pw = (pw * M) & W
+    return di, dr
 
 
 def default_threads() -> int:

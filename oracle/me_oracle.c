@@ -517,6 +517,8 @@ typedef struct {
     const tables* T;
     uint64_t begin, end;
     int want_rows;
+    int want_digest;          /* or_digest: hash the survivors instead of storing them */
+    uint64_t dig_idx, dig_rec, dig_pow; /* running digests and M^n (see or_digest) */
     uint64_t* idx;
     or_breakdown* rows;
     uint64_t n, cap;
@@ -528,7 +530,22 @@ typedef struct {
     or_cfg dec_cfg;
 } walk_t;
 
+static uint64_t dig_mix(uint64_t x);
+#define DIG_C 0x9E3779B97F4A7C15ull
+#define DIG_M 0xD1B54A32D192ED03ull
+
 static int push(walk_t* w, uint64_t idx_mask, const or_breakdown* r) {
+    if (w->want_digest) {
+        /* survivor j (= w->n) of the piece contributes g(record) * M^j */
+        uint64_t v[8] = {idx_mask, r->params, r->grads, r->optim, r->act_layers, r->act_embed, r->act_head, r->total};
+        uint64_t gi = dig_mix(idx_mask + DIG_C), gr = DIG_C;
+        for (int k = 0; k < 8; k++) gr = dig_mix(gr ^ v[k]);
+        w->dig_idx += gi * w->dig_pow;
+        w->dig_rec += gr * w->dig_pow;
+        w->dig_pow *= DIG_M;
+        w->n++;
+        return OR_OK;
+    }
     if (!w->want_rows) { w->n++; return OR_OK; }
     if (w->n == w->cap) {
         uint64_t nc = w->cap ? w->cap * 2 : 1024;
@@ -746,4 +763,97 @@ int or_sweep(const or_space* sp, uint64_t begin, uint64_t end, uint64_t* idx_mas
     if (status) return status;
     if ((idx_mask || rows) && n > cap) return OR_ERANGE;
     return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* whole-chunk digests (verification of full-size sweeps)              */
+/* ------------------------------------------------------------------ */
+
+/* splitmix64 finaliser */
+static uint64_t dig_mix(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+
+static uint64_t dig_pow(uint64_t n) {
+    uint64_t r = 1, b = DIG_M;
+    while (n) {
+        if (n & 1) r *= b;
+        b *= b;
+        n >>= 1;
+    }
+    return r;
+}
+
+typedef struct {
+    walk_t* w;
+    uint32_t n_pieces;
+    uint32_t next; /* atomically incremented */
+} piece_pool;
+
+static void* digest_thread(void* arg) {
+    piece_pool* pp = (piece_pool*)arg;
+    for (;;) {
+        uint32_t k = __atomic_fetch_add(&pp->next, 1u, __ATOMIC_RELAXED);
+        if (k >= pp->n_pieces) break;
+        if (pp->w[k].end > pp->w[k].begin) walk(&pp->w[k]);
+    }
+    return NULL;
+}
+
+int or_digest(const or_space* sp, uint64_t begin, uint64_t end, uint64_t chunk, int n_threads, uint64_t* out) {
+    int st = space_ok(sp);
+    if (st) return st;
+    if (!out || !chunk) return OR_EINVAL;
+    uint64_t size;
+    if ((st = or_space_size(sp, &size))) return st;
+    if (end == 0 || end > size) end = size;
+    if (begin > end) begin = end;
+    if (n_threads < 1) n_threads = 1;
+    const uint64_t n_chunks = (end - begin + chunk - 1) / chunk;
+    const uint32_t per = (uint32_t)n_threads; /* pieces per chunk */
+    const uint64_t n_pieces = n_chunks * per;
+    tables T;
+    if ((st = build_tables(sp, &T))) return st;
+    walk_t* ws = (walk_t*)calloc(n_pieces ? n_pieces : 1, sizeof(walk_t));
+    pthread_t* th = (pthread_t*)calloc((size_t)n_threads, sizeof(pthread_t));
+    if (!ws || !th) { free(ws); free(th); free_tables(&T); return OR_ENOMEM; }
+    for (uint64_t c = 0; c < n_chunks; c++) {
+        const uint64_t cb = begin + c * chunk, ce = cb + chunk < end ? cb + chunk : end;
+        for (uint32_t q = 0; q < per; q++) {
+            walk_t* w = &ws[c * per + q];
+            w->sp = sp;
+            w->T = &T;
+            w->begin = cb + (ce - cb) * q / per;
+            w->end = cb + (ce - cb) * (q + 1) / per;
+            w->want_digest = 1;
+            w->dig_pow = 1;
+        }
+    }
+    piece_pool pool = {ws, (uint32_t)n_pieces, 0};
+    for (int i = 0; i < n_threads; i++) pthread_create(&th[i], NULL, digest_thread, &pool);
+    for (int i = 0; i < n_threads; i++) pthread_join(th[i], NULL);
+    int status = OR_OK;
+    for (uint64_t c = 0; c < n_chunks; c++) {
+        uint64_t* o = out + c * OR_DIGEST_WORDS;
+        memset(o, 0, OR_DIGEST_WORDS * sizeof(uint64_t));
+        for (uint32_t q = 0; q < per; q++) {
+            const walk_t* w = &ws[c * per + q];
+            if (w->status && !status) status = w->status;
+            /* pieces in order: D(A B) = D(A) + M^|A| D(B) */
+            const uint64_t shift = dig_pow(o[0]);
+            o[9] += shift * w->dig_idx;
+            o[10] += shift * w->dig_rec;
+            o[0] += w->n;
+            for (uint32_t k = 0; k < 8; k++) o[1 + k] += w->cap_counts[k];
+        }
+    }
+    free(ws);
+    free(th);
+    free_tables(&T);
+    return status;
 }

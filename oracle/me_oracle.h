@@ -113,6 +113,21 @@ int or_sweep(const or_space* sp, uint64_t begin, uint64_t end, uint64_t* idx_mas
 int or_points(const or_space* sp, const uint64_t* points, uint64_t n, or_breakdown* rows,
               uint32_t* masks);
 
+/* Whole-chunk verification (test infrastructure): [begin, end) (end = 0: the
+ * whole space) cut into chunks of `chunk` indices; per chunk c the
+ * OR_DIGEST_WORDS words out[c*11 ..]: survivor count, 8 per-capacity counts,
+ * the index digest and the record digest of the chunk's survivors in
+ * ascending index order, position j = 0, 1, ... within the chunk:
+ *   D = sum_j g(r_j) * M^j mod 2^64,  M = 0xD1B54A32D192ED03,
+ *   g_index(r)  = mix(r_0 + C),
+ *   g_record(r) = h <- C; for k = 0..7: h <- mix(h ^ r_k); h
+ * with r = (index | mask << 56, params, grads, optim, act_layers, act_embed,
+ * act_head, total), C = 0x9E3779B97F4A7C15 and mix the splitmix64
+ * finaliser.  The hash is a verification device, not part of the method. */
+#define OR_DIGEST_WORDS 11
+int or_digest(const or_space* sp, uint64_t begin, uint64_t end, uint64_t chunk, int n_threads,
+              uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -224,6 +224,13 @@ class Result:
               "me_result_rank")
         return out
 
+    def digest(self):
+        """(index digest, record digest) of the result's rows (me_result_digest;
+        collective for a sharded comm result)."""
+        a = (ctypes.c_uint64 * 2)()
+        check(lib().me_result_digest(self.h, a), "me_result_digest")
+        return a[0], a[1]
+
     def free(self):
         if self.h:
             lib().me_result_free(self.h)
@@ -253,6 +260,10 @@ class Comm:
         check(lib().me_comm_init(uid, rank, world, device, ctypes.byref(h)), "me_comm_init")
         self.h = h
         self.rank, self.world = rank, world
+
+    def check(self):
+        """raise if NCCL recorded an asynchronous error on this communicator"""
+        check(lib().me_comm_check(self.h), "me_comm_check")
 
     def destroy(self):
         if self.h:

@@ -103,6 +103,8 @@ def lib() -> ctypes.CDLL:
             "me_result_timing": ([ctypes.c_void_p, P(ctypes.c_float)], ctypes.c_int),
             "me_result_free": ([ctypes.c_void_p], None),
             "me_result_rank": ([ctypes.c_void_p, u32, P(u64)], ctypes.c_int),
+            "me_result_digest": ([ctypes.c_void_p, P(u64)], ctypes.c_int),
+            "me_comm_check": ([ctypes.c_void_p], ctypes.c_int),
             "me_partition": ([u64, u64, ctypes.c_int, ctypes.c_int, P(u64), P(u64)], ctypes.c_int),
             "me_join_counts": ([P(u64), ctypes.c_int, u32, u32, ctypes.c_int, P(u64), P(u64), P(u64)], ctypes.c_int),
             "me_comm_unique_id": ([P(u8)], ctypes.c_int),
@@ -125,7 +127,7 @@ def lib() -> ctypes.CDLL:
 EXPORTS = ("me_estimate", "me_estimate_stage", "me_estimate_batch", "me_space_size", "me_decode", "me_plan_create", "me_plan_size", "me_plan_table_bytes",
            "me_plan_sweep", "me_plan_free", "me_sweep", "me_result_counts", "me_result_cap_counts",
            "me_result_columns", "me_result_copy_to_host", "me_result_status", "me_result_wait",
-           "me_result_timing", "me_result_free", "me_result_rank", "me_partition", "me_join_counts", "me_comm_unique_id", "me_comm_init", "me_comm_rank",
+           "me_result_timing", "me_result_free", "me_result_rank", "me_result_digest", "me_comm_check", "me_partition", "me_join_counts", "me_comm_unique_id", "me_comm_init", "me_comm_rank",
            "me_comm_destroy", "me_strerror", "me_last_error_detail", "me_version")
 
 

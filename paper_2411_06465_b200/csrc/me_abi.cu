@@ -103,51 +103,42 @@ struct me_plan {
     Alloc A;
     int device = 0;
     std::vector<void*> owned;  // device allocations owned by the plan
-    // Launch shape.  A sweep is processed in sub-ranges of <= kMaxSub indices;
-    // each is cut into tiles of kTile indices (they fix the output offsets) and
-    // the count pass walks n_spans spans of whole tiles.  The count and write
-    // passes run on their own grids.
     int sms = 148;
-    uint32_t max_spans = 0, max_tiles = 0;
-    uint32_t count_bps = 0, write_bps = 0;  // resident blocks per SM used by each pass
-    uint32_t grid_mode = 1;                 // 1 = one span / tile per warp (ME_GRID_MODE)
-    // count pass on the caller's stream (1) or on the plan's own stream,
-    // overlapping the write pass of the previous sub-range (0; ME_SERIAL).
-    // Default: overlapped for the row-table pipeline (its K1 is issue bound,
-    // its K3 memory bound), serial for the others.
-    int serial = -1;
-    // Two scratch sets, alternated by successive sub-ranges, so that the count
-    // pass of sub-range i+1 (on the plan's count stream) overlaps the write pass
-    // of sub-range i (on the caller's stream).
+    // K0 (rows) + scan on the plan's own stream, overlapping the output kernel
+    // of the previous sub-range on the caller's stream (0), or everything on
+    // the caller's stream (1; ME_SERIAL)
+    int serial = 0;
+    // Scratch sets, alternated by successive sub-ranges, so that K0 of
+    // sub-range i+1 (plan stream) overlaps the output kernel of sub-range i
+    // (caller's stream).
     struct Scratch {
-        uint32_t* tile_rel = nullptr;   // rank of a tile's first survivor inside its span
-        uint32_t* tile_cnt = nullptr;   // survivors of a tile
-        uint4* tile_ck = nullptr;       // walker checkpoint of a tile's first index
-        uint32_t* span_count = nullptr;
-        uint64_t* span_off = nullptr;
-        uint32_t* span_caps = nullptr;
-        // row-table pipeline (pipe 2)
         RowEnt* rows = nullptr;         // the sub-range's rows
         StEnt* st = nullptr;            // their last-stage terms per digit (stage_max)
+        uint32_t* rcnt = nullptr;       // pipe 3: survivors per row
+        uint32_t* ucnt = nullptr;       // pipe 3: survivors per 32-row unit
+        uint64_t* uoff = nullptr;       // pipe 3: output row of each unit's first survivor
+        // descriptor pipeline (pipe 2)
         uint2* rck = nullptr;           // span checkpoints {row, offset}
         uint64_t* desc = nullptr;       // survivor descriptors, span_len slots per span
         uint32_t* rcount = nullptr;     // survivors per span
         uint32_t* rbcount = nullptr;    // survivors per stage-kernel block (kStageWarps spans)
         uint64_t* roff = nullptr;       // output row of each block's first survivor
-        uint32_t* rnext = nullptr;      // expand kernel: next span to take
-        cudaEvent_t free_ev = nullptr;  // recorded after the write pass that last used it
+        uint32_t* rnext = nullptr;      // output kernel: next unit / span to take
+        cudaEvent_t free_ev = nullptr;  // recorded after the kernel that last used the set
     } scratch[kMaxSets];
     uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
-    // write-mode pipeline: 2 = row table + descriptors (K0 rows, K1 stage,
-    // scan, K3 expand; default), 0 = count / scan / write passes (ME_PIPE).
-    // COUNT mode always uses the count pass.
-    uint32_t pipe = 2;
+    // 3 = row-count pipeline (K0 rows + counts, scan, K3 fused test+compact+
+    // store; default), 2 = descriptor pipeline (K0 rows, K1 stage kernel
+    // writing survivor descriptors, scan, K3 expand; ME_PIPE=2).  COUNT mode
+    // is K0 + scan of pipe 3 in both.
+    uint32_t pipe = 3;
     uint32_t rspan_tiles = 16;          // pipe 2: tiles per K1 span (ME_ROWS_SPAN)
     uint32_t max_rspans = 0, max_rows = 0;
-    uint32_t d32 = 0;                   // 32-bit survivor descriptors (no span touches > 255 rows)
-    int expand_bps[4] = {0, 0, 0, 0};   // co-resident K3 blocks per SM per output mode
+    uint32_t d32 = 0;                   // pipe 2: 32-bit survivor descriptors
+    int expand_bps[4] = {0, 0, 0, 0};   // pipe 2: co-resident K3 blocks per SM per output mode
+    int fused_bps[4] = {0, 0, 0, 0};    // pipe 3: resident K3 blocks per SM per output mode
     uint32_t turn = 0;
-    cudaStream_t cstream = nullptr;     // count + scan passes
+    cudaStream_t cstream = nullptr;     // K0 + scan
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
 };
 
@@ -168,14 +159,24 @@ struct me_result {
     uint64_t g_rows = 0;
     me_comm* comm = nullptr;
     bool gather = false;
-    cudaEvent_t ev[5] = {};
-    std::vector<cudaEvent_t> tev;  // per sub-range: count start/end, scan end, write start/end
+    // ev[0] sweep start (plan stream), ev[1] unused, ev[2] K0/scan work done
+    // (plan stream), ev[3] output kernels done, ev[4] result complete (caller's
+    // stream), ev[5] entry (caller's stream)
+    cudaEvent_t ev[6] = {};
+    std::vector<cudaEvent_t> tev;  // per sub-range: rows start/end, scan end, output start/end
     bool ran_count = false, ran_write = false;
     // host-side results (valid after `resolved`)
     bool resolved = false;
     uint64_t local = 0, global = 0, offset = 0;
     uint64_t caps[8] = {};
 };
+
+// floor(cap * num / den), clamped to 2^63 (every total is < 2^63, so the
+// clamp never changes a verdict; the exact quotient may not fit 64 bits)
+static uint64_t threshold_of(uint64_t cap, me_threshold thr) {
+    const unsigned __int128 q = (unsigned __int128)cap * thr.num / thr.den;
+    return q >= ((unsigned __int128)1 << 63) ? (1ull << 63) : (uint64_t)q;
+}
 
 static int plan_create(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
                        me_threshold thr, int device, void* stream, me_alloc_fn al, me_free_fn fr, void* ctx,
@@ -193,6 +194,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
         delete P;
         return err(ME_ECUDA, "no CUDA device");
     }
@@ -211,11 +213,10 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     DevModel* dm;
     std::vector<DevModel> dmodels;
     for (const me_model& m : H.models) dmodels.push_back(dev_model(m));
-    uint32_t *dcls, *dlo, *dlt;
+    uint32_t *dcls, *dlo, *dlt, *dpb, *dsu;
     uint64_t *dsp, *dlp, *dsr;
     DevTuple* dtu;
     DevPair* dpr;
-    uint32_t* dpb;
     if ((st = upload(P->A, dmodels, &dm)) || (P->owned.push_back(dm), false) ||
         (st = upload(P->A, H.model_class, &dcls)) || (P->owned.push_back(dcls), false) ||
         (st = upload(P->A, H.seg_prefix, &dsp)) || (P->owned.push_back(dsp), false) ||
@@ -225,7 +226,8 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         (st = upload(P->A, H.list_prefix, &dlp)) || (P->owned.push_back(dlp), false) ||
         (st = upload(P->A, H.tuples, &dtu)) || (P->owned.push_back(dtu), false) ||
         (st = upload(P->A, H.pairs, &dpr)) || (P->owned.push_back(dpr), false) ||
-        (st = upload(P->A, H.pair_b, &dpb)) || (P->owned.push_back(dpb), false)) {
+        (st = upload(P->A, H.pair_b, &dpb)) || (P->owned.push_back(dpb), false) ||
+        (st = upload(P->A, H.pair_su, &dsu)) || (P->owned.push_back(dsu), false)) {
         me_plan_free(P);
         return st;
     }
@@ -239,6 +241,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.tuples = dtu;
     D.pairs = dpr;
     D.pair_b = dpb;
+    D.pair_su = dsu;
     D.n_seg = (uint32_t)(H.seg_prefix.size() - 1);
     D.n_world = (uint32_t)H.world.size();
     D.n_pairs = (uint32_t)H.pairs.size();
@@ -253,22 +256,16 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.thr_max = 0;
     uint32_t q_max = 0;
     for (size_t q = 0; q < H.caps.size(); q++) {
-        D.thr[q] = (uint64_t)(((unsigned __int128)H.caps[q] * thr.num) / thr.den);
+        D.thr[q] = threshold_of(H.caps[q], thr);
         D.thr1[q] = (D.thr[q] < (1ull << 62) ? D.thr[q] : (1ull << 62)) + 1;
         if (q == 0 || D.thr[q] > D.thr_max) D.thr_max = D.thr[q], q_max = (uint32_t)q;
     }
-    D.cslot[0] = q_max;  // swap slots 0 and q_max for the count pass
+    D.cslot[0] = q_max;  // slot 0 holds thr_max (survivor test of the stage kernel)
     D.cslot[q_max] = 0;
     for (int k = 0; k < 8; k++) D.thr1c[k] = D.thr1[D.cslot[k]];
-    // launch shape: spans = 96 per SM (divisible by every grid of 1..4
-    // resident 8-warp blocks per SM, so the grid-stride over spans is even)
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
-    P->max_spans = (uint32_t)P->sms * 96;
-    P->max_tiles = n_tiles_of(31, 31 + kMaxSub) + 1;
-    if (const char* e = getenv("ME_GRID_MODE")) P->grid_mode = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
-    if (const char* e = getenv("ME_PIPE")) P->pipe = atoi(e) == 0 ? 0u : 2u;
-    if (P->serial < 0) P->serial = P->pipe == 2 ? 0 : 1;
+    if (const char* e = getenv("ME_PIPE")) P->pipe = atoi(e) == 2 ? 2u : 3u;
     if (const char* e = getenv("ME_ROWS_SPAN")) P->rspan_tiles = (uint32_t)atoi(e);
     if (P->rspan_tiles < 1) P->rspan_tiles = 1;
     {
@@ -277,7 +274,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         P->max_rspans = (eff_tiles + P->rspan_tiles - 1) / P->rspan_tiles + 1;
         P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
         // (tests: a small cap exercises the cutting of sub-ranges by rows; >= 64
-        // so that the < 32 rows before a sub-range's first index always fit)
+        // so that the < 32 rows before a pipe-2 sub-range's first index fit)
         if (const char* e = getenv("ME_MAX_ROWS")) P->max_rows = std::min(P->max_rows, (uint32_t)std::max(64, atoi(e)));
         if (P->max_rows < 1) P->max_rows = 1;
         // a span of L positions touches at most ceil(L / min_w) + 1 rows
@@ -287,59 +284,46 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         P->d32 = L <= 65536 && min_w != UINT64_MAX && (L + min_w - 1) / min_w + 1 <= 256 ? 1u : 0u;
         if (const char* e = getenv("ME_DESC64")) P->d32 = atoi(e) ? 0u : P->d32;
     }
-    // K3 grid: 2 blocks per SM saturate HBM and leave registers for the
-    // overlapped K1 of the next sub-range (measured: 3 per SM, all the
-    // registers, is 7% slower on C5; 1 per SM cannot keep HBM busy)
+    // pipe 2 K3 grid: 2 blocks per SM saturate HBM and leave registers for the
+    // overlapped K1 of the next sub-range
     int ebps = 2;
     if (const char* e = getenv("ME_EXPAND_BPS")) ebps = std::max(1, atoi(e));
-    for (int m = 1; m < 4; m++)
-        P->expand_bps[m] = std::min(expand_blocks_per_sm((me_out_mode)m, D.n_cap), ebps);
-    const int occ_c = sweep_blocks_per_sm(0, D.n_cap), occ_w = sweep_blocks_per_sm(2, D.n_cap);
-    // both passes resident at once: the write pass (memory/latency bound) and
-    // the count pass of the next sub-range (issue bound) share every SM
-    P->write_bps = (uint32_t)(occ_w > 2 ? 2 : occ_w);
-    P->count_bps = (uint32_t)(occ_c > 2 ? 2 : occ_c);
-    if (const char* e = getenv("ME_WRITE_BPS")) P->write_bps = (uint32_t)atoi(e);
-    if (const char* e = getenv("ME_COUNT_BPS")) P->count_bps = (uint32_t)atoi(e);
-    if (P->write_bps < 1) P->write_bps = 1;
-    if (P->count_bps < 1) P->count_bps = 1;
+    int fbps = 0;  // 0 = as many as fit
+    if (const char* e = getenv("ME_FUSED_BPS")) fbps = std::max(1, atoi(e));
+    for (int m = 1; m < 4; m++) {
+        if (P->pipe == 2) P->expand_bps[m] = std::min(expand_blocks_per_sm((me_out_mode)m, D.n_cap), ebps);
+        const int fb = fused_blocks_per_sm((me_out_mode)m, D.n_cap);
+        P->fused_bps[m] = fbps ? std::min(fb, fbps) : fb;
+    }
     if (const char* e = getenv("ME_SETS")) P->n_sets = (uint32_t)std::min(std::max(atoi(e), 2), (int)kMaxSets);
+    const uint32_t max_units = fused_units_of(P->max_rows) + 1;
     for (uint32_t si = 0; si < P->n_sets; si++) {
         me_plan::Scratch& sc = P->scratch[si];
-        sc.tile_rel = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
-        sc.tile_cnt = (uint32_t*)P->A.get((size_t)P->max_tiles * 4);
-        P->owned.push_back(sc.tile_cnt);
-        sc.tile_ck = (uint4*)P->A.get((size_t)P->max_tiles * 16);
-        sc.span_count = (uint32_t*)P->A.get((size_t)P->max_spans * 4);
-        sc.span_off = (uint64_t*)P->A.get((size_t)P->max_spans * 8);
-        sc.span_caps = (uint32_t*)P->A.get((size_t)P->max_spans * 8 * 4);
-        P->owned.push_back(sc.tile_rel);
-        P->owned.push_back(sc.tile_ck);
-        P->owned.push_back(sc.span_count);
-        P->owned.push_back(sc.span_off);
-        P->owned.push_back(sc.span_caps);
-        bool rows_ok = true;
+        sc.rows = (RowEnt*)P->A.get((size_t)P->max_rows * sizeof(RowEnt));
+        sc.rcnt = (uint32_t*)P->A.get((size_t)P->max_rows * 4);
+        sc.ucnt = (uint32_t*)P->A.get((size_t)max_units * 4);
+        sc.uoff = (uint64_t*)P->A.get((size_t)max_units * 8);
+        sc.rnext = (uint32_t*)P->A.get(256);
+        for (void* x : {(void*)sc.rows, (void*)sc.rcnt, (void*)sc.ucnt, (void*)sc.uoff, (void*)sc.rnext})
+            P->owned.push_back(x);
+        bool ok = sc.rows && sc.rcnt && sc.ucnt && sc.uoff && sc.rnext;
         if (P->pipe == 2) {
             const size_t span_len = (size_t)P->rspan_tiles * kTile;
-            sc.rows = (RowEnt*)P->A.get((size_t)P->max_rows * sizeof(RowEnt));
             sc.rck = (uint2*)P->A.get((size_t)P->max_rspans * 8);
             sc.desc = (uint64_t*)P->A.get((size_t)P->max_rspans * span_len * 8);
             sc.rcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
             sc.roff = (uint64_t*)P->A.get((size_t)P->max_rspans * 8);
             sc.rbcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
-            sc.rnext = (uint32_t*)P->A.get(256);
-            for (void* x : {(void*)sc.rows, (void*)sc.rck, (void*)sc.desc, (void*)sc.rcount, (void*)sc.roff,
-                            (void*)sc.rbcount, (void*)sc.rnext})
+            for (void* x : {(void*)sc.rck, (void*)sc.desc, (void*)sc.rcount, (void*)sc.roff, (void*)sc.rbcount})
                 P->owned.push_back(x);
-            rows_ok = sc.rows && sc.rck && sc.desc && sc.rcount && sc.roff && sc.rbcount && sc.rnext;
-            if (H.stage_max) {
-                sc.st = (StEnt*)P->A.get((size_t)P->max_rows * H.n_rcdo * sizeof(StEnt));
-                P->owned.push_back(sc.st);
-                rows_ok = rows_ok && sc.st;
-            }
+            ok = ok && sc.rck && sc.desc && sc.rcount && sc.roff && sc.rbcount;
         }
-        if (!sc.tile_rel || !sc.tile_cnt || !sc.tile_ck || !sc.span_count || !sc.span_off || !sc.span_caps ||
-            !rows_ok) {
+        if (H.stage_max) {
+            sc.st = (StEnt*)P->A.get((size_t)P->max_rows * H.n_rcdo * sizeof(StEnt));
+            P->owned.push_back(sc.st);
+            ok = ok && sc.st;
+        }
+        if (!ok) {
             me_plan_free(P);
             return err(ME_ENOMEM, "scratch allocation");
         }
@@ -352,9 +336,13 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (cudaStreamCreateWithFlags(&P->cstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ready_ev, cudaEventDisableTiming) != cudaSuccess) {
         me_plan_free(P);
-        return cuda_err(cudaGetLastError(), "count stream");
+        return cuda_err(cudaGetLastError(), "plan stream");
     }
     cudaEventRecord(P->ready_ev, (cudaStream_t)stream);
+    if (cudaError_t ce = cudaGetLastError()) {
+        me_plan_free(P);
+        return cuda_err(ce, "plan_create");
+    }
     *out = P;
     return ME_OK;
 }
@@ -374,10 +362,10 @@ extern "C" int me_plan_size(const me_plan* plan, uint64_t* n) {
 extern "C" int me_plan_table_bytes(const me_plan* plan, uint64_t* bytes) {
     if (!plan || !bytes) return err(ME_EINVAL, "null argument");
     const HostSpace& H = plan->hs;
-    *bytes = H.models.size() * sizeof(me_model) + H.model_class.size() * 4 + H.seg_prefix.size() * 8 +
-             H.seg_row.size() * 8 +
-             H.list_off.size() * 4 + H.list_tuple.size() * 4 + H.list_prefix.size() * 8 +
-             H.tuples.size() * sizeof(DevTuple) + H.pairs.size() * sizeof(DevPair);
+    *bytes = H.models.size() * sizeof(DevModel) + H.model_class.size() * 4 + H.seg_prefix.size() * 8 +
+             H.seg_row.size() * 8 + H.list_off.size() * 4 + H.list_tuple.size() * 4 + H.list_prefix.size() * 8 +
+             H.tuples.size() * sizeof(DevTuple) + H.pairs.size() * sizeof(DevPair) + H.pair_b.size() * 4 +
+             H.pair_su.size() * 4;
     return ME_OK;
 }
 
@@ -385,7 +373,11 @@ extern "C" void me_plan_free(me_plan* P) {
     if (!P) return;
     {
         DeviceGuard g(P->device);
+        // the scratch sets may still be read by an output kernel on a sweep's
+        // stream (free_ev) or written by K0 on the plan stream
         if (P->cstream) cudaStreamSynchronize(P->cstream);
+        for (auto& sc : P->scratch)
+            if (sc.free_ev) cudaEventSynchronize(sc.free_ev);
         for (void* p : P->owned) P->A.put(p);
         for (auto& sc : P->scratch)
             if (sc.free_ev) cudaEventDestroy(sc.free_ev);
@@ -398,10 +390,10 @@ extern "C" void me_plan_free(me_plan* P) {
 static void result_release(me_result* R) {
     if (!R) return;
     DeviceGuard g(R->plan ? R->plan->device : -1);
-    // the count stream and the caller's stream may still use the buffers
+    // the plan stream and the caller's stream may still use the buffers
     if (R->ev[2]) cudaEventSynchronize(R->ev[2]);
     if (R->ev[4]) cudaEventSynchronize(R->ev[4]);
-    for (int i = 0; i < 5; i++)
+    for (int i = 0; i < 6; i++)
         if (R->ev[i]) cudaEventDestroy(R->ev[i]);
     for (cudaEvent_t x : R->tev) cudaEventDestroy(x);
     R->A.put(R->stats);
@@ -420,6 +412,98 @@ static int n_cols_of(me_out_mode m) {
 static uint64_t words_of(me_out_mode m) { return m == ME_OUT_RECORDS ? ME_N_COLS : 1; }
 
 static int resolve(me_result* R);
+
+// One pass of the hot path over [b, e): sub-ranges of at most
+// kMaxSub indices and max_rows rows; per sub-range K0 (+ K1 for pipe 2) and
+// the scan on the plan stream `cs`, the output kernel on the caller's stream
+// `st`.  write = false: counts only.  Accumulates stats[0] (survivors) and
+// stats[1 + j] (per capacity); the caller orders `st` after `cs` afterwards.
+static int run_pipeline(me_plan* P, me_result* R, uint64_t b, uint64_t e, cudaStream_t cs, cudaStream_t st,
+                        me_out_mode mode, bool write, Cols cols, uint64_t capacity) {
+    const HostSpace& H = P->hs;
+    if (cudaMemsetAsync(R->stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
+    const bool pipe2 = P->pipe == 2 && write;
+    const auto seg_of = [&](uint64_t g) {
+        return (uint32_t)(std::upper_bound(H.seg_row.begin(), H.seg_row.end(), g) - H.seg_row.begin() - 1);
+    };
+    for (uint64_t lo = b, hi = b; lo < e; lo = hi) {
+        hi = e - lo < kMaxSub ? e : lo + kMaxSub;
+        uint64_t g0;
+        if (pipe2) {
+            // the sub-range also holds at most max_rows rows (the rows covering
+            // [lo & ~31, lo) are < 32 and max_rows >= 64)
+            g0 = H.row_of(lo & ~31ull);
+        } else {
+            // sub-ranges end at row boundaries: only the call's own first and
+            // last rows can be cut
+            g0 = H.row_of(lo);
+            if (hi < e) {
+                const uint64_t cut = H.row_start(H.row_of(hi));
+                if (cut > lo) hi = cut;
+            }
+        }
+        if (H.row_of(hi - 1) + 1 - g0 > P->max_rows) {
+            const uint64_t cut = H.row_start(g0 + P->max_rows);
+            if (cut > lo) hi = cut;
+        }
+        const uint32_t n_rows = (uint32_t)(H.row_of(hi - 1) + 1 - g0);
+        // segments of rows g0 and g0 + n_rows - 1 (K0 searches only between them)
+        const uint32_t seg_lo = seg_of(g0);
+        const uint32_t n_seg_sub = seg_of(g0 + n_rows - 1) - seg_lo + 2;
+        me_plan::Scratch& sc = P->scratch[P->turn++ % P->n_sets];
+        cudaEvent_t tev[5];
+        for (auto& x : tev) {
+            if (cudaEventCreate(&x) != cudaSuccess) return cuda_err(cudaGetLastError(), "cudaEventCreate");
+            R->tev.push_back(x);
+        }
+        cudaStreamWaitEvent(cs, sc.free_ev, 0);
+        cudaEventRecord(tev[0], cs);
+        cudaError_t ce;
+        if (pipe2) {
+            const uint32_t n_tiles = n_tiles_of(lo, hi);
+            const uint32_t n_rsp = (n_tiles + P->rspan_tiles - 1) / P->rspan_tiles;
+            ce = launch_rows(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, P->rspan_tiles, sc.rows, sc.st, sc.rck, cs);
+            if (ce == cudaSuccess)
+                ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, P->d32, sc.rcount,
+                                  sc.rbcount, mode, cs);
+            if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
+            cudaEventRecord(tev[1], cs);
+            ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kStageWarps - 1) / kStageWarps, 0, sc.roff, R->stats, cs);
+            if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
+            cudaEventRecord(tev[2], cs);
+            cudaStreamWaitEvent(st, tev[2], 0);
+            cudaEventRecord(tev[3], st);
+            ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, P->d32, sc.rck, sc.rcount,
+                               sc.roff, mode, cols, capacity, R->stats, (uint32_t)(P->sms * P->expand_bps[mode]),
+                               sc.rnext, st);
+            if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
+            cudaEventRecord(tev[4], st);
+            cudaEventRecord(sc.free_ev, st);
+            continue;
+        }
+        ce = launch_rowcount(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.rows, sc.st, sc.rcnt, sc.ucnt,
+                             R->stats, cs);
+        if (ce != cudaSuccess) return cuda_err(ce, "row kernel");
+        cudaEventRecord(tev[1], cs);
+        ce = launch_scan(sc.ucnt, nullptr, fused_units_of(n_rows), 0, sc.uoff, R->stats, cs);
+        if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
+        cudaEventRecord(tev[2], cs);
+        if (write) {
+            cudaStreamWaitEvent(st, tev[2], 0);
+            cudaEventRecord(tev[3], st);
+            ce = launch_fused(P->ds, sc.rows, sc.st, sc.rcnt, sc.ucnt, sc.uoff, n_rows, lo, hi, mode, cols, capacity,
+                              (uint32_t)(P->sms * P->fused_bps[mode]), sc.rnext, st);
+            if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
+            cudaEventRecord(tev[4], st);
+            cudaEventRecord(sc.free_ev, st);
+        } else {
+            cudaEventRecord(tev[3], cs);
+            cudaEventRecord(tev[4], cs);
+            cudaEventRecord(sc.free_ev, cs);
+        }
+    }
+    return ME_OK;
+}
 
 static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_result** out) {
     if (!P || !o || !out) return err(ME_EINVAL, "null argument");
@@ -455,104 +539,22 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         result_release(R);
         return s;
     };
-    for (int i = 0; i < 5; i++)
+    for (int i = 0; i < 6; i++)
         if (cudaEventCreate(&R->ev[i]) != cudaSuccess) return fail(cuda_err(cudaErrorUnknown, "cudaEventCreate"));
     R->stats = (uint64_t*)R->A.get(9 * 8);
     if (!R->stats) return fail(err(ME_ENOMEM, "stats allocation"));
 
-    // Sub-ranges of <= kMaxSub indices.  Count + scan run on the plan's count
-    // stream, which waits only for the tables and for the write pass that last
-    // used the scratch set, so the count of sub-range i+1 runs while the
-    // caller's stream still writes the columns of sub-range i.
+    // K0 + scan run on the plan stream, which waits for the tables, for this
+    // call's entry point on the caller's stream (the stats block was handed out
+    // there) and, per sub-range, for the output kernel that last used the
+    // scratch set; so K0 of sub-range i+1 runs while the caller's stream still
+    // writes the rows of sub-range i.
     cudaStream_t cs = P->serial ? st : P->cstream;
+    cudaEventRecord(R->ev[5], st);
+    cudaStreamWaitEvent(cs, R->ev[5], 0);
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
-    auto pipeline = [&](uint64_t* stats, bool write, Cols cols, uint64_t capacity) -> int {
-        if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
-        const bool rows_pipe = P->pipe == 2 && write;
-        for (uint64_t lo = b, hi = b; lo < e; lo = hi) {
-            hi = e - lo < kMaxSub ? e : lo + kMaxSub;
-            uint64_t g0 = 0;
-            uint32_t n_rows = 0, seg_lo = 0, n_seg_sub = 0;
-            if (rows_pipe) {
-                // the sub-range also holds at most max_rows rows (the rows
-                // covering [lo & ~31, lo) are < 32 and max_rows >= 1: hi > lo)
-                const HostSpace& H = P->hs;
-                g0 = H.row_of(lo & ~31ull);
-                if (H.row_of(hi - 1) + 1 - g0 > P->max_rows) {
-                    const uint64_t cut = H.row_start(g0 + P->max_rows);
-                    if (cut > lo) hi = cut;
-                }
-                n_rows = (uint32_t)(H.row_of(hi - 1) + 1 - g0);
-                // segments of rows g0 and g0 + n_rows - 1 (K0 searches only between them)
-                const auto seg_of = [&](uint64_t g) {
-                    return (uint32_t)(std::upper_bound(H.seg_row.begin(), H.seg_row.end(), g) - H.seg_row.begin() - 1);
-                };
-                seg_lo = seg_of(g0);
-                n_seg_sub = seg_of(g0 + n_rows - 1) - seg_lo + 2;
-            }
-            me_plan::Scratch& sc = P->scratch[P->turn++ % P->n_sets];
-            const uint32_t n_tiles = n_tiles_of(lo, hi);
-            const uint32_t n_spans = n_tiles < P->max_spans ? n_tiles : P->max_spans;
-            // grid_mode 0: persistent grids of bps resident blocks per SM;
-            // 1: one unit (span / tile) per warp, so the block scheduler
-            // interleaves the blocks of the concurrent count and write passes
-            auto grid = [&](uint32_t bps, uint32_t units) {
-                uint32_t gb = (uint32_t)P->sms * bps, need = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
-                return P->grid_mode || gb > need ? need : gb;
-            };
-            cudaEvent_t tev[5];
-            for (auto& x : tev) {
-                if (cudaEventCreate(&x) != cudaSuccess) return cuda_err(cudaGetLastError(), "cudaEventCreate");
-                R->tev.push_back(x);
-            }
-            cudaStreamWaitEvent(cs, sc.free_ev, 0);
-            if (rows_pipe) {
-                // K0 rows + K1 stage + scan on the count stream, K3 on the caller's
-                const uint32_t n_rsp = (n_tiles + P->rspan_tiles - 1) / P->rspan_tiles;
-                cudaEventRecord(tev[0], cs);
-                cudaError_t ce = launch_rows(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, P->rspan_tiles, sc.rows, sc.st,
-                                                sc.rck, cs);
-                if (ce == cudaSuccess)
-                    ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, P->d32,
-                                      sc.rcount, sc.rbcount, o->mode, cs);
-                if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
-                cudaEventRecord(tev[1], cs);
-                ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kStageWarps - 1) / kStageWarps, 0, sc.roff, stats,
-                                 cs);
-                if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
-                cudaEventRecord(tev[2], cs);
-                cudaStreamWaitEvent(st, tev[2], 0);
-                cudaEventRecord(tev[3], st);
-                ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, P->d32, sc.rck, sc.rcount,
-                                   sc.roff, o->mode, cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[o->mode]),
-                                   sc.rnext, st);
-                if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
-                cudaEventRecord(tev[4], st);
-                cudaEventRecord(sc.free_ev, st);
-                continue;
-            }
-            cudaEventRecord(tev[0], cs);
-            cudaError_t ce = launch_count(P->ds, lo, hi, n_spans, grid(P->count_bps, n_spans), sc.tile_rel,
-                                          sc.tile_cnt, sc.tile_ck, sc.span_count, sc.span_caps, cs);
-            if (ce != cudaSuccess) return cuda_err(ce, "count kernel");
-            cudaEventRecord(tev[1], cs);
-            ce = launch_scan(sc.span_count, sc.span_caps, n_spans, P->ds.n_cap, sc.span_off, stats, cs);
-            if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
-            cudaEventRecord(tev[2], cs);
-            cudaStreamWaitEvent(st, tev[2], 0);
-            cudaEventRecord(tev[3], st);
-            if (write) {
-                ce = launch_write(P->ds, lo, hi, grid(P->write_bps, n_tiles), sc.tile_ck, sc.tile_rel, sc.tile_cnt,
-                                  sc.span_off, o->mode, cols, capacity, st);
-                if (ce != cudaSuccess) return cuda_err(ce, "write kernel");
-            }
-            cudaEventRecord(tev[4], st);
-            cudaEventRecord(sc.free_ev, st);  // scratch set reusable after this point of the caller's stream
-        }
-        return ME_OK;
-    };
     cudaEventRecord(R->ev[0], cs);
     Cols cols{};
     if (nc && len) {
@@ -563,9 +565,11 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             }
             R->capacity = o->out_capacity;
         } else {
-            // exact allocation: a count-only pipeline first (synchronises the host once)
-            if ((rc = pipeline(R->stats, false, cols, 0))) return fail(rc);
+            // exact allocation: a counting pass first (K0 + scan; synchronises the host once)
+            if ((rc = run_pipeline(P, R, b, e, cs, st, o->mode, false, cols, 0))) return fail(rc);
             uint64_t cnt = 0;
+            cudaEventRecord(R->ev[2], cs);
+            cudaStreamWaitEvent(st, R->ev[2], 0);
             if (cudaMemcpyAsync(&cnt, R->stats, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
                 cudaStreamSynchronize(st) != cudaSuccess)
                 return fail(cuda_err(cudaGetLastError(), "count readback"));
@@ -580,10 +584,11 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
     }
-    if ((rc = pipeline(R->stats, nc != 0, cols, R->capacity))) return fail(rc);
+    if ((rc = run_pipeline(P, R, b, e, cs, st, o->mode, nc != 0, cols, R->capacity))) return fail(rc);
     R->ran_count = len != 0;
     R->ran_write = nc && len;
     cudaEventRecord(R->ev[2], cs);
+    cudaStreamWaitEvent(st, R->ev[2], 0);  // stats complete before anything on the caller's stream reads them
     cudaEventRecord(R->ev[3], st);
     if (o->comm) {
         R->gathered = (uint64_t*)R->A.get((size_t)o->comm->nranks * 9 * 8);
@@ -593,23 +598,45 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         if (R->gather && nc) {
             if ((rc = resolve(R))) return fail(rc);
             // variable-size allgather of the columns: one broadcast per rank
-            std::vector<uint64_t> cnt(o->comm->nranks), off(o->comm->nranks + 1, 0);
-            std::vector<uint64_t> h(o->comm->nranks * 9);
+            const int nr_ = o->comm->nranks;
+            std::vector<uint64_t> cnt(nr_), off(nr_ + 1, 0);
+            std::vector<uint64_t> h((size_t)nr_ * 9);
             if (cudaMemcpy(h.data(), R->gathered, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
                 return fail(cuda_err(cudaGetLastError(), "gathered readback"));
-            for (int r = 0; r < o->comm->nranks; r++) {
-                cnt[r] = h[r * 9];
+            for (int r = 0; r < nr_; r++) {
+                cnt[r] = h[(size_t)r * 9];
                 off[r + 1] = off[r] + cnt[r];
             }
-            R->g_rows = off[o->comm->nranks];
-            for (int j = 0; j < nc; j++) {
+            R->g_rows = off[nr_];
+            // every rank must enter the broadcasts or none: agree on failures
+            // (caller columns overflowed, allocation failed) first
+            uint64_t bad = R->capacity < R->local ? 1u : 0u;
+            for (int j = 0; j < nc && !bad; j++) {
                 R->gcols[j] = (uint64_t*)R->A.get(R->g_rows * 8 * words_of(o->mode));
-                if (!R->gcols[j]) return fail(err(ME_ENOMEM, "gathered column allocation"));
+                if (!R->gcols[j]) bad = 2;
             }
-            if (R->capacity < R->local) return fail(err(ME_ERANGE, "caller columns overflowed; cannot gather"));
+            uint64_t* dflag = (uint64_t*)R->A.get((size_t)(nr_ + 1) * 8);
+            if (!dflag) return fail(err(ME_ENOMEM, "flag buffer"));  // (allocation of a few bytes)
+            std::vector<uint64_t> flags(nr_, 0);
+            if (cudaMemcpyAsync(dflag, &bad, 8, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+                R->A.put(dflag);
+                return fail(cuda_err(cudaGetLastError(), "flag upload"));
+            }
+            nr = ncclAllGather(dflag, dflag + 1, 1, ncclUint64, o->comm->nccl, st);
+            cudaError_t fe = nr == ncclSuccess ? cudaMemcpyAsync(flags.data(), dflag + 1, (size_t)nr_ * 8,
+                                                                 cudaMemcpyDeviceToHost, st)
+                                               : cudaSuccess;
+            if (fe == cudaSuccess) fe = cudaStreamSynchronize(st);
+            R->A.put(dflag);
+            if (nr != ncclSuccess) return fail(err(ME_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr)));
+            if (fe != cudaSuccess) return fail(cuda_err(fe, "flag readback"));
+            uint64_t any = 0;
+            for (uint64_t f : flags) any |= f;
+            if (any & 1) return fail(err(ME_ERANGE, "a rank's caller columns overflowed; cannot gather"));
+            if (any) return fail(err(ME_ENOMEM, "a rank could not allocate the gathered columns"));
             ncclGroupStart();
             for (int j = 0; j < nc; j++)
-                for (int r = 0; r < o->comm->nranks; r++) {
+                for (int r = 0; r < nr_; r++) {
                     if (!cnt[r]) continue;
                     const uint64_t wd = words_of(o->mode);
                     nr = ncclBroadcast(r == o->comm->rank ? (const void*)R->cols[j] : nullptr,
@@ -622,6 +649,7 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
     }
     cudaEventRecord(R->ev[4], st);
+    if (cudaError_t ce = cudaGetLastError()) return fail(cuda_err(ce, "me_plan_sweep"));
     R->own_plan = own_plan;
     *out = R;
     return ME_OK;
@@ -763,17 +791,76 @@ extern "C" int me_result_rank(me_result* R, uint32_t cap, uint64_t* best_index) 
     me_plan* P = R->plan;
     DeviceGuard g(P->device);
     const size_t n_seg = P->hs.seg_prefix.size() - 1;
-    uint64_t *dkey = nullptr, *didx = nullptr;
-    CU(cudaMalloc(&dkey, n_seg * 8));
-    cudaError_t ce = cudaMalloc(&didx, n_seg * 8);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(dkey, 0xFF, n_seg * 8, R->stream);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(didx, 0xFF, n_seg * 8, R->stream);
+    // scratch from the result's allocator, ordered on its stream
+    uint64_t* dkey = (uint64_t*)R->A.get(n_seg * 16);
+    if (!dkey) return err(ME_ENOMEM, "rank scratch");
+    uint64_t* didx = dkey + n_seg;
+    cudaError_t ce = cudaMemsetAsync(dkey, 0xFF, n_seg * 16, R->stream);
     if (ce == cudaSuccess) ce = launch_rank(P->ds, cols[0], (uint32_t)words_of(R->mode), rows, cap, dkey, didx, R->stream);
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(best_index, didx, n_seg * 8, cudaMemcpyDeviceToHost, R->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(R->stream);
-    cudaFree(dkey);
-    cudaFree(didx);
+    R->A.put(dkey);
     if (ce != cudaSuccess) return cuda_err(ce, "me_result_rank");
+    return ME_OK;
+}
+
+extern "C" int me_result_digest(me_result* R, uint64_t* digest) {
+    if (!R || !digest) return err(ME_EINVAL, "null argument");
+    if (R->mode == ME_OUT_COUNT) return err(ME_EINVAL, "a COUNT result has no rows to digest");
+    uint64_t* cols[ME_N_COLS];
+    uint64_t rows = 0;
+    int st = me_result_columns(R, cols, &rows);
+    if (st) return st;
+    if (!(R->gather) && R->local > R->capacity) return err(ME_ERANGE, "caller columns overflowed");
+    DeviceGuard g(R->plan->device);
+    const bool sharded = R->comm && !R->gather;
+    const int nr = sharded ? R->comm->nranks : 1;
+    uint64_t* d = (uint64_t*)R->A.get((size_t)(2 + 2 * nr) * 8);
+    if (!d) return err(ME_ENOMEM, "digest scratch");
+    const uint32_t n_cols = R->mode == ME_OUT_FULL ? ME_N_COLS : 1;
+    cudaError_t ce = launch_digest(cols, n_cols, (uint32_t)words_of(R->mode), rows, d, R->stream);
+    std::vector<uint64_t> h((size_t)2 * nr);
+    if (ce == cudaSuccess && sharded) {
+        // collective: every rank's digest, merged in rank order with the
+        // global offsets: D = sum_r M^offset_r D_r
+        ncclResult_t r = ncclAllGather(d, d + 2, 2, ncclUint64, R->comm->nccl, R->stream);
+        if (r != ncclSuccess) {
+            R->A.put(d);
+            return err(ME_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+        }
+        ce = cudaMemcpyAsync(h.data(), d + 2, h.size() * 8, cudaMemcpyDeviceToHost, R->stream);
+    } else if (ce == cudaSuccess) {
+        ce = cudaMemcpyAsync(h.data(), d, 16, cudaMemcpyDeviceToHost, R->stream);
+    }
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(R->stream);
+    R->A.put(d);
+    if (ce != cudaSuccess) return cuda_err(ce, "me_result_digest");
+    if (!sharded) {
+        digest[0] = h[0];
+        digest[1] = R->mode == ME_OUT_INDEX ? 0 : h[1];
+        return ME_OK;
+    }
+    std::vector<uint64_t> all((size_t)nr * 9);
+    CU(cudaMemcpy(all.data(), R->gathered, all.size() * 8, cudaMemcpyDeviceToHost));
+    uint64_t off = 0, di = 0, dr = 0;
+    for (int r = 0; r < nr; r++) {
+        const uint64_t sh = digest_pow_host(off);
+        di += sh * h[2 * r];
+        dr += sh * h[2 * r + 1];
+        off += all[(size_t)r * 9];
+    }
+    digest[0] = di;
+    digest[1] = R->mode == ME_OUT_INDEX ? 0 : dr;
+    return ME_OK;
+}
+
+extern "C" int me_comm_check(me_comm* c) {
+    if (!c) return err(ME_EINVAL, "null comm");
+    ncclResult_t a = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(c->nccl, &a);
+    if (r != ncclSuccess) return err(ME_ENCCL, std::string("ncclCommGetAsyncError: ") + ncclGetErrorString(r));
+    if (a != ncclSuccess && a != ncclInProgress)
+        return err(ME_ENCCL, std::string("asynchronous NCCL error: ") + ncclGetErrorString(a));
     return ME_OK;
 }
 
@@ -806,11 +893,13 @@ extern "C" int me_estimate_batch(const me_model* models, uint32_t n_models, cons
     if (!n) return ME_OK;
     cudaStream_t st = (cudaStream_t)stream;
     std::vector<void*> tmp;
+    // scratch: stream-ordered allocations on the caller's stream (the call has
+    // no allocator argument; me.h: cudaMallocAsync when none is given)
     auto stage_in = [&](const void* p, size_t bytes, const void** dp) -> int {
         if (!p) { *dp = nullptr; return ME_OK; }
         if (is_device_ptr(p)) { *dp = p; return ME_OK; }
         void* d = nullptr;
-        CU(cudaMalloc(&d, bytes));
+        CU(cudaMallocAsync(&d, bytes, st));
         tmp.push_back(d);
         CU(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, st));
         *dp = d;
@@ -820,7 +909,7 @@ extern "C" int me_estimate_batch(const me_model* models, uint32_t n_models, cons
         if (!p) { *dp = nullptr; return ME_OK; }
         if (is_device_ptr(p)) { *dp = p; return ME_OK; }
         void* d = nullptr;
-        CU(cudaMalloc(&d, bytes));
+        CU(cudaMallocAsync(&d, bytes, st));
         tmp.push_back(d);
         *dp = d;
         return ME_OK;
@@ -833,13 +922,14 @@ extern "C" int me_estimate_batch(const me_model* models, uint32_t n_models, cons
         } else {
             c = caps[q];
         }
-        thr_h[q] = (uint64_t)(((unsigned __int128)c * thr.num) / thr.den);
+        thr_h[q] = threshold_of(c, thr);
     }
     const void *dm, *di, *dc, *dt;
     void *dout, *dmask, *dstat;
     int rc;
     auto cleanup = [&]() {
-        for (void* p : tmp) cudaFree(p);
+        for (void* p : tmp) cudaFreeAsync(p, st);
+        cudaStreamSynchronize(st);
     };
     if ((rc = stage_in(models, (size_t)n_models * sizeof(me_model), &dm)) ||
         (rc = stage_in(ids, n * 4, &di)) || (rc = stage_in(cfgs, n * sizeof(me_parallel), &dc)) ||
@@ -852,7 +942,7 @@ extern "C" int me_estimate_batch(const me_model* models, uint32_t n_models, cons
     if (status && is_device_ptr(status)) {
         dstat = status;
     } else {
-        if (cudaMalloc(&dstat, n) != cudaSuccess) { cleanup(); return cuda_err(cudaGetLastError(), "cudaMalloc"); }
+        if (cudaMallocAsync(&dstat, n, st) != cudaSuccess) { cleanup(); return cuda_err(cudaGetLastError(), "cudaMallocAsync"); }
         tmp.push_back(dstat);
     }
     cudaError_t ce = launch_estimate((const me_model*)dm, n_models, (const uint32_t*)di, (const me_parallel*)dc,
@@ -894,11 +984,13 @@ extern "C" int me_estimate_stage(const me_model* model, const me_parallel* cfg, 
     h.m = *model;
     h.c = *cfg;
     Buf* d = nullptr;
-    CU(cudaMalloc(&d, sizeof(Buf)));
-    cudaError_t ce = cudaMemcpy(d, &h, sizeof(Buf), cudaMemcpyHostToDevice);
-    if (ce == cudaSuccess) ce = launch_estimate_stage(&d->m, &d->c, stage, &d->b, &d->which, &d->status, nullptr);
-    if (ce == cudaSuccess) ce = cudaMemcpy(&h, d, sizeof(Buf), cudaMemcpyDeviceToHost);
-    cudaFree(d);
+    cudaStream_t s0 = nullptr;  // the legacy default stream, like me_estimate
+    CU(cudaMallocAsync(&d, sizeof(Buf), s0));
+    cudaError_t ce = cudaMemcpyAsync(d, &h, sizeof(Buf), cudaMemcpyHostToDevice, s0);
+    if (ce == cudaSuccess) ce = launch_estimate_stage(&d->m, &d->c, stage, &d->b, &d->which, &d->status, s0);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&h, d, sizeof(Buf), cudaMemcpyDeviceToHost, s0);
+    cudaFreeAsync(d, s0);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s0);
     if (ce != cudaSuccess) return cuda_err(ce, "me_estimate_stage");
     if (h.status) return err(h.status, "estimator precondition failed");
     *out = h.b;
@@ -1035,4 +1127,4 @@ extern "C" const char* me_strerror(int s) {
 
 extern "C" const char* me_last_error_detail(void) { return g_detail.c_str(); }
 
-extern "C" const char* me_version(void) { return "me-b200 0.1.0 sm_100a"; }
+extern "C" const char* me_version(void) { return "me-b200 0.2.0 sm_100a"; }

@@ -1,0 +1,421 @@
+// me_fused.cu -- the row-count sweep pipeline (sm_100a), DESIGN.md §6.
+//
+// A row is a run of configurations sharing (model, N, t, c, p, d); its
+// configurations are its valid (b, s) pairs x the (rc, do) digits, in that
+// order.  For one digit every estimator term is affine in the pair's tokens
+// per microbatch u = b s / c (paper mode: the in-flight count is p), so the
+// total is strictly increasing in u and "total <= threshold" (the 80% rule,
+// P:27) holds exactly for the pairs with u up to a bound.  Per
+// sub-range of the flat index space:
+//
+//  K0 rowcount_kernel  one thread per row: the row's coefficients (make_row,
+//                      Eq.6/7/10/12-17), its survivors per capacity -- per
+//                      digit a binary search over the row's u values sorted
+//                      ascending, evaluating the total at each probe -- the
+//                      survivor bound umax (the largest surviving u) per
+//                      digit, and per 32-row unit the survivor count;
+//                      a global batch (R17: the in-flight count depends on
+//                      b) or a row cut by the range is evaluated config by
+//                      config instead;
+//  scan                unit counts -> output offsets (scan_kernel);
+//  K3 fused_kernel     warps take 32-row units in order: per row with
+//                      survivors, 32 consecutive configurations per round,
+//                      survivor test (u <= umax: one compare), ballot
+//                      compaction, the survivors' eight output values and
+//                      their stores (records: two 32-byte stores per lane,
+//                      one contiguous run per round).
+//
+// Every configuration is tested once (K3); K0 works per row.  No per-survivor
+// intermediate goes through HBM: the only scratch traffic is the 128-byte row
+// entry per row with survivors.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "me_dev.cuh"
+#include "me_kernels.cuh"
+
+namespace me {
+
+namespace {
+
+// one (rc, do) digit of a row: stage 0 total = ms + u K; with NEXT-1 and p >= 2
+// also the last stage, msL + u kL
+struct Digit {
+    uint64_t ms, K, msL, kL;
+    bool two;
+};
+
+__device__ __forceinline__ bool fits(const Digit& c, uint32_t u, uint64_t thr) {
+    if (c.ms + (uint64_t)u * c.K > thr) return false;
+    return !c.two || c.msL + (uint64_t)u * c.kL <= thr;
+}
+
+// number of leading entries of the ascending su[0, n) that fit under thr
+__device__ __forceinline__ uint32_t count_fit(const uint32_t* __restrict__ su, uint32_t n, const Digit& c,
+                                              uint64_t thr) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (fits(c, __ldg(su + mid), thr)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------- K0
+template <int NCAP>
+__global__ void __launch_bounds__(256) rowcount_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows,
+                                                       const uint32_t seg_lo, const uint32_t n_seg_sub,
+                                                       const uint64_t lo, const uint64_t hi,
+                                                       RowEnt* __restrict__ rows, StEnt* __restrict__ st,
+                                                       uint32_t* __restrict__ rcnt, uint32_t* __restrict__ ucnt,
+                                                       uint64_t* __restrict__ stats) {
+    __shared__ uint32_t s_cap[NCAP];
+    if (threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t cnt = 0;
+    uint32_t capc[NCAP];
+#pragma unroll
+    for (int q = 0; q < NCAP; q++) capc[q] = 0;
+    if (k < n_rows) {
+        const RowId I = row_id(S, g0 + k, seg_lo, n_seg_sub);
+        RowCoef R;
+        make_row(I.M, I.tu.t, I.tu.c, I.tu.p, I.tu.d, I.L0, S.zero_stage, R);
+        const bool two = S.stage_max && I.tu.p >= 2;
+        RowEnt e = row_entry(I, R, two);
+        const uint32_t n_sel = 1u << S.lg_rcdo;
+        // the row's window of the range: [a, b) of its positions
+        const uint32_t a = I.rs < lo ? (uint32_t)(lo - I.rs) : 0u;
+        const uint32_t b = I.rs + I.tu.w > hi ? (uint32_t)(hi - I.rs) : I.tu.w;
+        const bool full = a == 0 && b == I.tu.w;
+        Digit dg[4];
+        for (uint32_t sel = 0; sel < n_sel; sel++) {
+            const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+            Digit& c = dg[sel];
+            c.ms = dopt ? R.ms1 : R.ms0;
+            // per-token bytes with p in flight (paper mode): p (lam + e8) + mu + hc
+            c.K = (uint64_t)I.tu.p * ((rc ? R.lam1 : R.lam0) + R.e8) + (rc ? R.bt + R.hc : R.hc);
+            c.two = two;
+            c.msL = c.kL = 0;
+            if (two) {
+                const StEnt x = last_stage(I, rc, dopt, S.zero_stage);
+                st[(size_t)k << S.lg_rcdo | sel] = x;
+                c.msL = x.msL;
+                c.kL = x.kL;
+            }
+            if (!S.gbs_mode) {
+                const uint32_t* su = S.pair_su + I.tu.pair_off;
+                const uint32_t nm = count_fit(su, I.tu.n_pairs, c, S.thr_max);
+                e.umax[sel] = nm ? __ldg(su + nm - 1) : 0u;  // u >= 1: 0 admits nothing
+                if (full) {
+                    cnt += nm;
+#pragma unroll
+                    for (int q = 0; q < NCAP; q++)
+                        if (q < (int)S.n_cap) capc[q] += S.thr[q] >= S.thr_max ? nm : count_fit(su, nm, c, S.thr[q]);
+                }
+            }
+        }
+        if (!full || S.gbs_mode) {
+            // config by config over the window: in-flight count min(p, m) of
+            // each pair (R17), or a row cut by the range
+            const DevPair* pp = S.pairs + I.tu.pair_off;
+            for (uint32_t pos = a; pos < b; pos++) {
+                const uint32_t sel = pos & (n_sel - 1u);
+                const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+                const DevPair pr = pp[pos >> S.lg_rcdo];
+                uint64_t tot = config_total(R, pr.u, pr.m, rc, dopt);
+                if (two) {
+                    const uint64_t tl = dg[sel].msL + (uint64_t)pr.u * dg[sel].kL;
+                    tot = tl > tot ? tl : tot;
+                }
+                cnt += tot <= S.thr_max ? 1u : 0u;
+#pragma unroll
+                for (int q = 0; q < NCAP; q++) capc[q] += (q < (int)S.n_cap && tot <= S.thr[q]) ? 1u : 0u;
+            }
+        }
+        rows[k] = e;
+        rcnt[k] = cnt;
+    }
+    // survivors per 32-row unit (a unit is one warp of this kernel)
+    const uint32_t unit_cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && k < n_rows) ucnt[k >> 5] = unit_cnt;
+#pragma unroll
+    for (int q = 0; q < NCAP; q++) {
+        const uint32_t c = __reduce_add_sync(0xffffffffu, capc[q]);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cap + q, c);
+    }
+    __syncthreads();
+    if (threadIdx.x < NCAP && s_cap[threadIdx.x])
+        atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------- K3
+constexpr uint32_t kUnit = 32;         // rows per unit
+constexpr uint32_t kPairsSmem = 2048;  // pairs pool in shared memory when it fits (16 KB)
+constexpr uint32_t kFusedWarps = kThreads / 32;
+
+// Lane-constant values of one row for the lane's (rc, do) digit.
+struct Lane {
+    uint64_t v1, v2, v3;  // params, grads, optim
+    uint64_t ms;          // their sum
+    uint64_t lam, mu;     // layer bytes per token per in-flight microbatch: n_inf lam + mu
+    uint64_t e8, hc;      // embedding bytes per token per microbatch, LM-head bytes per token
+    uint64_t c4, c5, K;   // paper mode: p lam + mu, p e8, c4 + c5 + hc
+    uint32_t p, umax;
+    // NEXT-1 last stage
+    uint64_t msL, kL, parL, graL, optimL, layL, hcL;
+};
+
+template <bool GBS, bool STMAX>
+__device__ __forceinline__ void lane_of(const DevSpace& S, const RowEnt& R, const StEnt* __restrict__ st,
+                                        uint64_t kg, uint32_t sel, Lane& C) {
+    const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+    const uint64_t psi = R.psi;
+    C.v1 = dopt ? R.par1 : 2ull * psi;
+    C.v2 = dopt ? R.gra1 : 4ull * psi;
+    C.v3 = dopt ? R.optim1 : 12ull * psi;
+    C.ms = dopt ? R.ms1 : R.ms0;
+    C.lam = rc ? R.lam1 : R.lam0;
+    C.mu = rc ? R.bt : 0ull;
+    C.e8 = R.e8;
+    C.hc = R.hc;
+    C.p = R.p;
+    C.umax = sel == 0 ? R.umax[0] : sel == 1 ? R.umax[1] : sel == 2 ? R.umax[2] : R.umax[3];
+    C.c4 = (uint64_t)C.p * C.lam + C.mu;
+    C.c5 = (uint64_t)C.p * C.e8;
+    C.K = C.c4 + C.c5 + C.hc;
+    if (STMAX && R.two) {
+        const StEnt* x = st + (kg << S.lg_rcdo | sel);
+        C.msL = __ldg(&x->msL);
+        C.kL = __ldg(&x->kL);
+        C.parL = __ldg(&x->parL);
+        C.graL = __ldg(&x->graL);
+        C.optimL = __ldg(&x->optimL);
+        C.layL = __ldg(&x->layL);
+        C.hcL = __ldg(&x->hcL);
+    }
+}
+
+// one row's survivors: rounds of 32 consecutive positions of its window
+template <int MODE, int NCAP, bool GBS, bool STMAX>
+__device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, const StEnt* __restrict__ st,
+                                          uint64_t kg, const DevPair* __restrict__ pairs, uint64_t lo, uint64_t hi,
+                                          uint32_t cnt, uint64_t off, const Cols& cols, uint64_t capacity,
+                                          uint32_t lane) {
+    const uint64_t rs = R.rs;
+    const uint32_t w = R.w;
+    const uint32_t a = rs < lo ? (uint32_t)(lo - rs) : 0u;
+    const uint32_t b = rs + w > hi ? (uint32_t)(hi - rs) : w;
+    const bool all = cnt == b - a;  // every configuration of the window survives: no test
+    const uint32_t sel = (a + lane) & ((1u << S.lg_rcdo) - 1u);  // 32 is a multiple of the digit count
+    Lane C;
+    lane_of<GBS, STMAX>(S, R, st, kg, sel, C);
+    const bool two = STMAX && R.two;
+    const DevPair* pp = pairs + R.pair_off;
+    const uint32_t lanes_lt = (1u << lane) - 1u;
+    uint32_t done = 0;
+    for (uint32_t p0 = a; p0 < b; p0 += 32) {
+        const uint32_t pos = p0 + lane;
+        const bool valid = pos < b;
+        const DevPair pr = valid ? pp[pos >> S.lg_rcdo] : DevPair{0u, 0u};
+        const uint32_t u = pr.u;
+        uint64_t c4 = C.c4, c5 = C.c5, tot;
+        if (GBS) {
+            const uint32_t n_inf = min(C.p, pr.m);  // R17
+            c4 = (uint64_t)n_inf * C.lam + C.mu;
+            c5 = (uint64_t)n_inf * C.e8;
+            tot = C.ms + (uint64_t)u * (c4 + c5 + C.hc);
+        } else {
+            tot = C.ms + (uint64_t)u * C.K;
+        }
+        bool s;
+        if (all) {
+            s = valid;
+        } else if (!GBS) {
+            s = valid && u <= C.umax;
+        } else {
+            uint64_t t2 = tot;
+            if (two) {
+                const uint64_t tl = C.msL + (uint64_t)u * C.kL;
+                t2 = tl > t2 ? tl : t2;
+            }
+            s = valid && t2 <= S.thr_max;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, s);
+        if (s) {
+            uint64_t v[8];
+            v[1] = C.v1;
+            v[2] = C.v2;
+            v[3] = C.v3;
+            v[4] = (uint64_t)u * c4;
+            v[5] = (uint64_t)u * c5;
+            v[6] = (uint64_t)u * C.hc;
+            v[7] = tot;
+            if (two) {
+                const uint64_t tl = C.msL + (uint64_t)u * C.kL;
+                if (tl > tot) {  // the last stage decides (ties: stage 0)
+                    v[1] = C.parL;
+                    v[2] = C.graL;
+                    v[3] = C.optimL;
+                    v[4] = (uint64_t)u * C.layL;
+                    v[5] = 0;
+                    v[6] = (uint64_t)u * C.hcL;
+                    v[7] = tl;
+                }
+            }
+            v[0] = (rs + pos) | ((uint64_t)cap_mask_n<NCAP>(S, ~v[7]) << 56);
+            const uint64_t o = off + done + __popc(bal & lanes_lt);
+            if (o < capacity) {
+                if (MODE == 3) {
+                    store_record(cols.c[0] + o * 8, v);
+                } else if (MODE == 2) {
+#pragma unroll
+                    for (int c = 0; c < 8; c++) cols.c[c][o] = v[c];
+                } else {
+                    cols.c[0][o] = v[0];
+                }
+            }
+        }
+        done += __popc(bal);
+    }
+}
+
+template <int MODE, int NCAP, bool GBS, bool STMAX>
+__device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __restrict__ rows,
+                                            const StEnt* __restrict__ st, const uint32_t* __restrict__ rcnt,
+                                            const uint32_t* __restrict__ ucnt, const uint64_t* __restrict__ uoff,
+                                            uint32_t n_rows, uint32_t n_units, uint64_t lo, uint64_t hi,
+                                            const Cols& cols, uint64_t capacity, const DevPair* pairs,
+                                            RowEnt* srow, uint32_t* next_unit) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t unit = 0;
+    while (true) {
+        // units are taken in order from a counter (their survivors vary)
+        if (lane == 0) unit = atomicAdd(next_unit, 1u);
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+        if (unit >= n_units) break;
+        if (!__ldg(ucnt + unit)) continue;
+        const uint32_t k0 = unit * kUnit;
+        const uint32_t nr = min(kUnit, n_rows - k0);
+        const uint32_t c = lane < nr ? __ldg(rcnt + k0 + lane) : 0u;
+        uint32_t inc = c;  // inclusive warp scan of the row counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        const uint64_t base = __ldg(uoff + unit);
+        // the unit's rows into the warp's shared copy (coalesced 16-byte loads)
+        __syncwarp();
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(rows + k0);
+            uint4* dst = reinterpret_cast<uint4*>(srow);
+            const uint32_t n16 = nr * (uint32_t)(sizeof(RowEnt) / 16);
+            for (uint32_t i = lane; i < n16; i += 32) dst[i] = __ldg(src + i);
+        }
+        __syncwarp();
+        uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
+        while (nz) {
+            const uint32_t i = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
+            const uint64_t oi = base + (__shfl_sync(0xffffffffu, inc, i) - ci);
+            fused_row<MODE, NCAP, GBS, STMAX>(S, srow[i], st, (uint64_t)k0 + i, pairs, lo, hi, ci, oi, cols,
+                                              capacity, lane);
+        }
+    }
+}
+
+template <int MODE, int NCAP>
+__global__ void __launch_bounds__(kThreads, 2)
+    fused_kernel(const DevSpace S, const RowEnt* __restrict__ rows, const StEnt* __restrict__ st,
+                 const uint32_t* __restrict__ rcnt, const uint32_t* __restrict__ ucnt,
+                 const uint64_t* __restrict__ uoff, const uint32_t n_rows, const uint32_t n_units, const uint64_t lo,
+                 const uint64_t hi, const Cols cols, const uint64_t capacity, uint32_t* __restrict__ next_unit) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    DevPair* s_pairs = reinterpret_cast<DevPair*>(smem);
+    RowEnt* s_rows = reinterpret_cast<RowEnt*>(smem + kPairsSmem * sizeof(DevPair));
+    const bool pairs_smem = S.n_pairs <= kPairsSmem;
+    if (pairs_smem)
+        for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_pairs[i] = S.pairs[i];
+    __syncthreads();
+    const DevPair* pairs = pairs_smem ? s_pairs : S.pairs;
+    RowEnt* srow = s_rows + (threadIdx.x >> 5) * kUnit;
+#define ME_FUSED(GBS, STMAX)                                                                                     \
+    fused_units<MODE, NCAP, GBS, STMAX>(S, rows, st, rcnt, ucnt, uoff, n_rows, n_units, lo, hi, cols, capacity, \
+                                        pairs, srow, next_unit)
+    if (S.stage_max) {
+        if (S.gbs_mode) ME_FUSED(true, true);
+        else ME_FUSED(false, true);
+    } else {
+        if (S.gbs_mode) ME_FUSED(true, false);
+        else ME_FUSED(false, false);
+    }
+#undef ME_FUSED
+}
+
+constexpr size_t kFusedSmem = kPairsSmem * sizeof(DevPair) + (size_t)kFusedWarps * kUnit * sizeof(RowEnt);
+
+uint32_t ncap_pad3(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
+
+template <int MODE>
+void* fused_fn_(uint32_t n_cap) {
+    switch (ncap_pad3(n_cap)) {
+        case 1: return reinterpret_cast<void*>(&fused_kernel<MODE, 1>);
+        case 2: return reinterpret_cast<void*>(&fused_kernel<MODE, 2>);
+        case 4: return reinterpret_cast<void*>(&fused_kernel<MODE, 4>);
+        default: return reinterpret_cast<void*>(&fused_kernel<MODE, 8>);
+    }
+}
+void* fused_fn(me_out_mode mode, uint32_t n_cap) {
+    return mode == ME_OUT_RECORDS ? fused_fn_<3>(n_cap) : mode == ME_OUT_FULL ? fused_fn_<2>(n_cap) : fused_fn_<1>(n_cap);
+}
+void* rowcount_fn(uint32_t n_cap) {
+    switch (ncap_pad3(n_cap)) {
+        case 1: return reinterpret_cast<void*>(&rowcount_kernel<1>);
+        case 2: return reinterpret_cast<void*>(&rowcount_kernel<2>);
+        case 4: return reinterpret_cast<void*>(&rowcount_kernel<4>);
+        default: return reinterpret_cast<void*>(&rowcount_kernel<8>);
+    }
+}
+
+}  // namespace
+
+int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap) {
+    void* fn = fused_fn(mode, n_cap);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmem) != cudaSuccess)
+        return 1;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, kFusedSmem) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+
+uint32_t fused_units_of(uint32_t n_rows) { return (n_rows + kUnit - 1) / kUnit; }
+
+cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
+                            uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
+                            uint64_t* stats, cudaStream_t stream) {
+    const uint32_t blocks = (n_rows + 255) / 256;
+    void* args[] = {(void*)&S,  (void*)&g0,   (void*)&n_rows, (void*)&seg_lo, (void*)&n_seg_sub, (void*)&lo,
+                    (void*)&hi, (void*)&rows, (void*)&st,     (void*)&rcnt,   (void*)&ucnt,      (void*)&stats};
+    return cudaLaunchKernel(rowcount_fn(S.n_cap), dim3(blocks ? blocks : 1), dim3(256), args, 0, stream);
+}
+
+cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,
+                         const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
+                         me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, uint32_t* next_unit,
+                         cudaStream_t stream) {
+    const uint32_t n_units = fused_units_of(n_rows);
+    const uint32_t need = (n_units + kFusedWarps - 1) / kFusedWarps;
+    if (n_blocks > need) n_blocks = need ? need : 1;
+    void* args[] = {(void*)&S,      (void*)&rows,    (void*)&st, (void*)&rcnt, (void*)&ucnt,
+                    (void*)&uoff,   (void*)&n_rows,  (void*)&n_units, (void*)&lo, (void*)&hi,
+                    (void*)&cols,   (void*)&capacity, (void*)&next_unit};
+    cudaError_t ce = cudaMemsetAsync(next_unit, 0, 4, stream);
+    if (ce != cudaSuccess) return ce;
+    return cudaLaunchKernel(fused_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, kFusedSmem, stream);
+}
+
+}  // namespace me

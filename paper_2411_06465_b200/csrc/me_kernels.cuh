@@ -33,6 +33,7 @@ struct DevSpace {
     const DevTuple* tuples;
     const DevPair* pairs;
     const uint32_t* pair_b;       // micro-batch size of each pair (planner only)
+    const uint32_t* pair_su;      // per pair list: its u values sorted ascending (row-count pipeline)
     uint32_t n_seg, n_world;
     uint32_t n_pairs;             // pooled (b, s) pairs
     uint32_t lg_rcdo, rcdo_rc, rcdo_do;
@@ -216,7 +217,8 @@ struct __align__(16) RowEnt {
     uint64_t par1, gra1;
     uint64_t optim1, rs;           // rs = flat index of the row's first config
     // survivor bound per (rc, do) digit: total <= thr_max  <=>  u <= umax
-    // (paper mode; with the largest stage when stage_max); unused with gbs
+    // (paper mode; with the largest stage when stage_max); unused with gbs.
+    // Row-count pipeline: the largest surviving u of the row (0 = none)
     uint32_t umax[4];
 };
 // NEXT-1: last-stage terms of one row for one (rc, do) digit (64 B)
@@ -244,22 +246,9 @@ constexpr uint64_t kMaxSub = 1ull << 28;           // indices per count/scan/wri
 uint32_t ncap_stride(uint32_t n_cap);
 // tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
 uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
-// resident blocks per SM of a pass (0 = count, 1 = INDEX write, 2 = FULL write)
-int sweep_blocks_per_sm(int pass, uint32_t n_cap);
-// count pass over [lo, hi) cut into n_spans spans of whole tiles: per tile its
-// walker checkpoint {seg, j, r, span} and the rank of its first survivor in the
-// span; per span its survivor count and per-capacity counts
-cudaError_t launch_count(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_spans, uint32_t n_blocks,
-                         uint32_t* tile_rel, uint32_t* tile_cnt, uint4* tile_ck, uint32_t* span_count,
-                         uint32_t* span_caps, cudaStream_t st);
 // span offsets = running total stats[0] + exclusive prefix; stats accumulate
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st);
-// write pass over [lo, hi): survivors of tile t stored from row
-// span_off[span(t)] + tile_rel[t]
-cudaError_t launch_write(const DevSpace& S, uint64_t lo, uint64_t hi, uint32_t n_blocks, const uint4* tile_ck,
-                         const uint32_t* tile_rel, const uint32_t* tile_cnt, const uint64_t* span_off,
-                         me_out_mode mode, Cols cols, uint64_t capacity, cudaStream_t st);
 // row-table pipeline (me_rows.cu): K0 rows [g0, g0 + n_rows) of the range
 // [lo, hi) + span checkpoints, K1 survivors -> descriptors + span counts, K3
 // descriptors -> output rows (and stats[1 + j] per capacity)
@@ -274,6 +263,23 @@ cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st
                           uint32_t span_tiles, const uint64_t* desc, uint32_t d32, const uint2* span_ck,
                           const uint32_t* span_count, const uint64_t* block_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
                           uint32_t n_blocks, uint32_t* next_span, cudaStream_t stream);
+// row-count pipeline (me_fused.cu): K0 rows [g0, g0 + n_rows) of the range
+// [lo, hi) with their survivor counts (rcnt, per 32-row unit ucnt, per
+// capacity into stats[1 + j]); K3 rows with survivors -> output rows
+cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
+                            uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
+                            uint64_t* stats, cudaStream_t stream);
+cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,
+                         const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
+                         me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, uint32_t* next_unit,
+                         cudaStream_t stream);
+int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
+uint32_t fused_units_of(uint32_t n_rows);
+// order-dependent digest of a result's rows (me_result_digest): out[0] index
+// digest, out[1] record digest (words = 8 for records, cols = FULL columns)
+cudaError_t launch_digest(const uint64_t* const* cols, uint32_t n_cols, uint32_t words, uint64_t n, uint64_t* out,
+                          cudaStream_t stream);
+uint64_t digest_pow_host(uint64_t n);  // M^n mod 2^64 (merging digests of consecutive pieces)
 // NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
 // (rank key of DESIGN.md §9); best_key / best_index initialised to ~0.
 // stride = u64 words between rows of the index column (8 for RECORDS)

@@ -31,40 +31,12 @@
 
 #include <cstdlib>
 
+#include "me_dev.cuh"
 #include "me_kernels.cuh"
 
 namespace me {
 
 namespace {
-
-__device__ __forceinline__ uint32_t upper_bound_u64(const uint64_t* __restrict__ a, uint32_t n, uint64_t x) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) <= x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// total <= thr  <=>  thr1 + ~total carries out of 64 bits (thr1 = thr + 1)
-__device__ __forceinline__ uint32_t le_shift(uint32_t acc, uint64_t ntot, uint64_t thr1) {
-    asm("{\n\t.reg .u32 t;\n\t"
-        "add.cc.u32 t, %1, %2;\n\t"
-        "addc.cc.u32 t, %3, %4;\n\t"
-        "addc.u32 %0, %0, %0;\n\t}"
-        : "+r"(acc)
-        : "r"((uint32_t)ntot), "r"((uint32_t)thr1), "r"((uint32_t)(ntot >> 32)), "r"((uint32_t)(thr1 >> 32)));
-    return acc;
-}
-
-template <int NCAP>
-__device__ __forceinline__ uint32_t cap_mask_n(const DevSpace& S, uint64_t ntot) {
-    uint32_t mask = 0;
-#pragma unroll
-    for (int q = NCAP - 1; q >= 0; q--) mask = le_shift(mask, ntot, S.thr1[q]);
-    return mask;
-}
 
 // lane-constant selections of a row's coefficients for the lane's (rc, do)
 struct LaneCoef {
@@ -382,13 +354,6 @@ __device__ __forceinline__ void stage_one(const DevSpace& S, const RowEnt* __res
 }
 
 // ---------------------------------------------------------------- K3
-// (no "memory" clobber: the kernel never reads what it stores, so the
-// loads of later survivors may be scheduled ahead of these stores)
-__device__ __forceinline__ void store_record(uint64_t* q, const uint64_t (&v)[8]) {
-    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(q), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3]));
-    asm volatile("st.global.v4.u64 [%0+32], {%1, %2, %3, %4};" ::"l"(q), "l"(v[4]), "l"(v[5]), "l"(v[6]), "l"(v[7]));
-}
-
 // per-lane capacity counters: 16-bit fields, capacities 4j .. 4j + 3 in word j
 // (the mask bits spread to bit 16 i by one multiply)
 template <int NCAP>

@@ -85,6 +85,7 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
     tuples.clear();
     pairs.clear();
     pair_b.clear();
+    pair_su.clear();
     tup_begin.assign(1, 0);
     std::map<std::pair<uint32_t, uint32_t>, std::pair<uint32_t, uint32_t>> pool;  // (c, d|0) -> (off, n)
     std::vector<uint32_t> tvals, pvals;
@@ -115,6 +116,8 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
                                 pair_b.push_back(b);
                             }
                         it = pool.emplace(key, std::make_pair(off, (uint32_t)pairs.size() - off)).first;
+                        for (size_t q = off; q < pairs.size(); q++) pair_su.push_back(pairs[q].u);
+                        std::sort(pair_su.begin() + off, pair_su.end());
                     }
                     DevTuple tu;
                     tu.t = t; tu.c = c; tu.p = p; tu.d = d;

@@ -65,6 +65,7 @@ class HostSpace {
     std::vector<uint32_t> tup_begin;
     std::vector<DevPair> pairs;
     std::vector<uint32_t> pair_b;       // micro-batch size of each pooled pair (planner)
+    std::vector<uint32_t> pair_su;      // per pooled pair list: its u values sorted ascending
     std::vector<uint32_t> model_class;  // per model
     uint32_t n_class = 0;
     std::vector<uint32_t> list_off;     // n_class * n_world + 1

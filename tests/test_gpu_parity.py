@@ -338,14 +338,15 @@ def test_sweep_zero_stages(me, oracle_mod, zero, stage_max):
     assert_same(me, res, *oracle_rows(oracle_mod, sp), me.ME_OUT_FULL)
 
 
-@pytest.mark.parametrize("env", [{"ME_PIPE": "0"}, {"ME_DESC64": "1"}, {"ME_SERIAL": "1"}, {"ME_EXPAND_U": "4"},
-                                 {"ME_SETS": "3"}],
-                         ids=["pipe0", "desc64", "serial", "u4", "sets3"])
+@pytest.mark.parametrize("env", [{"ME_PIPE": "2"}, {"ME_PIPE": "2", "ME_DESC64": "1"}, {"ME_SERIAL": "1"},
+                                 {"ME_PIPE": "2", "ME_SERIAL": "1"}, {"ME_PIPE": "2", "ME_EXPAND_U": "4"},
+                                 {"ME_SETS": "3"}, {"ME_FUSED_BPS": "1"}],
+                         ids=["pipe2", "pipe2-desc64", "serial", "pipe2-serial", "pipe2-u4", "sets3", "fused-1bps"])
 def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
     """The selectable pipelines and kernel variants (read at plan creation)
-    give the same rows: count/scan/write passes, the row-table pipeline with
-    64-bit descriptors, serial streams, 4 survivors per lane in the expand
-    kernel, three scratch sets."""
+    give the same rows: the descriptor pipeline (pipe 2, with 64-bit
+    descriptors, 4 survivors per lane in its expand kernel), serial streams,
+    three scratch sets, one fused-kernel block per SM."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     spaces = [mi.config("C3", uneven=1),
@@ -360,12 +361,14 @@ def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
             assert_same(me, res, *ref, mode)
 
 
+@pytest.mark.parametrize("pipe", ["3", "2"])
 @pytest.mark.parametrize("max_rows", [64, 1000])
-def test_subranges_cut_by_rows(me, oracle_mod, monkeypatch, max_rows):
+def test_subranges_cut_by_rows(me, oracle_mod, monkeypatch, max_rows, pipe):
     """Sub-ranges of the row-table pipeline are also cut at max_rows rows
     (2^21 in production; a small cap here): offsets chain across the cuts and
     the result equals the oracle, for the full range and for ragged ranges."""
     monkeypatch.setenv("ME_MAX_ROWS", str(max_rows))
+    monkeypatch.setenv("ME_PIPE", pipe)
     sp = mi.Space(models=mi.random_models(20, seed=13), world=[16, 48, 64, 128], caps_gb=[40, 80, 192],
                   mbs=[1, 2, 4], seq=[2048, 4096, 8192], uneven=1)
     plan = me.Plan(sp)
