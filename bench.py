@@ -6,16 +6,22 @@ grid (247,776 shapes) x world sizes 8..16384 x every 4D factorisation x
 mbs 1..16 x seq 4K..128K x recompute x distributed optimizer, uneven PP
 allowed, capacities 40/80/94/192 GiB -- 8.4e10 valid configurations, which the
 north star partitions over the 8 GPUs of one box.  Every step sweeps ALL of
-C5 whatever N is ("scaling": "strong"): the index space is cut into calls of
-N * CHUNK consecutive configs and each call is split evenly over the ranks.
+C5 whatever N is ("scaling": "strong"): the index space is cut into blocks of
+CHUNK = 2^28 consecutive configs; at N = 1 each block is one me_plan_sweep
+call; at N > 1 (default --partition cyclic) the blocks are dealt round-robin
+by libme (me_cyclic_block: rank r sweeps blocks r, r + N, ... alone) and one
+me_result_join per step joins them (NCCL allgather of every block's counts and
+an exclusive scan on the device: global offsets).  --partition even: calls of
+N * CHUNK configs, each split evenly over the ranks by the library with a join
+per call.
 
 A step = one pass of the whole hot path over the whole space: decode ->
-estimate -> 80% filter -> order-preserving compaction into FULL records
-(8 u64 columns) -- every call's columns are written to HBM (two column sets
-alternate) -- with the NCCL allgather of the per-call survivor counts (global
-offsets) when N > 1.
+estimate -> 80% filter -> order-preserving compaction into 64-byte records
+(RECORDS; --mode full|index|count) -- every call's rows are written to HBM
+(two caller buffers alternate).  The INDEX and COUNT modes are timed too and
+reported under "modes".
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode full|index|count]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode records|full|index|count]
   python bench.py --impl reference ...   (the CPU oracle on the host cores)
 """
 from __future__ import annotations
@@ -48,10 +54,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-modes", action="store_true", help="skip the INDEX / COUNT extra keys")
     ap.add_argument("--partition", default="cyclic", choices=["cyclic", "even"],
-                    help="N>1: cyclic = rank r sweeps calls r, r+N, ... of CHUNK configs on its own and the "
-                         "per-call counts are joined by one allgather per step; even = every call covers "
-                         "N*CHUNK configs split evenly over the ranks by the library (one join per call)")
+                    help="N>1: cyclic = libme's cyclic deal: rank r sweeps blocks r, r+N, ... of CHUNK configs "
+                         "on its own and me_result_join joins every block's counts with one NCCL allgather per "
+                         "step; even = every call covers N*CHUNK configs split evenly over the ranks by the "
+                         "library (one join per call)")
     return ap.parse_args()
 
 
@@ -124,29 +132,42 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def cpu_baseline(sp, begin, end, budget_s=12.0):
-    """The oracle (unchanged) on the host cores over a bounded, deterministic
-    sample of the workload: evenly spaced windows of the bench range."""
+def oracle_rate(sp, begin, end, threads, n, wins=4):
+    """configs/s of the oracle (unchanged) over `wins` evenly spaced windows of
+    n/wins configs of [begin, end).  The oracle walks its enumeration from
+    index 0 to a window (table build + skip); that overhead is measured with a
+    1-config window at the same offset and subtracted, so the rate counts the
+    evaluation of the window's configurations only."""
     import oracle
-    threads = oracle.default_threads()
-    # calibrate
-    t = time.perf_counter()
-    cal = 1_000_000
-    oracle.sweep(sp, begin, begin + cal, rows=False, threads=threads)
-    dt = time.perf_counter() - t
-    rate = cal / max(dt, 1e-6)
-    n = int(min(end - begin, max(cal, rate * budget_s)))
-    wins = 4
     per = max(1, n // wins)
-    done, t0 = 0, time.perf_counter()
+    done, net = 0, 0.0
     for w in range(wins):
         s = begin + (end - begin) * w // wins
+        t = time.perf_counter()
+        oracle.sweep(sp, s, s + 1, rows=False, threads=1)
+        over = time.perf_counter() - t
+        t = time.perf_counter()
         oracle.sweep(sp, s, s + per, rows=False, threads=threads)
+        net += max(1e-9, time.perf_counter() - t - over)
         done += per
-    el = time.perf_counter() - t0
-    return {"value": done / el, "unit": "configs/s", "cores": threads, "kind": "oracle",
-            "sample": f"{wins} evenly spaced windows of {per} configs of the first eighth of {WORKLOAD} "
-                      f"(survivor counts, all estimator terms evaluated), {done} configs in {el:.1f} s"}
+    return done / net, done, net
+
+
+def cpu_baseline(sp, begin, end, budget_s=12.0):
+    """The oracle (unchanged) on the host cores over a bounded, deterministic
+    sample of the workload: evenly spaced windows of the bench range, with all
+    host threads and with one thread."""
+    import oracle
+    threads = oracle.default_threads()
+    r1, n1, t1 = oracle_rate(sp, begin, end, 1, 200_000)
+    n = int(min(end - begin, max(1_000_000, r1 * threads * budget_s)))
+    rate, done, el = oracle_rate(sp, begin, end, threads, n)
+    return {"value": rate, "unit": "configs/s", "cores": threads, "kind": "oracle",
+            "value_1thread": r1,
+            "sample": f"4 evenly spaced windows of the first eighth of {WORKLOAD}: {done} configs on {threads} "
+                      f"threads in {el:.1f} s and {n1} configs on 1 thread in {t1:.1f} s (survivor counts, every "
+                      "estimator term evaluated; the oracle's table build and walk to each window are measured "
+                      "with a 1-config window and subtracted)"}
 
 
 def run_reference(args):
@@ -164,9 +185,12 @@ def run_reference(args):
     for i in range(args.warmup + args.steps):
         s = b + (e - b) * (i % 97) // 97
         t = time.perf_counter()
+        oracle.sweep(sp, s, s + 1, rows=False, threads=1)
+        over = time.perf_counter() - t  # table build + walk to the window (subtracted)
+        t = time.perf_counter()
         oracle.sweep(sp, s, s + per, rows=False, threads=threads)
         if i >= args.warmup:
-            times.append(time.perf_counter() - t)
+            times.append(max(1e-9, time.perf_counter() - t - over))
     el = sum(times)
     v = per * args.steps / el
     line = {"impl": "reference", "metric": "estimator configs/sec", "value": v, "unit": "configs/s",
@@ -175,106 +199,60 @@ def run_reference(args):
             "data": "synthetic", "config": {"workload": args.workload, "sample_per_step": per},
             "cpu_baseline": {"value": v, "unit": "configs/s", "cores": threads, "kind": "oracle",
                              "sample": f"{per} consecutive configs per step at evenly spaced offsets of the "
-                                       f"first eighth of {args.workload}"},
+                                       f"first eighth of {args.workload} (the oracle's walk to each window, "
+                                       "measured with a 1-config window, subtracted)"},
             "e2e": {"value": v, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-    import torch
-    import torch.distributed as dist
+def run_steps(torch, dist, me, plan, calls, mode, ring, flush, stream, steps, warmup, world, comm, cyclic, n_blocks,
+              clocks=None):
+    """W untimed + K timed steps of the hot path; returns (ms max over ranks,
+    per-call timings, this rank's survivors, the job's survivors) per step."""
+    ncols = 0 if mode == me.ME_OUT_COUNT else 1
 
-    import me_inputs as mi
-    import paper_2411_06465_b200 as me
-    from paper_2411_06465_b200.cyclic import cyclic_calls, cyclic_join, n_calls
-
-    rank, world, local = dist_env()
-    assert world == args.gpus or world == 1, "launch N>1 with torchrun"
-    torch.cuda.set_device(local)
-    dev = local
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    mode = {"records": me.ME_OUT_RECORDS, "full": me.ME_OUT_FULL, "index": me.ME_OUT_INDEX,
-            "count": me.ME_OUT_COUNT}[args.mode]
-    # u64 words written per survivor (FULL: 8 columns, RECORDS: one 64-byte row)
-    ncols = {me.ME_OUT_RECORDS: 8, me.ME_OUT_FULL: 8, me.ME_OUT_INDEX: 1, me.ME_OUT_COUNT: 0}[mode]
-
-    sp = mi.config(args.workload)
-    stream = torch.cuda.Stream(device=dev)
-    plan = me.Plan(sp, device=dev, stream=stream.cuda_stream)
-    total = plan.size
-    # this job: units 0..world-1; each me_plan_sweep call covers world*CHUNK
-    # consecutive configs, split evenly over the ranks by the library
-    job_b, job_e = 0, total
-    calls = []
-    s = job_b
-    while s < job_e:
-        e = min(job_e, s + CHUNK * world)
-        calls.append((s, e))
-        s = e
-    comm = me.Comm(dev) if world > 1 else None
-    calls_even = calls
-    cyclic = world > 1 and args.partition == "cyclic"
-    if cyclic:
-        # whole CHUNK-config calls dealt round-robin: neighbouring chunks have
-        # similar survivor density, so every rank writes about as many rows,
-        # and no rank waits for the others until the step's single join
-        calls = cyclic_calls(job_b, job_e, CHUNK, rank, world)
-        calls_total = n_calls(job_b, job_e, CHUNK)
-    sweep_comm = None if cyclic else comm
-
-    def join(results):
-        """a8 for the cyclic partition: one allgather of every call's count"""
-        return cyclic_join([r.counts()[0] for r in results], calls_total, world, device=dev)
-
-    ring = [out_buffers(torch, me, mode, CHUNK + 64, device=dev) for _ in range(2)]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-
-    def step(collect=None):
+    def step():
         out = []
         for q, (b, e) in enumerate(calls):
-            r = plan.sweep(b, e, mode=mode, out_cols=ring[q & 1] if ncols else None, comm=sweep_comm)
-            out.append(r)
+            out.append(plan.sweep(b, e, mode=mode, out_cols=ring[q & 1] if ncols else None,
+                                  comm=None if cyclic else comm,
+                                  partition=me.ME_PART_CYCLIC if cyclic else me.ME_PART_EVEN))
         if cyclic:
-            joined.append(join(out)[2])
+            # a8: one NCCL allgather of every block's counts + device scan (libme)
+            me.result_join(out, n_blocks, comm)
         return out
-
-    joined = []
 
     def drain(results, timings=None):
         n_local = n_global = 0
-        for r in results:
+        for i, r in enumerate(results):
             if r.status() != 0:
                 raise RuntimeError("caller columns overflowed")
             lo, gl, off = r.counts()
             n_local += lo
-            n_global += gl
+            n_global = gl if cyclic else n_global + gl
             if timings is not None:
                 timings.append(r.timing())
+        for r in results:
             r.free()
         return n_local, n_global
 
-    # warmup
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             flush.zero_()
             drain(step())
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(dev)
     timings = []
-    with clocks:
+    import contextlib
+    with (clocks if clocks is not None else contextlib.nullcontext()):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             ev0.record(stream)
             all_res = []
-            for _ in range(args.steps):
+            for _ in range(steps):
                 flush.zero_()
                 all_res.append(step())
             ev1.record(stream)
@@ -288,105 +266,171 @@ def main():
         lo, gl = drain(res, timings)
         n_local += lo
         n_global += gl
-    if cyclic:
-        n_global = sum(joined[-args.steps:])
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{torch.cuda.current_device()}")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    configs = (job_e - job_b) * args.steps
-    value = configs / (ms_max / 1e3)
+    return float(t.item()), timings, n_local // steps, n_global // steps
 
-    # per-kernel device times (CUDA events on the sweep stream)
-    count_ms = sum(x[1] for x in timings)
-    write_ms = sum(x[3] for x in timings)
+
+def ncu_summary():
+    """per-kernel ncu figures of one C5 chunk at HEAD (scripts/ncu_summary.py)"""
+    for name in ("r2_final", "r2"):
+        f = ROOT / "profiles" / name / "ncu_chunk40.json"
+        if f.exists():
+            return json.loads(f.read_text()), f"profiles/{name}/ncu_chunk40.json"
+    return None, None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import me_inputs as mi
+    import paper_2411_06465_b200 as me
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "launch N>1 with torchrun"
+    torch.cuda.set_device(local)
+    dev = local
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    modes = {"records": me.ME_OUT_RECORDS, "full": me.ME_OUT_FULL, "index": me.ME_OUT_INDEX, "count": me.ME_OUT_COUNT}
+    mode = modes[args.mode]
+    # u64 words written per survivor (FULL: 8 columns, RECORDS: one 64-byte row)
+    words = {me.ME_OUT_RECORDS: 8, me.ME_OUT_FULL: 8, me.ME_OUT_INDEX: 1, me.ME_OUT_COUNT: 0}
+
+    sp = mi.config(args.workload)
+    stream = torch.cuda.Stream(device=dev)
+    plan = me.Plan(sp, device=dev, stream=stream.cuda_stream)
+    total = plan.size
+    comm = me.Comm(dev) if world > 1 else None
+    cyclic = world > 1 and args.partition == "cyclic"
+    n_blocks = 0
+    if cyclic:
+        # a8 (libme): CHUNK-config blocks dealt round-robin (me_cyclic_block);
+        # rank r sweeps blocks r, r + N, ... alone, one me_result_join per step
+        calls, n_blocks = me.cyclic_blocks(0, total, CHUNK, rank, world)
+    else:
+        # N = 1: the space in CHUNK-config calls; N > 1 "even": calls of
+        # N * CHUNK configs, each split evenly over the ranks by the library
+        step_len = CHUNK * world
+        calls = [(s, min(total, s + step_len)) for s in range(0, total, step_len)]
+
+    def ring_for(m):
+        return [out_buffers(torch, me, m, CHUNK + 64, device=dev) for _ in range(2)]
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    clocks = ClockSampler(dev)
+    ring = ring_for(mode)
+    ms_max, timings, surv_local, surv_global = run_steps(torch, dist, me, plan, calls, mode, ring, flush, stream,
+                                                         args.steps, args.warmup, world, comm, cyclic, n_blocks,
+                                                         clocks=clocks)
+    del ring
+    value = total * args.steps / (ms_max / 1e3)
+
+    # per-kernel device times (CUDA events on the streams the kernels run on:
+    # K0 rows + scan on the plan stream, the output kernel K3 on the sweep stream)
+    rows_ms = sum(x[1] for x in timings)
     scan_ms = sum(x[2] for x in timings)
+    out_ms = sum(x[3] for x in timings)
     n_launch = len(timings)
-    survivors_local_per_step = n_local // args.steps
     peaks, peak_src = measured_peaks()
-    # per-kernel ncu summary of one C5 chunk (scripts/gpu_prof.sh +
-    # scripts/ncu_summary.py): DRAM traffic and warp instructions per round
-    ncu = ROOT / "profiles" / "ncu_chunk40.json"
-    ncu_k = json.loads(ncu.read_text()).get("kernels", {}) if ncu.exists() else {}
-    ncu_c = json.loads(ncu.read_text()) if ncu.exists() else {}
-
-    def ncu_kernel(prefix):
-        return next((v for k, v in ncu_k.items() if k.startswith(prefix)), None)
-
-    # integer-issue roofline of the pass that evaluates every config (the
-    # stage kernel K1; COUNT mode: the count kernel): warp instructions per
-    # round of 32 configs from the ncu capture x this rank's rounds, over the
-    # pass's CUDA-event time (with overlapped passes that time includes
-    # sharing the SMs with the previous sub-range's expand kernel)
-    issue = None
-    kname = "count_kernel" if mode == me.ME_OUT_COUNT else "stage_kernel"
-    kk = ncu_kernel(kname)
-    ipr = kk and kk.get("warp_instr_per_round")
-    if ipr and count_ms > 0:
-        clock = peaks.get("sm_max_mhz", 1965.0) * 1e6
-        issue_peak = 148 * 4 * clock
-        ach = (job_e - job_b) // world * args.steps / 32 * ipr / (count_ms / 1e3)
-        issue = {"bound": "alu", "kernel": f"{kname} (evaluates every config)", "achieved": ach,
-                 "peak": issue_peak, "unit": "warp-instr/s", "frac": ach / issue_peak, "traffic": 0,
-                 "instr_per_round_ncu": ipr,
-                 "peak_source": "148 SMs x 4 SMSPs x 1 warp-instr/cycle x sm_max_mhz (MEASURED_PEAKS.json)"}
+    ncu, ncu_src = ncu_summary()
     if mode != me.ME_OUT_COUNT:
-        bytes_write = survivors_local_per_step * 8 * ncols * args.steps
-        achieved = bytes_write / (write_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": f"expand_kernel<{int(mode)},4> (writes every survivor row)",
+        bytes_out = surv_local * 8 * words[mode] * args.steps
+        achieved = bytes_out / (out_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": f"fused_kernel<{int(mode)},4> (K3: tests every configuration of the rows "
+                                          "with survivors, writes every survivor row)",
                 "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                "traffic": None, "peak_source": f"{peak_src} hbm_gbs (copy)",
-                "algorithmic_bytes_per_launch": bytes_write / max(1, n_launch),
-                "avg_launch_ms": write_ms / max(1, n_launch)}
-        ek = ncu_kernel("expand_kernel")
-        if ek:
-            roof["traffic"] = ek["dram_bytes_read"] + ek["dram_bytes_write"]
-            roof["traffic_note"] = (f"ncu DRAM bytes (read {ek['dram_bytes_read']:.4g} + write "
-                                    f"{ek['dram_bytes_write']:.4g}) of the expand kernel of C5 chunk "
-                                    f"{ncu_c['chunk']}, algorithmic {ncu_c['algorithmic_write_bytes']} B for that "
-                                    "launch; the reads are the 8-byte survivor descriptors and the row table")
+                "traffic": None, "peak_source": f"{peak_src} hbm_gbs (copy, MEASURED_PEAKS.json)",
+                "algorithmic_bytes_per_launch": bytes_out / max(1, n_launch),
+                "avg_launch_ms": out_ms / max(1, n_launch)}
+        k3 = ncu and ncu["kernels"].get("fused_kernel")
+        if k3:
+            roof["traffic"] = k3["dram_bytes_read"] + k3["dram_bytes_write"]
+            roof["traffic_note"] = (f"ncu DRAM bytes (read {k3['dram_bytes_read']:.4g} + write "
+                                    f"{k3['dram_bytes_write']:.4g}) of K3 on C5 chunk {ncu['chunk']}, algorithmic "
+                                    f"{ncu['algorithmic_write_bytes']} B for that launch ({ncu_src}); the reads are "
+                                    "the 128-byte row entries of rows with survivors")
         mb = ROOT / "profiles" / "r1_v4" / "microbench.json"
         if mb.exists():
             w = json.loads(mb.read_text())["write_only_gbs"]
             roof["write_only_peak_gbs"] = w
             roof["frac_of_write_only"] = achieved / w
-        if issue:
-            roof["stage_pass_issue"] = issue
     else:
-        roof = issue or {"bound": "alu", "kernel": "count_kernel<4> (count pass)", "achieved": None, "peak": None,
-                         "unit": "warp-instr/s", "frac": None, "traffic": 0}
+        roof = {"bound": "alu", "kernel": "rowcount_kernel (K0: every row, per-capacity survivor counts)",
+                "achieved": None, "peak": None, "unit": "warp-instr/s", "frac": None, "traffic": 0}
+    # integer-issue roofline (ncu, each kernel alone on the GPU: 148 SMs x 4
+    # SMSPs x 1 warp-instruction / cycle)
+    issue = None
+    if ncu:
+        issue = {"source": ncu_src, "chunk": ncu["chunk"], "configs": ncu["configs"],
+                 "peak": "1 warp-instr / cycle / SMSP (148 x 4 x clock)"}
+        for k in ("rowcount_kernel", "fused_kernel"):
+            v = ncu["kernels"].get(k)
+            if v:
+                issue[k] = {"issue_frac": v.get("issue_frac"), "warp_instr": v.get("warp_instr"),
+                            "thread_instr_per_config": v.get("thread_instr_per_config")}
+        if mode == me.ME_OUT_COUNT and issue.get("rowcount_kernel"):
+            roof.update({"frac": issue["rowcount_kernel"]["issue_frac"], "traffic_note": "issue fraction from ncu"})
     line = {
         "metric": "estimator configs/sec", "value": value, "unit": "configs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic",
-        "config": {"workload": args.workload, "space_configs": total, "configs_per_gpu_per_step": (job_e - job_b) // world,
-                   "per_step": "all of C5 (strong scaling)", "mode": args.mode, "chunk_configs_per_rank": CHUNK,
+        "config": {"workload": args.workload, "space_configs": total, "configs_per_gpu_per_step": total // world,
+                   "per_step": "all of C5 (strong scaling)", "mode": args.mode, "chunk_configs": CHUNK,
                    "caps_gib": sp.caps_gb, "threshold": "4/5", "l2": "flushed (256 MiB write) before every step; "
-                   "outputs (GBs per step) also exceed L2", "parallelism": f"index-space partition x{world}"
-                   + (f", {args.partition} calls of {CHUNK} configs" if world > 1 else "")},
-        "feasible_per_step": n_global // args.steps,
-        "kernel_ms_per_step": {"count": count_ms / args.steps, "scan": scan_ms / args.steps,
-                               "write": write_ms / args.steps},
+                   "outputs (GBs per step) also exceed L2",
+                   "parallelism": f"index-space partition x{world}" + (
+                       f", libme cyclic blocks of {CHUNK} configs + me_result_join (NCCL allgather, device scan)"
+                       if cyclic else (", libme even split per call" if world > 1 else ""))},
+        "feasible_per_step": surv_global,
+        "kernel_ms_per_step": {"rows_K0": rows_ms / args.steps, "scan": scan_ms / args.steps,
+                               "output_K3": out_ms / args.steps},
         "roofline": roof,
-        # per sub-range: row, stage, scan, expand kernels (COUNT: count, scan)
-        "gpu_launches": 4 * n_launch if mode != me.ME_OUT_COUNT else 2 * n_launch,
+        # per call: K0 rows, scan, K3 (COUNT: K0, scan); + the join kernel per step (N > 1)
+        "gpu_launches": (3 if mode != me.ME_OUT_COUNT else 2) * n_launch + (args.steps if cyclic else 0),
         "clocks": clocks.summary(),
     }
+    if issue:
+        line["int_issue"] = issue
+    # the other output modes on the same workload (extra keys)
+    if not args.no_modes:
+        extra = {}
+        for name in ("index", "count"):
+            if name == args.mode:
+                continue
+            m = modes[name]
+            ring = ring_for(m)
+            ms_m, tm, sl, sg = run_steps(torch, dist, me, plan, calls, m, ring, flush, stream, args.steps,
+                                         args.warmup, world, comm, cyclic, n_blocks)
+            del ring
+            extra[name] = {"value": total * args.steps / (ms_m / 1e3), "unit": "configs/s",
+                           "ms_per_step": ms_m / args.steps, "feasible_per_step": sg,
+                           "kernel_ms_per_step": {"rows_K0": sum(x[1] for x in tm) / args.steps,
+                                                  "scan": sum(x[2] for x in tm) / args.steps,
+                                                  "output_K3": sum(x[3] for x in tm) / args.steps}}
+        line["modes"] = extra
 
     # e2e: the public API with host buffers -- plan creation (host tables +
-    # H2D) and a D2H of every survivor column inside the timed region
+    # H2D) and a D2H of every survivor row inside the timed region
     if not args.no_e2e:
-        e2e_ms, h2d, d2h = e2e_run(me, sp, dev, world, comm, calls_even, mode, ncols, args.e2e_steps, stream)
+        e2e_ms, h2d, d2h = e2e_run(me, sp, dev, world, comm, calls, cyclic, n_blocks, mode, words[mode] > 0,
+                                   args.e2e_steps, stream)
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        line["e2e"] = {"value": (job_e - job_b) * args.e2e_steps / (float(t.item()) / 1e3), "unit": "configs/s",
+        line["e2e"] = {"value": total * args.e2e_steps / (float(t.item()) / 1e3), "unit": "configs/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps}
     if rank == 0 and not args.no_cpu:
         b0, e0 = unit_range(total, 0)
         line["cpu_baseline"] = cpu_baseline(sp, b0, e0)
     if comm:
+        comm.check()
         comm.destroy()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -408,30 +452,40 @@ def out_buffers(torch, me, mode, rows, **kw):
     return [flat] if mode == me.ME_OUT_RECORDS else list(flat.view(8, rows).unbind(0))
 
 
-def e2e_run(me, sp, dev, world, comm, calls, mode, ncols, steps, stream):
-    """End to end through the C ABI: host description in, host columns out."""
+def e2e_run(me, sp, dev, world, comm, calls, cyclic, n_blocks, mode, rows_out, steps, stream):
+    """End to end through the C ABI: host description in (plan creation: host
+    tables + H2D), host rows out (D2H of every survivor row of this rank)."""
     import ctypes
 
     import torch
     HOST_ROWS = 1 << 26
     host = out_buffers(torch, me, mode, HOST_ROWS, pin_memory=True)
     ring = out_buffers(torch, me, mode, CHUNK + 64, device=dev)
+    wd = 8 if mode in (me.ME_OUT_RECORDS, me.ME_OUT_FULL) else 1
     h2d = d2h = 0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
         plan = me.Plan(sp, device=dev, stream=stream.cuda_stream)
         h2d += plan.table_bytes  # enumeration tables built on the host and uploaded
+        results = []
         for (b, e) in calls:
-            r = plan.sweep(b, e, mode=mode, out_cols=ring if ncols else None, comm=comm)
+            r = plan.sweep(b, e, mode=mode, out_cols=ring if rows_out else None, comm=None if cyclic else comm,
+                           partition=me.ME_PART_CYCLIC if cyclic else me.ME_PART_EVEN)
             lo, gl, off = r.counts()
-            if ncols:
+            if rows_out:
                 arr = (ctypes.c_void_p * 8)(*([h.data_ptr() for h in host] + [None] * (8 - len(host))))
                 for first in range(0, lo, HOST_ROWS):
                     n = min(HOST_ROWS, lo - first)
                     me.check(me.lib().me_result_copy_to_host(r.h, first, n, arr), "me_result_copy_to_host")
-                d2h += lo * 8 * ncols
+                d2h += lo * 8 * wd
             d2h += 8
+            results.append(r)
+        if cyclic:
+            me.result_join(results, n_blocks, comm)
+            results[0].counts()
+            d2h += 8 * 17
+        for r in results:
             r.free()
         plan.free()
     torch.cuda.synchronize()

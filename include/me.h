@@ -153,10 +153,21 @@ typedef struct me_comm me_comm;
 typedef struct me_plan me_plan;
 typedef struct me_result me_result;
 
+/* Multi-GPU partition of a sweep (north star (3)):
+ *  ME_PART_EVEN    with comm, [begin, end) is split into nranks contiguous
+ *                  equal parts, this rank sweeps its own, and the call joins
+ *                  them (NCCL allgather of the counts: global offsets)
+ *  ME_PART_CYCLIC  this call is one block of a cyclic deal (me_cyclic_block):
+ *                  [begin, end) is swept by this rank alone with no
+ *                  collective; the blocks of a job are joined afterwards by
+ *                  one me_result_join (one allgather for all of them) */
+typedef enum { ME_PART_EVEN = 0, ME_PART_CYCLIC = 1 } me_sweep_partition;
+
 typedef struct {
     uint64_t begin, end;   /* flat index range; end = 0 -> end of the space.
-                              With comm, [begin, end) is split into nranks
-                              contiguous equal parts and this rank does its own. */
+                              With comm and ME_PART_EVEN, [begin, end) is split
+                              into nranks contiguous equal parts and this rank
+                              does its own. */
     me_out_mode mode;
     int device;            /* CUDA device ordinal (me_sweep only; a plan keeps its own) */
     void* stream;          /* cudaStream_t; NULL = the legacy default stream */
@@ -176,6 +187,8 @@ typedef struct {
      * and me_result_status() then returns ME_ERANGE. */
     uint64_t* const* out_cols;
     uint64_t out_capacity;
+    me_sweep_partition partition; /* ME_PART_EVEN (default) or ME_PART_CYCLIC */
+    uint32_t _pad2;
 } me_sweep_opts;
 
 /* me_estimate: Eq.18 and its parts for one configuration, evaluated by the same
@@ -296,6 +309,24 @@ int me_result_rank(me_result* r, uint32_t cap, uint64_t* best_index);
 int me_partition(uint64_t begin, uint64_t end, int rank, int nranks, uint64_t* lo, uint64_t* hi);
 int me_join_counts(const uint64_t* stats, int nranks, uint32_t stride, uint32_t n_cap, int rank,
                    uint64_t* offset, uint64_t* global, uint64_t* cap_global);
+
+/* Cyclic partition (a8): [begin, end) cut into n_blocks blocks of `block`
+ * indices (the last may be shorter); block q belongs to rank q mod nranks.
+ * me_cyclic_block: this rank's k-th block [lo, hi) (block q = k*nranks + rank)
+ * and the number of blocks; ME_ERANGE when the rank has no k-th block.
+ * Host-only.  Dealing whole blocks round-robin evens out the survivor density
+ * of neighbouring blocks, and no rank waits for another until the join. */
+int me_cyclic_block(uint64_t begin, uint64_t end, uint64_t block, int rank, int nranks, uint64_t k, uint64_t* lo,
+                    uint64_t* hi, uint64_t* n_blocks);
+/* The deferred join of a cyclic partition: results[k] must be the ME_PART_CYCLIC
+ * sweep of this rank's k-th block (all of this rank's blocks, one plan and
+ * stream).  COLLECTIVE over comm: one ncclAllGather of every block's counts,
+ * then an exclusive scan over the blocks in global order on the device.
+ * Asynchronous on the results' stream.  Afterwards me_result_counts gives for
+ * each result its local count, the job's global count, and the global position
+ * of its first row (rank_offset); me_result_cap_counts the job's per-capacity
+ * counts.  The results keep the join alive. */
+int me_result_join(me_result* const* results, uint32_t n, uint64_t n_blocks, me_comm* comm);
 
 /* NCCL communicator over nranks processes (one per GPU).  rank 0 creates the
  * unique id with me_comm_unique_id and the caller distributes it (e.g. with

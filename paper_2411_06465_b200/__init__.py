@@ -18,7 +18,8 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import _abi
-from ._abi import (ME_N_COLS, ME_OUT_COUNT, ME_OUT_FULL, ME_OUT_INDEX, ME_OUT_RECORDS, MEError, check, lib, me_breakdown,
+from ._abi import (ME_N_COLS, ME_OUT_COUNT, ME_OUT_FULL, ME_OUT_INDEX, ME_OUT_RECORDS, ME_PART_CYCLIC, ME_PART_EVEN,
+                   MEError, check, lib, me_breakdown,
                    me_cfg_range, me_cluster, me_model, me_model_range, me_parallel, me_sweep_opts, me_threshold)
 
 lib()  # fail at import time when libme.so is absent
@@ -292,10 +293,11 @@ class Plan:
         self.table_bytes = n.value
 
     def sweep(self, begin: int = 0, end: int = 0, mode: int = ME_OUT_FULL, out_cols=None, comm: Optional[Comm] = None,
-              gather: bool = False) -> Result:
+              gather: bool = False, partition: int = ME_PART_EVEN) -> Result:
         """me_plan_sweep.  out_cols: optional list of torch int64 device tensors
         (8 for FULL, 1 for INDEX) of equal length = capacity; RECORDS: one
-        tensor of 8 * capacity elements."""
+        tensor of 8 * capacity elements.  partition = ME_PART_CYCLIC: this call
+        is one block of a cyclic deal (see cyclic_blocks / result_join)."""
         cols_arr = None
         cap = 0
         if out_cols is not None:
@@ -303,7 +305,7 @@ class Plan:
                                                        [None] * (ME_N_COLS - len(out_cols))))
             cap = min(t.numel() for t in out_cols) // (8 if mode == ME_OUT_RECORDS else 1)
         o = me_sweep_opts(begin, end, mode, self.device, self.stream, _abi.me_alloc_fn(), _abi.me_free_fn(), None,
-                          comm.h if comm else None, 1 if gather else 0, 0, cols_arr, cap)
+                          comm.h if comm else None, 1 if gather else 0, 0, cols_arr, cap, partition, 0)
         h = ctypes.c_void_p()
         check(lib().me_plan_sweep(self.h, ctypes.byref(o), ctypes.byref(h)), "me_plan_sweep")
         return Result(h.value, self, mode, self.c.n_cap, user_cols=out_cols)
@@ -327,3 +329,26 @@ def me_sweep(sp, begin: int = 0, end: int = 0, mode: int = ME_OUT_FULL, device: 
     r = plan.sweep(begin, end, mode, comm=comm, gather=gather)
     r._plan_ref = plan
     return r
+
+
+def cyclic_blocks(begin: int, end: int, block: int, rank: int, nranks: int):
+    """a8 cyclic partition (me_cyclic_block): this rank's blocks [(lo, hi)] in
+    order (block q of [begin, end) belongs to rank q mod nranks) and the total
+    number of blocks."""
+    out, k = [], 0
+    lo, hi, nb = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    while True:
+        st = lib().me_cyclic_block(begin, end, block, rank, nranks, k, ctypes.byref(lo), ctypes.byref(hi),
+                                   ctypes.byref(nb))
+        if st == _abi.ME_ERANGE:
+            return out, nb.value
+        check(st, "me_cyclic_block")
+        out.append((lo.value, hi.value))
+        k += 1
+
+
+def result_join(results: Sequence["Result"], n_blocks: int, comm: "Comm"):
+    """a8 deferred join (me_result_join): one NCCL allgather of every block's
+    counts and the exclusive scan on the device; collective over comm."""
+    arr = (ctypes.c_void_p * max(1, len(results)))(*[r.h.value for r in results])
+    check(lib().me_result_join(arr, len(results), n_blocks, comm.h), "me_result_join")

@@ -11,6 +11,7 @@ LIB_PATH = PKG / "libme.so"
 
 ME_OK, ME_EINVAL, ME_EDIV, ME_EOVERFLOW, ME_ENOMEM, ME_ECUDA, ME_ENCCL, ME_ERANGE = range(8)
 ME_OUT_COUNT, ME_OUT_INDEX, ME_OUT_FULL, ME_OUT_RECORDS = 0, 1, 2, 3
+ME_PART_EVEN, ME_PART_CYCLIC = 0, 1
 ME_N_COLS = 8
 
 u8, u32, u64 = ctypes.c_uint8, ctypes.c_uint32, ctypes.c_uint64
@@ -57,7 +58,7 @@ class me_sweep_opts(ctypes.Structure):
     _fields_ = [("begin", u64), ("end", u64), ("mode", ctypes.c_int), ("device", ctypes.c_int),
                 ("stream", ctypes.c_void_p), ("alloc", me_alloc_fn), ("free", me_free_fn),
                 ("alloc_ctx", ctypes.c_void_p), ("comm", ctypes.c_void_p), ("gather", u32), ("_pad", u32),
-                ("out_cols", P(ctypes.c_void_p)), ("out_capacity", u64)]
+                ("out_cols", P(ctypes.c_void_p)), ("out_capacity", u64), ("partition", ctypes.c_int), ("_pad2", u32)]
 
 
 class MEError(RuntimeError):
@@ -105,6 +106,8 @@ def lib() -> ctypes.CDLL:
             "me_result_rank": ([ctypes.c_void_p, u32, P(u64)], ctypes.c_int),
             "me_result_digest": ([ctypes.c_void_p, P(u64)], ctypes.c_int),
             "me_comm_check": ([ctypes.c_void_p], ctypes.c_int),
+            "me_cyclic_block": ([u64, u64, u64, ctypes.c_int, ctypes.c_int, u64, P(u64), P(u64), P(u64)], ctypes.c_int),
+            "me_result_join": ([P(ctypes.c_void_p), u32, u64, ctypes.c_void_p], ctypes.c_int),
             "me_partition": ([u64, u64, ctypes.c_int, ctypes.c_int, P(u64), P(u64)], ctypes.c_int),
             "me_join_counts": ([P(u64), ctypes.c_int, u32, u32, ctypes.c_int, P(u64), P(u64), P(u64)], ctypes.c_int),
             "me_comm_unique_id": ([P(u8)], ctypes.c_int),
@@ -127,7 +130,7 @@ def lib() -> ctypes.CDLL:
 EXPORTS = ("me_estimate", "me_estimate_stage", "me_estimate_batch", "me_space_size", "me_decode", "me_plan_create", "me_plan_size", "me_plan_table_bytes",
            "me_plan_sweep", "me_plan_free", "me_sweep", "me_result_counts", "me_result_cap_counts",
            "me_result_columns", "me_result_copy_to_host", "me_result_status", "me_result_wait",
-           "me_result_timing", "me_result_free", "me_result_rank", "me_result_digest", "me_comm_check", "me_partition", "me_join_counts", "me_comm_unique_id", "me_comm_init", "me_comm_rank",
+           "me_result_timing", "me_result_free", "me_result_rank", "me_result_digest", "me_comm_check", "me_cyclic_block", "me_result_join", "me_partition", "me_join_counts", "me_comm_unique_id", "me_comm_init", "me_comm_rank",
            "me_comm_destroy", "me_strerror", "me_last_error_detail", "me_version")
 
 

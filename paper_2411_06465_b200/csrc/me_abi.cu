@@ -140,6 +140,30 @@ struct me_plan {
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // K0 + scan
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
+    // Survivor counts of a sweep are accumulated on the plan stream in a
+    // plan-owned slot (the result's own stats block comes from the caller's
+    // allocator on the caller's stream, so the plan stream may not touch it
+    // without waiting for everything queued there before); the caller's stream
+    // copies the slot into the result.  stat_ev[j]: that copy is done.
+    static constexpr uint32_t kStatSlots = 8;
+    uint64_t* pstats = nullptr;         // kStatSlots x 16 u64
+    cudaEvent_t stat_ev[kStatSlots] = {};
+    uint32_t stat_turn = 0;
+};
+
+// a8: the deferred join of a cyclic partition (me_result_join), shared by the
+// results it joined.  out (device): [0] global survivors, [1..8] per capacity,
+// [9..16] unused, [17 + k] global position of the first row of this rank's
+// k-th result.
+struct JoinState {
+    Alloc A;
+    uint64_t* buf = nullptr;   // gather buffer + out
+    uint64_t* out = nullptr;
+    uint32_t n = 0;            // this rank's results
+    cudaEvent_t done = nullptr;
+    int refs = 0;
+    bool resolved = false;
+    std::vector<uint64_t> host;
 };
 
 struct me_result {
@@ -165,6 +189,9 @@ struct me_result {
     cudaEvent_t ev[6] = {};
     std::vector<cudaEvent_t> tev;  // per sub-range: rows start/end, scan end, output start/end
     bool ran_count = false, ran_write = false;
+    JoinState* join = nullptr;     // set by me_result_join
+    uint32_t join_k = 0;           // this result's position in the join
+    me_sweep_partition partition = ME_PART_EVEN;
     // host-side results (valid after `resolved`)
     bool resolved = false;
     uint64_t local = 0, global = 0, offset = 0;
@@ -333,6 +360,19 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         }
         cudaEventRecord(sc.free_ev, (cudaStream_t)stream);
     }
+    P->pstats = (uint64_t*)P->A.get((size_t)me_plan::kStatSlots * 16 * 8);
+    if (!P->pstats) {
+        me_plan_free(P);
+        return err(ME_ENOMEM, "stats slots");
+    }
+    P->owned.push_back(P->pstats);
+    for (auto& x : P->stat_ev) {
+        if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) {
+            me_plan_free(P);
+            return cuda_err(cudaGetLastError(), "cudaEventCreate");
+        }
+        cudaEventRecord(x, (cudaStream_t)stream);
+    }
     if (cudaStreamCreateWithFlags(&P->cstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ready_ev, cudaEventDisableTiming) != cudaSuccess) {
         me_plan_free(P);
@@ -378,9 +418,13 @@ extern "C" void me_plan_free(me_plan* P) {
         if (P->cstream) cudaStreamSynchronize(P->cstream);
         for (auto& sc : P->scratch)
             if (sc.free_ev) cudaEventSynchronize(sc.free_ev);
+        for (auto& x : P->stat_ev)
+            if (x) cudaEventSynchronize(x);
         for (void* p : P->owned) P->A.put(p);
         for (auto& sc : P->scratch)
             if (sc.free_ev) cudaEventDestroy(sc.free_ev);
+        for (auto& x : P->stat_ev)
+            if (x) cudaEventDestroy(x);
         if (P->ready_ev) cudaEventDestroy(P->ready_ev);
         if (P->cstream) cudaStreamDestroy(P->cstream);
     }
@@ -396,6 +440,15 @@ static void result_release(me_result* R) {
     for (int i = 0; i < 6; i++)
         if (R->ev[i]) cudaEventDestroy(R->ev[i]);
     for (cudaEvent_t x : R->tev) cudaEventDestroy(x);
+    if (R->join && --R->join->refs == 0) {
+        JoinState* J = R->join;
+        if (J->done) {
+            cudaEventSynchronize(J->done);
+            cudaEventDestroy(J->done);
+        }
+        J->A.put(J->buf);
+        delete J;
+    }
     R->A.put(R->stats);
     R->A.put(R->gathered);
     if (R->own_cols)
@@ -418,10 +471,10 @@ static int resolve(me_result* R);
 // the scan on the plan stream `cs`, the output kernel on the caller's stream
 // `st`.  write = false: counts only.  Accumulates stats[0] (survivors) and
 // stats[1 + j] (per capacity); the caller orders `st` after `cs` afterwards.
-static int run_pipeline(me_plan* P, me_result* R, uint64_t b, uint64_t e, cudaStream_t cs, cudaStream_t st,
-                        me_out_mode mode, bool write, Cols cols, uint64_t capacity) {
+static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, uint64_t e, cudaStream_t cs,
+                        cudaStream_t st, me_out_mode mode, bool write, Cols cols, uint64_t capacity) {
     const HostSpace& H = P->hs;
-    if (cudaMemsetAsync(R->stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
+    if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
     const bool pipe2 = P->pipe == 2 && write;
     const auto seg_of = [&](uint64_t g) {
         return (uint32_t)(std::upper_bound(H.seg_row.begin(), H.seg_row.end(), g) - H.seg_row.begin() - 1);
@@ -468,13 +521,13 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t b, uint64_t e, cudaSt
                                   sc.rbcount, mode, cs);
             if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
             cudaEventRecord(tev[1], cs);
-            ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kStageWarps - 1) / kStageWarps, 0, sc.roff, R->stats, cs);
+            ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kStageWarps - 1) / kStageWarps, 0, sc.roff, stats, cs);
             if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
             cudaEventRecord(tev[2], cs);
             cudaStreamWaitEvent(st, tev[2], 0);
             cudaEventRecord(tev[3], st);
             ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, P->d32, sc.rck, sc.rcount,
-                               sc.roff, mode, cols, capacity, R->stats, (uint32_t)(P->sms * P->expand_bps[mode]),
+                               sc.roff, mode, cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[mode]),
                                sc.rnext, st);
             if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
             cudaEventRecord(tev[4], st);
@@ -482,17 +535,17 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t b, uint64_t e, cudaSt
             continue;
         }
         ce = launch_rowcount(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.rows, sc.st, sc.rcnt, sc.ucnt,
-                             R->stats, cs);
+                             stats, !write, cs);
         if (ce != cudaSuccess) return cuda_err(ce, "row kernel");
         cudaEventRecord(tev[1], cs);
-        ce = launch_scan(sc.ucnt, nullptr, fused_units_of(n_rows), 0, sc.uoff, R->stats, cs);
+        ce = launch_scan(sc.ucnt, nullptr, fused_units_of(n_rows), 0, sc.uoff, stats, cs);
         if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
         cudaEventRecord(tev[2], cs);
         if (write) {
             cudaStreamWaitEvent(st, tev[2], 0);
             cudaEventRecord(tev[3], st);
             ce = launch_fused(P->ds, sc.rows, sc.st, sc.rcnt, sc.ucnt, sc.uoff, n_rows, lo, hi, mode, cols, capacity,
-                              (uint32_t)(P->sms * P->fused_bps[mode]), sc.rnext, st);
+                              (uint32_t)(P->sms * P->fused_bps[mode]), sc.rnext, stats, st);
             if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
             cudaEventRecord(tev[4], st);
             cudaEventRecord(sc.free_ev, st);
@@ -515,7 +568,8 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     uint64_t b = o->begin, e = o->end ? o->end : total;
     if (e > total) e = total;
     if (b > e) b = e;
-    if (o->comm) {
+    if (o->partition != ME_PART_EVEN && o->partition != ME_PART_CYCLIC) return err(ME_EINVAL, "bad partition");
+    if (o->comm && o->partition == ME_PART_EVEN) {
         uint64_t lo = 0, hi = 0;
         me_partition(b, e, o->comm->rank, o->comm->nranks, &lo, &hi);
         b = lo;
@@ -531,8 +585,11 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     R->n_cap = P->ds.n_cap;
     R->begin = b;
     R->end = e;
-    R->comm = o->comm;
-    R->gather = o->comm && o->gather;
+    R->partition = o->partition;
+    // a CYCLIC call is one block of a cyclic deal: swept by this rank alone,
+    // joined with the others later by me_result_join
+    R->comm = o->partition == ME_PART_EVEN ? o->comm : nullptr;
+    R->gather = R->comm && o->gather;
     int rc = ME_OK;
     auto fail = [&](int s) {
         R->own_plan = false;
@@ -544,14 +601,15 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     R->stats = (uint64_t*)R->A.get(9 * 8);
     if (!R->stats) return fail(err(ME_ENOMEM, "stats allocation"));
 
-    // K0 + scan run on the plan stream, which waits for the tables, for this
-    // call's entry point on the caller's stream (the stats block was handed out
-    // there) and, per sub-range, for the output kernel that last used the
-    // scratch set; so K0 of sub-range i+1 runs while the caller's stream still
-    // writes the rows of sub-range i.
+    // K0 + scan run on the plan stream, which waits for the tables and, per
+    // sub-range, for the output kernel that last used the scratch set: K0 of
+    // sub-range i+1 (or of the next call) runs while the caller's stream still
+    // writes the rows of sub-range i.  Counts go to a plan-owned slot (see
+    // me_plan::pstats) that the caller's stream copies into the result.
     cudaStream_t cs = P->serial ? st : P->cstream;
-    cudaEventRecord(R->ev[5], st);
-    cudaStreamWaitEvent(cs, R->ev[5], 0);
+    const uint32_t slot = P->stat_turn++ % me_plan::kStatSlots;
+    uint64_t* pst = P->pstats + (size_t)slot * 16;
+    cudaStreamWaitEvent(cs, P->stat_ev[slot], 0);
     cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const int nc = n_cols_of(o->mode);
     const uint64_t len = e - b;
@@ -566,11 +624,11 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
             R->capacity = o->out_capacity;
         } else {
             // exact allocation: a counting pass first (K0 + scan; synchronises the host once)
-            if ((rc = run_pipeline(P, R, b, e, cs, st, o->mode, false, cols, 0))) return fail(rc);
+            if ((rc = run_pipeline(P, R, pst, b, e, cs, st, o->mode, false, cols, 0))) return fail(rc);
             uint64_t cnt = 0;
             cudaEventRecord(R->ev[2], cs);
             cudaStreamWaitEvent(st, R->ev[2], 0);
-            if (cudaMemcpyAsync(&cnt, R->stats, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            if (cudaMemcpyAsync(&cnt, pst, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
                 cudaStreamSynchronize(st) != cudaSuccess)
                 return fail(cuda_err(cudaGetLastError(), "count readback"));
             R->own_cols = true;
@@ -584,13 +642,16 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
         }
         for (int j = 0; j < ME_N_COLS; j++) cols.c[j] = R->cols[j];
     }
-    if ((rc = run_pipeline(P, R, b, e, cs, st, o->mode, nc != 0, cols, R->capacity))) return fail(rc);
+    if ((rc = run_pipeline(P, R, pst, b, e, cs, st, o->mode, nc != 0, cols, R->capacity))) return fail(rc);
     R->ran_count = len != 0;
     R->ran_write = nc && len;
     cudaEventRecord(R->ev[2], cs);
-    cudaStreamWaitEvent(st, R->ev[2], 0);  // stats complete before anything on the caller's stream reads them
+    cudaStreamWaitEvent(st, R->ev[2], 0);  // counts complete before the caller's stream reads them
+    if (cudaMemcpyAsync(R->stats, pst, 9 * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return fail(cuda_err(cudaGetLastError(), "stats copy"));
+    cudaEventRecord(P->stat_ev[slot], st);
     cudaEventRecord(R->ev[3], st);
-    if (o->comm) {
+    if (o->comm && o->partition == ME_PART_EVEN) {
         R->gathered = (uint64_t*)R->A.get((size_t)o->comm->nranks * 9 * 8);
         if (!R->gathered) return fail(err(ME_ENOMEM, "gather buffer"));
         ncclResult_t nr = ncclAllGather(R->stats, R->gathered, 9, ncclUint64, o->comm->nccl, st);
@@ -682,6 +743,18 @@ static int resolve(me_result* R) {
     for (int q = 0; q < 8; q++) R->caps[q] = h[1 + q];
     R->global = R->local;
     R->offset = 0;
+    if (R->join) {
+        JoinState* J = R->join;
+        if (!J->resolved) {
+            CU(cudaEventSynchronize(J->done));
+            J->host.resize(17 + (size_t)J->n);
+            CU(cudaMemcpy(J->host.data(), J->out, J->host.size() * 8, cudaMemcpyDeviceToHost));
+            J->resolved = true;
+        }
+        R->global = J->host[0];
+        for (int q = 0; q < 8; q++) R->caps[q] = J->host[1 + q];
+        R->offset = J->host[17 + R->join_k];
+    }
     if (R->comm) {
         std::vector<uint64_t> all((size_t)R->comm->nranks * 9);
         CU(cudaMemcpy(all.data(), R->gathered, all.size() * 8, cudaMemcpyDeviceToHost));
@@ -1062,6 +1135,79 @@ extern "C" int me_join_counts(const uint64_t* stats, int nranks, uint32_t stride
     }
     if (offset) *offset = off;
     if (global) *global = tot;
+    return ME_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// a8: cyclic partition + deferred join
+// ---------------------------------------------------------------------------
+extern "C" int me_cyclic_block(uint64_t begin, uint64_t end, uint64_t block, int rank, int nranks, uint64_t k,
+                               uint64_t* lo, uint64_t* hi, uint64_t* n_blocks) {
+    if (!block || nranks < 1 || rank < 0 || rank >= nranks || end < begin)
+        return err(ME_EINVAL, "bad cyclic partition arguments");
+    const uint64_t nb = (end - begin + block - 1) / block;
+    if (n_blocks) *n_blocks = nb;
+    const uint64_t q = k * (uint64_t)nranks + (uint64_t)rank;
+    if (k >= nb || q >= nb) return err(ME_ERANGE, "this rank has no such block");
+    if (lo) *lo = begin + q * block;
+    if (hi) *hi = std::min(end, begin + (q + 1) * block);
+    return ME_OK;
+}
+
+extern "C" int me_result_join(me_result* const* rs, uint32_t n, uint64_t n_blocks, me_comm* comm) {
+    if (!rs || !comm) return err(ME_EINVAL, "null argument");
+    const uint64_t N = (uint64_t)comm->nranks, r = (uint64_t)comm->rank;
+    const uint64_t mine = n_blocks > r ? (n_blocks - r + N - 1) / N : 0;
+    if (n != mine) return err(ME_EINVAL, "me_result_join needs exactly this rank's blocks of the cyclic deal");
+    const uint64_t kmax = (n_blocks + N - 1) / N;
+    me_result* R0 = n ? rs[0] : nullptr;
+    for (uint32_t k = 0; k < n; k++) {
+        if (!rs[k] || rs[k]->partition != ME_PART_CYCLIC) return err(ME_EINVAL, "results must come from CYCLIC sweeps");
+        if (rs[k]->join) return err(ME_EINVAL, "a result is already joined");
+        if (rs[k]->plan != R0->plan || rs[k]->stream != R0->stream)
+            return err(ME_EINVAL, "joined results must share a plan and stream");
+    }
+    if (!R0) return err(ME_EINVAL, "this rank has no blocks: nothing to join into");
+    DeviceGuard g(R0->plan->device);
+    cudaStream_t st = R0->stream;
+    JoinState* J = new (std::nothrow) JoinState();
+    if (!J) return err(ME_ENOMEM, "host allocation");
+    J->A = R0->A;
+    J->n = n;
+    const size_t local = (size_t)kmax * 9, all = (size_t)N * kmax * 9;
+    J->buf = (uint64_t*)J->A.get((local + all + 17 + kmax) * 8);
+    if (!J->buf) {
+        delete J;
+        return err(ME_ENOMEM, "join buffer");
+    }
+    J->out = J->buf + local + all;
+    auto bail = [&](int s) {
+        cudaStreamSynchronize(st);
+        J->A.put(J->buf);
+        if (J->done) cudaEventDestroy(J->done);
+        delete J;
+        return s;
+    };
+    if (cudaEventCreateWithFlags(&J->done, cudaEventDisableTiming) != cudaSuccess)
+        return bail(cuda_err(cudaGetLastError(), "cudaEventCreate"));
+    // this rank's per-block counts, in block order (the results' stats were
+    // written on this stream)
+    cudaError_t ce = cudaMemsetAsync(J->buf, 0, local * 8, st);
+    for (uint32_t k = 0; k < n && ce == cudaSuccess; k++)
+        ce = cudaMemcpyAsync(J->buf + (size_t)k * 9, rs[k]->stats, 72, cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess) return bail(cuda_err(ce, "join staging"));
+    ncclResult_t nr = ncclAllGather(J->buf, J->buf + local, local, ncclUint64, comm->nccl, st);
+    if (nr != ncclSuccess) return bail(err(ME_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr)));
+    ce = launch_join(J->buf + local, comm->nranks, comm->rank, (uint32_t)kmax, n_blocks, J->out, st);
+    if (ce != cudaSuccess) return bail(cuda_err(ce, "join kernel"));
+    cudaEventRecord(J->done, st);
+    for (uint32_t k = 0; k < n; k++) {
+        rs[k]->join = J;
+        rs[k]->join_k = k;
+        rs[k]->resolved = false;
+        J->refs++;
+    }
     return ME_OK;
 }
 

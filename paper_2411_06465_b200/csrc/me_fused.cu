@@ -64,16 +64,21 @@ __device__ __forceinline__ uint32_t count_fit(const uint32_t* __restrict__ su, u
 }
 
 // ---------------------------------------------------------------- K0
-template <int NCAP>
-__global__ void __launch_bounds__(256) rowcount_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows,
-                                                       const uint32_t seg_lo, const uint32_t n_seg_sub,
-                                                       const uint64_t lo, const uint64_t hi,
-                                                       RowEnt* __restrict__ rows, StEnt* __restrict__ st,
-                                                       uint32_t* __restrict__ rcnt, uint32_t* __restrict__ ucnt,
-                                                       uint64_t* __restrict__ stats) {
+// CAPS: count the survivors of every capacity too (COUNT mode; the output
+// kernel counts them from the masks it computes anyway in the other modes).
+// Blocks of kRowThreads threads at <= 64 registers, so that K0 of the next
+// sub-range fits beside the resident output-kernel blocks.
+constexpr uint32_t kRowThreads = 128;
+
+template <int NCAP, bool CAPS>
+__global__ void __launch_bounds__(kRowThreads, 8)
+    rowcount_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows, const uint32_t seg_lo,
+                    const uint32_t n_seg_sub, const uint64_t lo, const uint64_t hi, RowEnt* __restrict__ rows,
+                    StEnt* __restrict__ st, uint32_t* __restrict__ rcnt, uint32_t* __restrict__ ucnt,
+                    uint64_t* __restrict__ stats) {
     __shared__ uint32_t s_cap[NCAP];
-    if (threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
-    __syncthreads();
+    if (CAPS && threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
+    if (CAPS) __syncthreads();
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
     uint32_t capc[NCAP];
@@ -85,15 +90,18 @@ __global__ void __launch_bounds__(256) rowcount_kernel(const DevSpace S, const u
         make_row(I.M, I.tu.t, I.tu.c, I.tu.p, I.tu.d, I.L0, S.zero_stage, R);
         const bool two = S.stage_max && I.tu.p >= 2;
         RowEnt e = row_entry(I, R, two);
-        const uint32_t n_sel = 1u << S.lg_rcdo;
+        const uint32_t lg = S.lg_rcdo, n_sel = 1u << lg;
         // the row's window of the range: [a, b) of its positions
         const uint32_t a = I.rs < lo ? (uint32_t)(lo - I.rs) : 0u;
         const uint32_t b = I.rs + I.tu.w > hi ? (uint32_t)(hi - I.rs) : I.tu.w;
         const bool full = a == 0 && b == I.tu.w;
-        Digit dg[4];
-        for (uint32_t sel = 0; sel < n_sel; sel++) {
+        const uint32_t* su = S.pair_su + I.tu.pair_off;
+        const DevPair* pp = S.pairs + I.tu.pair_off;
+#pragma unroll
+        for (uint32_t sel = 0; sel < 4; sel++) {
+            if (sel >= n_sel) break;
             const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
-            Digit& c = dg[sel];
+            Digit c;
             c.ms = dopt ? R.ms1 : R.ms0;
             // per-token bytes with p in flight (paper mode): p (lam + e8) + mu + hc
             c.K = (uint64_t)I.tu.p * ((rc ? R.lam1 : R.lam0) + R.e8) + (rc ? R.bt + R.hc : R.hc);
@@ -101,38 +109,38 @@ __global__ void __launch_bounds__(256) rowcount_kernel(const DevSpace S, const u
             c.msL = c.kL = 0;
             if (two) {
                 const StEnt x = last_stage(I, rc, dopt, S.zero_stage);
-                st[(size_t)k << S.lg_rcdo | sel] = x;
+                st[(size_t)k << lg | sel] = x;
                 c.msL = x.msL;
                 c.kL = x.kL;
             }
             if (!S.gbs_mode) {
-                const uint32_t* su = S.pair_su + I.tu.pair_off;
                 const uint32_t nm = count_fit(su, I.tu.n_pairs, c, S.thr_max);
                 e.umax[sel] = nm ? __ldg(su + nm - 1) : 0u;  // u >= 1: 0 admits nothing
                 if (full) {
                     cnt += nm;
+                    if (CAPS) {
 #pragma unroll
-                    for (int q = 0; q < NCAP; q++)
-                        if (q < (int)S.n_cap) capc[q] += S.thr[q] >= S.thr_max ? nm : count_fit(su, nm, c, S.thr[q]);
+                        for (int q = 0; q < NCAP; q++)
+                            if (q < (int)S.n_cap) capc[q] += S.thr[q] >= S.thr_max ? nm : count_fit(su, nm, c, S.thr[q]);
+                    }
                 }
             }
-        }
-        if (!full || S.gbs_mode) {
-            // config by config over the window: in-flight count min(p, m) of
-            // each pair (R17), or a row cut by the range
-            const DevPair* pp = S.pairs + I.tu.pair_off;
-            for (uint32_t pos = a; pos < b; pos++) {
-                const uint32_t sel = pos & (n_sel - 1u);
-                const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
-                const DevPair pr = pp[pos >> S.lg_rcdo];
-                uint64_t tot = config_total(R, pr.u, pr.m, rc, dopt);
-                if (two) {
-                    const uint64_t tl = dg[sel].msL + (uint64_t)pr.u * dg[sel].kL;
-                    tot = tl > tot ? tl : tot;
-                }
-                cnt += tot <= S.thr_max ? 1u : 0u;
+            if (!full || S.gbs_mode) {
+                // config by config over the window's positions of this digit:
+                // in-flight count min(p, m) of each pair (R17), or a cut row
+                for (uint32_t pos = a + ((sel - a) & (n_sel - 1u)); pos < b; pos += n_sel) {
+                    const DevPair pr = pp[pos >> lg];
+                    uint64_t tot = config_total(R, pr.u, pr.m, rc, dopt);
+                    if (two) {
+                        const uint64_t tl = c.msL + (uint64_t)pr.u * c.kL;
+                        tot = tl > tot ? tl : tot;
+                    }
+                    cnt += tot <= S.thr_max ? 1u : 0u;
+                    if (CAPS) {
 #pragma unroll
-                for (int q = 0; q < NCAP; q++) capc[q] += (q < (int)S.n_cap && tot <= S.thr[q]) ? 1u : 0u;
+                        for (int q = 0; q < NCAP; q++) capc[q] += (q < (int)S.n_cap && tot <= S.thr[q]) ? 1u : 0u;
+                    }
+                }
             }
         }
         rows[k] = e;
@@ -141,14 +149,16 @@ __global__ void __launch_bounds__(256) rowcount_kernel(const DevSpace S, const u
     // survivors per 32-row unit (a unit is one warp of this kernel)
     const uint32_t unit_cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((threadIdx.x & 31) == 0 && k < n_rows) ucnt[k >> 5] = unit_cnt;
+    if (CAPS) {
 #pragma unroll
-    for (int q = 0; q < NCAP; q++) {
-        const uint32_t c = __reduce_add_sync(0xffffffffu, capc[q]);
-        if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cap + q, c);
+        for (int q = 0; q < NCAP; q++) {
+            const uint32_t c = __reduce_add_sync(0xffffffffu, capc[q]);
+            if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cap + q, c);
+        }
+        __syncthreads();
+        if (threadIdx.x < NCAP && s_cap[threadIdx.x])
+            atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
     }
-    __syncthreads();
-    if (threadIdx.x < NCAP && s_cap[threadIdx.x])
-        atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------- K3
@@ -199,11 +209,33 @@ __device__ __forceinline__ void lane_of(const DevSpace& S, const RowEnt& R, cons
 }
 
 // one row's survivors: rounds of 32 consecutive positions of its window
+// per-lane capacity counters: 16-bit fields, capacities 4j .. 4j + 3 in word j
+// (the mask bits spread to bit 16 i by one multiply); flushed per unit
+template <int NCAP>
+struct CapPack {
+    uint64_t w[(NCAP + 3) / 4];
+    __device__ __forceinline__ CapPack() {
+#pragma unroll
+        for (int j = 0; j < (NCAP + 3) / 4; j++) w[j] = 0;
+    }
+    __device__ __forceinline__ void add(uint32_t mask) {
+#pragma unroll
+        for (int j = 0; j < (NCAP + 3) / 4; j++)
+            w[j] += ((uint64_t)((mask >> (4 * j)) & 0xFu) * 0x0000200040008001ull) & 0x0001000100010001ull;
+    }
+    __device__ __forceinline__ void flush(uint32_t (&capc)[NCAP]) {
+#pragma unroll
+        for (int q = 0; q < NCAP; q++) capc[q] += (uint32_t)(w[q / 4] >> (16 * (q % 4))) & 0xFFFFu;
+#pragma unroll
+        for (int j = 0; j < (NCAP + 3) / 4; j++) w[j] = 0;
+    }
+};
+
 template <int MODE, int NCAP, bool GBS, bool STMAX>
 __device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, const StEnt* __restrict__ st,
                                           uint64_t kg, const DevPair* __restrict__ pairs, uint64_t lo, uint64_t hi,
                                           uint32_t cnt, uint64_t off, const Cols& cols, uint64_t capacity,
-                                          uint32_t lane) {
+                                          CapPack<NCAP>& pk, uint32_t lane) {
     const uint64_t rs = R.rs;
     const uint32_t w = R.w;
     const uint32_t a = rs < lo ? (uint32_t)(lo - rs) : 0u;
@@ -265,7 +297,9 @@ __device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, co
                     v[7] = tl;
                 }
             }
-            v[0] = (rs + pos) | ((uint64_t)cap_mask_n<NCAP>(S, ~v[7]) << 56);
+            const uint32_t mask = cap_mask_n<NCAP>(S, ~v[7]);
+            pk.add(mask);
+            v[0] = (rs + pos) | ((uint64_t)mask << 56);
             const uint64_t o = off + done + __popc(bal & lanes_lt);
             if (o < capacity) {
                 if (MODE == 3) {
@@ -288,7 +322,7 @@ __device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __r
                                             const uint32_t* __restrict__ ucnt, const uint64_t* __restrict__ uoff,
                                             uint32_t n_rows, uint32_t n_units, uint64_t lo, uint64_t hi,
                                             const Cols& cols, uint64_t capacity, const DevPair* pairs,
-                                            RowEnt* srow, uint32_t* next_unit) {
+                                            RowEnt* srow, uint32_t* next_unit, uint32_t (&capc)[NCAP]) {
     const uint32_t lane = threadIdx.x & 31;
     uint32_t unit = 0;
     while (true) {
@@ -317,24 +351,30 @@ __device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __r
         }
         __syncwarp();
         uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
+        CapPack<NCAP> pk;  // <= 32 rows x w / 32 survivors per lane per unit: fits 16 bits
         while (nz) {
             const uint32_t i = __ffs(nz) - 1;
             nz &= nz - 1;
             const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
             const uint64_t oi = base + (__shfl_sync(0xffffffffu, inc, i) - ci);
             fused_row<MODE, NCAP, GBS, STMAX>(S, srow[i], st, (uint64_t)k0 + i, pairs, lo, hi, ci, oi, cols,
-                                              capacity, lane);
+                                              capacity, pk, lane);
         }
+        pk.flush(capc);
     }
 }
 
+// stats[1 + j] += survivors for capacity j (one atomic per block and capacity)
 template <int MODE, int NCAP>
 __global__ void __launch_bounds__(kThreads, 2)
     fused_kernel(const DevSpace S, const RowEnt* __restrict__ rows, const StEnt* __restrict__ st,
                  const uint32_t* __restrict__ rcnt, const uint32_t* __restrict__ ucnt,
                  const uint64_t* __restrict__ uoff, const uint32_t n_rows, const uint32_t n_units, const uint64_t lo,
-                 const uint64_t hi, const Cols cols, const uint64_t capacity, uint32_t* __restrict__ next_unit) {
+                 const uint64_t hi, const Cols cols, const uint64_t capacity, uint32_t* __restrict__ next_unit,
+                 uint64_t* __restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_cap[NCAP];
+    if (threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
     DevPair* s_pairs = reinterpret_cast<DevPair*>(smem);
     RowEnt* s_rows = reinterpret_cast<RowEnt*>(smem + kPairsSmem * sizeof(DevPair));
     const bool pairs_smem = S.n_pairs <= kPairsSmem;
@@ -343,9 +383,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     const DevPair* pairs = pairs_smem ? s_pairs : S.pairs;
     RowEnt* srow = s_rows + (threadIdx.x >> 5) * kUnit;
+    uint32_t capc[NCAP];
+#pragma unroll
+    for (int q = 0; q < NCAP; q++) capc[q] = 0;
 #define ME_FUSED(GBS, STMAX)                                                                                     \
     fused_units<MODE, NCAP, GBS, STMAX>(S, rows, st, rcnt, ucnt, uoff, n_rows, n_units, lo, hi, cols, capacity, \
-                                        pairs, srow, next_unit)
+                                        pairs, srow, next_unit, capc)
     if (S.stage_max) {
         if (S.gbs_mode) ME_FUSED(true, true);
         else ME_FUSED(false, true);
@@ -354,6 +397,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         else ME_FUSED(false, false);
     }
 #undef ME_FUSED
+#pragma unroll
+    for (int q = 0; q < NCAP; q++) {
+        const uint32_t c = __reduce_add_sync(0xffffffffu, capc[q]);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cap + q, c);
+    }
+    __syncthreads();
+    if (threadIdx.x < NCAP && s_cap[threadIdx.x])
+        atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
 }
 
 constexpr size_t kFusedSmem = kPairsSmem * sizeof(DevPair) + (size_t)kFusedWarps * kUnit * sizeof(RowEnt);
@@ -372,14 +423,16 @@ void* fused_fn_(uint32_t n_cap) {
 void* fused_fn(me_out_mode mode, uint32_t n_cap) {
     return mode == ME_OUT_RECORDS ? fused_fn_<3>(n_cap) : mode == ME_OUT_FULL ? fused_fn_<2>(n_cap) : fused_fn_<1>(n_cap);
 }
-void* rowcount_fn(uint32_t n_cap) {
+template <bool CAPS>
+void* rowcount_fn_(uint32_t n_cap) {
     switch (ncap_pad3(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&rowcount_kernel<1>);
-        case 2: return reinterpret_cast<void*>(&rowcount_kernel<2>);
-        case 4: return reinterpret_cast<void*>(&rowcount_kernel<4>);
-        default: return reinterpret_cast<void*>(&rowcount_kernel<8>);
+        case 1: return reinterpret_cast<void*>(&rowcount_kernel<1, CAPS>);
+        case 2: return reinterpret_cast<void*>(&rowcount_kernel<2, CAPS>);
+        case 4: return reinterpret_cast<void*>(&rowcount_kernel<4, CAPS>);
+        default: return reinterpret_cast<void*>(&rowcount_kernel<8, CAPS>);
     }
 }
+void* rowcount_fn(uint32_t n_cap, bool caps) { return caps ? rowcount_fn_<true>(n_cap) : rowcount_fn_<false>(n_cap); }
 
 }  // namespace
 
@@ -396,23 +449,23 @@ uint32_t fused_units_of(uint32_t n_rows) { return (n_rows + kUnit - 1) / kUnit; 
 
 cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
                             uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
-                            uint64_t* stats, cudaStream_t stream) {
-    const uint32_t blocks = (n_rows + 255) / 256;
+                            uint64_t* stats, bool caps, cudaStream_t stream) {
+    const uint32_t blocks = (n_rows + kRowThreads - 1) / kRowThreads;
     void* args[] = {(void*)&S,  (void*)&g0,   (void*)&n_rows, (void*)&seg_lo, (void*)&n_seg_sub, (void*)&lo,
                     (void*)&hi, (void*)&rows, (void*)&st,     (void*)&rcnt,   (void*)&ucnt,      (void*)&stats};
-    return cudaLaunchKernel(rowcount_fn(S.n_cap), dim3(blocks ? blocks : 1), dim3(256), args, 0, stream);
+    return cudaLaunchKernel(rowcount_fn(S.n_cap, caps), dim3(blocks ? blocks : 1), dim3(kRowThreads), args, 0, stream);
 }
 
 cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,
                          const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
                          me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, uint32_t* next_unit,
-                         cudaStream_t stream) {
+                         uint64_t* stats, cudaStream_t stream) {
     const uint32_t n_units = fused_units_of(n_rows);
     const uint32_t need = (n_units + kFusedWarps - 1) / kFusedWarps;
     if (n_blocks > need) n_blocks = need ? need : 1;
     void* args[] = {(void*)&S,      (void*)&rows,    (void*)&st, (void*)&rcnt, (void*)&ucnt,
                     (void*)&uoff,   (void*)&n_rows,  (void*)&n_units, (void*)&lo, (void*)&hi,
-                    (void*)&cols,   (void*)&capacity, (void*)&next_unit};
+                    (void*)&cols,   (void*)&capacity, (void*)&next_unit, (void*)&stats};
     cudaError_t ce = cudaMemsetAsync(next_unit, 0, 4, stream);
     if (ce != cudaSuccess) return ce;
     return cudaLaunchKernel(fused_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, kFusedSmem, stream);

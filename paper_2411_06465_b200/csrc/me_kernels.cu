@@ -18,7 +18,7 @@ namespace {
 // one block: exclusive scan of the span counts into u64 offsets starting at
 // the running total stats[0]; stats[0] and stats[1 + q] accumulate the totals
 // of this sub-range
-__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__ counts, uint32_t n,
+__global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ counts, uint32_t n,
                                                     const uint32_t* __restrict__ span_caps, uint32_t n_spans,
                                                     uint32_t ncap_stride, uint32_t n_cap,
                                                     uint64_t* __restrict__ offs, uint64_t* __restrict__ stats) {
@@ -68,6 +68,59 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* __restrict__
     for (uint32_t i = lo; i < hi; i++) {
         offs[i] = run;
         run += counts[i];
+    }
+}
+
+
+// a8 deferred join: g = every rank's per-block stats (nranks x kmax x 9, rank
+// r's k-th block is global block q = k * nranks + r); out[0] = global
+// survivors, out[1..8] per capacity, out[17 + k] = global position of this
+// rank's k-th block (exclusive scan over q < n_blocks in order)
+__global__ void __launch_bounds__(1024) join_kernel(const uint64_t* __restrict__ g, uint32_t nranks, uint32_t rank,
+                                                    uint32_t kmax, uint64_t n_blocks, uint64_t* __restrict__ out) {
+    __shared__ uint64_t s_warp[32];
+    __shared__ uint64_t s_caps[8];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid < 8) s_caps[tid] = 0;
+    const uint64_t chunk = (n_blocks + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = min(n_blocks, tid * chunk), hi = min(n_blocks, lo + chunk);
+    auto row = [&](uint64_t q) { return g + ((q % nranks) * (uint64_t)kmax + q / nranks) * 9; };
+    uint64_t sum = 0, caps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t q = lo; q < hi; q++) {
+        const uint64_t* x = row(q);
+        sum += x[0];
+        for (int c = 0; c < 8; c++) caps[c] += x[1 + c];
+    }
+    __syncthreads();
+    for (int c = 0; c < 8; c++) {
+        uint64_t v = caps[c];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd((unsigned long long*)&s_caps[c], (unsigned long long)v);
+    }
+    uint64_t inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        const uint64_t v = lane < nw ? s_warp[lane] : 0;
+        uint64_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane < nw) s_warp[lane] = x - v;
+        if (lane == 31) out[0] = x;
+    }
+    __syncthreads();
+    if (tid < 8) out[1 + tid] = s_caps[tid];
+    uint64_t run = s_warp[wid] + inc - sum;
+    for (uint64_t q = lo; q < hi; q++) {
+        if (q % nranks == rank) out[17 + q / nranks] = run;
+        run += row(q)[0];
     }
 }
 
@@ -193,8 +246,14 @@ uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
 
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st) {
-    scan_kernel<<<1, 1024, 0, st>>>(span_count, n_spans, span_caps, n_spans, ncap_stride(n_cap), n_cap, span_off,
+    scan_kernel<<<1, 256, 0, st>>>(span_count, n_spans, span_caps, n_spans, ncap_stride(n_cap), n_cap, span_off,
                                     stats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_join(const uint64_t* gathered, int nranks, int rank, uint32_t kmax, uint64_t n_blocks,
+                        uint64_t* out, cudaStream_t st) {
+    join_kernel<<<1, 1024, 0, st>>>(gathered, (uint32_t)nranks, (uint32_t)rank, kmax, n_blocks, out);
     return cudaGetLastError();
 }
 

@@ -266,20 +266,24 @@ cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st
 // row-count pipeline (me_fused.cu): K0 rows [g0, g0 + n_rows) of the range
 // [lo, hi) with their survivor counts (rcnt, per 32-row unit ucnt, per
 // capacity into stats[1 + j]); K3 rows with survivors -> output rows
+// caps: K0 also counts every capacity (COUNT mode); otherwise K3 does
 cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
                             uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
-                            uint64_t* stats, cudaStream_t stream);
+                            uint64_t* stats, bool caps, cudaStream_t stream);
 cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,
                          const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
                          me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, uint32_t* next_unit,
-                         cudaStream_t stream);
+                         uint64_t* stats, cudaStream_t stream);
 int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
 uint32_t fused_units_of(uint32_t n_rows);
 // order-dependent digest of a result's rows (me_result_digest): out[0] index
 // digest, out[1] record digest (words = 8 for records, cols = FULL columns)
 cudaError_t launch_digest(const uint64_t* const* cols, uint32_t n_cols, uint32_t words, uint64_t n, uint64_t* out,
                           cudaStream_t stream);
-uint64_t digest_pow_host(uint64_t n);  // M^n mod 2^64 (merging digests of consecutive pieces)
+uint64_t digest_pow_host(uint64_t n);
+// a8 deferred join of a cyclic partition (me_result_join): see join_kernel
+cudaError_t launch_join(const uint64_t* gathered, int nranks, int rank, uint32_t kmax, uint64_t n_blocks,
+                        uint64_t* out, cudaStream_t st);  // M^n mod 2^64 (merging digests of consecutive pieces)
 // NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
 // (rank key of DESIGN.md §9); best_key / best_index initialised to ~0.
 // stride = u64 words between rows of the index column (8 for RECORDS)

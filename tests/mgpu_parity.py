@@ -1,8 +1,14 @@
-"""Multi-GPU parity (run under torchrun, one rank per GPU; launched by
-tests/test_gpu_multi.py).  Every rank sweeps its contiguous share of the space
-through the C ABI with an NCCL communicator; the allgather of counts gives
-global offsets, the optional gather gives every rank all columns.  The global
-result must equal the oracle's single-process result bit for bit."""
+"""Multi-GPU parity (run under torchrun, one rank per GPU -- also with a
+single rank, which drives the NCCL code with nranks = 1; launched by
+tests/test_gpu_multi.py).  Through the C ABI with an NCCL communicator:
+ - even partition: every rank sweeps its contiguous share; the allgather of
+   counts gives global offsets, the optional gather gives every rank all
+   columns; the collective digest of the sharded result is the digest of the
+   global result;
+ - cyclic partition (a8, bench.py's default): blocks dealt round-robin
+   (me_cyclic_block), swept alone, joined by me_result_join (one NCCL
+   allgather + a device scan).
+The global result must equal the oracle's single-process result bit for bit."""
 import os
 import sys
 from pathlib import Path
@@ -55,9 +61,38 @@ def main():
                     ok &= o == len(cat)
                     cat += l
                 ok &= np.array_equal(np.array(cat, dtype=np.uint64), ridx)
+            # the collective digest of the sharded result = the global result's
+            dg = r2.digest()
+            if rank == 0:
+                ok &= dg == (oracle.digest_of_rows(ridx, rrows)[0], 0)
+                ok &= r.digest() == oracle.digest_of_rows(ridx, rrows)
             r.free()
             r2.free()
+            # cyclic deal of blocks + one deferred join
+            for block in (1000, 7777):
+                e = end or plan.size
+                blocks, nb = me.cyclic_blocks(begin, e, block, rank, world)
+                res = [plan.sweep(lo_, hi_, mode=me.ME_OUT_RECORDS, partition=me.ME_PART_CYCLIC) for lo_, hi_ in blocks]
+                if res:
+                    me.result_join(res, nb, comm)
+                mine = []
+                for rr in res:
+                    lo3, gl3, off3 = rr.counts()
+                    mine.append((off3, gl3, rr.cap_counts(), rr.to_host()["index_mask"].tolist()))
+                parts = [None] * world
+                dist.all_gather_object(parts, mine)
+                if rank == 0:
+                    ridx, rrows, rn, rcaps = oracle.sweep(sp, begin, e, threads=4)
+                    allb = sorted(x for p_ in parts for x in p_)
+                    cat = []
+                    for off3, gl3, cc3, rows3 in allb:
+                        ok &= off3 == len(cat) and gl3 == rn and cc3 == rcaps
+                        cat += rows3
+                    ok &= np.array_equal(np.array(cat, dtype=np.uint64), ridx)
+                for rr in res:
+                    rr.free()
         plan.free()
+    comm.check()
     flag = torch.tensor([1 if ok else 0], device=f"cuda:{local}")
     dist.broadcast(flag, 0)
     comm.destroy()

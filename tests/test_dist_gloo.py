@@ -94,32 +94,30 @@ def test_bench_units_partition_space():
 
 
 def cyclic_worker(rank, world, port, space_name, chunk, q):
-    """bench.py's default N>1 partition: rank r sweeps calls r, r+N, ... alone
-    (here with the oracle), cyclic_join allgathers the per-call counts."""
+    """bench.py's default N>1 partition: rank r sweeps blocks r, r+N, ... of
+    the libme cyclic deal (me_cyclic_block) alone -- here with the oracle --
+    and the per-block counts are allgathered (gloo here; libme's
+    me_result_join does it with NCCL and a device scan on the GPU)."""
     import oracle
-    from paper_2411_06465_b200.cyclic import cyclic_calls, cyclic_join, n_calls
+    import paper_2411_06465_b200 as me
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         sp = mi.config(space_name)
         total = oracle.space_size(sp)
         for (b, e) in ((0, total), (5, total - 3)):
-            mine = cyclic_calls(b, e, chunk, rank, world)
+            mine, nq = me.cyclic_blocks(b, e, chunk, rank, world)
             idx = [oracle.sweep(sp, cb, ce)[0].tolist() for cb, ce in mine]
-            off, cnt, glob = cyclic_join([len(x) for x in idx], n_calls(b, e, chunk), world)
             parts = [None] * world
             dist.all_gather_object(parts, (mine, idx))
             if rank == 0:
                 ref_idx, _, ref_n, _ = oracle.sweep(sp, b, e)
-                nq = n_calls(b, e, chunk)
-                calls = [parts[q % world][0][q // world] for q in range(nq)]
-                got = [parts[q % world][1][q // world] for q in range(nq)]
+                calls = [parts[x % world][0][x // world] for x in range(nq)]
+                got = [parts[x % world][1][x // world] for x in range(nq)]
                 cat = [x for g in got for x in g]
-                ok = (cat == [int(x) for x in ref_idx] and glob == ref_n
+                ok = (cat == [int(x) for x in ref_idx] and len(cat) == ref_n
                       and calls[0][0] == b and calls[-1][1] == e
-                      and all(calls[i][1] == calls[i + 1][0] for i in range(nq - 1))
-                      and cnt.tolist() == [len(g) for g in got]
-                      and off.tolist() == [sum(len(g) for g in got[:i]) for i in range(nq)])
+                      and all(calls[i][1] == calls[i + 1][0] for i in range(nq - 1)))
                 q.put((b, e, ok))
         dist.barrier()
     finally:
@@ -141,13 +139,19 @@ def test_two_rank_cyclic_partition_and_join(chunk):
     assert all(ok for _, _, ok in results), results
 
 
-def test_cyclic_calls_cover_range():
-    from paper_2411_06465_b200.cyclic import cyclic_calls, n_calls
-    for b, e, chunk, world in ((0, 100, 7, 3), (5, 6, 4, 4), (3, 3, 2, 2), (0, 1 << 36, 1 << 28, 8)):
-        calls = sorted(c for r in range(world) for c in cyclic_calls(b, e, chunk, r, world))
-        assert len(calls) == n_calls(b, e, chunk)
+def test_cyclic_blocks_cover_range():
+    import paper_2411_06465_b200 as me
+    for b, e, chunk, world in ((0, 100, 7, 3), (5, 6, 4, 4), (3, 3, 2, 2), (0, 1 << 36, 1 << 28, 8), (0, 10, 3, 8)):
+        per = [me.cyclic_blocks(b, e, chunk, r, world) for r in range(world)]
+        nq = per[0][1]
+        assert nq == (-(-(e - b) // chunk) if e > b else 0)
+        calls = sorted(c for blocks, _ in per for c in blocks)
+        assert len(calls) == nq
+        for r, (blocks, _) in enumerate(per):
+            assert blocks == sorted(blocks)
+            assert all((lo - b) // chunk % world == r for lo, _ in blocks)
         if calls:
             assert calls[0][0] == b and calls[-1][1] == e
             assert all(calls[i][1] == calls[i + 1][0] for i in range(len(calls) - 1))
-    with pytest.raises(ValueError):
-        cyclic_calls(0, 10, 0, 0, 1)
+    with pytest.raises(me.MEError):
+        me.cyclic_blocks(0, 10, 0, 0, 1)
