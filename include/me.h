@@ -289,15 +289,44 @@ void me_result_free(me_result* r);
  * Synchronous. */
 int me_result_digest(me_result* r, uint64_t digest[2]);
 
-/* NEXT-2 planner (the search heuristics of P:552-593): for every
- * (model, N) segment of the plan (n_models * n_world entries, model-major),
- * the flat index of the best row of an INDEX or FULL result that is feasible
- * for capacity `cap`, or UINT64_MAX when none is.  Rank key (DESIGN.md §9,
- * reading R27): smallest t*c*p, largest micro batch (P:564,
- * P:587), smallest p (bubble (p-1)/m), smallest t (CP before TP,
- * P:580-582), recompute off, smallest index.  best_index: host array.
- * Sharded multi-GPU results must have been gathered.  Synchronous. */
-int me_result_rank(me_result* r, uint32_t cap, uint64_t* best_index);
+/* NEXT-2 planner (the search heuristics of
+ * P:552-593).  For every (model, N) segment of the plan (n_models * n_world
+ * entries, model-major), the k best rows of an INDEX, FULL or RECORDS result
+ * by the survey's rank key, smallest first:
+ *   1. class green < yellow < red (caption P:420: total <= 80% of the
+ *      capacity, <= 100%, above): green = bit green_cap of the row's capacity
+ *      mask; yellow = not green but bit yellow_cap (e.g. a second capacity
+ *      5C/4 under the 4/5 rule, = C at 100%; ME_RANK_NONE: no yellow class);
+ *      red = neither (such rows are in a result only through a third
+ *      capacity, e.g. UINT64_MAX bytes, which admits every configuration);
+ *   2. t <= gpus_per_node first (0 = no node bound);
+ *   3. smallest t*c*p; 4. largest mbs;
+ *   5. smallest p (pipeline bubble (p-1)/m); 6. smallest c;
+ *   7. smallest t; then recompute off first, then the smallest index.
+ * out: host array of n_seg * k rows, segment-major; a segment with fewer
+ * than k result rows has index = UINT64_MAX in the rest.  Each row carries its
+ * decoded configuration and the 1F1B schedule statistics:
+ * microbatches m = gbs/(d*b) (0 when gbs = 0: the paper mode has no global
+ * batch) and the bubble fraction (p-1)/m as bubble_num / bubble_den.  Sharded
+ * multi-GPU results must have been gathered.  Synchronous; scratch from the
+ * result's allocator. */
+#define ME_RANK_NONE 0xFFFFFFFFu
+typedef struct {
+    uint32_t green_cap, yellow_cap; /* capacity slots (yellow_cap may be ME_RANK_NONE) */
+    uint32_t gpus_per_node;         /* 0 = no TP <= node preference */
+    uint32_t k;                     /* rows per segment, >= 1 */
+} me_rank_opts;
+typedef struct {
+    uint64_t index;                 /* flat index, UINT64_MAX = no row */
+    uint64_t key;                   /* packed rank key (smaller is better) */
+    uint32_t model_id, world_size;
+    me_parallel cfg;
+    uint32_t cls;                   /* 0 green, 1 yellow, 2 red */
+    uint32_t microbatches;          /* m = gbs/(d*b); 0 in paper mode (gbs = 0) */
+    uint32_t bubble_num, bubble_den; /* (p - 1) / m; 0/0 in paper mode */
+    uint32_t _pad;
+} me_rank_row;
+int me_result_rank(me_result* r, const me_rank_opts* opts, me_rank_row* out);
 
 /* Host logic of the multi-GPU path (host-only, no device needed).
  * me_partition: rank's contiguous share [lo, hi) of [begin, end) with

@@ -319,3 +319,86 @@ def digest_of_rows(idx_mask, rows):
 
 def default_threads() -> int:
     return max(1, len(os.sched_getaffinity(0)))
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2 planner reference (test infrastructure): schedule statistics, the
+# 3-class colouring and the survey's ranking, restated in plain Python over
+# the oracle's own enumeration and totals.  Small spaces only.
+# ---------------------------------------------------------------------------
+
+def enumerate_configs(sp):
+    """The canonical enumeration as plain nested loops, in index
+    order: yields (index, model_id, N, dict(d, t, c, p, b, s, rc, dopt))."""
+    idx = 0
+    for mid, (h, f, L, a, k, v) in enumerate(sp.models):
+        for N in sp.world:
+            for t in range(1, N + 1):
+                if N % t:
+                    continue
+                for c in range(1, N // t + 1):
+                    if (N // t) % c:
+                        continue
+                    for p in range(1, N // t // c + 1):
+                        if (N // t // c) % p:
+                            continue
+                        d = N // (t * c * p)
+                        if k % t or v % t or f % t or p > L or (not sp.uneven and L % p):
+                            continue
+                        if (sp.max_t and t > sp.max_t) or (sp.max_c and c > sp.max_c) or (sp.max_p and p > sp.max_p):
+                            continue
+                        if sp.gpus_per_node and t > sp.gpus_per_node:
+                            continue
+                        for b in sp.mbs:
+                            for s in sp.seq:
+                                if s % c or (sp.gbs and sp.gbs % (d * b)):
+                                    continue
+                                for rc in (0, 1):
+                                    if not (sp.rc_mask >> rc) & 1:
+                                        continue
+                                    for dopt in (0, 1):
+                                        if not (sp.do_mask >> dopt) & 1:
+                                            continue
+                                        yield idx, mid, N, dict(d=d, t=t, c=c, p=p, b=b, s=s, rc=rc, dopt=dopt)
+                                        idx += 1
+
+
+def schedule_stats(gbs, d, b, p):
+    """SPEC S:226-244 / P:566-567: microbatches m = GBS/(d b), the 1F1B pipeline
+    bubble fraction (p - 1)/m as (numerator, denominator), and the per-stage
+    peak in-flight microbatches min(m, p - i)."""
+    if gbs % (d * b):
+        raise ValueError("(d b) must divide the global batch")
+    m = gbs // (d * b)
+    return m, (p - 1, m), [min(m, p - i) for i in range(p)]
+
+
+def feasibility_class(total, cap_bytes, num=4, den=5):
+    """Caption P:420 / SPEC S:325-331: 0 green (total <= num/den of the
+    capacity, ties green, R3), 1 yellow (<= the capacity), 2 red."""
+    if total * den <= cap_bytes * num:
+        return 0
+    return 1 if total <= cap_bytes else 2
+
+
+def rank(sp, cap_bytes, gpus_per_node=0, k=1, num=4, den=5):
+    """Per (model, N) segment, the k best configurations of the space by the
+    survey's key: (1) class green <
+    yellow < red, (2) t <= gpus_per_node before t > gpus_per_node (P:48-49,
+    P:564), (3) ascending t*c*p, (4) descending b,
+    (5) ascending p (bubble), (6) ascending c, (7) ascending t; then
+    recompute off first and the smallest index.  Returns {segment: [(index,
+    class, (t, c, p, b))...]} over every configuration of the space (red
+    included), segment = model_id * len(world) + world position."""
+    import dataclasses
+    everything = dataclasses.replace(sp, caps_gb=[], caps_bytes=[(1 << 64) - 1], thr_num=1, thr_den=1)
+    idx, rows, n, _ = sweep(everything, threads=default_threads())
+    totals = {int(i) & ((1 << 56) - 1): int(r[6]) for i, r in zip(idx, rows)}
+    segs = {}
+    for i, mid, N, cfg in enumerate_configs(sp):
+        cls = feasibility_class(totals[i], cap_bytes, num, den)
+        node = 1 if gpus_per_node and cfg["t"] > gpus_per_node else 0
+        key = (cls, node, cfg["t"] * cfg["c"] * cfg["p"], -cfg["b"], cfg["p"], cfg["c"], cfg["t"], cfg["rc"], i)
+        segs.setdefault(mid * len(sp.world) + sp.world.index(N), []).append(
+            (key, (i, cls, (cfg["t"], cfg["c"], cfg["p"], cfg["b"]))))
+    return {s: [x for _, x in sorted(v)[:k]] for s, v in segs.items()}

@@ -216,14 +216,28 @@ class Result:
         check(lib().me_result_copy_to_host(self.h, first, n, hp), "me_result_copy_to_host")
         return dict(zip(COLUMNS, arrays))
 
-    def rank(self, cap: int = 0) -> np.ndarray:
-        """NEXT-2: best feasible flat index per (model, N) segment for capacity
-        `cap` (me_result_rank); UINT64_MAX where none."""
+    def rank(self, green_cap: int = 0, yellow_cap: Optional[int] = None, gpus_per_node: int = 0, k: int = 1):
+        """NEXT-2 (me_result_rank): per (model, N) segment the k best rows by the
+        survey's key; a list per segment of dicts (index, class 0/1/2 = green /
+        yellow / red, t, c, p, d, b, s, rc, dopt, microbatches, bubble as
+        (p - 1, m)), rows past a segment's result rows omitted."""
         n_seg = len(self.plan.c.models) * len(self.plan.c.world)
-        out = np.zeros(n_seg, dtype=np.uint64)
-        check(lib().me_result_rank(self.h, cap, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))),
-              "me_result_rank")
-        return out
+        out = (_abi.me_rank_row * (n_seg * k))()
+        o = _abi.me_rank_opts(green_cap, _abi.ME_RANK_NONE if yellow_cap is None else yellow_cap, gpus_per_node, k)
+        check(lib().me_result_rank(self.h, ctypes.byref(o), out), "me_result_rank")
+        segs = []
+        for s_ in range(n_seg):
+            rows = []
+            for q in range(k):
+                x = out[s_ * k + q]
+                if x.index == 0xFFFFFFFFFFFFFFFF:
+                    break
+                c = x.cfg
+                rows.append(dict(index=x.index, key=x.key, cls=x.cls, model_id=x.model_id, world=x.world_size,
+                                 t=c.tp, c=c.cp, p=c.pp, d=c.dp, b=c.mbs, s=c.seq, rc=c.recompute, dopt=c.dist_opt,
+                                 microbatches=x.microbatches, bubble=(x.bubble_num, x.bubble_den)))
+            segs.append(rows)
+        return segs
 
     def digest(self):
         """(index digest, record digest) of the result's rows (me_result_digest;

@@ -61,6 +61,18 @@ class me_sweep_opts(ctypes.Structure):
                 ("out_cols", P(ctypes.c_void_p)), ("out_capacity", u64), ("partition", ctypes.c_int), ("_pad2", u32)]
 
 
+ME_RANK_NONE = 0xFFFFFFFF
+
+
+class me_rank_opts(ctypes.Structure):
+    _fields_ = [("green_cap", u32), ("yellow_cap", u32), ("gpus_per_node", u32), ("k", u32)]
+
+
+class me_rank_row(ctypes.Structure):
+    _fields_ = [("index", u64), ("key", u64), ("model_id", u32), ("world_size", u32), ("cfg", me_parallel),
+                ("cls", u32), ("microbatches", u32), ("bubble_num", u32), ("bubble_den", u32), ("_pad", u32)]
+
+
 class MEError(RuntimeError):
     def __init__(self, status: int, call: str, detail: str = ""):
         super().__init__(f"{call}: status {status} ({strerror(status)}) {detail}")
@@ -103,7 +115,7 @@ def lib() -> ctypes.CDLL:
             "me_result_wait": ([ctypes.c_void_p], ctypes.c_int),
             "me_result_timing": ([ctypes.c_void_p, P(ctypes.c_float)], ctypes.c_int),
             "me_result_free": ([ctypes.c_void_p], None),
-            "me_result_rank": ([ctypes.c_void_p, u32, P(u64)], ctypes.c_int),
+            "me_result_rank": ([ctypes.c_void_p, P(me_rank_opts), P(me_rank_row)], ctypes.c_int),
             "me_result_digest": ([ctypes.c_void_p, P(u64)], ctypes.c_int),
             "me_comm_check": ([ctypes.c_void_p], ctypes.c_int),
             "me_cyclic_block": ([u64, u64, u64, ctypes.c_int, ctypes.c_int, u64, P(u64), P(u64), P(u64)], ctypes.c_int),

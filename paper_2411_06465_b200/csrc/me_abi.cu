@@ -852,9 +852,11 @@ extern "C" int me_result_timing(me_result* R, float* ms) {
 
 extern "C" void me_result_free(me_result* R) { result_release(R); }
 
-extern "C" int me_result_rank(me_result* R, uint32_t cap, uint64_t* best_index) {
-    if (!R || !best_index) return err(ME_EINVAL, "null argument");
-    if (cap >= R->n_cap) return err(ME_EINVAL, "capacity index out of range");
+extern "C" int me_result_rank(me_result* R, const me_rank_opts* o, me_rank_row* out) {
+    if (!R || !o || !out) return err(ME_EINVAL, "null argument");
+    if (o->k < 1) return err(ME_EINVAL, "k must be >= 1");
+    if (o->green_cap >= R->n_cap || (o->yellow_cap != ME_RANK_NONE && o->yellow_cap >= R->n_cap))
+        return err(ME_EINVAL, "capacity slot out of range");
     if (R->mode == ME_OUT_COUNT) return err(ME_EINVAL, "ranking needs an INDEX, FULL or RECORDS result");
     if (R->comm && !R->gather) return err(ME_EINVAL, "ranking a sharded result needs gather = 1");
     uint64_t* cols[ME_N_COLS];
@@ -862,18 +864,42 @@ extern "C" int me_result_rank(me_result* R, uint32_t cap, uint64_t* best_index) 
     int st = me_result_columns(R, cols, &rows);
     if (st) return st;
     me_plan* P = R->plan;
+    const HostSpace& H = P->hs;
     DeviceGuard g(P->device);
-    const size_t n_seg = P->hs.seg_prefix.size() - 1;
+    const size_t n_seg = H.seg_prefix.size() - 1, m = n_seg * o->k;
     // scratch from the result's allocator, ordered on its stream
-    uint64_t* dkey = (uint64_t*)R->A.get(n_seg * 16);
-    if (!dkey) return err(ME_ENOMEM, "rank scratch");
-    uint64_t* didx = dkey + n_seg;
-    cudaError_t ce = cudaMemsetAsync(dkey, 0xFF, n_seg * 16, R->stream);
-    if (ce == cudaSuccess) ce = launch_rank(P->ds, cols[0], (uint32_t)words_of(R->mode), rows, cap, dkey, didx, R->stream);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(best_index, didx, n_seg * 8, cudaMemcpyDeviceToHost, R->stream);
+    uint64_t* keys = (uint64_t*)R->A.get((rows ? rows : 1) * 8);
+    uint64_t* sel = (uint64_t*)R->A.get(m * 8);
+    uint64_t* dout = (uint64_t*)R->A.get(m * 16);
+    std::vector<uint64_t> h(2 * m);
+    cudaError_t ce = keys && sel && dout ? cudaSuccess : cudaErrorMemoryAllocation;
+    if (ce == cudaSuccess)
+        ce = launch_rank(P->ds, cols[0], (uint32_t)words_of(R->mode), rows, o->green_cap,
+                         o->yellow_cap == ME_RANK_NONE ? 8u : o->yellow_cap, o->gpus_per_node, o->k, keys, sel, dout,
+                         R->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(h.data(), dout, m * 16, cudaMemcpyDeviceToHost, R->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(R->stream);
-    R->A.put(dkey);
+    R->A.put(keys);
+    R->A.put(sel);
+    R->A.put(dout);
+    if (ce == cudaErrorMemoryAllocation) return err(ME_ENOMEM, "rank scratch");
     if (ce != cudaSuccess) return cuda_err(ce, "me_result_rank");
+    // decode the selected rows on the host (n_seg * k of them)
+    for (size_t i = 0; i < m; i++) {
+        me_rank_row x{};
+        x.index = h[2 * i] == ~0ull ? ~0ull : (h[2 * i] & ((1ull << 56) - 1));
+        x.key = h[2 * i + 1];
+        if (x.index != ~0ull) {
+            if (H.decode(x.index, &x.model_id, &x.world_size, &x.cfg)) return err(ME_ECUDA, "rank decode");
+            x.cls = (uint32_t)(x.key >> 62);
+            if (H.gbs) {
+                x.microbatches = (uint32_t)(H.gbs / ((uint64_t)x.cfg.dp * x.cfg.mbs));
+                x.bubble_num = x.cfg.pp - 1;
+                x.bubble_den = x.microbatches;
+            }
+        }
+        out[i] = x;
+    }
     return ME_OK;
 }
 

@@ -284,11 +284,13 @@ uint64_t digest_pow_host(uint64_t n);
 // a8 deferred join of a cyclic partition (me_result_join): see join_kernel
 cudaError_t launch_join(const uint64_t* gathered, int nranks, int rank, uint32_t kmax, uint64_t n_blocks,
                         uint64_t* out, cudaStream_t st);  // M^n mod 2^64 (merging digests of consecutive pieces)
-// NEXT-2 planner: per (model, N) segment the best surviving row for capacity j
-// (rank key of DESIGN.md §9); best_key / best_index initialised to ~0.
-// stride = u64 words between rows of the index column (8 for RECORDS)
-cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint32_t stride, uint64_t n_rows, uint32_t cap,
-                        uint64_t* best_key, uint64_t* best_index, cudaStream_t st);
+// NEXT-2 planner (me_rank.cu): per result row its packed rank key (keys),
+// per segment the k best rows (sel, segment-major), their index|mask words and
+// keys (out, 2 words per selected row).  stride = u64 words between rows of the
+// index column (8 for RECORDS)
+cudaError_t launch_rank(const DevSpace& S, const uint64_t* index_col, uint32_t stride, uint64_t n_rows,
+                        uint32_t green, uint32_t yellow, uint32_t gpn, uint32_t k, uint64_t* keys, uint64_t* sel,
+                        uint64_t* out, cudaStream_t st);
 // one configuration, one stage or (stage = 0xFFFFFFFF) the largest stage (NEXT-1)
 cudaError_t launch_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,
                                   uint32_t* which, int* status, cudaStream_t st);

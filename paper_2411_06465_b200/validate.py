@@ -18,14 +18,18 @@ import numpy as np
 GIB = 1 << 30
 
 
-def classify(runs: Sequence[dict], stage_max: bool = False) -> List[dict]:
+def classify(runs: Sequence[dict]) -> List[dict]:
     """runs: dicts with model_shape (h, h_ffn, L, a, k, v), d, t, p, c, b, s,
-    optional gbs, cap_gb.  Returns the runs with total (bytes) and colour."""
-    from . import me_estimate_batch, me_estimate_stage, STAGE_ARGMAX
+    optional gbs, cap_gb.  Returns the runs with total (bytes) and colour.
+    The colours are the GPU's capacity masks (me_estimate_batch): bit j at the
+    4/5 rule = green for capacity j, at 1/1 = within capacity j."""
+    from . import me_estimate_batch
 
     shapes: List[Tuple[int, ...]] = []
     index: Dict[Tuple[int, ...], int] = {}
-    ids, cfgs, caps = [], [], []
+    ids, cfgs, slot = [], [], []
+    caps = sorted({int(r["cap_gb"]) for r in runs})
+    cap_bytes = [c * GIB for c in caps]
     for r in runs:
         key = tuple(r["model_shape"])
         if key not in index:
@@ -33,22 +37,19 @@ def classify(runs: Sequence[dict], stage_max: bool = False) -> List[dict]:
             shapes.append(key)
         ids.append(index[key])
         cfgs.append(dict(d=r["d"], t=r["t"], p=r["p"], c=r["c"], b=r["b"], s=r["s"], gbs=r.get("gbs", 0)))
-        caps.append(int(r["cap_gb"]) * GIB)
-    if stage_max:
-        totals = np.array([me_estimate_stage(shapes[i], STAGE_ARGMAX, **c)[0]["total"] for i, c in zip(ids, cfgs)],
-                          dtype=np.uint64)
-    else:
-        rows, _, status = me_estimate_batch(shapes, ids, cfgs)
-        if status.any():
-            bad = int(np.flatnonzero(status)[0])
-            raise ValueError(f"run {bad}: estimator precondition failed (status {int(status[bad])})")
-        totals = rows[:, 6]
+        slot.append(caps.index(int(r["cap_gb"])))
+    rows, m80, status = me_estimate_batch(shapes, ids, cfgs, caps_bytes=cap_bytes, thr=(4, 5))
+    if status.any():
+        bad = int(np.flatnonzero(status)[0])
+        raise ValueError(f"run {bad}: estimator precondition failed (status {int(status[bad])})")
+    _, m100, _ = me_estimate_batch(shapes, ids, cfgs, caps_bytes=cap_bytes, thr=(1, 1))
+    totals = [int(t) for t in rows[:, 6]]
+    green = [bool(m80[i] >> q & 1) for i, q in enumerate(slot)]
+    within = [bool(m100[i] >> q & 1) for i, q in enumerate(slot)]
     out = []
-    for r, tot, cap in zip(runs, totals, caps):
-        tot = int(tot)
-        # exact integer tests: green <=> total * 5 <= cap * 4 ("80% ... or less")
-        colour = "green" if tot * 5 <= cap * 4 else ("yellow" if tot <= cap else "red")
-        out.append(dict(r, total=tot, colour=colour))
+    for r, tot, g, w in zip(runs, totals, green, within):
+        colour = "green" if g else ("yellow" if w else "red")
+        out.append(dict(r, total=int(tot), colour=colour))
     return out
 
 

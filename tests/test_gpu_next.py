@@ -46,60 +46,86 @@ def test_safety_rule_confusion(me, oracle_mod):
     assert rep["rule_holds"] and rep["green_oom"] == 0 and rep["red_trained"] == 0
 
 
-def ref_rank(oracle_mod, sp, cap):
-    """NEXT-2 rank key of DESIGN.md §9 restated over the oracle's survivors."""
-    idx, rows, n, caps = oracle_mod.sweep(sp)
-    best = {}
-    for v in idx:
-        v = int(v)
-        if not (v >> (56 + cap)) & 1:
-            continue
-        i = v & ((1 << 56) - 1)
-        mid, N, cfg = oracle_mod.decode(sp, i)
-        key = (cfg["t"] * cfg["c"] * cfg["p"], -cfg["b"], cfg["p"], cfg["t"], cfg["rc"], i)
-        seg = mid * len(sp.world) + sp.world.index(N)
-        if seg not in best or key < best[seg][0]:
-            best[seg] = (key, i)
-    out = [0xFFFFFFFFFFFFFFFF] * (len(sp.models) * len(sp.world))
-    for seg, (_, i) in best.items():
-        out[seg] = i
-    return out
+def three_class(sp, C):
+    """the space swept with capacities {C, 5C/4, UINT64_MAX} under the 4/5 rule:
+    bit 0 = green (<= 80% of C), bit 1 = green or yellow (<= C), bit 2 = any
+    (red included); 4 | C makes 5C/4 * 4/5 = C exact"""
+    import dataclasses
+    assert C % 4 == 0
+    return dataclasses.replace(sp, caps_gb=[], caps_bytes=[C, 5 * C // 4, (1 << 64) - 1], thr_num=4, thr_den=5)
 
 
-@pytest.mark.parametrize("name", ["C1", "C3", "rand"])
+@pytest.mark.parametrize("name", ["C1", "C3", "rand", "a100"])
 @pytest.mark.parametrize("mode", [1, 2, 3], ids=["index", "full", "records"])
-def test_rank_matches_reference(me, oracle_mod, name, mode):
+def test_rank_matches_oracle(me, oracle_mod, name, mode):
+    """me_result_rank's top-k per segment (survey key, classes from the masks)
+    equals oracle.rank's (classes from the exact totals, plain tuple sort)."""
+    gpn = 4
     if name == "rand":
-        sp = mi.Space(models=mi.random_models(4, seed=41), world=[16, 24, 64], caps_gb=[40, 80, 192],
-                      mbs=[1, 2, 4], seq=[4096, 8192], uneven=1)
+        sp = mi.Space(models=mi.random_models(4, seed=41), world=[16, 24, 64], caps_gb=[], mbs=[1, 2, 4],
+                      seq=[4096, 8192], uneven=1)
+        C = 24 << 30
+    elif name == "a100":
+        sp = mi.Space(models=[mi.PRESETS["llama3.1-8b"]], world=[8, 16, 32, 64, 128, 256], caps_gb=[],
+                      mbs=[1, 2, 4, 8], seq=[8192], gbs=1024, rc_mask=1, do_mask=2)
+        C, gpn = 40 << 30, 8
     else:
         sp = mi.config(name)
-    plan = me.Plan(sp)
-    res = plan.sweep(mode=mode)
-    for cap in range(len(sp.caps_gb)):
-        got = res.rank(cap).tolist()
-        assert got == ref_rank(oracle_mod, sp, cap), (name, cap)
+        C = 80 << 30
+    k = 5
+    res = me.Plan(three_class(sp, C)).sweep(mode=mode)
+    got = res.rank(green_cap=0, yellow_cap=1, gpus_per_node=gpn, k=k)
+    ref = oracle_mod.rank(sp, C, gpus_per_node=gpn, k=k)
+    n_seg = len(sp.models) * len(sp.world)
+    for seg in range(n_seg):
+        g = [(r["index"], r["cls"], (r["t"], r["c"], r["p"], r["b"])) for r in got[seg]]
+        assert g == ref.get(seg, []), (name, seg)
+        for r in got[seg]:
+            if sp.gbs:
+                assert r["microbatches"] == sp.gbs // (r["d"] * r["b"])
+                assert r["bubble"] == (r["p"] - 1, r["microbatches"])
 
 
 def test_rank_picks_paper_choice(me):
-    """Llama-3.1-8B, s = 8192, A100 40 GB, 256 GPUs: the best
-    green configuration by the rank key is (TP, CP, PP, MBS) = (4, 1, 1, 1):
-    the smallest TP x CP x PP that fits, with the largest MBS that stays
-    green; the paper's fastest run there, (4, 1, 1, 2) at
-    34.21 GB, is yellow -- ranking at 100% of the capacity
-    selects it."""
-    sp = mi.Space(models=[mi.PRESETS["llama3.1-8b"]], world=[256], caps_gb=[40], mbs=[1, 2, 4, 8],
-                  seq=[8192], gbs=1024, rc_mask=1, do_mask=2, max_t=8, gpus_per_node=8)
-    plan = me.Plan(sp)
-    res = plan.sweep(mode=me.ME_OUT_INDEX)
-    best = int(res.rank(0)[0])
-    mid, N, cfg = me.me_decode(sp, best)
-    assert (cfg["t"], cfg["c"], cfg["p"], cfg["b"]) == (4, 1, 1, 1), cfg
-    import dataclasses
-    sp100 = dataclasses.replace(sp, thr_num=1, thr_den=1)
-    res = me.Plan(sp100).sweep(mode=me.ME_OUT_INDEX)
-    mid, N, cfg = me.me_decode(sp100, int(res.rank(0)[0]))
-    assert (cfg["t"], cfg["c"], cfg["p"], cfg["b"]) == (4, 1, 1, 2), cfg
+    """Llama-3.1-8B, s = 8192, A100 40 GB, GBS 1,024: at 16 GPUs the
+    top green row is (4, 1, 1, 1) (bold 194.97); at 256 GPUs
+    the paper's optimum (4, 1, 1, 2) is yellow and ranks first once
+    the yellow class counts as feasible (yellow_cap as the green slot), the
+    best green one being (4, 1, 1, 1).  (2, 1, 2, 1) has 128 microbatches on 32
+    GPUs and 16 on 256: the bubble grows 8x."""
+    sp = mi.Space(models=[mi.PRESETS["llama3.1-8b"]], world=[16, 32, 256], caps_gb=[], mbs=[1, 2, 4, 8],
+                  seq=[8192], gbs=1024, rc_mask=1, do_mask=2, max_t=8)
+    res = me.Plan(three_class(sp, 40 << 30)).sweep(mode=me.ME_OUT_INDEX)
+    top = res.rank(green_cap=0, yellow_cap=1, gpus_per_node=8, k=1)
+    assert [(r[0]["t"], r[0]["c"], r[0]["p"], r[0]["b"], r[0]["cls"]) for r in top] == [(4, 1, 1, 1, 0)] * 3
+    top100 = res.rank(green_cap=1, gpus_per_node=8, k=1)
+    assert (top100[2][0]["t"], top100[2][0]["c"], top100[2][0]["p"], top100[2][0]["b"]) == (4, 1, 1, 2)
+    allrows = res.rank(green_cap=0, yellow_cap=1, gpus_per_node=8, k=10000)
+    bub = {}
+    for seg, N in enumerate(sp.world):
+        for r in allrows[seg]:
+            if (r["t"], r["c"], r["p"], r["b"]) == (2, 1, 2, 1):
+                bub[N] = r["bubble"]
+    assert bub[32] == (1, 128) and bub[256] == (1, 16)
+
+
+def test_three_class_colouring_with_red(me, oracle_mod):
+    """all three classes of a sweep from the masks (capacities C, 5C/4 and
+    UINT64_MAX under 4/5): every configuration is in the result, red ones
+    with bit 2 only; compared with the exact totals"""
+    C = 40 << 30
+    sp = mi.Space(models=[mi.PRESETS["llama3.1-8b"], mi.PRESETS["llama2-13b"]], world=[64, 256], caps_gb=[],
+                  mbs=[1, 2, 4, 8], seq=[4096, 8192, 16384], gbs=1024)
+    sp3 = three_class(sp, C)
+    res = me.Plan(sp3).sweep(mode=me.ME_OUT_RECORDS)
+    got = res.to_host()
+    assert res.counts()[0] == oracle_mod.space_size(sp)
+    mask = got["index_mask"] >> np.uint64(56)
+    cls = np.where(mask & np.uint64(1), 0, np.where(mask & np.uint64(2), 1, 2))
+    ref = np.array([oracle_mod.feasibility_class(int(t), C) for t in got["total"]])
+    assert np.array_equal(cls, ref) and set(ref.tolist()) == {0, 1, 2}
+    idx, rows, n, caps = oracle_mod.sweep(sp3)
+    assert np.array_equal(got["index_mask"], idx)
 
 
 def test_three_class_colouring_sweep(me, oracle_mod):
