@@ -73,6 +73,17 @@ typedef struct {
     uint8_t zero_stage; /* NEXT-4, with dist_opt: 0/1 = optimizer states sharded
                            over d*c (the paper); 2 = also the FP32 gradients;
                            3 = also the BF16 weights (ZeRO-2/3, extension) */
+    /* NEXT-4 variants (extensions; 0 = the paper), DESIGN.md §3:
+     *  sp_off   1 = sequence parallelism off (R28: the attention and
+     *           FFN inputs and the RMSNorm inputs stay whole on every TP rank)
+     *  vpp      virtual pipeline stages per GPU: interleaved 1F1B with vpp
+     *           model chunks of L/(p vpp) layers (R29; needs p >= 2, p vpp | L,
+     *           no uneven split, with gbs a microbatch count divisible by p);
+     *           0 or 1 = the paper's 1F1B
+     *  w_bytes, g_bytes, o_bytes  bytes per parameter of weights, gradients,
+     *           optimizer states (R30; 0 = 2, 4, 12 of the ledger P:192-199),
+     *           e.g. FP8 weights w_bytes = 1; at most 8, 8, 16 */
+    uint8_t sp_off, vpp, w_bytes, g_bytes, o_bytes, _pad0, _pad1, _pad2;
 } me_parallel;
 
 /* Stage-0 per-GPU bytes (Eq.18 split by the ledger of P:192-199):
@@ -121,6 +132,11 @@ typedef struct {
     uint8_t recompute_mask, dist_opt_mask, allow_uneven_pp, stage_policy;
     uint32_t gbs, max_tp, max_cp, max_pp;
     uint32_t zero_stage; /* me_parallel.zero_stage of every configuration (0..3) */
+    /* me_parallel.sp_off, vpp, w_bytes, g_bytes, o_bytes of every configuration;
+     * vpp >= 2 drops the tuples with p = 1 or p vpp not dividing L (and with a
+     * global batch the (b, s) pairs whose microbatch count p does not divide)
+     * and excludes allow_uneven_pp and ME_STAGE_MAX (ME_EINVAL) */
+    uint8_t sp_off, vpp, w_bytes, g_bytes, o_bytes, _pad0, _pad1, _pad2;
 } me_cfg_range;
 
 /* Output modes of a sweep:

@@ -54,6 +54,11 @@ class Space:
     thr_den: int = 5
     stage_max: int = 0  # 1 = NEXT-1: feasibility of the largest pipeline stage
     zero_stage: int = 0  # NEXT-4: 2 / 3 = gradients / also weights sharded with the optimizer
+    sp_off: int = 0  # NEXT-4: 1 = sequence parallelism off
+    vpp: int = 0  # NEXT-4: virtual pipeline stages per GPU (interleaved 1F1B); 0/1 = off
+    wb: int = 0  # NEXT-4: bytes per parameter of weights / gradients / optimizer states (0 = 2 / 4 / 12)
+    gb: int = 0
+    ob: int = 0
     name: str = ""
     caps_bytes: Optional[List[int]] = None  # capacities given in bytes (overrides caps_gb)
 

@@ -44,7 +44,8 @@ class Model(ctypes.Structure):
 class Cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in ("d", "t", "p", "c", "b", "s", "gbs", "L0")] + [
         ("rc", ctypes.c_uint8), ("dopt", ctypes.c_uint8), ("uneven", ctypes.c_uint8),
-        ("zero", ctypes.c_uint8)]
+        ("zero", ctypes.c_uint8), ("sp_off", ctypes.c_uint8), ("vpp", ctypes.c_uint8), ("wb", ctypes.c_uint8),
+        ("gb", ctypes.c_uint8), ("ob", ctypes.c_uint8)]
 
 
 class Breakdown(ctypes.Structure):
@@ -69,7 +70,9 @@ class SpaceC(ctypes.Structure):
                 ("uneven", ctypes.c_uint8), ("stage_max", ctypes.c_uint8),
                 ("gbs", ctypes.c_uint32), ("max_t", ctypes.c_uint32), ("max_c", ctypes.c_uint32),
                 ("max_p", ctypes.c_uint32), ("thr_num", ctypes.c_uint32),
-                ("thr_den", ctypes.c_uint32), ("zero_stage", ctypes.c_uint32)]
+                ("thr_den", ctypes.c_uint32), ("zero_stage", ctypes.c_uint32),
+                ("sp_off", ctypes.c_uint8), ("vpp", ctypes.c_uint8), ("wb", ctypes.c_uint8), ("gb", ctypes.c_uint8),
+                ("ob", ctypes.c_uint8), ("_pad", ctypes.c_uint8 * 3)]
 
 
 _lib = None
@@ -137,8 +140,9 @@ def activation_per_layer(shape, s, b):
     return _scalar(lib().or_activation_per_layer, shape, s, b)
 
 
-def make_cfg(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0, zero=0) -> Cfg:
-    return Cfg(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, zero)
+def make_cfg(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0, zero=0, sp_off=0, vpp=0, wb=0, gb=0,
+             ob=0) -> Cfg:
+    return Cfg(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, zero, sp_off, vpp, wb, gb, ob)
 
 
 def first_stage_layers(shape, **cfg):
@@ -203,7 +207,9 @@ class _SpaceHolder:
         self.c = SpaceC(self.models, len(sp.models), self.world, len(sp.world), self.caps, len(cb),
                         sp.gpus_per_node, self.mbs, len(sp.mbs), self.seq, len(sp.seq),
                         sp.rc_mask, sp.do_mask, sp.uneven, getattr(sp, "stage_max", 0), sp.gbs, sp.max_t, sp.max_c,
-                        sp.max_p, sp.thr_num, sp.thr_den, getattr(sp, "zero_stage", 0))
+                        sp.max_p, sp.thr_num, sp.thr_den, getattr(sp, "zero_stage", 0),
+                        getattr(sp, "sp_off", 0), getattr(sp, "vpp", 0), getattr(sp, "wb", 0), getattr(sp, "gb", 0),
+                        getattr(sp, "ob", 0))
 
 
 def space_size(sp) -> int:
@@ -345,6 +351,8 @@ def enumerate_configs(sp):
                         d = N // (t * c * p)
                         if k % t or v % t or f % t or p > L or (not sp.uneven and L % p):
                             continue
+                        if sp.vpp >= 2 and (p < 2 or L % (p * sp.vpp)):
+                            continue
                         if (sp.max_t and t > sp.max_t) or (sp.max_c and c > sp.max_c) or (sp.max_p and p > sp.max_p):
                             continue
                         if sp.gpus_per_node and t > sp.gpus_per_node:
@@ -352,6 +360,8 @@ def enumerate_configs(sp):
                         for b in sp.mbs:
                             for s in sp.seq:
                                 if s % c or (sp.gbs and sp.gbs % (d * b)):
+                                    continue
+                                if sp.gbs and sp.vpp >= 2 and (sp.gbs // (d * b)) % p:
                                     continue
                                 for rc in (0, 1):
                                     if not (sp.rc_mask >> rc) & 1:

@@ -206,11 +206,26 @@ uint32_t or_first_stage_layers(const or_model* m, const or_cfg* c) {
     return 0;
 }
 
+/* bytes per parameter (R30): the ledger of P:192-199 unless overridden */
+static uint32_t w_bytes(const or_cfg* c) { return c->wb ? c->wb : 2; }
+static uint32_t g_bytes(const or_cfg* c) { return c->gb ? c->gb : 4; }
+static uint32_t o_bytes(const or_cfg* c) { return c->ob ? c->ob : 12; }
+
 static int cfg_check(const or_model* m, const or_cfg* c) {
     int st = model_ok(m);
     if (st) return st;
     if (!c || !c->d || !c->t || !c->p || !c->c || !c->b || !c->s) return OR_EINVAL;
     if (c->zero > 3) return OR_EINVAL;
+    if (c->sp_off > 1 || c->wb > 8 || c->gb > 8 || c->ob > 16) return OR_EINVAL;
+    /* R29 interleaved 1F1B (Megatron's schedule): p >= 2 stages of v model
+     * chunks of L/(p v) layers each, and with a global batch a number of
+     * microbatches that is a multiple of p */
+    if (c->vpp >= 2) {
+        if (c->uneven || c->L0) return OR_EINVAL;
+        if (c->p < 2 || m->L % (c->p * c->vpp)) return OR_EDIV;
+        if (c->gbs && c->gbs % ((uint64_t)c->d * c->b) == 0 && (c->gbs / ((uint64_t)c->d * c->b)) % c->p)
+            return OR_EDIV;
+    }
     /* R10: t | k (then t | a because k | a), t | v, t | h_ffn */
     if (m->k % c->t || m->v % c->t || m->f % c->t) return OR_EDIV;
     /* Eq.17: c splits the sequence */
@@ -235,16 +250,69 @@ static int cfg_check(const or_model* m, const or_cfg* c) {
  * (ZeRO): zero = 2 also divides the gradients, zero = 3 also
  * the weights, with the same ceil rule. */
 static void model_state_bytes(rat psi, const or_cfg* c, rat* params, rat* grads, rat* optim) {
-    *params = rmul(RI(2), psi);
-    *grads = rmul(RI(4), psi);
-    *optim = rmul(RI(12), psi);
+    *params = rmul(RI(w_bytes(c)), psi);
+    *grads = rmul(RI(g_bytes(c)), psi);
+    *optim = rmul(RI(o_bytes(c)), psi);
     if (c->dopt) {
         rat share = rdiv(psi, RI((i128)c->d * c->c)); /* Psi_s / (d c) */
         i128 ceil_share = (share.n + share.d - 1) / share.d;
-        *optim = rmul(RI(12), RI(ceil_share));
-        if (c->zero >= 2) *grads = rmul(RI(4), RI(ceil_share));
-        if (c->zero >= 3) *params = rmul(RI(2), RI(ceil_share));
+        *optim = rmul(RI(o_bytes(c)), RI(ceil_share));
+        if (c->zero >= 2) *grads = rmul(RI(g_bytes(c)), RI(ceil_share));
+        if (c->zero >= 3) *params = rmul(RI(w_bytes(c)), RI(ceil_share));
     }
+}
+
+/* Per-layer activation bytes on one TP x CP rank.  SP on (the paper, Eq.15 +
+ * Eq.17): sbh/(tc) (12 + 4k/a + 8 h_ffn/h).  SP off (R28: "the
+ * input to the FFN cannot be parallelized. Additionally, RMSNorm is not
+ * parallelized"): the inputs of the attention and FFN blocks and the two
+ * RMSNorm inputs (2 + 2 + 4 = 8 sbh of Eq.11-12) stay whole on every TP rank,
+ * the rest is split: sbh/c (8 + (4 + 4k/a + 8 h_ffn/h)/t). */
+static rat layer_bytes(const or_model* m, const or_cfg* c) {
+    rat sbh_c = R((i128)c->s * c->b * m->h, (i128)c->c);
+    if (!c->sp_off) return rmul(rdiv(sbh_c, RI(c->t)), eq12_bracket(m));
+    rat split = radd(radd(RI(4), rmul(RI(4), R(m->k, m->a))), rmul(RI(8), R(m->f, m->h)));
+    return rmul(sbh_c, radd(RI(8), rdiv(split, RI(c->t))));
+}
+/* one layer's input, 2sbh (kept per layer under recompute, R20): /t with SP */
+static rat layer_input_bytes(const or_model* m, const or_cfg* c) {
+    rat x = R((i128)2 * c->s * c->b * m->h, (i128)c->c);
+    return c->sp_off ? x : rdiv(x, RI(c->t));
+}
+/* the embedding input per microbatch, Eq.13 literal (R13): 8sbh, /t with SP */
+static rat embed_bytes(const or_model* m, const or_cfg* c) {
+    rat x = R((i128)8 * c->s * c->b * m->h, (i128)c->c);
+    return c->sp_off ? x : rdiv(x, RI(c->t));
+}
+/* the LM head per microbatch, Eq.14: FP32 logits 4sbv (vocab-parallel: /t)
+ * plus the output RMSNorm and linear inputs 2sbh + 2sbh (/t with SP) */
+static rat head_bytes(const or_model* m, const or_cfg* c) {
+    rat logits = R((i128)4 * c->s * c->b * m->v, (i128)c->t * c->c);
+    rat inputs = R((i128)4 * c->s * c->b * m->h, (i128)c->c);
+    return radd(logits, c->sp_off ? inputs : rdiv(inputs, RI(c->t)));
+}
+
+/* In-flight work on stage 0.  1F1B (Eq.16; R17): n_inf = p
+ * microbatches of L0 layers each, n_inf = min(p, m) with a global batch.
+ * Interleaved 1F1B (R29, Megatron's schedule with v chunks of L/(p v) layers
+ * per GPU): the first GPU runs 2(p-1) + (v-1)p warm-up forwards and one more
+ * before its first backward, so it holds p v + p - 1 chunk-microbatches (all
+ * m v of them when m = p), of which min(m, 2p) belong to chunk 0, the one
+ * with the embedding.  Returns the (layer x microbatch) count of the layer
+ * activations and the microbatch count of the embedding input. */
+static void stage0_inflight(const or_model* m, const or_cfg* c, uint32_t L0, uint64_t* layer_mb, uint64_t* embed_mb) {
+    uint64_t mb = UINT64_MAX; /* microbatches per step: unbounded in paper mode */
+    if (c->gbs) mb = c->gbs / ((uint64_t)c->d * c->b);
+    if (c->vpp < 2) {
+        uint64_t n_inf = c->p < mb ? c->p : mb;
+        *layer_mb = n_inf * L0;
+        *embed_mb = n_inf;
+        return;
+    }
+    uint64_t v = c->vpp, p = c->p;
+    uint64_t chunks = mb == p ? p * v : p * v + p - 1;
+    *layer_mb = chunks * (m->L / (p * v));
+    *embed_mb = mb < 2 * p ? mb : 2 * p;
 }
 int or_estimate(const or_model* m, const or_cfg* c, or_breakdown* out) {
     int st = cfg_check(m, c);
@@ -253,18 +321,15 @@ int or_estimate(const or_model* m, const or_cfg* c, or_breakdown* out) {
     int bad = 0;
     uint32_t L0 = or_first_stage_layers(m, c);
 
-    /* in-flight microbatches on stage 0: Eq.16 holds p; R17 caps it
-     * at m = gbs/(d b) when a global batch is given */
-    uint64_t n_inf = c->p;
-    if (c->gbs) {
-        uint64_t mb = c->gbs / ((uint64_t)c->d * c->b);
-        if (mb < n_inf) n_inf = mb;
-    }
+    /* in-flight work on stage 0: Eq.16 holds p microbatches of L0
+     * layers; R17 caps it at m = gbs/(d b); R29 interleaved 1F1B */
+    uint64_t layer_mb, embed_mb;
+    stage0_inflight(m, c, L0, &layer_mb, &embed_mb);
 
     /* model states: ledger P:192-199 (weight BF16 2 B, grad FP32 4 B, Adam
-     * master/momentum/variance FP32 4+4+4 B), sharding Eq.5 / Eq.10 (optimizer
-     * over d*c; R9: gradients not sharded), Eq.4 when the distributed optimizer
-     * is off (R21) */
+     * master/momentum/variance FP32 4+4+4 B; R30 other byte policies), sharding
+     * Eq.5 / Eq.10 (optimizer over d*c; R9: gradients not sharded), Eq.4 when
+     * the distributed optimizer is off (R21) */
     rat psi = psi_stage0(m, c->t, c->p, L0);
     uint64_t psi_s = to_u64(psi, &bad);
     rat params, grads, optim;
@@ -274,17 +339,16 @@ int or_estimate(const or_model* m, const or_cfg* c, or_breakdown* out) {
      *   sbh/(tc) * ( (12 + 4k/a + 8h_ffn/h) n_inf L0 + 8 n_inf + delta_{p,1} 4(1 + v/h) )
      * n_inf L0 = L in paper mode (R16); the 8p embedding term keeps its printed h
      * (R13); the LM-head term only at p = 1 (R14).  Recompute (R20, extension):
-     * the layer part becomes 2 n_inf L0 + (12 + 4k/a + 8h_ffn/h). */
-    rat sbh_tc = R((i128)c->s * c->b * m->h, (i128)c->t * c->c);
-    rat br = eq12_bracket(m);
+     * every layer keeps its input, plus one layer's full set.  SP off (R28):
+     * layer_bytes / embed_bytes / head_bytes above. */
     rat layers;
     if (c->rc)
-        layers = rmul(sbh_tc, radd(RI((i128)2 * n_inf * L0), br));
+        layers = radd(rmul(RI((i128)layer_mb), layer_input_bytes(m, c)), layer_bytes(m, c));
     else
-        layers = rmul(sbh_tc, rmul(br, RI((i128)n_inf * L0)));
-    rat embed = rmul(sbh_tc, RI((i128)8 * n_inf));
+        layers = rmul(RI((i128)layer_mb), layer_bytes(m, c));
+    rat embed = rmul(RI((i128)embed_mb), embed_bytes(m, c));
     rat head = RI(0);
-    if (c->p == 1) head = rmul(sbh_tc, rmul(RI(4), radd(RI(1), R(m->v, m->h))));
+    if (c->p == 1) head = head_bytes(m, c);
 
     or_breakdown r;
     r.params = to_u64(params, &bad);
@@ -337,7 +401,7 @@ uint32_t or_stage_layers(const or_model* m, const or_cfg* c, uint32_t i) {
 int or_estimate_stage(const or_model* m, const or_cfg* c, uint32_t i, or_breakdown* out) {
     int st = cfg_check(m, c);
     if (st) return st;
-    if (i >= c->p) return OR_EINVAL;
+    if (i >= c->p || c->vpp >= 2) return OR_EINVAL; /* per-stage view: non-interleaved 1F1B only */
     g_overflow = 0;
     int bad = 0;
     uint32_t Li = or_stage_layers(m, c, i);
@@ -356,12 +420,10 @@ int or_estimate_stage(const or_model* m, const or_cfg* c, uint32_t i, or_breakdo
     else if (last) psi = radd(radd(rdiv(rmul(h, v), T), h), layer_part); /* Eq.9 */
     rat params, grads, optim;
     model_state_bytes(psi, c, &params, &grads, &optim);
-    rat sbh_tc = R((i128)c->s * c->b * m->h, (i128)c->t * c->c);
-    rat br = eq12_bracket(m);
-    rat layers = c->rc ? rmul(sbh_tc, radd(RI((i128)2 * n_i * Li), br))
-                       : rmul(sbh_tc, rmul(br, RI((i128)n_i * Li)));
-    rat embed = first ? rmul(sbh_tc, RI((i128)8 * n_i)) : RI(0);
-    rat head = last ? rmul(RI((i128)n_i), rmul(sbh_tc, rmul(RI(4), radd(RI(1), R(m->v, m->h))))) : RI(0);
+    rat layers = c->rc ? radd(rmul(RI((i128)n_i * Li), layer_input_bytes(m, c)), layer_bytes(m, c))
+                       : rmul(RI((i128)n_i * Li), layer_bytes(m, c));
+    rat embed = first ? rmul(RI((i128)n_i), embed_bytes(m, c)) : RI(0);
+    rat head = last ? rmul(RI((i128)n_i), head_bytes(m, c)) : RI(0);
     or_breakdown r;
     r.params = to_u64(params, &bad);
     r.grads = to_u64(grads, &bad);
@@ -428,6 +490,7 @@ static int build_tuples(const or_space* sp, uint32_t N, tuplist* out) {
                         uint32_t b = sp->mbs[bi], s = sp->seq[si];
                         if (s % c) continue;
                         if (sp->gbs && sp->gbs % ((uint64_t)d * b)) continue;
+                        if (sp->gbs && sp->vpp >= 2 && (sp->gbs / ((uint64_t)d * b)) % p) continue; /* R29 */
                         pairs++;
                     }
                 if (n == cap) {
@@ -451,6 +514,7 @@ static int valid_static(const or_space* sp, const or_model* m, const tup* u) {
     if (m->k % u->t || m->v % u->t || m->f % u->t) return 0;
     if (u->p > m->L) return 0;
     if (!sp->uneven && m->L % u->p) return 0;
+    if (sp->vpp >= 2 && (u->p < 2 || m->L % (u->p * sp->vpp))) return 0; /* R29 */
     if (sp->max_t && u->t > sp->max_t) return 0;
     if (sp->max_c && u->c > sp->max_c) return 0;
     if (sp->max_p && u->p > sp->max_p) return 0;
@@ -464,6 +528,8 @@ static int space_ok(const or_space* sp) {
         return OR_EINVAL;
     if (sp->n_caps > 8 || (sp->n_caps && !sp->cap_bytes)) return OR_EINVAL;
     if (!(sp->rc_mask & 3) || !(sp->do_mask & 3) || sp->zero_stage > 3) return OR_EINVAL;
+    if (sp->sp_off > 1 || sp->wb > 8 || sp->gb > 8 || sp->ob > 16) return OR_EINVAL;
+    if (sp->vpp >= 2 && (sp->uneven || sp->stage_max)) return OR_EINVAL;
     if (!sp->thr_num || !sp->thr_den || sp->thr_num > 1024 || sp->thr_den > 1024) return OR_EINVAL;
     for (uint32_t i = 0; i < sp->n_models; i++)
         if (model_ok(&sp->models[i])) return OR_EINVAL;
@@ -583,6 +649,7 @@ static void walk(walk_t* w) {
                         uint32_t b = sp->mbs[bi], s = sp->seq[si];
                         if (s % u->c) continue;
                         if (sp->gbs && sp->gbs % ((uint64_t)u->d * b)) continue;
+                        if (sp->gbs && sp->vpp >= 2 && (sp->gbs / ((uint64_t)u->d * b)) % u->p) continue;
                         for (uint32_t rc = 0; rc < 2; rc++) {
                             if (!((sp->rc_mask >> rc) & 1)) continue;
                             for (uint32_t dopt = 0; dopt < 2; dopt++) {
@@ -595,6 +662,11 @@ static void walk(walk_t* w) {
                                     c.rc = (uint8_t)rc; c.dopt = (uint8_t)dopt;
                                     c.uneven = sp->uneven;
                                     c.zero = (uint8_t)sp->zero_stage;
+                                    c.sp_off = sp->sp_off;
+                                    c.vpp = sp->vpp;
+                                    c.wb = sp->wb;
+                                    c.gb = sp->gb;
+                                    c.ob = sp->ob;
                                     if (w->decode_only) {
                                         w->dec_model = mi;
                                         w->dec_world = sp->world[ni];
@@ -668,6 +740,7 @@ int or_points(const or_space* sp, const uint64_t* points, uint64_t n, or_breakdo
                         uint32_t b = sp->mbs[bi], s = sp->seq[si];
                         if (s % u->c) continue;
                         if (sp->gbs && sp->gbs % ((uint64_t)u->d * b)) continue;
+                        if (sp->gbs && sp->vpp >= 2 && (sp->gbs / ((uint64_t)u->d * b)) % u->p) continue;
                         for (uint32_t rc = 0; rc < 2; rc++) {
                             if (!((sp->rc_mask >> rc) & 1)) continue;
                             for (uint32_t dopt = 0; dopt < 2; dopt++) {
@@ -680,6 +753,11 @@ int or_points(const or_space* sp, const uint64_t* points, uint64_t n, or_breakdo
                                     c.rc = (uint8_t)rc; c.dopt = (uint8_t)dopt;
                                     c.uneven = sp->uneven;
                                     c.zero = (uint8_t)sp->zero_stage;
+                                    c.sp_off = sp->sp_off;
+                                    c.vpp = sp->vpp;
+                                    c.wb = sp->wb;
+                                    c.gb = sp->gb;
+                                    c.ob = sp->ob;
                                     or_breakdown r;
                                     st = sp->stage_max ? or_estimate_max(m, &c, &r, NULL)
                                                        : or_estimate(m, &c, &r);

@@ -51,6 +51,14 @@ typedef struct {
     uint8_t zero;     /* NEXT-4 (extension): with dopt, 0/1 = optimizer states
                          sharded over d*c (the paper, ZeRO stage 1); 2 = also the
                          FP32 gradients; 3 = also the BF16 weights (ZeRO-2/3) */
+    /* NEXT-4 variants (extensions, DESIGN.md §3 R28-R30); 0 = the paper */
+    uint8_t sp_off;   /* 1 = sequence parallelism off (the FFN input
+                         and the RMSNorms are then not parallelized) */
+    uint8_t vpp;      /* virtual pipeline stages per GPU (interleaved 1F1B);
+                         0 or 1 = the paper's non-interleaved 1F1B */
+    uint8_t wb, gb, ob; /* bytes per parameter of weights, gradients and
+                         optimizer states (ledger P:192-199: 2, 4, 12; 0 =
+                         that default), e.g. FP8 weights wb = 1 */
 } or_cfg;
 
 /* Eq.18 split into the ledger of P:192-199 and the three activation groups. */
@@ -71,6 +79,7 @@ typedef struct {
     uint32_t gbs, max_t, max_c, max_p;           /* 0 = unlimited */
     uint32_t thr_num, thr_den;                   /* feasible <=> total*den <= cap*num */
     uint32_t zero_stage;                         /* or_cfg.zero of every configuration */
+    uint8_t sp_off, vpp, wb, gb, ob, _pad[3];    /* or_cfg's NEXT-4 fields of every configuration */
 } or_space;
 
 /* Eq.1, Eq.2, Eq.3 */

@@ -33,8 +33,9 @@ def version() -> str:
     return lib().me_version().decode()
 
 
-def _parallel(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0, zero=0) -> me_parallel:
-    return me_parallel(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, zero)
+def _parallel(d, t, p, c, b, s, gbs=0, L0=0, rc=0, dopt=1, uneven=0, zero=0, sp_off=0, vpp=0, wb=0, gb=0,
+              ob=0) -> me_parallel:
+    return me_parallel(d, t, p, c, b, s, gbs, L0, rc, dopt, uneven, zero, sp_off, vpp, wb, gb, ob)
 
 
 def me_estimate(shape, **cfg) -> Dict[str, int]:
@@ -90,7 +91,9 @@ class _SpaceC:
         self.cl = me_cluster(self.world, len(sp.world), self.caps, len(cb), sp.gpus_per_node)
         self.cr = me_cfg_range(self.mbs, len(sp.mbs), self.seq, len(sp.seq), sp.rc_mask, sp.do_mask, sp.uneven,
                                getattr(sp, "stage_max", 0),
-                               sp.gbs, sp.max_t, sp.max_c, sp.max_p, getattr(sp, "zero_stage", 0))
+                               sp.gbs, sp.max_t, sp.max_c, sp.max_p, getattr(sp, "zero_stage", 0),
+                               getattr(sp, "sp_off", 0), getattr(sp, "vpp", 0), getattr(sp, "wb", 0),
+                               getattr(sp, "gb", 0), getattr(sp, "ob", 0))
         self.thr = me_threshold(sp.thr_num, sp.thr_den)
         self.n_cap = len(cb)
 
@@ -110,6 +113,9 @@ def me_decode(sp, index: int):
                           ctypes.byref(world), ctypes.byref(out)), "me_decode")
     cfg = dict(d=out.dp, t=out.tp, p=out.pp, c=out.cp, b=out.mbs, s=out.seq, gbs=out.gbs, rc=out.recompute,
                dopt=out.dist_opt)
+    for k in ("sp_off", "vpp"):
+        if getattr(out, k):
+            cfg[k] = getattr(out, k)
     return mid.value, world.value, cfg
 
 

@@ -24,7 +24,8 @@ class me_model(ctypes.Structure):
 
 class me_parallel(ctypes.Structure):
     _fields_ = [(n, u32) for n in ("dp", "tp", "pp", "cp", "mbs", "seq", "gbs", "first_stage_layers")] + [
-        ("recompute", u8), ("dist_opt", u8), ("allow_uneven_pp", u8), ("zero_stage", u8)]
+        ("recompute", u8), ("dist_opt", u8), ("allow_uneven_pp", u8), ("zero_stage", u8)] + [
+        (n, u8) for n in ("sp_off", "vpp", "w_bytes", "g_bytes", "o_bytes", "_pad0", "_pad1", "_pad2")]
 
 
 class me_breakdown(ctypes.Structure):
@@ -47,7 +48,8 @@ class me_cluster(ctypes.Structure):
 class me_cfg_range(ctypes.Structure):
     _fields_ = [("mbs", P(u32)), ("n_mbs", u32), ("seq", P(u32)), ("n_seq", u32),
                 ("recompute_mask", u8), ("dist_opt_mask", u8), ("allow_uneven_pp", u8), ("stage_policy", u8),
-                ("gbs", u32), ("max_tp", u32), ("max_cp", u32), ("max_pp", u32), ("zero_stage", u32)]
+                ("gbs", u32), ("max_tp", u32), ("max_cp", u32), ("max_pp", u32), ("zero_stage", u32)] + [
+        (n, u8) for n in ("sp_off", "vpp", "w_bytes", "g_bytes", "o_bytes", "_pad0", "_pad1", "_pad2")]
 
 
 me_alloc_fn = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)

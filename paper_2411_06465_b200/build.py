@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libme.so"
-SOURCES = ["me_space.cpp", "me_kernels.cu", "me_rows.cu", "me_fused.cu", "me_digest.cu", "me_rank.cu", "me_abi.cu"]
+SOURCES = ["me_space.cpp", "me_kernels.cu", "me_fused.cu", "me_digest.cu", "me_rank.cu", "me_abi.cu"]
 HEADERS = ["me_space.hpp", "me_kernels.cuh", "me_dev.cuh"]
 
 

@@ -114,29 +114,15 @@ struct me_plan {
     struct Scratch {
         RowEnt* rows = nullptr;         // the sub-range's rows
         StEnt* st = nullptr;            // their last-stage terms per digit (stage_max)
-        uint32_t* rcnt = nullptr;       // pipe 3: survivors per row
-        uint32_t* ucnt = nullptr;       // pipe 3: survivors per 32-row unit
-        uint64_t* uoff = nullptr;       // pipe 3: output row of each unit's first survivor
-        // descriptor pipeline (pipe 2)
-        uint2* rck = nullptr;           // span checkpoints {row, offset}
-        uint64_t* desc = nullptr;       // survivor descriptors, span_len slots per span
-        uint32_t* rcount = nullptr;     // survivors per span
-        uint32_t* rbcount = nullptr;    // survivors per stage-kernel block (kStageWarps spans)
-        uint64_t* roff = nullptr;       // output row of each block's first survivor
-        uint32_t* rnext = nullptr;      // output kernel: next unit / span to take
+        uint32_t* rcnt = nullptr;       // survivors per row
+        uint32_t* ucnt = nullptr;       // survivors per 32-row unit
+        uint64_t* uoff = nullptr;       // output row of each unit's first survivor
+        uint32_t* rnext = nullptr;      // output kernel: next unit to take
         cudaEvent_t free_ev = nullptr;  // recorded after the kernel that last used the set
     } scratch[kMaxSets];
     uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
-    // 3 = row-count pipeline (K0 rows + counts, scan, K3 fused test+compact+
-    // store; default), 2 = descriptor pipeline (K0 rows, K1 stage kernel
-    // writing survivor descriptors, scan, K3 expand; ME_PIPE=2).  COUNT mode
-    // is K0 + scan of pipe 3 in both.
-    uint32_t pipe = 3;
-    uint32_t rspan_tiles = 16;          // pipe 2: tiles per K1 span (ME_ROWS_SPAN)
-    uint32_t max_rspans = 0, max_rows = 0;
-    uint32_t d32 = 0;                   // pipe 2: 32-bit survivor descriptors
-    int expand_bps[4] = {0, 0, 0, 0};   // pipe 2: co-resident K3 blocks per SM per output mode
-    int fused_bps[4] = {0, 0, 0, 0};    // pipe 3: resident K3 blocks per SM per output mode
+    uint32_t max_rows = 0;              // rows per sub-range
+    int fused_bps[4] = {0, 0, 0, 0};    // resident K3 blocks per SM per output mode
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // K0 + scan
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
@@ -279,6 +265,14 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.gbs_mode = H.gbs ? 1u : 0u;
     D.stage_max = H.stage_max ? 1u : 0u;
     D.zero_stage = H.zero_stage;
+    {
+        const Policy Q = make_policy(H.zero_stage, H.sp_off, H.vpp, H.wb, H.gb, H.ob);
+        D.sp_off = Q.sp_off;
+        D.vpp = Q.vpp;
+        D.wb = Q.wb;
+        D.gb = Q.gb;
+        D.ob = Q.ob;
+    }
     for (int q = 0; q < 8; q++) D.thr[q] = 0, D.thr1[q] = 1, D.cslot[q] = (uint32_t)q;
     D.thr_max = 0;
     uint32_t q_max = 0;
@@ -292,33 +286,13 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     for (int k = 0; k < 8; k++) D.thr1c[k] = D.thr1[D.cslot[k]];
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
-    if (const char* e = getenv("ME_PIPE")) P->pipe = atoi(e) == 2 ? 2u : 3u;
-    if (const char* e = getenv("ME_ROWS_SPAN")) P->rspan_tiles = (uint32_t)atoi(e);
-    if (P->rspan_tiles < 1) P->rspan_tiles = 1;
-    {
-        const uint64_t eff = H.total + 64 < kMaxSub ? H.total + 64 : kMaxSub;
-        const uint32_t eff_tiles = n_tiles_of(31, 31 + eff) + 1;
-        P->max_rspans = (eff_tiles + P->rspan_tiles - 1) / P->rspan_tiles + 1;
-        P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
-        // (tests: a small cap exercises the cutting of sub-ranges by rows; >= 64
-        // so that the < 32 rows before a pipe-2 sub-range's first index fit)
-        if (const char* e = getenv("ME_MAX_ROWS")) P->max_rows = std::min(P->max_rows, (uint32_t)std::max(64, atoi(e)));
-        if (P->max_rows < 1) P->max_rows = 1;
-        // a span of L positions touches at most ceil(L / min_w) + 1 rows
-        uint64_t min_w = UINT64_MAX;
-        for (uint32_t t : H.list_tuple) min_w = std::min<uint64_t>(min_w, H.tuples[t].w);
-        const uint64_t L = (uint64_t)P->rspan_tiles * kTile;
-        P->d32 = L <= 65536 && min_w != UINT64_MAX && (L + min_w - 1) / min_w + 1 <= 256 ? 1u : 0u;
-        if (const char* e = getenv("ME_DESC64")) P->d32 = atoi(e) ? 0u : P->d32;
-    }
-    // pipe 2 K3 grid: 2 blocks per SM saturate HBM and leave registers for the
-    // overlapped K1 of the next sub-range
-    int ebps = 2;
-    if (const char* e = getenv("ME_EXPAND_BPS")) ebps = std::max(1, atoi(e));
+    P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
+    // (tests: a small cap exercises the cutting of sub-ranges by rows)
+    if (const char* e = getenv("ME_MAX_ROWS")) P->max_rows = std::min(P->max_rows, (uint32_t)std::max(1, atoi(e)));
+    if (P->max_rows < 1) P->max_rows = 1;
     int fbps = 0;  // 0 = as many as fit
     if (const char* e = getenv("ME_FUSED_BPS")) fbps = std::max(1, atoi(e));
     for (int m = 1; m < 4; m++) {
-        if (P->pipe == 2) P->expand_bps[m] = std::min(expand_blocks_per_sm((me_out_mode)m, D.n_cap), ebps);
         const int fb = fused_blocks_per_sm((me_out_mode)m, D.n_cap);
         P->fused_bps[m] = fbps ? std::min(fb, fbps) : fb;
     }
@@ -334,17 +308,6 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         for (void* x : {(void*)sc.rows, (void*)sc.rcnt, (void*)sc.ucnt, (void*)sc.uoff, (void*)sc.rnext})
             P->owned.push_back(x);
         bool ok = sc.rows && sc.rcnt && sc.ucnt && sc.uoff && sc.rnext;
-        if (P->pipe == 2) {
-            const size_t span_len = (size_t)P->rspan_tiles * kTile;
-            sc.rck = (uint2*)P->A.get((size_t)P->max_rspans * 8);
-            sc.desc = (uint64_t*)P->A.get((size_t)P->max_rspans * span_len * 8);
-            sc.rcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
-            sc.roff = (uint64_t*)P->A.get((size_t)P->max_rspans * 8);
-            sc.rbcount = (uint32_t*)P->A.get((size_t)P->max_rspans * 4);
-            for (void* x : {(void*)sc.rck, (void*)sc.desc, (void*)sc.rcount, (void*)sc.roff, (void*)sc.rbcount})
-                P->owned.push_back(x);
-            ok = ok && sc.rck && sc.desc && sc.rcount && sc.roff && sc.rbcount;
-        }
         if (H.stage_max) {
             sc.st = (StEnt*)P->A.get((size_t)P->max_rows * H.n_rcdo * sizeof(StEnt));
             P->owned.push_back(sc.st);
@@ -467,33 +430,25 @@ static uint64_t words_of(me_out_mode m) { return m == ME_OUT_RECORDS ? ME_N_COLS
 static int resolve(me_result* R);
 
 // One pass of the hot path over [b, e): sub-ranges of at most
-// kMaxSub indices and max_rows rows; per sub-range K0 (+ K1 for pipe 2) and
-// the scan on the plan stream `cs`, the output kernel on the caller's stream
+// kMaxSub indices and max_rows rows; per sub-range K0 and the scan on the plan
+// stream `cs`, the output kernel K3 on the caller's stream
 // `st`.  write = false: counts only.  Accumulates stats[0] (survivors) and
 // stats[1 + j] (per capacity); the caller orders `st` after `cs` afterwards.
 static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, uint64_t e, cudaStream_t cs,
                         cudaStream_t st, me_out_mode mode, bool write, Cols cols, uint64_t capacity) {
     const HostSpace& H = P->hs;
     if (cudaMemsetAsync(stats, 0, 9 * 8, cs) != cudaSuccess) return cuda_err(cudaGetLastError(), "memset");
-    const bool pipe2 = P->pipe == 2 && write;
     const auto seg_of = [&](uint64_t g) {
         return (uint32_t)(std::upper_bound(H.seg_row.begin(), H.seg_row.end(), g) - H.seg_row.begin() - 1);
     };
     for (uint64_t lo = b, hi = b; lo < e; lo = hi) {
         hi = e - lo < kMaxSub ? e : lo + kMaxSub;
-        uint64_t g0;
-        if (pipe2) {
-            // the sub-range also holds at most max_rows rows (the rows covering
-            // [lo & ~31, lo) are < 32 and max_rows >= 64)
-            g0 = H.row_of(lo & ~31ull);
-        } else {
-            // sub-ranges end at row boundaries: only the call's own first and
-            // last rows can be cut
-            g0 = H.row_of(lo);
-            if (hi < e) {
-                const uint64_t cut = H.row_start(H.row_of(hi));
-                if (cut > lo) hi = cut;
-            }
+        // sub-ranges end at row boundaries: only the call's own first and last
+        // rows can be cut
+        const uint64_t g0 = H.row_of(lo);
+        if (hi < e) {
+            const uint64_t cut = H.row_start(H.row_of(hi));
+            if (cut > lo) hi = cut;
         }
         if (H.row_of(hi - 1) + 1 - g0 > P->max_rows) {
             const uint64_t cut = H.row_start(g0 + P->max_rows);
@@ -512,28 +467,6 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
         cudaStreamWaitEvent(cs, sc.free_ev, 0);
         cudaEventRecord(tev[0], cs);
         cudaError_t ce;
-        if (pipe2) {
-            const uint32_t n_tiles = n_tiles_of(lo, hi);
-            const uint32_t n_rsp = (n_tiles + P->rspan_tiles - 1) / P->rspan_tiles;
-            ce = launch_rows(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, P->rspan_tiles, sc.rows, sc.st, sc.rck, cs);
-            if (ce == cudaSuccess)
-                ce = launch_stage(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.rck, sc.desc, P->d32, sc.rcount,
-                                  sc.rbcount, mode, cs);
-            if (ce != cudaSuccess) return cuda_err(ce, "row / stage kernel");
-            cudaEventRecord(tev[1], cs);
-            ce = launch_scan(sc.rbcount, nullptr, (n_rsp + kStageWarps - 1) / kStageWarps, 0, sc.roff, stats, cs);
-            if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
-            cudaEventRecord(tev[2], cs);
-            cudaStreamWaitEvent(st, tev[2], 0);
-            cudaEventRecord(tev[3], st);
-            ce = launch_expand(P->ds, sc.rows, sc.st, lo, hi, P->rspan_tiles, sc.desc, P->d32, sc.rck, sc.rcount,
-                               sc.roff, mode, cols, capacity, stats, (uint32_t)(P->sms * P->expand_bps[mode]),
-                               sc.rnext, st);
-            if (ce != cudaSuccess) return cuda_err(ce, "expand kernel");
-            cudaEventRecord(tev[4], st);
-            cudaEventRecord(sc.free_ev, st);
-            continue;
-        }
         ce = launch_rowcount(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.rows, sc.st, sc.rcnt, sc.ucnt,
                              stats, !write, cs);
         if (ce != cudaSuccess) return cuda_err(ce, "row kernel");

@@ -45,6 +45,11 @@ __device__ __forceinline__ uint32_t upper_bound_u64(const uint64_t* __restrict__
     return lo;
 }
 
+// the space's variant policy (me_cfg_range)
+__device__ __forceinline__ Policy policy_of(const DevSpace& S) {
+    return Policy{S.zero_stage, S.sp_off, S.vpp, S.wb, S.gb, S.ob};
+}
+
 // The row of sub-range table entry k (global row g): segment by binary search
 // over the segments of the sub-range, then its model, tuple and first index.
 struct RowId {
@@ -76,8 +81,9 @@ __device__ __forceinline__ RowEnt row_entry(const RowId& I, const RowCoef& R, bo
     e.pair_off = I.tu.pair_off;
     e.p = I.tu.p;
     e.two = two ? 1u : 0u;
-    e.ms0 = R.ms0;
-    e.ms1 = R.ms1;
+    e.nlay = R.nlay;
+    e.nemb = R.nemb;
+    e._r0 = e._r1 = 0;
     e.lam0 = R.lam0;
     e.lam1 = R.lam1;
     e.e8 = R.e8;
@@ -94,9 +100,9 @@ __device__ __forceinline__ RowEnt row_entry(const RowId& I, const RowCoef& R, bo
 
 // NEXT-1: the last stage (floor((L - L0)/(p - 1)) layers, one microbatch in
 // flight) of a row for digit (rc, do), as per-token coefficients
-__device__ __forceinline__ StEnt last_stage(const RowId& I, uint32_t rc, uint32_t dopt, uint32_t zero) {
+__device__ __forceinline__ StEnt last_stage(const RowId& I, uint32_t rc, uint32_t dopt, const Policy& Q) {
     const uint32_t Ll = (I.M.layers - I.L0) / (I.tu.p - 1);
-    const TermsT<uint64_t> T = stage_terms<uint64_t>(I.M, I.tu.t, I.tu.c, I.tu.d, false, true, Ll, 1u, 1u, rc, dopt, zero);
+    const TermsT<uint64_t> T = stage_terms<uint64_t>(I.M, I.tu.t, I.tu.c, I.tu.d, false, true, Ll, 1u, 1u, rc, dopt, Q);
     StEnt x;
     x.msL = T.params + T.grads + T.optim;
     x.kL = T.layers + T.head;

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(kRowThreads, 8)
     if (k < n_rows) {
         const RowId I = row_id(S, g0 + k, seg_lo, n_seg_sub);
         RowCoef R;
-        make_row(I.M, I.tu.t, I.tu.c, I.tu.p, I.tu.d, I.L0, S.zero_stage, R);
+        const Policy Q = policy_of(S);
+        make_row(I.M, I.tu.t, I.tu.c, I.tu.p, I.tu.d, I.L0, Q, R);
         const bool two = S.stage_max && I.tu.p >= 2;
         RowEnt e = row_entry(I, R, two);
         const uint32_t lg = S.lg_rcdo, n_sel = 1u << lg;
@@ -103,12 +104,12 @@ __global__ void __launch_bounds__(kRowThreads, 8)
             const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
             Digit c;
             c.ms = dopt ? R.ms1 : R.ms0;
-            // per-token bytes with p in flight (paper mode): p (lam + e8) + mu + hc
-            c.K = (uint64_t)I.tu.p * ((rc ? R.lam1 : R.lam0) + R.e8) + (rc ? R.bt + R.hc : R.hc);
+            // per-token bytes in paper mode: n_lay lam + mu + n_emb e8 + hc
+            c.K = (uint64_t)R.nlay * (rc ? R.lam1 : R.lam0) + (rc ? R.bt : 0ull) + (uint64_t)R.nemb * R.e8 + R.hc;
             c.two = two;
             c.msL = c.kL = 0;
             if (two) {
-                const StEnt x = last_stage(I, rc, dopt, S.zero_stage);
+                const StEnt x = last_stage(I, rc, dopt, Q);
                 st[(size_t)k << lg | sel] = x;
                 c.msL = x.msL;
                 c.kL = x.kL;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kRowThreads, 8)
                 // in-flight count min(p, m) of each pair (R17), or a cut row
                 for (uint32_t pos = a + ((sel - a) & (n_sel - 1u)); pos < b; pos += n_sel) {
                     const DevPair pr = pp[pos >> lg];
-                    uint64_t tot = config_total(R, pr.u, pr.m, rc, dopt);
+                    uint64_t tot = config_total(R, pr.u, pr.m, rc, dopt, S.vpp);
                     if (two) {
                         const uint64_t tl = c.msL + (uint64_t)pr.u * c.kL;
                         tot = tl > tot ? tl : tot;
@@ -170,9 +171,9 @@ constexpr uint32_t kFusedWarps = kThreads / 32;
 struct Lane {
     uint64_t v1, v2, v3;  // params, grads, optim
     uint64_t ms;          // their sum
-    uint64_t lam, mu;     // layer bytes per token per in-flight microbatch: n_inf lam + mu
+    uint64_t lam, mu;     // layer bytes per token: n_lay lam + mu
     uint64_t e8, hc;      // embedding bytes per token per microbatch, LM-head bytes per token
-    uint64_t c4, c5, K;   // paper mode: p lam + mu, p e8, c4 + c5 + hc
+    uint64_t c4, c5, K;   // paper mode: n_lay lam + mu, n_emb e8, c4 + c5 + hc
     uint32_t p, umax;
     // NEXT-1 last stage
     uint64_t msL, kL, parL, graL, optimL, layL, hcL;
@@ -183,18 +184,18 @@ __device__ __forceinline__ void lane_of(const DevSpace& S, const RowEnt& R, cons
                                         uint64_t kg, uint32_t sel, Lane& C) {
     const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
     const uint64_t psi = R.psi;
-    C.v1 = dopt ? R.par1 : 2ull * psi;
-    C.v2 = dopt ? R.gra1 : 4ull * psi;
-    C.v3 = dopt ? R.optim1 : 12ull * psi;
-    C.ms = dopt ? R.ms1 : R.ms0;
+    C.v1 = dopt ? R.par1 : (uint64_t)S.wb * psi;
+    C.v2 = dopt ? R.gra1 : (uint64_t)S.gb * psi;
+    C.v3 = dopt ? R.optim1 : (uint64_t)S.ob * psi;
+    C.ms = C.v1 + C.v2 + C.v3;
     C.lam = rc ? R.lam1 : R.lam0;
     C.mu = rc ? R.bt : 0ull;
     C.e8 = R.e8;
     C.hc = R.hc;
     C.p = R.p;
     C.umax = sel == 0 ? R.umax[0] : sel == 1 ? R.umax[1] : sel == 2 ? R.umax[2] : R.umax[3];
-    C.c4 = (uint64_t)C.p * C.lam + C.mu;
-    C.c5 = (uint64_t)C.p * C.e8;
+    C.c4 = (uint64_t)R.nlay * C.lam + C.mu;
+    C.c5 = (uint64_t)R.nemb * C.e8;
     C.K = C.c4 + C.c5 + C.hc;
     if (STMAX && R.two) {
         const StEnt* x = st + (kg << S.lg_rcdo | sel);
@@ -255,9 +256,9 @@ __device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, co
         const uint32_t u = pr.u;
         uint64_t c4 = C.c4, c5 = C.c5, tot;
         if (GBS) {
-            const uint32_t n_inf = min(C.p, pr.m);  // R17
-            c4 = (uint64_t)n_inf * C.lam + C.mu;
-            c5 = (uint64_t)n_inf * C.e8;
+            // in-flight counts of this pair's m microbatches (R17, R29)
+            c4 = (uint64_t)n_layer_mb(C.p, S.vpp, pr.m) * C.lam + C.mu;
+            c5 = (uint64_t)n_embed_mb(C.p, S.vpp, pr.m) * C.e8;
             tot = C.ms + (uint64_t)u * (c4 + c5 + C.hc);
         } else {
             tot = C.ms + (uint64_t)u * C.K;

@@ -131,7 +131,13 @@ __device__ int estimate_one(const me_model& Min, const me_parallel& P, me_breakd
         return ME_EINVAL;
     if (M.heads % M.kv_heads || M.hidden % M.heads) return ME_EINVAL;
     if (!P.dp || !P.tp || !P.pp || !P.cp || !P.mbs || !P.seq || P.zero_stage > 3) return ME_EINVAL;
+    if (P.sp_off > 1 || P.w_bytes > 8 || P.g_bytes > 8 || P.o_bytes > 16) return ME_EINVAL;
     const uint32_t t = P.tp, c = P.cp, p = P.pp, d = P.dp, L = M.layers;
+    if (P.vpp >= 2) {  // R29 interleaved 1F1B: p >= 2 stages of vpp chunks of L/(p vpp) layers
+        if (P.allow_uneven_pp || P.first_stage_layers) return ME_EINVAL;
+        if (p < 2 || L % (p * P.vpp)) return ME_EDIV;
+        if (P.gbs && P.gbs % ((uint64_t)d * P.mbs) == 0 && (P.gbs / ((uint64_t)d * P.mbs)) % p) return ME_EDIV;
+    }
     if (M.kv_heads % t || M.vocab % t || M.ffn_hidden % t) return ME_EDIV;  // R10
     if (P.seq % c) return ME_EDIV;
     if (p > L) return ME_EDIV;
@@ -150,14 +156,15 @@ __device__ int estimate_one(const me_model& Min, const me_parallel& P, me_breakd
     // exact shadow in 128 bits for the overflow verdict; the values returned
     // come from the same u64 code the sweep runs
     const DevModel DM = dev_model(M);
+    const Policy Q = make_policy(P.zero_stage, P.sp_off, P.vpp, P.w_bytes, P.g_bytes, P.o_bytes);
     RowCoefT<unsigned __int128> W;
-    make_row(DM, t, c, p, d, L0, (uint32_t)P.zero_stage, W);
-    const TermsT<unsigned __int128> T2 = config_terms(W, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u);
+    make_row(DM, t, c, p, d, L0, Q, W);
+    const TermsT<unsigned __int128> T2 = config_terms(W, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u, Q);
     const unsigned __int128 lim = (unsigned __int128)1 << 63;
     if (W.psi >= lim || W.ms0 >= lim || T2.total >= lim) return ME_EOVERFLOW;
     RowCoef R;
-    make_row(DM, t, c, p, d, L0, (uint32_t)P.zero_stage, R);
-    const TermsT<uint64_t> T = config_terms(R, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u);
+    make_row(DM, t, c, p, d, L0, Q, R);
+    const TermsT<uint64_t> T = config_terms(R, u, m, P.recompute ? 1u : 0u, P.dist_opt ? 1u : 0u, Q);
     out.params = T.params;
     out.grads = T.grads;
     out.optim = T.optim;
@@ -177,6 +184,8 @@ __device__ int estimate_stage_one(const me_model& M, const me_parallel& P, uint3
     if (st) return st;
     const uint32_t t = P.tp, c = P.cp, p = P.pp, d = P.dp, L = M.layers;
     if (stage != 0xFFFFFFFFu && stage >= p) return ME_EINVAL;
+    if (P.vpp >= 2) return ME_EINVAL;  // the per-stage view covers non-interleaved 1F1B
+    const Policy Q = make_policy(P.zero_stage, P.sp_off, P.vpp, P.w_bytes, P.g_bytes, P.o_bytes);
     const uint32_t L0 = P.first_stage_layers ? P.first_stage_layers : first_stage_layers_auto(L, p);
     const uint32_t u = (P.seq / c) * P.mbs;
     const uint64_t m = P.gbs ? P.gbs / ((uint64_t)d * P.mbs) : 0xFFFFFFFFull;
@@ -190,10 +199,9 @@ __device__ int estimate_stage_one(const me_model& M, const me_parallel& P, uint3
         const uint32_t n_i = (uint32_t)((uint64_t)(p - i) < m ? (uint64_t)(p - i) : m);
         const uint32_t rc = P.recompute ? 1u : 0u, dopt = P.dist_opt ? 1u : 0u;
         const TermsT<unsigned __int128> W = stage_terms<unsigned __int128>(DM, t, c, d, i == 0, i == p - 1, Li, n_i,
-                                                                           u, rc, dopt, P.zero_stage);
+                                                                           u, rc, dopt, Q);
         if (W.total >= lim) return ME_EOVERFLOW;
-        const TermsT<uint64_t> T = stage_terms<uint64_t>(DM, t, c, d, i == 0, i == p - 1, Li, n_i, u, rc, dopt,
-                                                         P.zero_stage);
+        const TermsT<uint64_t> T = stage_terms<uint64_t>(DM, t, c, d, i == 0, i == p - 1, Li, n_i, u, rc, dopt, Q);
         if (!have || T.total > out.total) {
             out = me_breakdown{T.params, T.grads, T.optim, T.layers, T.embed, T.head, T.total};
             which = i;
@@ -238,11 +246,6 @@ inline uint32_t ncap_stride_(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 
 }  // namespace
 
 uint32_t ncap_stride(uint32_t n_cap) { return ncap_stride_(n_cap); }
-
-uint32_t n_tiles_of(uint64_t lo, uint64_t hi) {
-    const uint64_t base = lo & ~31ull;
-    return hi > lo ? (uint32_t)((hi - base + kTile - 1) / kTile) : 0u;
-}
 
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st) {

@@ -41,6 +41,8 @@ struct DevSpace {
     uint32_t gbs_mode;            // 1 = a global batch bounds the in-flight microbatches (R17)
     uint32_t stage_max;           // 1 = feasibility of the largest pipeline stage (NEXT-1)
     uint32_t zero_stage;          // 2 / 3 = gradients / also weights sharded with the optimizer (NEXT-4)
+    uint32_t sp_off, vpp;         // NEXT-4: sequence parallelism off (R28); virtual pipeline stages (R29)
+    uint32_t wb, gb, ob;          // NEXT-4: bytes per parameter of weights / gradients / optimizer states (R30)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
     uint64_t thr_max;             // the largest threshold: survivor <=> total <= thr_max
     // thr_j + 1 with thr_j clamped to 2^62 (every total is < 2^58): the sweep
@@ -52,21 +54,51 @@ struct DevSpace {
     uint32_t cslot[8];
 };
 
+// The estimator's variant policy of a configuration (the paper: all zero /
+// default): ZeRO stage (NEXT-4), sequence parallelism off (R28), virtual
+// pipeline stages of interleaved 1F1B (R29), bytes per parameter (R30).
+struct Policy {
+    uint32_t zero, sp_off, vpp, wb, gb, ob;
+};
+
+__host__ __device__ inline Policy make_policy(uint32_t zero, uint32_t sp_off, uint32_t vpp, uint32_t wb, uint32_t gb,
+                                              uint32_t ob) {
+    return Policy{zero, sp_off, vpp < 2 ? 1u : vpp, wb ? wb : 2u, gb ? gb : 4u, ob ? ob : 12u};
+}
+
+// In-flight work on the first pipeline stage for m microbatches per step
+// (0xFFFFFFFF = unbounded, the paper mode): the microbatch count of the layer
+// activations (in units of the row's layers-per-chunk, see lam0) and of the
+// embedding input.  1F1B (Eq.16, R17): min(p, m) for both.  Interleaved 1F1B
+// (R29, Megatron): the first GPU holds p v + p - 1 chunk-microbatches (m v if
+// m = p), min(m, 2p) of them of chunk 0 (the embedding's).
+__host__ __device__ inline uint32_t n_layer_mb(uint32_t p, uint32_t vpp, uint32_t m) {
+    if (vpp < 2) return p < m ? p : m;
+    return m == p ? p * vpp : p * vpp + p - 1;
+}
+__host__ __device__ inline uint32_t n_embed_mb(uint32_t p, uint32_t vpp, uint32_t m) {
+    if (vpp < 2) return p < m ? p : m;
+    return m < 2 * p ? m : 2 * p;
+}
+
 // Per (model, tuple) coefficients: every estimator term of a config in this
-// row is an affine function of its tokens-per-microbatch u and in-flight count.
+// row is an affine function of its tokens-per-microbatch u and in-flight counts.
 template <typename U>
 struct RowCoefT {
     U psi;        // Psi_s, Eq.6 (p = 1) / Eq.7 (p > 1) with L/p -> L0
-    U optim1;     // 12 ceil(Psi_s / (d c))   (Eq.10 + reading R8)
-    U par1, gra1; // weight / gradient bytes with the distributed optimizer: 2 Psi_s / 4 Psi_s
-                  // (R9), or 2 / 4 ceil(Psi_s / (d c)) at ZeRO stage 3 / >= 2 (NEXT-4)
+    U optim1;     // ob ceil(Psi_s / (d c))   (Eq.10 + reading R8; ob = 12, R30)
+    U par1, gra1; // weight / gradient bytes with the distributed optimizer: wb Psi_s / gb Psi_s
+                  // (R9), or wb / gb ceil(Psi_s / (d c)) at ZeRO stage 3 / >= 2 (NEXT-4)
     U ms0, ms1;   // model-state bytes with the distributed optimizer off / on
-    U lam0;       // L0 * B_t                 (rc = 0 layer bytes per token per mb)
-    U lam1;       // 2 ht L0                  (rc = 1: kept layer inputs, R20)
-    U bt;         // B_t = 12 ht + 4 hd k/t + 8 h_ffn/t   (Eq.12 / Eq.15 per token)
-    U e8;         // 8 ht                     (Eq.13 per token per mb, reading R13)
-    U hc;         // [p = 1] 4 (ht + v/t)     (Eq.14, delta_{p,1} of Eq.16)
+    U lam0;       // Lx * B_t   (rc = 0 layer bytes per token per in-flight unit; Lx = L0, or
+                  //             L/(p v) layers per chunk with interleaving)
+    U lam1;       // 2 hx Lx    (rc = 1: kept layer inputs, R20; hx = h/t, or h with SP off)
+    U bt;         // B_t = 12 ht + 4 hd k/t + 8 h_ffn/t   (Eq.12 / Eq.15 per token; SP off:
+                  //       8 h + 4 ht + 4 hd k/t + 8 h_ffn/t, R28)
+    U e8;         // 8 hx       (Eq.13 per token per mb, reading R13)
+    U hc;         // [p = 1] 4 (ht + v/t)  (Eq.14, delta_{p,1} of Eq.16; SP off: 4 (h + v/t))
     uint32_t p;
+    uint32_t nlay, nemb;  // paper mode (m unbounded): n_layer_mb, n_embed_mb
 };
 using RowCoef = RowCoefT<uint64_t>;
 
@@ -82,10 +114,11 @@ __device__ __forceinline__ uint32_t div_u32(uint32_t x, uint32_t d) {
 }
 
 // Row coefficients.  All divisions are exact under the validity rules
-// (t | k | a | h, t | v, t | h_ffn) except the optimizer ceil (R8).
+// (t | k | a | h, t | v, t | h_ffn, p v | L with interleaving) except the
+// optimizer ceil (R8).
 template <typename U>
 __device__ __forceinline__ void make_row(const DevModel& M, uint32_t t, uint32_t c, uint32_t p,
-                                         uint32_t d, uint32_t L0, uint32_t zero, RowCoefT<U>& R) {
+                                         uint32_t d, uint32_t L0, const Policy& Q, RowCoefT<U>& R) {
     const uint32_t h = M.hidden;
     const uint32_t hd = M.head_dim;
     uint32_t ht, kt, vt, ft;
@@ -114,17 +147,21 @@ __device__ __forceinline__ void make_row(const DevModel& M, uint32_t t, uint32_t
     } else {
         share = (R.psi + dc - 1) / dc;
     }
-    R.optim1 = (U)12 * share;
-    R.par1 = zero >= 3 ? (U)2 * share : (U)2 * R.psi;
-    R.gra1 = zero >= 2 ? (U)4 * share : (U)4 * R.psi;
-    R.ms0 = (U)18 * R.psi;
+    R.optim1 = (U)Q.ob * share;
+    R.par1 = Q.zero >= 3 ? (U)Q.wb * share : (U)Q.wb * R.psi;
+    R.gra1 = Q.zero >= 2 ? (U)Q.gb * share : (U)Q.gb * R.psi;
+    R.ms0 = (U)(Q.wb + Q.gb + Q.ob) * R.psi;
     R.ms1 = R.par1 + R.gra1 + R.optim1;
-    R.bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft;
-    R.lam0 = (U)L0 * R.bt;
-    R.lam1 = (U)2 * ht * L0;
-    R.e8 = (U)8 * ht;
-    R.hc = (p == 1) ? (U)4 * ((U)ht + vt) : (U)0;
+    const uint32_t hx = Q.sp_off ? h : ht;  // whole on every TP rank without SP (R28)
+    R.bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft + (Q.sp_off ? (U)8 * (h - ht) : (U)0);
+    const uint32_t Lx = Q.vpp >= 2 ? M.layers / (p * Q.vpp) : L0;
+    R.lam0 = (U)Lx * R.bt;
+    R.lam1 = (U)2 * hx * Lx;
+    R.e8 = (U)8 * hx;
+    R.hc = (p == 1) ? (U)4 * ((U)hx + vt) : (U)0;
     R.p = p;
+    R.nlay = n_layer_mb(p, Q.vpp, 0xFFFFFFFFu);
+    R.nemb = n_embed_mb(p, Q.vpp, 0xFFFFFFFFu);
 }
 
 template <typename U>
@@ -136,81 +173,65 @@ struct TermsT {
 // microbatches -- Eq.6 (single stage), Eq.7 (first), Eq.8 (middle), Eq.9
 // (last: the final norm and the LM head); embedding input on the first stage,
 // LM-head activations on the last.  For the first stage this is make_row +
-// config_terms term by term.
+// config_terms term by term.  Non-interleaved 1F1B only.
 template <typename U>
 __device__ __forceinline__ TermsT<U> stage_terms(const DevModel& M, uint32_t t, uint32_t c, uint32_t d, bool first,
                                                  bool last, uint32_t Li, uint32_t n_i, uint32_t u, uint32_t rc,
-                                                 uint32_t dopt, uint32_t zero) {
+                                                 uint32_t dopt, const Policy& Q) {
     const uint32_t h = M.hidden, hd = M.head_dim;
     const uint32_t ht = div_u32(h, t), kt = div_u32(M.kv_heads, t), vt = div_u32(M.vocab, t),
                    ft = div_u32(M.ffn_hidden, t);
+    const uint32_t hx = Q.sp_off ? h : ht;
     const U per_layer = (U)2 * h * ht + (U)2 * h * hd * kt + (U)3 * h * ft + (U)2 * h;
     const U ends = first && last ? (U)2 * h * vt + h : (first ? (U)h * vt : (last ? (U)h * vt + h : (U)0));
     const U psi = ends + (U)Li * per_layer;
     const uint32_t dc = d * c;
     const U share = (psi + dc - 1) / dc;
-    const U bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft;
+    const U bt = (U)12 * ht + (U)4 * hd * kt + (U)8 * ft + (Q.sp_off ? (U)8 * (h - ht) : (U)0);
     TermsT<U> T;
-    T.params = dopt && zero >= 3 ? (U)2 * share : (U)2 * psi;
-    T.grads = dopt && zero >= 2 ? (U)4 * share : (U)4 * psi;
-    T.optim = dopt ? (U)12 * share : (U)12 * psi;
-    T.layers = (U)u * (rc ? (U)2 * ht * n_i * Li + bt : (U)n_i * Li * bt);
-    T.embed = first ? (U)u * ((U)8 * ht * n_i) : (U)0;
-    T.head = last ? (U)u * ((U)4 * ((U)ht + vt) * n_i) : (U)0;
+    T.params = dopt && Q.zero >= 3 ? (U)Q.wb * share : (U)Q.wb * psi;
+    T.grads = dopt && Q.zero >= 2 ? (U)Q.gb * share : (U)Q.gb * psi;
+    T.optim = dopt ? (U)Q.ob * share : (U)Q.ob * psi;
+    T.layers = (U)u * (rc ? (U)2 * hx * n_i * Li + bt : (U)n_i * Li * bt);
+    T.embed = first ? (U)u * ((U)8 * hx * n_i) : (U)0;
+    T.head = last ? (U)u * ((U)4 * ((U)hx + vt) * n_i) : (U)0;
     T.total = T.params + T.grads + T.optim + T.layers + T.embed + T.head;
     return T;
 }
 
-// total only (count pass): model states + u * (n_inf * a_rc + b_rc)
-__device__ __forceinline__ uint64_t config_total(const RowCoef& R, uint32_t u, uint32_t m,
-                                                 uint32_t rc, uint32_t dopt) {
-    const uint32_t n_inf = min(R.p, m);
-    const uint64_t a = rc ? (R.lam1 + R.e8) : (R.lam0 + R.e8);
-    const uint64_t b = rc ? (R.bt + R.hc) : R.hc;
-    const uint64_t K = (uint64_t)n_inf * a + b;
+// total only: model states + u * (n_lay lam + mu + n_emb e8 + hc), with the
+// in-flight counts of m microbatches (0xFFFFFFFF = paper mode)
+__device__ __forceinline__ uint64_t config_total(const RowCoef& R, uint32_t u, uint32_t m, uint32_t rc,
+                                                 uint32_t dopt, uint32_t vpp) {
+    const uint32_t nl = n_layer_mb(R.p, vpp, m), ne = n_embed_mb(R.p, vpp, m);
+    const uint64_t K = (uint64_t)nl * (rc ? R.lam1 : R.lam0) + (rc ? R.bt : 0ull) + (uint64_t)ne * R.e8 + R.hc;
     return (dopt ? R.ms1 : R.ms0) + (uint64_t)u * K;
-}
-
-// the six terms without their sum (the write pass reuses config_total's value,
-// which equals the sum term by term)
-template <typename U>
-__device__ __forceinline__ TermsT<U> config_terms_no_total(const RowCoefT<U>& R, uint32_t u, uint32_t m,
-                                                           uint32_t rc, uint32_t dopt) {
-    const uint32_t n_inf = min(R.p, m);
-    TermsT<U> T;
-    T.params = dopt ? R.par1 : (U)2 * R.psi;
-    T.grads = dopt ? R.gra1 : (U)4 * R.psi;
-    T.optim = dopt ? R.optim1 : (U)12 * R.psi;
-    T.layers = (U)u * (rc ? ((U)n_inf * R.lam1 + R.bt) : (U)n_inf * R.lam0);
-    T.embed = (U)u * ((U)n_inf * R.e8);
-    T.head = (U)u * R.hc;
-    T.total = 0;
-    return T;
 }
 
 // all six terms (single estimates); total = their sum, equal to config_total
 // term by term
 template <typename U>
-__device__ __forceinline__ TermsT<U> config_terms(const RowCoefT<U>& R, uint32_t u, uint32_t m,
-                                                  uint32_t rc, uint32_t dopt) {
-    const uint32_t n_inf = min(R.p, m);
+__device__ __forceinline__ TermsT<U> config_terms(const RowCoefT<U>& R, uint32_t u, uint32_t m, uint32_t rc,
+                                                  uint32_t dopt, const Policy& Q) {
+    const uint32_t nl = n_layer_mb(R.p, Q.vpp, m), ne = n_embed_mb(R.p, Q.vpp, m);
     TermsT<U> T;
-    T.params = dopt ? R.par1 : (U)2 * R.psi;
-    T.grads = dopt ? R.gra1 : (U)4 * R.psi;
-    T.optim = dopt ? R.optim1 : (U)12 * R.psi;
-    T.layers = (U)u * (rc ? ((U)n_inf * R.lam1 + R.bt) : (U)n_inf * R.lam0);
-    T.embed = (U)u * ((U)n_inf * R.e8);
+    T.params = dopt ? R.par1 : (U)Q.wb * R.psi;
+    T.grads = dopt ? R.gra1 : (U)Q.gb * R.psi;
+    T.optim = dopt ? R.optim1 : (U)Q.ob * R.psi;
+    T.layers = (U)u * (rc ? ((U)nl * R.lam1 + R.bt) : (U)nl * R.lam0);
+    T.embed = (U)u * ((U)ne * R.e8);
     T.head = (U)u * R.hc;
     T.total = T.params + T.grads + T.optim + T.layers + T.embed + T.head;
     return T;
 }
 
-// ---- row-table pipeline (me_rows.cu) --------------------------------------
+// ---- row-count pipeline (me_fused.cu) -------------------------------------
 // One row of the sub-range table (128 B): the row's RowCoef, first index and
 // pair offset; uint4-loadable prefix {w, pair_off, p, two}.
 struct __align__(16) RowEnt {
     uint32_t w, pair_off, p, two;  // two: NEXT-1 last stage may decide (stage_max and p >= 2)
-    uint64_t ms0, ms1;
+    uint32_t nlay, nemb;           // paper-mode in-flight counts (RowCoef)
+    uint32_t _r0, _r1;
     uint64_t lam0, lam1;
     uint64_t e8, bt;
     uint64_t hc, psi;
@@ -226,11 +247,6 @@ struct __align__(16) StEnt {
     uint64_t msL, kL, parL, graL, optimL, layL, hcL, _pad;
 };
 constexpr uint32_t kMaxRows = 1u << 21;  // rows of one sub-range (descriptor row field: 24 bits)
-// warps (spans) per stage-kernel block; the scan runs over these blocks
-#ifndef ME_STAGE_WARPS
-#define ME_STAGE_WARPS 4
-#endif
-constexpr uint32_t kStageWarps = ME_STAGE_WARPS;
 
 // ---- launch wrappers (me_kernels.cu) ------------------------------------
 struct Cols {
@@ -238,31 +254,12 @@ struct Cols {
 };
 
 constexpr int kThreads = 256;
-constexpr int kWarpsPerBlock = kThreads / 32;
-constexpr uint32_t kTileRounds = 16;               // rounds of 32 indices per tile
-constexpr uint32_t kTile = kTileRounds * 32;       // 512 indices
-constexpr uint64_t kMaxSub = 1ull << 28;           // indices per count/scan/write sub-range
+constexpr uint64_t kMaxSub = 1ull << 28;           // indices per sub-range of a sweep
 
 uint32_t ncap_stride(uint32_t n_cap);
-// tiles of [lo, hi) (tile 0 starts at lo rounded down to a multiple of 32)
-uint32_t n_tiles_of(uint64_t lo, uint64_t hi);
 // span offsets = running total stats[0] + exclusive prefix; stats accumulate
 cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
                         uint64_t* span_off, uint64_t* stats, cudaStream_t st);
-// row-table pipeline (me_rows.cu): K0 rows [g0, g0 + n_rows) of the range
-// [lo, hi) + span checkpoints, K1 survivors -> descriptors + span counts, K3
-// descriptors -> output rows (and stats[1 + j] per capacity)
-int expand_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
-cudaError_t launch_rows(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
-                        uint64_t lo, uint64_t hi, uint32_t span_tiles, RowEnt* rows, StEnt* st, uint2* span_ck,
-                        cudaStream_t stream);
-cudaError_t launch_stage(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
-                         uint32_t span_tiles, const uint2* span_ck, uint64_t* desc, uint32_t d32, uint32_t* span_count,
-                         uint32_t* block_count, me_out_mode mode, cudaStream_t stream);
-cudaError_t launch_expand(const DevSpace& S, const RowEnt* rows, const StEnt* st, uint64_t lo, uint64_t hi,
-                          uint32_t span_tiles, const uint64_t* desc, uint32_t d32, const uint2* span_ck,
-                          const uint32_t* span_count, const uint64_t* block_off, me_out_mode mode, Cols cols, uint64_t capacity, uint64_t* stats,
-                          uint32_t n_blocks, uint32_t* next_span, cudaStream_t stream);
 // row-count pipeline (me_fused.cu): K0 rows [g0, g0 + n_rows) of the range
 // [lo, hi) with their survivor counts (rcnt, per 32-row unit ucnt, per
 // capacity into stats[1 + j]); K3 rows with survivors -> output rows

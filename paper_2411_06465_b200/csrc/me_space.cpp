@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <unordered_map>
 
 namespace me {
@@ -41,6 +42,15 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
     stage_max = cr->stage_policy;
     if (cr->zero_stage > 3) return fail(detail, ME_EINVAL, "zero_stage must be 0..3");
     zero_stage = (uint8_t)cr->zero_stage;
+    if (cr->sp_off > 1 || cr->w_bytes > 8 || cr->g_bytes > 8 || cr->o_bytes > 16)
+        return fail(detail, ME_EINVAL, "sp_off must be 0/1, w_bytes/g_bytes <= 8, o_bytes <= 16");
+    sp_off = cr->sp_off;
+    vpp = cr->vpp < 2 ? 0 : cr->vpp;
+    wb = cr->w_bytes;
+    gb = cr->g_bytes;
+    ob = cr->o_bytes;
+    if (vpp && (uneven || stage_max))
+        return fail(detail, ME_EINVAL, "interleaved 1F1B (vpp >= 2) excludes allow_uneven_pp and ME_STAGE_MAX");
 
     for (size_t i = 0; i < models.size(); i++) {
         const me_model& m = models[i];
@@ -87,7 +97,7 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
     pair_b.clear();
     pair_su.clear();
     tup_begin.assign(1, 0);
-    std::map<std::pair<uint32_t, uint32_t>, std::pair<uint32_t, uint32_t>> pool;  // (c, d|0) -> (off, n)
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::pair<uint32_t, uint32_t>> pool;  // (c, d|0, p|0) -> (off, n)
     std::vector<uint32_t> tvals, pvals;
     for (uint32_t N : world) {
         for (uint32_t t = 1; t <= N; t++) {
@@ -101,14 +111,13 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
                     if ((N / t / c) % p) continue;
                     if (max_p && p > max_p) continue;
                     uint32_t d = N / t / c / p;
-                    auto key = std::make_pair(c, gbs ? d : 0u);
+                    auto key = std::make_tuple(c, gbs ? d : 0u, gbs && vpp ? p : 0u);
                     auto it = pool.find(key);
                     if (it == pool.end()) {
                         uint32_t off = (uint32_t)pairs.size();
                         for (uint32_t b : mbs)
                             for (uint32_t s : seq) {
-                                if (s % c) continue;
-                                if (gbs && gbs % ((uint64_t)d * b)) continue;
+                                if (!pair_ok(c, d, p, b, s)) continue;
                                 DevPair pr;
                                 pr.u = (s / c) * b;
                                 pr.m = gbs ? (uint32_t)(gbs / ((uint64_t)d * b)) : 0xFFFFFFFFu;
@@ -152,7 +161,10 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
         }
         for (size_t q = 0; q < pvals.size(); q++) {
             uint32_t p = pvals[q];
-            sig[tvals.size() + q] = (p <= m.layers && (uneven || m.layers % p == 0)) ? '1' : '0';
+            sig[tvals.size() + q] = (p <= m.layers && (uneven || m.layers % p == 0) &&
+                                     (!vpp || (p >= 2 && m.layers % (p * vpp) == 0)))
+                                        ? '1'
+                                        : '0';
         }
         auto it = cls_of.find(sig);
         if (it == cls_of.end()) {
@@ -250,8 +262,7 @@ int HostSpace::decode(uint64_t index, uint32_t* model_id, uint32_t* world_size,
     uint32_t k = 0, b = 0, s = 0;
     for (uint32_t bb : mbs) {
         for (uint32_t ss : seq) {
-            if (ss % tu.c) continue;
-            if (gbs && gbs % ((uint64_t)tu.d * bb)) continue;
+            if (!pair_ok(tu.c, tu.d, tu.p, bb, ss)) continue;
             if (k == q) { b = bb; s = ss; }
             k++;
         }
@@ -263,6 +274,11 @@ int HostSpace::decode(uint64_t index, uint32_t* model_id, uint32_t* world_size,
     c.dist_opt = (uint8_t)((rcdo_do >> sel) & 1);
     c.allow_uneven_pp = uneven;
     c.zero_stage = zero_stage;
+    c.sp_off = sp_off;
+    c.vpp = vpp;
+    c.w_bytes = wb;
+    c.g_bytes = gb;
+    c.o_bytes = ob;
     if (model_id) *model_id = mdl;
     if (world_size) *world_size = world[n];
     if (out) *out = c;

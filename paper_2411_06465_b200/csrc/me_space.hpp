@@ -42,6 +42,14 @@ struct Limits {            // domain of exact u64 evaluation (me.h, me_sweep)
 
 class HostSpace {
   public:
+    // (b, s) pair of tuple (c, d, p) kept: c | s, and with a global batch
+    // (d b) | gbs (R17) and, interleaved, p | gbs/(d b) (R29)
+    bool pair_ok(uint32_t c, uint32_t d, uint32_t p, uint32_t b, uint32_t s) const {
+        if (s % c) return false;
+        if (!gbs) return true;
+        if (gbs % ((uint64_t)d * b)) return false;
+        return vpp < 2 || (gbs / ((uint64_t)d * b)) % p == 0;
+    }
     // returns ME_* status; `detail` receives a message on failure
     int build(const me_model_range* models, const me_cluster* cluster, const me_cfg_range* cfg,
               bool for_sweep, std::string* detail);
@@ -57,6 +65,7 @@ class HostSpace {
     std::vector<uint64_t> caps;
     uint32_t gpus_per_node = 0, gbs = 0, max_t = 0, max_c = 0, max_p = 0;
     uint8_t rc_mask = 0, do_mask = 0, uneven = 0, stage_max = 0, zero_stage = 0;
+    uint8_t sp_off = 0, vpp = 0, wb = 0, gb = 0, ob = 0;  // NEXT-4 variants of every configuration
     // (rc, do) digits of the innermost axes
     uint32_t n_rcdo = 0, lg_rcdo = 0, rcdo_rc = 0, rcdo_do = 0;
 

@@ -338,15 +338,12 @@ def test_sweep_zero_stages(me, oracle_mod, zero, stage_max):
     assert_same(me, res, *oracle_rows(oracle_mod, sp), me.ME_OUT_FULL)
 
 
-@pytest.mark.parametrize("env", [{"ME_PIPE": "2"}, {"ME_PIPE": "2", "ME_DESC64": "1"}, {"ME_SERIAL": "1"},
-                                 {"ME_PIPE": "2", "ME_SERIAL": "1"}, {"ME_PIPE": "2", "ME_EXPAND_U": "4"},
-                                 {"ME_SETS": "3"}, {"ME_FUSED_BPS": "1"}],
-                         ids=["pipe2", "pipe2-desc64", "serial", "pipe2-serial", "pipe2-u4", "sets3", "fused-1bps"])
+@pytest.mark.parametrize("env", [{"ME_SERIAL": "1"}, {"ME_SETS": "3"}, {"ME_FUSED_BPS": "1"},
+                                 {"ME_SERIAL": "1", "ME_FUSED_BPS": "1"}],
+                         ids=["serial", "sets3", "fused-1bps", "serial-1bps"])
 def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
-    """The selectable pipelines and kernel variants (read at plan creation)
-    give the same rows: the descriptor pipeline (pipe 2, with 64-bit
-    descriptors, 4 survivors per lane in its expand kernel), serial streams,
-    three scratch sets, one fused-kernel block per SM."""
+    """The launch variants (read at plan creation) give the same rows: serial
+    streams, three scratch sets, one fused-kernel block per SM."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     spaces = [mi.config("C3", uneven=1),
@@ -361,14 +358,13 @@ def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
             assert_same(me, res, *ref, mode)
 
 
-@pytest.mark.parametrize("pipe", ["3", "2"])
-@pytest.mark.parametrize("max_rows", [64, 1000])
-def test_subranges_cut_by_rows(me, oracle_mod, monkeypatch, max_rows, pipe):
-    """Sub-ranges of the row-table pipeline are also cut at max_rows rows
-    (2^21 in production; a small cap here): offsets chain across the cuts and
-    the result equals the oracle, for the full range and for ragged ranges."""
+@pytest.mark.parametrize("max_rows", [1, 64, 1000])
+def test_subranges_cut_by_rows(me, oracle_mod, monkeypatch, max_rows):
+    """Sub-ranges are also cut at max_rows rows (2^21 in production; a small
+    cap here, down to one row per sub-range): offsets chain across the cuts
+    and the result equals the oracle, for the full range and for ragged
+    ranges."""
     monkeypatch.setenv("ME_MAX_ROWS", str(max_rows))
-    monkeypatch.setenv("ME_PIPE", pipe)
     sp = mi.Space(models=mi.random_models(20, seed=13), world=[16, 48, 64, 128], caps_gb=[40, 80, 192],
                   mbs=[1, 2, 4], seq=[2048, 4096, 8192], uneven=1)
     plan = me.Plan(sp)
@@ -377,3 +373,65 @@ def test_subranges_cut_by_rows(me, oracle_mod, monkeypatch, max_rows, pipe):
             res = plan.sweep(b, e, mode=mode)
             assert res.status() == 0
             assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e or plan.size), mode)
+
+
+# ---------------------------------------------------------------- NEXT-4: SP off, interleaved 1F1B, byte policies
+def test_estimate_variants(me, oracle_mod):
+    """me_estimate_batch / me_estimate_stage with the NEXT-4 variants (R28-R30)
+    equal the oracle, statuses included"""
+    rng = np.random.default_rng(43)
+    shapes = mi.random_models(10, seed=47) + [mi.PRESETS["llama3.1-70b"], mi.PRESETS["llama2-13b"]]
+    caps = [40 << 30, 80 << 30]
+    for shape in shapes:
+        cfgs = random_cfgs(rng, shape, 80)
+        for cfg in cfgs:
+            cfg["sp_off"] = int(rng.integers(0, 2))
+            cfg["vpp"] = int(rng.choice([0, 0, 2, 3, 4]))
+            cfg["wb"], cfg["gb"], cfg["ob"] = (int(x) for x in rng.choice([(0, 0, 0), (1, 4, 12), (1, 2, 12),
+                                                                           (2, 4, 6), (1, 1, 16)]))
+            cfg["zero"] = int(rng.integers(0, 4))
+            if cfg["vpp"] >= 2 and rng.random() < 0.7:
+                cfg.pop("L0", None)
+                cfg["uneven"] = 0
+                L = shape[2]
+                ps = [p for p in range(2, L + 1) if L % (p * cfg["vpp"]) == 0]
+                if ps:
+                    cfg["p"] = int(rng.choice(ps))
+        rows, mask, status = me.me_estimate_batch([shape], None, cfgs, caps_bytes=caps)
+        for i, cfg in enumerate(cfgs):
+            st = oracle_mod.estimate_status(shape, **cfg)
+            assert status[i] == st, (shape, cfg)
+            if st == 0:
+                e = oracle_mod.estimate(shape, **cfg)
+                assert rows[i].tolist() == [e[k] for k in oracle_mod.TERMS], (shape, cfg)
+                assert mask[i] == oracle_mod.cap_mask(e["total"], caps)
+                if cfg["p"] > 1 and cfg["vpp"] < 2:
+                    for stg in (0, cfg["p"] - 1):
+                        got, _ = me.me_estimate_stage(shape, stg, **cfg)
+                        assert got == oracle_mod.estimate_stage(shape, stg, **cfg), (shape, cfg, stg)
+
+
+def variant_spaces():
+    base = dict(models=mi.random_models(12, seed=53) + [mi.PRESETS["llama3.1-8b"], mi.PRESETS["llama3.1-70b"]],
+                world=[16, 24, 64], caps_gb=[24, 40, 80, 192], mbs=[1, 2, 4], seq=[4096, 16384])
+    yield "sp_off", mi.Space(**base, sp_off=1, uneven=1)
+    yield "sp_off_stage_max", mi.Space(**base, sp_off=1, uneven=1, stage_max=1)
+    yield "vpp2", mi.Space(**base, vpp=2)
+    yield "vpp3_gbs", mi.Space(**base, vpp=3, gbs=768)
+    yield "vpp2_gbs_sp_off", mi.Space(**base, vpp=2, gbs=1536, sp_off=1)
+    yield "fp8_weights", mi.Space(**base, wb=1, uneven=1, zero_stage=3)
+    yield "bf16_grads_8bit_adam", mi.Space(**base, gb=2, ob=6, gbs=960)
+
+
+@pytest.mark.parametrize("name,sp", list(variant_spaces()), ids=[n for n, _ in variant_spaces()])
+@pytest.mark.parametrize("mode", [0, 1, 3], ids=["count", "index", "records"])
+def test_sweep_variants(me, oracle_mod, name, sp, mode):
+    plan = me.Plan(sp)
+    assert plan.size == oracle_mod.space_size(sp) > 0
+    res = plan.sweep(mode=mode)
+    assert res.status() == 0
+    assert_same(me, res, *oracle_rows(oracle_mod, sp), mode)
+    if name in ("vpp2", "vpp3_gbs"):
+        # decode agrees on the reduced space
+        for i in (0, plan.size // 2, plan.size - 1):
+            assert me.me_decode(sp, i)[:2] == oracle_mod.decode(sp, i)[:2]

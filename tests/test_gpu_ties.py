@@ -63,10 +63,8 @@ SPACES = {
 }
 
 
-@pytest.mark.parametrize("pipe", ["3", "2"])
 @pytest.mark.parametrize("kind", list(SPACES))
-def test_exact_tie_every_path(me, oracle_mod, monkeypatch, kind, pipe):
-    monkeypatch.setenv("ME_PIPE", pipe)
+def test_exact_tie_every_path(me, oracle_mod, kind):
     kw = SPACES[kind]
     base = mi.Space(models=[mi.PRESETS["llama3.1-8b"], mi.PRESETS["llama2-13b"]], world=[16, 64],
                     caps_gb=[80], mbs=[1, 2, 4], seq=[4096, 8192], **kw)
