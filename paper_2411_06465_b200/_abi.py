@@ -4,10 +4,13 @@ or CPU fallback; loading fails loudly when the library is missing."""
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libme.so"
+# ME_CHECKED=1 loads the build with device-side bounds assertions
+# (libme_checked.so, paper_2411_06465_b200/build.py --checked); tests only
+LIB_PATH = PKG / ("libme_checked.so" if os.environ.get("ME_CHECKED") == "1" else "libme.so")
 
 ME_OK, ME_EINVAL, ME_EDIV, ME_EOVERFLOW, ME_ENOMEM, ME_ECUDA, ME_ENCCL, ME_ERANGE = range(8)
 ME_OUT_COUNT, ME_OUT_INDEX, ME_OUT_FULL, ME_OUT_RECORDS = 0, 1, 2, 3

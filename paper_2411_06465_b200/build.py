@@ -11,6 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libme.so"
+LIB_CHECKED = PKG / "libme_checked.so"  # device-side bounds assertions (-DME_CHECKS), for tests
 SOURCES = ["me_space.cpp", "me_kernels.cu", "me_fused.cu", "me_digest.cu", "me_rank.cu", "me_abi.cu"]
 HEADERS = ["me_space.hpp", "me_kernels.cuh", "me_dev.cuh"]
 
@@ -32,17 +33,18 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
-    if not LIB.exists():
+def stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "me.h", Path(__file__)]
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not stale(lib):
+        return lib
     nr = nccl_root()
     cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-lineinfo",
            "-gencode", "arch=compute_100a,code=sm_100a",
@@ -50,12 +52,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
            "-I", str(ROOT / "include"), "-I", str(nr / "include"),
            *[str(CSRC / s) for s in SOURCES],
            "-L", str(nr / "lib"), "-l:libnccl.so.2", f"-Xlinker=-rpath={nr / 'lib'}",
-           "-o", str(LIB) + ".tmp"]
+           *(["-DME_CHECKS"] if checked else []),
+           "-o", str(lib) + ".tmp"]
     subprocess.check_call(cmd)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force=True, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

@@ -4,6 +4,17 @@
 
 #include "me_kernels.cuh"
 
+// ME_CHECKS (the checked build, libme_checked.so; build.py): device-side
+// bounds assertions on every table, scratch, shared-memory and output index
+// the sweep kernels compute -- a failed check traps the kernel (the call then
+// returns ME_ECUDA).  compiled out of libme.so.
+#ifdef ME_CHECKS
+#include <cassert>
+#define ME_CHECK(cond) assert(cond)
+#else
+#define ME_CHECK(cond) ((void)0)
+#endif
+
 namespace me {
 
 // total <= thr  <=>  thr1 + ~total carries out of 64 bits (thr1 = thr + 1):
@@ -62,13 +73,16 @@ struct RowId {
 __device__ __forceinline__ RowId row_id(const DevSpace& S, uint64_t g, uint32_t seg_lo, uint32_t n_seg_sub) {
     RowId R;
     const uint32_t s = seg_lo + upper_bound_u64(S.seg_row + seg_lo, n_seg_sub, g) - 1;
+    ME_CHECK(s < S.n_seg && __ldg(S.seg_row + s) <= g && g < __ldg(S.seg_row + s + 1));
     const uint32_t m = s / S.n_world, n = s - m * S.n_world;
     const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(S.models + m));
     const uint4 m1 = __ldg(reinterpret_cast<const uint4*>(S.models + m) + 1);
     R.M = DevModel{m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, 0u};
     const uint32_t cls = __ldg(S.model_class + m);
     const uint32_t j = __ldg(S.list_off + cls * S.n_world + n) + (uint32_t)(g - __ldg(S.seg_row + s));
+    ME_CHECK(j < __ldg(S.list_off + cls * S.n_world + n + 1));
     R.tu = S.tuples[__ldg(S.list_tuple + j)];
+    ME_CHECK(R.tu.pair_off + R.tu.n_pairs <= S.n_pairs && R.tu.w == R.tu.n_pairs << S.lg_rcdo);
     R.rs = __ldg(S.seg_prefix + s) + __ldg(S.list_prefix + j);
     R.L0 = R.tu.p == 1 ? R.M.layers : div_u32(R.M.layers + R.tu.p - 1, R.tu.p);
     return R;

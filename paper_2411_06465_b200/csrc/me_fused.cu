@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(kRowThreads, 8)
                 // config by config over the window's positions of this digit:
                 // in-flight count min(p, m) of each pair (R17), or a cut row
                 for (uint32_t pos = a + ((sel - a) & (n_sel - 1u)); pos < b; pos += n_sel) {
+                    ME_CHECK((pos >> lg) < I.tu.n_pairs);
                     const DevPair pr = pp[pos >> lg];
                     uint64_t tot = config_total(R, pr.u, pr.m, rc, dopt, S.vpp);
                     if (two) {
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(kRowThreads, 8)
                 }
             }
         }
+        ME_CHECK(cnt <= b - a);
         rows[k] = e;
         rcnt[k] = cnt;
     }
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(kRowThreads, 8)
 constexpr uint32_t kUnit = 32;         // rows per unit
 constexpr uint32_t kPairsSmem = 2048;  // pairs pool in shared memory when it fits (16 KB)
 constexpr uint32_t kFusedWarps = kThreads / 32;
+constexpr size_t kFusedSmemBytes = kPairsSmem * sizeof(DevPair) + (size_t)kFusedWarps * kUnit * sizeof(RowEnt);
 
 // Lane-constant values of one row for the lane's (rc, do) digit.
 struct Lane {
@@ -252,6 +255,7 @@ __device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, co
     for (uint32_t p0 = a; p0 < b; p0 += 32) {
         const uint32_t pos = p0 + lane;
         const bool valid = pos < b;
+        ME_CHECK(!valid || (pos >> S.lg_rcdo) < (w >> S.lg_rcdo));
         const DevPair pr = valid ? pp[pos >> S.lg_rcdo] : DevPair{0u, 0u};
         const uint32_t u = pr.u;
         uint64_t c4 = C.c4, c5 = C.c5, tot;
@@ -315,6 +319,7 @@ __device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, co
         }
         done += __popc(bal);
     }
+    ME_CHECK(done == cnt);  // K3 finds exactly the survivors K0 counted
 }
 
 template <int MODE, int NCAP, bool GBS, bool STMAX>
@@ -333,6 +338,7 @@ __device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __r
         if (unit >= n_units) break;
         if (!__ldg(ucnt + unit)) continue;
         const uint32_t k0 = unit * kUnit;
+        ME_CHECK(k0 < n_rows);
         const uint32_t nr = min(kUnit, n_rows - k0);
         const uint32_t c = lane < nr ? __ldg(rcnt + k0 + lane) : 0u;
         uint32_t inc = c;  // inclusive warp scan of the row counts
@@ -356,6 +362,7 @@ __device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __r
         while (nz) {
             const uint32_t i = __ffs(nz) - 1;
             nz &= nz - 1;
+            ME_CHECK(i < nr);
             const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
             const uint64_t oi = base + (__shfl_sync(0xffffffffu, inc, i) - ci);
             fused_row<MODE, NCAP, GBS, STMAX>(S, srow[i], st, (uint64_t)k0 + i, pairs, lo, hi, ci, oi, cols,
@@ -381,6 +388,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const bool pairs_smem = S.n_pairs <= kPairsSmem;
     if (pairs_smem)
         for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_pairs[i] = S.pairs[i];
+    ME_CHECK(kPairsSmem * sizeof(DevPair) + (threadIdx.x >> 5) * kUnit * sizeof(RowEnt) + kUnit * sizeof(RowEnt) <=
+             kFusedSmemBytes);
     __syncthreads();
     const DevPair* pairs = pairs_smem ? s_pairs : S.pairs;
     RowEnt* srow = s_rows + (threadIdx.x >> 5) * kUnit;
@@ -408,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
 }
 
-constexpr size_t kFusedSmem = kPairsSmem * sizeof(DevPair) + (size_t)kFusedWarps * kUnit * sizeof(RowEnt);
+constexpr size_t kFusedSmem = kFusedSmemBytes;
 
 uint32_t ncap_pad3(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
 

@@ -17,6 +17,8 @@ def _build_libme():
     b = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(b)
     b.build()
+    if os.environ.get("ME_CHECKED") == "1":
+        b.build(checked=True)
 
 
 def pytest_configure(config):

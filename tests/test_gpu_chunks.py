@@ -86,7 +86,7 @@ def test_whole_chunks_match_oracle(me, name):
         res = plan.sweep(b, e, mode=me.ME_OUT_COUNT)
         assert res.counts()[0] == r["count"] and res.cap_counts() == r["caps"], r["chunk"]
         res.free()
-    if name == "C4":
+    if name == "C4" and len(rows) == -(-plan.size // CHUNK):
         # all chunks present: the whole feasible set of C4
         res = plan.sweep(0, 0, mode=me.ME_OUT_COUNT)
         assert res.counts()[0] == sum(r["count"] for r in rows)
@@ -113,9 +113,9 @@ def test_whole_space_in_one_call_matches_chunks(me):
     result equals the chunk digests merged in order."""
     import torch
     rows = golden("C4")
-    if not rows:
-        pytest.skip("no golden chunks")
     plan = me.Plan(mi.config("C4"))
+    if len(rows) != -(-plan.size // CHUNK):
+        pytest.skip("C4 golden incomplete")
     total = sum(r["count"] for r in rows)
     idx = torch.empty(total, dtype=torch.int64, device="cuda")
     res = plan.sweep(0, 0, mode=me.ME_OUT_INDEX, out_cols=[idx])
