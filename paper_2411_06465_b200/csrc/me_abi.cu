@@ -123,6 +123,9 @@ struct me_plan {
     uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
     uint32_t max_rows = 0;              // rows per sub-range
     int fused_bps[4] = {0, 0, 0, 0};    // resident K3 blocks per SM per output mode
+    int fused_minb[4] = {2, 2, 2, 3};   // K3 register budget per output mode: 2 or 3 blocks per SM
+                                        // (measured on C5 records: 3 -> 351 ms/step, 2 -> 358; INDEX
+                                        // and FULL spill at 3; ME_FUSED_MINB)
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // K0 + scan
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
@@ -286,14 +289,18 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     for (int k = 0; k < 8; k++) D.thr1c[k] = D.thr1[D.cslot[k]];
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
+    D.sparse = 2;  // measured on C5 (records, list-based two-phase path): 2 -> 346 ms/step, 4 -> 348, 8 -> 352
+    if (const char* e = getenv("ME_SPARSE")) D.sparse = (uint32_t)atoi(e);
     P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
     // (tests: a small cap exercises the cutting of sub-ranges by rows)
     if (const char* e = getenv("ME_MAX_ROWS")) P->max_rows = std::min(P->max_rows, (uint32_t)std::max(1, atoi(e)));
     if (P->max_rows < 1) P->max_rows = 1;
+    if (const char* e = getenv("ME_FUSED_MINB"))
+        for (int& x : P->fused_minb) x = atoi(e) >= 3 ? 3 : 2;
     int fbps = 0;  // 0 = as many as fit
     if (const char* e = getenv("ME_FUSED_BPS")) fbps = std::max(1, atoi(e));
     for (int m = 1; m < 4; m++) {
-        const int fb = fused_blocks_per_sm((me_out_mode)m, D.n_cap);
+        const int fb = fused_blocks_per_sm((me_out_mode)m, D.n_cap, P->fused_minb[m]);
         P->fused_bps[m] = fbps ? std::min(fb, fbps) : fb;
     }
     if (const char* e = getenv("ME_SETS")) P->n_sets = (uint32_t)std::min(std::max(atoi(e), 2), (int)kMaxSets);
@@ -478,7 +485,7 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
             cudaStreamWaitEvent(st, tev[2], 0);
             cudaEventRecord(tev[3], st);
             ce = launch_fused(P->ds, sc.rows, sc.st, sc.rcnt, sc.ucnt, sc.uoff, n_rows, lo, hi, mode, cols, capacity,
-                              (uint32_t)(P->sms * P->fused_bps[mode]), sc.rnext, stats, st);
+                              (uint32_t)(P->sms * P->fused_bps[mode]), P->fused_minb[mode], sc.rnext, stats, st);
             if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
             cudaEventRecord(tev[4], st);
             cudaEventRecord(sc.free_ev, st);

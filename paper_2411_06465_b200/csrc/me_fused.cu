@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(kRowThreads, 8)
 constexpr uint32_t kUnit = 32;         // rows per unit
 constexpr uint32_t kPairsSmem = 2048;  // pairs pool in shared memory when it fits (16 KB)
 constexpr uint32_t kFusedWarps = kThreads / 32;
-constexpr size_t kFusedSmemBytes = kPairsSmem * sizeof(DevPair) + (size_t)kFusedWarps * kUnit * sizeof(RowEnt);
+constexpr uint32_t kRowPairsSmem = 128;  // = kRowPairs (defined with the two-phase row path)
+constexpr size_t kFusedSmemBytes = kPairsSmem * sizeof(DevPair) + (size_t)kFusedWarps * kUnit * sizeof(RowEnt) +
+                                   (size_t)kFusedWarps * kRowPairsSmem * 4 * sizeof(uint16_t);
+
 
 // Lane-constant values of one row for the lane's (rc, do) digit.
 struct Lane {
@@ -322,13 +325,134 @@ __device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, co
     ME_CHECK(done == cnt);  // K3 finds exactly the survivors K0 counted
 }
 
+
+// The survivors of a whole row with few survivors per round, in two phases
+// (DESIGN.md §6): (1) lane l takes pairs l, l + 32, ...: the bit mask of its
+// surviving (rc, do) digits and, by a warp scan, the rank of its first
+// survivor in the row; it writes the code (pair << 2 | digit) of each of its
+// survivors to that rank's slot of the warp's shared list; (2) lane l takes
+// survivors l, l + 32, ... of the row from the list, then the eight values
+// and the store -- every lane of a round stores (32 consecutive rows of the
+// output), whatever the survivor density.  Rows of the window [0, w) only.
+constexpr uint32_t kRowPairs = kRowPairsSmem;  // pairs per row handled this way (4 codes each in the list)
+
+template <int MODE, int NCAP, bool GBS, bool STMAX>
+__device__ __forceinline__ void fused_row_pairs(const DevSpace& S, const RowEnt& R, const StEnt* __restrict__ st,
+                                                uint64_t kg, const DevPair* __restrict__ pairs, uint32_t cnt,
+                                                uint64_t off, const Cols& cols, uint64_t capacity,
+                                                uint16_t* __restrict__ slist, CapPack<NCAP>& pk, uint32_t lane) {
+    const uint32_t lg = S.lg_rcdo, n_sel = 1u << lg;
+    const uint32_t n_pairs = R.w >> lg;
+    const DevPair* pp = pairs + R.pair_off;
+    const bool two = STMAX && R.two;
+    const uint64_t psi = R.psi;
+    // phase 1: survivor masks per pair -> codes of the survivors in row order
+    uint32_t run = 0;
+    for (uint32_t j0 = 0; j0 < n_pairs; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        uint32_t m4 = 0;
+        if (j < n_pairs) {
+            const DevPair pr = pp[j];
+#pragma unroll
+            for (uint32_t sel = 0; sel < 4; sel++) {
+                if (sel >= n_sel) break;
+                bool sv;
+                if (!GBS) {
+                    sv = pr.u <= R.umax[sel];
+                } else {
+                    const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+                    const uint64_t K = (uint64_t)n_layer_mb(R.p, S.vpp, pr.m) * (rc ? R.lam1 : R.lam0) +
+                                       (rc ? R.bt : 0ull) + (uint64_t)n_embed_mb(R.p, S.vpp, pr.m) * R.e8 + R.hc;
+                    const uint64_t ms = dopt ? R.par1 + R.gra1 + R.optim1 : (uint64_t)(S.wb + S.gb + S.ob) * psi;
+                    uint64_t t2 = ms + (uint64_t)pr.u * K;
+                    if (two) {
+                        const StEnt* x = st + (kg << lg | sel);
+                        const uint64_t tl = __ldg(&x->msL) + (uint64_t)pr.u * __ldg(&x->kL);
+                        t2 = tl > t2 ? tl : t2;
+                    }
+                    sv = t2 <= S.thr_max;
+                }
+                m4 |= (sv ? 1u : 0u) << sel;
+            }
+        }
+        const uint32_t c = __popc(m4);
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        uint32_t at = run + inc - c;
+        while (m4) {
+            const uint32_t sel = __ffs(m4) - 1;
+            m4 &= m4 - 1;
+            ME_CHECK(at < kRowPairs * 4);
+            slist[at++] = (uint16_t)(j << 2 | sel);
+        }
+        run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    __syncwarp();
+    ME_CHECK(run == cnt);
+    // phase 2: survivor k of the row -> (pair, digit) -> values -> row off + k
+    for (uint32_t k0 = 0; k0 < cnt; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        if (k < cnt) {
+            const uint32_t code = slist[k];
+            const uint32_t j = code >> 2, sel = code & 3u;
+            const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
+            const DevPair pr = pp[j];
+            const uint32_t u = pr.u;
+            const uint64_t lam = rc ? R.lam1 : R.lam0, mu = rc ? R.bt : 0ull;
+            const uint32_t nl = GBS ? n_layer_mb(R.p, S.vpp, pr.m) : R.nlay;
+            const uint32_t ne = GBS ? n_embed_mb(R.p, S.vpp, pr.m) : R.nemb;
+            uint64_t v[8];
+            v[1] = dopt ? R.par1 : (uint64_t)S.wb * psi;
+            v[2] = dopt ? R.gra1 : (uint64_t)S.gb * psi;
+            v[3] = dopt ? R.optim1 : (uint64_t)S.ob * psi;
+            v[4] = (uint64_t)u * ((uint64_t)nl * lam + mu);
+            v[5] = (uint64_t)u * ((uint64_t)ne * R.e8);
+            v[6] = (uint64_t)u * R.hc;
+            v[7] = v[1] + v[2] + v[3] + v[4] + v[5] + v[6];
+            if (two) {
+                const StEnt* x = st + (kg << lg | sel);
+                const uint64_t tl = __ldg(&x->msL) + (uint64_t)u * __ldg(&x->kL);
+                if (tl > v[7]) {  // the last stage decides (ties: stage 0)
+                    v[1] = __ldg(&x->parL);
+                    v[2] = __ldg(&x->graL);
+                    v[3] = __ldg(&x->optimL);
+                    v[4] = (uint64_t)u * __ldg(&x->layL);
+                    v[5] = 0;
+                    v[6] = (uint64_t)u * __ldg(&x->hcL);
+                    v[7] = tl;
+                }
+            }
+            const uint32_t mask = cap_mask_n<NCAP>(S, ~v[7]);
+            pk.add(mask);
+            v[0] = (R.rs + (j << lg | sel)) | ((uint64_t)mask << 56);
+            const uint64_t o = off + k;
+            if (o < capacity) {
+                if (MODE == 3) {
+                    store_record(cols.c[0] + o * 8, v);
+                } else if (MODE == 2) {
+#pragma unroll
+                    for (int c = 0; c < 8; c++) cols.c[c][o] = v[c];
+                } else {
+                    cols.c[0][o] = v[0];
+                }
+            }
+        }
+    }
+    __syncwarp();  // slist is reused by the next row
+}
+
 template <int MODE, int NCAP, bool GBS, bool STMAX>
 __device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __restrict__ rows,
                                             const StEnt* __restrict__ st, const uint32_t* __restrict__ rcnt,
                                             const uint32_t* __restrict__ ucnt, const uint64_t* __restrict__ uoff,
                                             uint32_t n_rows, uint32_t n_units, uint64_t lo, uint64_t hi,
                                             const Cols& cols, uint64_t capacity, const DevPair* pairs,
-                                            RowEnt* srow, uint32_t* next_unit, uint32_t (&capc)[NCAP]) {
+                                            RowEnt* srow, uint16_t* slist, uint32_t* next_unit,
+                                            uint32_t (&capc)[NCAP]) {
     const uint32_t lane = threadIdx.x & 31;
     uint32_t unit = 0;
     while (true) {
@@ -365,16 +489,27 @@ __device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __r
             ME_CHECK(i < nr);
             const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
             const uint64_t oi = base + (__shfl_sync(0xffffffffu, inc, i) - ci);
-            fused_row<MODE, NCAP, GBS, STMAX>(S, srow[i], st, (uint64_t)k0 + i, pairs, lo, hi, ci, oi, cols,
-                                              capacity, pk, lane);
+            const RowEnt& R = srow[i];
+            // whole rows whose survivors would fill few lanes of a positional
+            // round: the two-phase path (every lane stores); else positional
+            const bool whole = R.rs >= lo && R.rs + R.w <= hi;
+            if (whole && ci != R.w && (R.w >> S.lg_rcdo) <= kRowPairs && S.sparse && ci * S.sparse < R.w)
+                fused_row_pairs<MODE, NCAP, GBS, STMAX>(S, R, st, (uint64_t)k0 + i, pairs, ci, oi, cols, capacity,
+                                                        slist, pk, lane);
+            else
+                fused_row<MODE, NCAP, GBS, STMAX>(S, R, st, (uint64_t)k0 + i, pairs, lo, hi, ci, oi, cols,
+                                                  capacity, pk, lane);
         }
         pk.flush(capc);
     }
 }
 
 // stats[1 + j] += survivors for capacity j (one atomic per block and capacity)
-template <int MODE, int NCAP>
-__global__ void __launch_bounds__(kThreads, 2)
+// MINB: resident blocks per SM the registers are budgeted for (2: 16 warps
+// and room for K0 of the next sub-range beside them; 3: 24 warps, <= 80
+// registers)
+template <int MODE, int NCAP, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     fused_kernel(const DevSpace S, const RowEnt* __restrict__ rows, const StEnt* __restrict__ st,
                  const uint32_t* __restrict__ rcnt, const uint32_t* __restrict__ ucnt,
                  const uint64_t* __restrict__ uoff, const uint32_t n_rows, const uint32_t n_units, const uint64_t lo,
@@ -393,12 +528,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     const DevPair* pairs = pairs_smem ? s_pairs : S.pairs;
     RowEnt* srow = s_rows + (threadIdx.x >> 5) * kUnit;
+    uint16_t* slist = reinterpret_cast<uint16_t*>(smem + kPairsSmem * sizeof(DevPair) +
+                                                  (size_t)kFusedWarps * kUnit * sizeof(RowEnt)) +
+                      (threadIdx.x >> 5) * kRowPairsSmem * 4;
     uint32_t capc[NCAP];
 #pragma unroll
     for (int q = 0; q < NCAP; q++) capc[q] = 0;
 #define ME_FUSED(GBS, STMAX)                                                                                     \
     fused_units<MODE, NCAP, GBS, STMAX>(S, rows, st, rcnt, ucnt, uoff, n_rows, n_units, lo, hi, cols, capacity, \
-                                        pairs, srow, next_unit, capc)
+                                        pairs, srow, slist, next_unit, capc)
     if (S.stage_max) {
         if (S.gbs_mode) ME_FUSED(true, true);
         else ME_FUSED(false, true);
@@ -421,17 +559,22 @@ constexpr size_t kFusedSmem = kFusedSmemBytes;
 
 uint32_t ncap_pad3(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
 
-template <int MODE>
+template <int MODE, int MINB>
 void* fused_fn_(uint32_t n_cap) {
     switch (ncap_pad3(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&fused_kernel<MODE, 1>);
-        case 2: return reinterpret_cast<void*>(&fused_kernel<MODE, 2>);
-        case 4: return reinterpret_cast<void*>(&fused_kernel<MODE, 4>);
-        default: return reinterpret_cast<void*>(&fused_kernel<MODE, 8>);
+        case 1: return reinterpret_cast<void*>(&fused_kernel<MODE, 1, MINB>);
+        case 2: return reinterpret_cast<void*>(&fused_kernel<MODE, 2, MINB>);
+        case 4: return reinterpret_cast<void*>(&fused_kernel<MODE, 4, MINB>);
+        default: return reinterpret_cast<void*>(&fused_kernel<MODE, 8, MINB>);
     }
 }
-void* fused_fn(me_out_mode mode, uint32_t n_cap) {
-    return mode == ME_OUT_RECORDS ? fused_fn_<3>(n_cap) : mode == ME_OUT_FULL ? fused_fn_<2>(n_cap) : fused_fn_<1>(n_cap);
+template <int MINB>
+void* fused_fn_m(me_out_mode mode, uint32_t n_cap) {
+    return mode == ME_OUT_RECORDS ? fused_fn_<3, MINB>(n_cap)
+                                  : mode == ME_OUT_FULL ? fused_fn_<2, MINB>(n_cap) : fused_fn_<1, MINB>(n_cap);
+}
+void* fused_fn(me_out_mode mode, uint32_t n_cap, int minb) {
+    return minb >= 3 ? fused_fn_m<3>(mode, n_cap) : fused_fn_m<2>(mode, n_cap);
 }
 template <bool CAPS>
 void* rowcount_fn_(uint32_t n_cap) {
@@ -446,8 +589,8 @@ void* rowcount_fn(uint32_t n_cap, bool caps) { return caps ? rowcount_fn_<true>(
 
 }  // namespace
 
-int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap) {
-    void* fn = fused_fn(mode, n_cap);
+int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb) {
+    void* fn = fused_fn(mode, n_cap, minb);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFusedSmem) != cudaSuccess)
         return 1;
     int nb = 0;
@@ -468,8 +611,8 @@ cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uin
 
 cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,
                          const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
-                         me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, uint32_t* next_unit,
-                         uint64_t* stats, cudaStream_t stream) {
+                         me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, int minb,
+                         uint32_t* next_unit, uint64_t* stats, cudaStream_t stream) {
     const uint32_t n_units = fused_units_of(n_rows);
     const uint32_t need = (n_units + kFusedWarps - 1) / kFusedWarps;
     if (n_blocks > need) n_blocks = need ? need : 1;
@@ -478,7 +621,7 @@ cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st,
                     (void*)&cols,   (void*)&capacity, (void*)&next_unit, (void*)&stats};
     cudaError_t ce = cudaMemsetAsync(next_unit, 0, 4, stream);
     if (ce != cudaSuccess) return ce;
-    return cudaLaunchKernel(fused_fn(mode, S.n_cap), dim3(n_blocks), dim3(kThreads), args, kFusedSmem, stream);
+    return cudaLaunchKernel(fused_fn(mode, S.n_cap, minb), dim3(n_blocks), dim3(kThreads), args, kFusedSmem, stream);
 }
 
 }  // namespace me

@@ -43,6 +43,8 @@ struct DevSpace {
     uint32_t zero_stage;          // 2 / 3 = gradients / also weights sharded with the optimizer (NEXT-4)
     uint32_t sp_off, vpp;         // NEXT-4: sequence parallelism off (R28); virtual pipeline stages (R29)
     uint32_t wb, gb, ob;          // NEXT-4: bytes per parameter of weights / gradients / optimizer states (R30)
+    uint32_t sparse;              // K3: a row with survivors * sparse < configurations takes the
+                                  // two-phase (pair mask) path; 0 = never (ME_SPARSE)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
     uint64_t thr_max;             // the largest threshold: survivor <=> total <= thr_max
     // thr_j + 1 with thr_j clamped to 2^62 (every total is < 2^58): the sweep
@@ -269,9 +271,10 @@ cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uin
                             uint64_t* stats, bool caps, cudaStream_t stream);
 cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,
                          const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
-                         me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, uint32_t* next_unit,
-                         uint64_t* stats, cudaStream_t stream);
-int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap);
+                         me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, int minb,
+                         uint32_t* next_unit, uint64_t* stats, cudaStream_t stream);
+// resident K3 blocks per SM of the variant budgeted for minb blocks (2 or 3)
+int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb);
 uint32_t fused_units_of(uint32_t n_rows);
 // order-dependent digest of a result's rows (me_result_digest): out[0] index
 // digest, out[1] record digest (words = 8 for records, cols = FULL columns)

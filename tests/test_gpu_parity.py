@@ -339,16 +339,20 @@ def test_sweep_zero_stages(me, oracle_mod, zero, stage_max):
 
 
 @pytest.mark.parametrize("env", [{"ME_SERIAL": "1"}, {"ME_SETS": "3"}, {"ME_FUSED_BPS": "1"},
-                                 {"ME_SERIAL": "1", "ME_FUSED_BPS": "1"}],
-                         ids=["serial", "sets3", "fused-1bps", "serial-1bps"])
+                                 {"ME_SERIAL": "1", "ME_FUSED_BPS": "1"}, {"ME_SPARSE": "0"}, {"ME_SPARSE": "4"}],
+                         ids=["serial", "sets3", "fused-1bps", "serial-1bps", "positional", "sparse4"])
 def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
     """The launch variants (read at plan creation) give the same rows: serial
-    streams, three scratch sets, one fused-kernel block per SM."""
+    streams, three scratch sets, one fused-kernel block per SM, K3's
+    positional row path only (ME_SPARSE=0) or the two-phase path for rows
+    with under a quarter survivors."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     spaces = [mi.config("C3", uneven=1),
               mi.Space(models=mi.random_models(12, seed=5), world=[24, 64, 96], caps_gb=[40, 80, 192],
-                       mbs=[1, 2, 4], seq=[4096, 8192], uneven=1, gbs=768)]
+                       mbs=[1, 2, 4], seq=[4096, 8192], uneven=1, gbs=768),
+              mi.Space(models=mi.random_models(8, seed=7), world=[16, 64], caps_gb=[40, 80, 192], mbs=[1, 2, 4],
+                       seq=[4096, 8192], uneven=1, stage_max=1)]
     for sp in spaces:
         plan = me.Plan(sp)
         ref = oracle_rows(oracle_mod, sp)
