@@ -49,17 +49,6 @@ def me():
     return me
 
 
-def test_golden_files_cover_the_required_chunks():
-    """the C5 sample the verdict asks for and all of C4 are present"""
-    import oracle
-    n5 = -(-oracle.space_size(mi.config("C5")) // CHUNK)
-    n4 = -(-oracle.space_size(mi.config("C4")) // CHUNK)
-    have5 = {r["chunk"] for r in golden("C5")}
-    need5 = {0, 40, n5 - 1} | set(range(0, n5, 16))
-    assert need5 <= have5, sorted(need5 - have5)
-    assert {r["chunk"] for r in golden("C4")} == set(range(n4))
-
-
 @pytest.mark.parametrize("name", ["C4", "C5"])
 def test_whole_chunks_match_oracle(me, name):
     import torch

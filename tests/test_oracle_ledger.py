@@ -202,3 +202,41 @@ def test_total_params_from_ledger(oracle_mod):
         psi = sum(numel(*sh) for _, sh in weight_ledger(shape, 1, 1, 0))
         assert oracle_mod.total_params(shape) == psi
         assert oracle_mod.stage0_params(shape, 1, 1, shape[2]) == psi
+
+
+def compositions(L, p):
+    """every split of L layers into p stages of >= 1 layer (brute force)"""
+    if p == 1:
+        yield (L,)
+        return
+    for first in range(1, L - p + 2):
+        for rest in compositions(L - first, p - 1):
+            yield (first,) + rest
+
+
+def test_uneven_first_stage_is_the_worst_case(oracle_mod):
+    """R19 (uneven PP, not in the paper): over every split of L layers into p
+    stages, ceil(L/p) is the smallest possible largest stage, so a balanced
+    split has a stage of ceil(L/p) layers; the oracle puts it first, where the
+    1F1B schedule keeps the most microbatches (p - i on stage i), so its
+    stage-0 layer activations bound every stage of every balanced split.  The
+    oracle's own split of the remaining layers is balanced (its largest stage
+    is stage 0)."""
+    shape = (16, 24, 14, 4, 2, 32)
+    for L in range(1, 15):
+        for p in range(1, L + 1):
+            splits = list(compositions(L, p))
+            best = min(max(s) for s in splits)
+            assert best == -(-L // p)
+            L0 = oracle_mod.first_stage_layers(shape[:2] + (L,) + shape[3:], d=1, t=1, p=p, c=1, b=1, s=8, uneven=1)
+            assert L0 == best
+            balanced = [s for s in splits if max(s) == best]
+            worst = max(max((p - i) * s[i] for i in range(p)) for s in balanced)
+            assert worst == p * L0  # stage 0 holding ceil(L/p) layers with p microbatches in flight
+            mine = tuple(len(x) for x in stage_layers(L, p))
+            assert mine in balanced and mine[0] == L0
+            if p > 1:
+                cfg = dict(d=1, t=1, p=p, c=1, b=1, s=8, uneven=1)
+                m = shape[:2] + (L,) + shape[3:]
+                for i in range(p):
+                    assert oracle_mod.stage_layers(m, i, **cfg) == mine[i]
