@@ -52,12 +52,11 @@ __device__ __forceinline__ bool fits(const Digit& c, uint32_t u, uint64_t thr) {
 }
 
 // number of leading entries of the ascending su[0, n) that fit under thr
-__device__ __forceinline__ uint32_t count_fit(const uint32_t* __restrict__ su, uint32_t n, const Digit& c,
-                                              uint64_t thr) {
+__device__ __forceinline__ uint32_t count_fit(const uint32_t* su, uint32_t n, const Digit& c, uint64_t thr) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (fits(c, __ldg(su + mid), thr)) lo = mid + 1;
+        if (fits(c, su[mid], thr)) lo = mid + 1;
         else hi = mid;
     }
     return lo;
@@ -67,8 +66,36 @@ __device__ __forceinline__ uint32_t count_fit(const uint32_t* __restrict__ su, u
 // CAPS: count the survivors of every capacity too (COUNT mode; the output
 // kernel counts them from the masks it computes anyway in the other modes).
 // Blocks of kRowThreads threads at <= 64 registers, so that K0 of the next
-// sub-range fits beside the resident output-kernel blocks.
+// sub-range fits beside the resident output-kernel blocks.  The sorted u
+// lists are staged in shared memory when they fit; a row's binary searches
+// (one per digit) run in lockstep, so their loads are in flight together.
 constexpr uint32_t kRowThreads = 128;
+constexpr uint32_t kSuSmem = 4096;  // sorted-u entries staged in shared memory (16 KB)
+
+// per digit q < n_sel (total ms_q + u K_q), the number of leading entries of
+// su[0, hi0_q) that fit under thr: the binary searches run in lockstep
+__device__ __forceinline__ void count_fit4(const uint32_t* su, const uint64_t (&ms)[4], const uint64_t (&K)[4],
+                                          uint32_t n_sel, const uint32_t (&hi0)[4], uint64_t thr,
+                                          uint32_t (&out)[4]) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) lo[q] = 0, hi[q] = (uint32_t)q < n_sel ? hi0[q] : 0u;
+    while (true) {
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (lo[q] < hi[q]) {
+                const uint32_t mid = (lo[q] + hi[q]) >> 1;
+                if (ms[q] + (uint64_t)su[mid] * K[q] <= thr) lo[q] = mid + 1;
+                else hi[q] = mid;
+                any = true;
+            }
+        }
+        if (!any) break;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) out[q] = lo[q];
+}
 
 template <int NCAP, bool CAPS>
 __global__ void __launch_bounds__(kRowThreads, 8)
@@ -77,8 +104,12 @@ __global__ void __launch_bounds__(kRowThreads, 8)
                     StEnt* __restrict__ st, uint32_t* __restrict__ rcnt, uint32_t* __restrict__ ucnt,
                     uint64_t* __restrict__ stats) {
     __shared__ uint32_t s_cap[NCAP];
+    __shared__ uint32_t s_su[kSuSmem];
     if (CAPS && threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
-    if (CAPS) __syncthreads();
+    const bool su_smem = !S.gbs_mode && S.n_pairs <= kSuSmem;
+    if (su_smem)
+        for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_su[i] = __ldg(S.pair_su + i);
+    __syncthreads();
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t cnt = 0;
     uint32_t capc[NCAP];
@@ -90,33 +121,62 @@ __global__ void __launch_bounds__(kRowThreads, 8)
         const Policy Q = policy_of(S);
         make_row(I.M, I.tu.t, I.tu.c, I.tu.p, I.tu.d, I.L0, Q, R);
         const bool two = S.stage_max && I.tu.p >= 2;
-        RowEnt e = row_entry(I, R, two);
+        rows[k] = row_entry(I, R, two);  // umax[] below
+        uint32_t umax[4] = {0, 0, 0, 0};
         const uint32_t lg = S.lg_rcdo, n_sel = 1u << lg;
         // the row's window of the range: [a, b) of its positions
         const uint32_t a = I.rs < lo ? (uint32_t)(lo - I.rs) : 0u;
         const uint32_t b = I.rs + I.tu.w > hi ? (uint32_t)(hi - I.rs) : I.tu.w;
         const bool full = a == 0 && b == I.tu.w;
-        const uint32_t* su = S.pair_su + I.tu.pair_off;
+        const uint32_t* su = (su_smem ? s_su : S.pair_su) + I.tu.pair_off;
         const DevPair* pp = S.pairs + I.tu.pair_off;
+        // per digit: stage-0 total = ms + u K in paper mode
+        uint64_t ms[4], K[4];
 #pragma unroll
         for (uint32_t sel = 0; sel < 4; sel++) {
-            if (sel >= n_sel) break;
+            ms[sel] = K[sel] = 0;
+            if (sel >= n_sel) continue;
             const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
-            Digit c;
-            c.ms = dopt ? R.ms1 : R.ms0;
+            ms[sel] = dopt ? R.ms1 : R.ms0;
             // per-token bytes in paper mode: n_lay lam + mu + n_emb e8 + hc
-            c.K = (uint64_t)R.nlay * (rc ? R.lam1 : R.lam0) + (rc ? R.bt : 0ull) + (uint64_t)R.nemb * R.e8 + R.hc;
-            c.two = two;
-            c.msL = c.kL = 0;
-            if (two) {
-                const StEnt x = last_stage(I, rc, dopt, Q);
-                st[(size_t)k << lg | sel] = x;
-                c.msL = x.msL;
-                c.kL = x.kL;
+            K[sel] = (uint64_t)R.nlay * (rc ? R.lam1 : R.lam0) + (rc ? R.bt : 0ull) + (uint64_t)R.nemb * R.e8 + R.hc;
+            if (two) st[(size_t)k << lg | sel] = last_stage(I, rc, dopt, Q);
+        }
+        if (!S.gbs_mode && !two) {
+            const uint32_t np = I.tu.n_pairs;
+            const uint32_t all4[4] = {np, np, np, np};
+            uint32_t nm[4];
+            count_fit4(su, ms, K, n_sel, all4, S.thr_max, nm);
+#pragma unroll
+            for (uint32_t sel = 0; sel < 4; sel++) {
+                if (sel >= n_sel) break;
+                umax[sel] = nm[sel] ? su[nm[sel] - 1] : 0u;  // u >= 1: 0 admits nothing
+                if (full) cnt += nm[sel];
             }
-            if (!S.gbs_mode) {
+            if (CAPS && full) {
+#pragma unroll
+                for (int q = 0; q < NCAP; q++) {
+                    if (q >= (int)S.n_cap) break;
+                    if (S.thr[q] >= S.thr_max) {
+                        capc[q] += nm[0] + nm[1] + nm[2] + nm[3];
+                    } else {
+                        uint32_t nq[4];
+                        count_fit4(su, ms, K, n_sel, nm, S.thr[q], nq);
+                        capc[q] += nq[0] + nq[1] + nq[2] + nq[3];
+                    }
+                }
+            }
+        } else if (!S.gbs_mode) {
+            // NEXT-1: the largest of two stage totals, one digit at a time
+            for (uint32_t sel = 0; sel < n_sel; sel++) {
+                const StEnt* x = st + ((size_t)k << lg | sel);
+                Digit c{ms[sel], K[sel], x->msL, x->kL, true};
                 const uint32_t nm = count_fit(su, I.tu.n_pairs, c, S.thr_max);
-                e.umax[sel] = nm ? __ldg(su + nm - 1) : 0u;  // u >= 1: 0 admits nothing
+                const uint32_t um = nm ? su[nm - 1] : 0u;
+                if (sel == 0) umax[0] = um;
+                else if (sel == 1) umax[1] = um;
+                else if (sel == 2) umax[2] = um;
+                else umax[3] = um;
                 if (full) {
                     cnt += nm;
                     if (CAPS) {
@@ -126,15 +186,21 @@ __global__ void __launch_bounds__(kRowThreads, 8)
                     }
                 }
             }
-            if (!full || S.gbs_mode) {
-                // config by config over the window's positions of this digit:
-                // in-flight count min(p, m) of each pair (R17), or a cut row
+        }
+        if (!full || S.gbs_mode) {
+            // config by config over the window: in-flight counts of each
+            // pair's m microbatches (R17, R29), or a cut row
+#pragma unroll
+            for (uint32_t sel = 0; sel < 4; sel++) {
+                if (sel >= n_sel) break;
+                const uint32_t rc = (S.rcdo_rc >> sel) & 1u, dopt = (S.rcdo_do >> sel) & 1u;
                 for (uint32_t pos = a + ((sel - a) & (n_sel - 1u)); pos < b; pos += n_sel) {
                     ME_CHECK((pos >> lg) < I.tu.n_pairs);
                     const DevPair pr = pp[pos >> lg];
                     uint64_t tot = config_total(R, pr.u, pr.m, rc, dopt, S.vpp);
                     if (two) {
-                        const uint64_t tl = c.msL + (uint64_t)pr.u * c.kL;
+                        const StEnt* x = st + ((size_t)k << lg | sel);
+                        const uint64_t tl = x->msL + (uint64_t)pr.u * x->kL;
                         tot = tl > tot ? tl : tot;
                     }
                     cnt += tot <= S.thr_max ? 1u : 0u;
@@ -146,7 +212,7 @@ __global__ void __launch_bounds__(kRowThreads, 8)
             }
         }
         ME_CHECK(cnt <= b - a);
-        rows[k] = e;
+        *reinterpret_cast<uint4*>(&rows[k].umax[0]) = make_uint4(umax[0], umax[1], umax[2], umax[3]);
         rcnt[k] = cnt;
     }
     // survivors per 32-row unit (a unit is one warp of this kernel)
