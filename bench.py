@@ -274,7 +274,7 @@ def run_steps(torch, dist, me, plan, calls, mode, ring, flush, stream, steps, wa
 
 def ncu_summary():
     """per-kernel ncu figures of one C5 chunk at HEAD (scripts/ncu_summary.py)"""
-    for name in ("r2_final", "r2"):
+    for name in ("r2_final", "r2b"):
         f = ROOT / "profiles" / name / "ncu_chunk40.json"
         if f.exists():
             return json.loads(f.read_text()), f"profiles/{name}/ncu_chunk40.json"
@@ -373,7 +373,8 @@ def main():
             v = ncu["kernels"].get(k)
             if v:
                 issue[k] = {"issue_frac": v.get("issue_frac"), "warp_instr": v.get("warp_instr"),
-                            "thread_instr_per_config": v.get("thread_instr_per_config")}
+                            "warp_instr_per_config": v.get("warp_instr_per_config"),
+                            "pipe_alu_pct": v.get("pipe_alu_pct"), "pipe_fma_pct": v.get("pipe_fma_pct")}
         if mode == me.ME_OUT_COUNT and issue.get("rowcount_kernel"):
             roof.update({"frac": issue["rowcount_kernel"]["issue_frac"], "traffic_note": "issue fraction from ncu"})
     line = {

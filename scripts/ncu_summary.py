@@ -45,7 +45,10 @@ for r in rows[2:]:
         continue  # keep the longest launch of each kernel
     name = base
     out["kernels"][name] = {
-        "warp_instr": inst, "thread_instr_per_config": tinst / configs if tinst else None,
+        "warp_instr": inst, "warp_instr_per_config": inst / configs if inst else None,
+        "thread_instr_per_config": tinst / configs if tinst else None,
+        "pipe_alu_pct": f(d, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+        "pipe_fma_pct": f(d, "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
         "issue_frac": inst / (cyc * nsm * 4) if inst and cyc else None,
         "duration_ms": f(d, "gpu__time_duration.sum"),
         "dram_bytes_read": f(d, "dram__bytes_read.sum"), "dram_bytes_write": f(d, "dram__bytes_write.sum"),
