@@ -123,9 +123,10 @@ struct me_plan {
     uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
     uint32_t max_rows = 0;              // rows per sub-range
     int fused_bps[4] = {0, 0, 0, 0};    // resident K3 blocks per SM per output mode
-    int fused_minb[4] = {2, 2, 2, 3};   // K3 register budget per output mode: 2 or 3 blocks per SM
-                                        // (measured on C5 records: 3 -> 351 ms/step, 2 -> 358; INDEX
-                                        // and FULL spill at 3; ME_FUSED_MINB)
+    int fused_minb[4] = {2, 3, 2, 3};   // K3 register budget per output mode: 2 or 3 blocks per SM
+                                        // (measured on C5: records 3 -> 351 ms/step, 2 -> 358; INDEX
+                                        // 3 -> 193, 2 -> 220 despite a few spilled registers; FULL
+                                        // spills more at 3; ME_FUSED_MINB)
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // K0 + scan
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
