@@ -123,8 +123,6 @@ struct me_plan {
     uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
     uint32_t max_rows = 0;              // rows per sub-range
     int fused_bps[4] = {0, 0, 0, 0};    // resident K3 blocks per SM per output mode
-    int onepass_bps[4] = {0, 0, 0, 0};  // the same for the one-pass kernel
-    int onepass = 0;                    // 1: K0 + scan + K3 as one kernel with a decoupled look-back (ME_ONEPASS)
     int fused_minb[4] = {2, 3, 2, 3};   // K3 register budget per output mode: 2 or 3 blocks per SM
                                         // (measured on C5: records 3 -> 351 ms/step, 2 -> 358; INDEX
                                         // 3 -> 193, 2 -> 220 despite a few spilled registers; FULL
@@ -302,12 +300,9 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         for (int& x : P->fused_minb) x = atoi(e) >= 3 ? 3 : 2;
     int fbps = 0;  // 0 = as many as fit
     if (const char* e = getenv("ME_FUSED_BPS")) fbps = std::max(1, atoi(e));
-    if (const char* e = getenv("ME_ONEPASS")) P->onepass = atoi(e) ? 1 : 0;
     for (int m = 1; m < 4; m++) {
         const int fb = fused_blocks_per_sm((me_out_mode)m, D.n_cap, P->fused_minb[m]);
         P->fused_bps[m] = fbps ? std::min(fb, fbps) : fb;
-        const int ob = onepass_blocks_per_sm((me_out_mode)m, D.n_cap, P->fused_minb[m]);
-        P->onepass_bps[m] = fbps ? std::min(ob, fbps) : ob;
     }
     if (const char* e = getenv("ME_SETS")) P->n_sets = (uint32_t)std::min(std::max(atoi(e), 2), (int)kMaxSets);
     const uint32_t max_units = fused_units_of(P->max_rows) + 1;
@@ -480,19 +475,6 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
         cudaStreamWaitEvent(cs, sc.free_ev, 0);
         cudaEventRecord(tev[0], cs);
         cudaError_t ce;
-        if (write && P->onepass) {
-            // one kernel on the caller's stream: rows, counts, look-back offsets, stores
-            cudaEventRecord(tev[1], cs);
-            cudaEventRecord(tev[2], cs);
-            cudaStreamWaitEvent(st, tev[2], 0);
-            cudaEventRecord(tev[3], st);
-            ce = launch_onepass(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.st, sc.uoff, mode, cols, capacity,
-                                (uint32_t)(P->sms * P->onepass_bps[mode]), P->fused_minb[mode], sc.rnext, stats, st);
-            if (ce != cudaSuccess) return cuda_err(ce, "one-pass kernel");
-            cudaEventRecord(tev[4], st);
-            cudaEventRecord(sc.free_ev, st);
-            continue;
-        }
         ce = launch_rowcount(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.rows, sc.st, sc.rcnt, sc.ucnt,
                              stats, !write, cs);
         if (ce != cudaSuccess) return cuda_err(ce, "row kernel");

@@ -658,164 +658,6 @@ void* fused_fn(me_out_mode mode, uint32_t n_cap, int minb) {
     return minb >= 3 ? fused_fn_m<3>(mode, n_cap) : fused_fn_m<2>(mode, n_cap);
 }
 
-// ---------------------------------------------------------------- one pass
-// K0 and K3 in one kernel (ME_ONEPASS): a warp takes a 32-row unit, computes
-// its rows into its shared copy (lane = row: row_count), publishes the unit's
-// survivor count, finds the unit's output offset by a decoupled look-back over
-// the earlier units' published counts / prefixes, publishes its inclusive
-// prefix and writes the survivors as K3 does.  No row entries, counts or
-// offsets go through HBM and no scan kernel runs.  Units are taken in order
-// from a counter, so every unit an earlier unit waits for is owned by a
-// running warp.  state[u]: 0 = not ready, (1 << 62) | count, (2 << 62) |
-// inclusive prefix; stats[0] holds the running total of earlier sub-ranges
-// when the kernel starts (read by unit 0) and this sub-range's end when it
-// finishes (written by the last unit).
-constexpr uint64_t kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
-
-__device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
-    return *reinterpret_cast<const volatile uint64_t*>(p);
-}
-__device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) { *reinterpret_cast<volatile uint64_t*>(p) = v; }
-
-constexpr size_t kOnepassSmem = kFusedSmemBytes + kSuSmem * sizeof(uint32_t);
-
-template <int MODE, int NCAP, bool GBS, bool STMAX>
-__device__ __forceinline__ void onepass_units(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t n_units,
-                                              uint32_t seg_lo, uint32_t n_seg_sub, uint64_t lo, uint64_t hi,
-                                              const uint32_t* su_base, StEnt* __restrict__ st,
-                                              uint64_t* __restrict__ state, const Cols& cols, uint64_t capacity,
-                                              const DevPair* pairs, RowEnt* srow, uint16_t* slist,
-                                              uint32_t* next_unit, uint64_t* stats, uint32_t (&capc)[NCAP]) {
-    const uint32_t lane = threadIdx.x & 31;
-    uint32_t unit = 0;
-    while (true) {
-        if (lane == 0) unit = atomicAdd(next_unit, 1u);
-        unit = __shfl_sync(0xffffffffu, unit, 0);
-        if (unit >= n_units) break;
-        const uint32_t k0 = unit * kUnit;
-        const uint32_t nr = min(kUnit, n_rows - k0);
-        __syncwarp();  // the previous unit's readers are done with srow
-        uint32_t c = 0;
-        if (lane < nr) {
-            uint32_t nocap[NCAP];
-            c = row_count<NCAP, false>(S, g0 + k0 + lane, k0 + lane, seg_lo, n_seg_sub, lo, hi, su_base,
-                                       srow + lane, st, nocap);
-        }
-        uint32_t inc = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= (uint32_t)o) inc += y;
-        }
-        const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
-        uint64_t base = 0;
-        if (lane == 0) {
-            if (unit == 0) {
-                base = ld_volatile(stats);
-            } else {
-                st_volatile(state + unit, kAgg | agg);
-                for (uint32_t j = unit - 1;; j--) {
-                    uint64_t v;
-                    do {
-                        v = ld_volatile(state + j);
-                    } while (!(v >> 62));
-                    base += v & kVal;
-                    if (v & kPre) break;
-                    ME_CHECK(j > 0);
-                }
-            }
-            st_volatile(state + unit, kPre | (base + agg));
-            if (unit == n_units - 1) st_volatile(stats, base + agg);
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        __syncwarp();  // srow (and st) written by every lane
-        uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
-        CapPack<NCAP> pk;
-        while (nz) {
-            const uint32_t i = __ffs(nz) - 1;
-            nz &= nz - 1;
-            const uint32_t ci = __shfl_sync(0xffffffffu, c, i);
-            const uint64_t oi = base + (__shfl_sync(0xffffffffu, inc, i) - ci);
-            const RowEnt& R = srow[i];
-            const bool whole = R.rs >= lo && R.rs + R.w <= hi;
-            if (whole && ci != R.w && (R.w >> S.lg_rcdo) <= kRowPairs && S.sparse && ci * S.sparse < R.w)
-                fused_row_pairs<MODE, NCAP, GBS, STMAX>(S, R, st, (uint64_t)k0 + i, pairs, ci, oi, cols, capacity,
-                                                        slist, pk, lane);
-            else
-                fused_row<MODE, NCAP, GBS, STMAX>(S, R, st, (uint64_t)k0 + i, pairs, lo, hi, ci, oi, cols,
-                                                  capacity, pk, lane);
-        }
-        pk.flush(capc);
-    }
-}
-
-template <int MODE, int NCAP, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-    onepass_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows, const uint32_t n_units,
-                   const uint32_t seg_lo, const uint32_t n_seg_sub, const uint64_t lo, const uint64_t hi,
-                   StEnt* __restrict__ st, uint64_t* __restrict__ state, const Cols cols, const uint64_t capacity,
-                   uint32_t* __restrict__ next_unit, uint64_t* __restrict__ stats) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t s_cap[NCAP];
-    if (threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
-    DevPair* s_pairs = reinterpret_cast<DevPair*>(smem);
-    RowEnt* s_rows = reinterpret_cast<RowEnt*>(smem + kPairsSmem * sizeof(DevPair));
-    uint32_t* s_su = reinterpret_cast<uint32_t*>(smem + kFusedSmemBytes);
-    const bool pairs_smem = S.n_pairs <= kPairsSmem;
-    const bool su_smem = !S.gbs_mode && S.n_pairs <= kSuSmem;
-    if (pairs_smem)
-        for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_pairs[i] = S.pairs[i];
-    if (su_smem)
-        for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_su[i] = __ldg(S.pair_su + i);
-    __syncthreads();
-    const DevPair* pairs = pairs_smem ? s_pairs : S.pairs;
-    RowEnt* srow = s_rows + (threadIdx.x >> 5) * kUnit;
-    uint16_t* slist = reinterpret_cast<uint16_t*>(smem + kPairsSmem * sizeof(DevPair) +
-                                                  (size_t)kFusedWarps * kUnit * sizeof(RowEnt)) +
-                      (threadIdx.x >> 5) * kRowPairsSmem * 4;
-    uint32_t capc[NCAP];
-#pragma unroll
-    for (int q = 0; q < NCAP; q++) capc[q] = 0;
-#define ME_ONEPASS(GBS, STMAX)                                                                                    \
-    onepass_units<MODE, NCAP, GBS, STMAX>(S, g0, n_rows, n_units, seg_lo, n_seg_sub, lo, hi,                     \
-                                          su_smem ? s_su : S.pair_su, st, state, cols, capacity, pairs, srow,    \
-                                          slist, next_unit, stats, capc)
-    if (S.stage_max) {
-        if (S.gbs_mode) ME_ONEPASS(true, true);
-        else ME_ONEPASS(false, true);
-    } else {
-        if (S.gbs_mode) ME_ONEPASS(true, false);
-        else ME_ONEPASS(false, false);
-    }
-#undef ME_ONEPASS
-#pragma unroll
-    for (int q = 0; q < NCAP; q++) {
-        const uint32_t c = __reduce_add_sync(0xffffffffu, capc[q]);
-        if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cap + q, c);
-    }
-    __syncthreads();
-    if (threadIdx.x < NCAP && s_cap[threadIdx.x])
-        atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
-}
-
-template <int MODE, int MINB>
-void* onepass_fn_(uint32_t n_cap) {
-    switch (ncap_pad3(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&onepass_kernel<MODE, 1, MINB>);
-        case 2: return reinterpret_cast<void*>(&onepass_kernel<MODE, 2, MINB>);
-        case 4: return reinterpret_cast<void*>(&onepass_kernel<MODE, 4, MINB>);
-        default: return reinterpret_cast<void*>(&onepass_kernel<MODE, 8, MINB>);
-    }
-}
-template <int MINB>
-void* onepass_fn_m(me_out_mode mode, uint32_t n_cap) {
-    return mode == ME_OUT_RECORDS ? onepass_fn_<3, MINB>(n_cap)
-                                  : mode == ME_OUT_FULL ? onepass_fn_<2, MINB>(n_cap) : onepass_fn_<1, MINB>(n_cap);
-}
-void* onepass_fn(me_out_mode mode, uint32_t n_cap, int minb) {
-    return minb >= 3 ? onepass_fn_m<3>(mode, n_cap) : onepass_fn_m<2>(mode, n_cap);
-}
-
 template <bool CAPS>
 void* rowcount_fn_(uint32_t n_cap) {
     switch (ncap_pad3(n_cap)) {
@@ -839,32 +681,6 @@ int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb) {
 }
 
 uint32_t fused_units_of(uint32_t n_rows) { return (n_rows + kUnit - 1) / kUnit; }
-
-int onepass_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb) {
-    void* fn = onepass_fn(mode, n_cap, minb);
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOnepassSmem) != cudaSuccess)
-        return 1;
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, kOnepassSmem) != cudaSuccess) return 1;
-    return nb > 0 ? nb : 1;
-}
-
-cudaError_t launch_onepass(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
-                           uint64_t lo, uint64_t hi, StEnt* st, uint64_t* state, me_out_mode mode, Cols cols,
-                           uint64_t capacity, uint32_t n_blocks, int minb, uint32_t* next_unit, uint64_t* stats,
-                           cudaStream_t stream) {
-    const uint32_t n_units = fused_units_of(n_rows);
-    const uint32_t need = (n_units + kFusedWarps - 1) / kFusedWarps;
-    if (n_blocks > need) n_blocks = need ? need : 1;
-    void* args[] = {(void*)&S,  (void*)&g0, (void*)&n_rows, (void*)&n_units, (void*)&seg_lo, (void*)&n_seg_sub,
-                    (void*)&lo, (void*)&hi, (void*)&st,     (void*)&state,   (void*)&cols,   (void*)&capacity,
-                    (void*)&next_unit, (void*)&stats};
-    cudaError_t ce = cudaMemsetAsync(next_unit, 0, 4, stream);
-    if (ce == cudaSuccess) ce = cudaMemsetAsync(state, 0, (size_t)n_units * 8, stream);
-    if (ce != cudaSuccess) return ce;
-    return cudaLaunchKernel(onepass_fn(mode, S.n_cap, minb), dim3(n_blocks), dim3(kThreads), args, kOnepassSmem,
-                            stream);
-}
 
 cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
                             uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,

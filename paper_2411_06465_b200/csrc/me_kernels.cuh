@@ -273,13 +273,6 @@ cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st,
                          const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
                          me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, int minb,
                          uint32_t* next_unit, uint64_t* stats, cudaStream_t stream);
-// K0 and K3 in one kernel with a decoupled look-back over the 32-row units
-// (state: n_units u64, zeroed here); stats[0] holds the running total
-cudaError_t launch_onepass(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
-                           uint64_t lo, uint64_t hi, StEnt* st, uint64_t* state, me_out_mode mode, Cols cols,
-                           uint64_t capacity, uint32_t n_blocks, int minb, uint32_t* next_unit, uint64_t* stats,
-                           cudaStream_t stream);
-int onepass_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb);
 // resident K3 blocks per SM of the variant budgeted for minb blocks (2 or 3)
 int fused_blocks_per_sm(me_out_mode mode, uint32_t n_cap, int minb);
 uint32_t fused_units_of(uint32_t n_rows);

@@ -82,23 +82,6 @@ def test_whole_chunks_match_oracle(me, name):
         assert res.cap_counts() == [sum(r["caps"][q] for r in rows) for q in range(4)]
 
 
-def test_onepass_chunks_match_oracle(me, monkeypatch):
-    """the one-pass kernel (ME_ONEPASS=1: rows, counts, look-back offsets and
-    stores in one kernel) on the C5 sample at full size"""
-    import torch
-    monkeypatch.setenv("ME_ONEPASS", "1")
-    rows = golden("C5")
-    if not rows:
-        pytest.skip("no golden chunks")
-    plan = me.Plan(mi.config("C5"))
-    rec = torch.empty(CHUNK * 8, dtype=torch.int64, device="cuda")
-    for r in rows:
-        res = plan.sweep(r["begin"], r["end"], mode=me.ME_OUT_RECORDS, out_cols=[rec])
-        assert res.counts()[0] == r["count"] and res.cap_counts() == r["caps"], r["chunk"]
-        assert res.digest() == (r["di"], r["dr"]), r["chunk"]
-        res.free()
-
-
 def test_full_columns_match_oracle_chunks(me):
     """FULL (eight columns) on the first and the dense chunk of C5"""
     import torch

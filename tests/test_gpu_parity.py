@@ -340,10 +340,9 @@ def test_sweep_zero_stages(me, oracle_mod, zero, stage_max):
 
 @pytest.mark.parametrize("env", [{"ME_SERIAL": "1"}, {"ME_SETS": "3"}, {"ME_FUSED_BPS": "1"},
                                  {"ME_SERIAL": "1", "ME_FUSED_BPS": "1"}, {"ME_SPARSE": "0"}, {"ME_SPARSE": "4"},
-                                 {"ME_ONEPASS": "1"}, {"ME_ONEPASS": "1", "ME_MAX_ROWS": "40"},
-                                 {"ME_ONEPASS": "1", "ME_FUSED_BPS": "1"}],
-                         ids=["serial", "sets3", "fused-1bps", "serial-1bps", "positional", "sparse4", "onepass",
-                              "onepass-rows40", "onepass-1bps"])
+                                 {"ME_FUSED_MINB": "2"}, {"ME_FUSED_MINB": "3"}],
+                         ids=["serial", "sets3", "fused-1bps", "serial-1bps", "positional", "sparse4", "minb2",
+                              "minb3"])
 def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
     """The launch variants (read at plan creation) give the same rows: serial
     streams, three scratch sets, one fused-kernel block per SM, K3's

@@ -63,10 +63,10 @@ SPACES = {
 }
 
 
-@pytest.mark.parametrize("onepass", ["0", "1"])
+@pytest.mark.parametrize("sparse", ["2", "0"], ids=["two-phase", "positional"])
 @pytest.mark.parametrize("kind", list(SPACES))
-def test_exact_tie_every_path(me, oracle_mod, monkeypatch, kind, onepass):
-    monkeypatch.setenv("ME_ONEPASS", onepass)
+def test_exact_tie_every_path(me, oracle_mod, monkeypatch, kind, sparse):
+    monkeypatch.setenv("ME_SPARSE", sparse)
     kw = SPACES[kind]
     base = mi.Space(models=[mi.PRESETS["llama3.1-8b"], mi.PRESETS["llama2-13b"]], world=[16, 64],
                     caps_gb=[80], mbs=[1, 2, 4], seq=[4096, 8192], **kw)
