@@ -70,9 +70,30 @@ struct RowId {
     uint32_t L0;  // first-stage layers (R19)
 };
 
-__device__ __forceinline__ RowId row_id(const DevSpace& S, uint64_t g, uint32_t seg_lo, uint32_t n_seg_sub) {
+// The segment holding row gw (seg_row[s] <= gw < seg_row[s + 1]) among
+// segments [lo, lo + n): a 32-ary search by the whole warp (each step the 32
+// lanes probe 32 evenly spaced segments; ~log32 n dependent loads instead of
+// log2 n).  Every lane of the warp calls it with the same gw.
+__device__ __forceinline__ uint32_t warp_segment(const uint64_t* __restrict__ seg_row, uint32_t lo, uint32_t n,
+                                                 uint64_t gw) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t hi = lo + n;  // answer in [lo, hi)
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t at = lo + lane * step;
+        const bool le = at < hi && __ldg(seg_row + at) <= gw;
+        const uint32_t last = 31 - __clz(__ballot_sync(0xffffffffu, le) | 1u);  // lane 0 probes lo: always true
+        lo += last * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
+// row_id given the segment of the warp's first row: a short forward walk (a
+// warp's 32 consecutive rows span few segments)
+__device__ __forceinline__ RowId row_id_from(const DevSpace& S, uint64_t g, uint32_t s) {
     RowId R;
-    const uint32_t s = seg_lo + upper_bound_u64(S.seg_row + seg_lo, n_seg_sub, g) - 1;
+    while (__ldg(S.seg_row + s + 1) <= g) s++;
     ME_CHECK(s < S.n_seg && __ldg(S.seg_row + s) <= g && g < __ldg(S.seg_row + s + 1));
     const uint32_t m = s / S.n_world, n = s - m * S.n_world;
     const uint4 m0 = __ldg(reinterpret_cast<const uint4*>(S.models + m));
@@ -86,6 +107,10 @@ __device__ __forceinline__ RowId row_id(const DevSpace& S, uint64_t g, uint32_t 
     R.rs = __ldg(S.seg_prefix + s) + __ldg(S.list_prefix + j);
     R.L0 = R.tu.p == 1 ? R.M.layers : div_u32(R.M.layers + R.tu.p - 1, R.tu.p);
     return R;
+}
+
+__device__ __forceinline__ RowId row_id(const DevSpace& S, uint64_t g, uint32_t seg_lo, uint32_t n_seg_sub) {
+    return row_id_from(S, g, seg_lo + upper_bound_u64(S.seg_row + seg_lo, n_seg_sub, g) - 1);
 }
 
 // RowEnt of a row: make_row's coefficients, first index and pair slice

@@ -102,12 +102,11 @@ __device__ __forceinline__ void count_fit4(const uint32_t* su, const uint64_t (&
 // the window [lo, hi) (returned) and, CAPS, per capacity (into capc).
 // su_base: the sorted-u lists (shared memory when staged).
 template <int NCAP, bool CAPS>
-__device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uint32_t k, uint32_t seg_lo,
-                                              uint32_t n_seg_sub, uint64_t lo, uint64_t hi,
-                                              const uint32_t* su_base, RowEnt* out, StEnt* __restrict__ st,
-                                              uint32_t (&capc)[NCAP]) {
+__device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uint32_t k, uint32_t seg,
+                                              uint64_t lo, uint64_t hi, const uint32_t* su_base, RowEnt* out,
+                                              StEnt* __restrict__ st, uint32_t (&capc)[NCAP]) {
     uint32_t cnt = 0;
-    const RowId I = row_id(S, g, seg_lo, n_seg_sub);
+    const RowId I = row_id_from(S, g, seg);
     RowCoef R;
     const Policy Q = policy_of(S);
     make_row(I.M, I.tu.t, I.tu.c, I.tu.p, I.tu.d, I.L0, Q, R);
@@ -225,9 +224,11 @@ __global__ void __launch_bounds__(kRowThreads, 8)
     uint32_t capc[NCAP];
 #pragma unroll
     for (int q = 0; q < NCAP; q++) capc[q] = 0;
+    // the segment of the warp's first row (all lanes, before the bounds test)
+    const uint64_t gw = g0 + (k & ~31u);
+    const uint32_t seg = gw < g0 + n_rows ? warp_segment(S.seg_row, seg_lo, n_seg_sub - 1, gw) : seg_lo;
     if (k < n_rows) {
-        cnt = row_count<NCAP, CAPS>(S, g0 + k, k, seg_lo, n_seg_sub, lo, hi, su_smem ? s_su : S.pair_su, rows + k, st,
-                                    capc);
+        cnt = row_count<NCAP, CAPS>(S, g0 + k, k, seg, lo, hi, su_smem ? s_su : S.pair_su, rows + k, st, capc);
         rcnt[k] = cnt;
     }
     // survivors per 32-row unit (a unit is one warp of this kernel)
