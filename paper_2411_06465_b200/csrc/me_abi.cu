@@ -292,6 +292,8 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
     D.sparse = 2;  // measured on C5 (records, list-based two-phase path): 2 -> 346 ms/step, 4 -> 348, 8 -> 352
     if (const char* e = getenv("ME_SPARSE")) D.sparse = (uint32_t)atoi(e);
+    D.k0_smem = 1;
+    if (const char* e = getenv("ME_K0_SMEM")) D.k0_smem = (uint32_t)atoi(e);
     P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
     // (tests: a small cap exercises the cutting of sub-ranges by rows)
     if (const char* e = getenv("ME_MAX_ROWS")) P->max_rows = std::min(P->max_rows, (uint32_t)std::max(1, atoi(e)));

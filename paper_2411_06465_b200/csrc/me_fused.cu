@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kRowThreads, 8)
     __shared__ uint32_t s_cap[NCAP];
     __shared__ uint32_t s_su[kSuSmem];
     if (CAPS && threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
-    const bool su_smem = !S.gbs_mode && S.n_pairs <= kSuSmem;
+    const bool su_smem = S.k0_smem && !S.gbs_mode && S.n_pairs <= kSuSmem;
     if (su_smem)
         for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_su[i] = __ldg(S.pair_su + i);
     __syncthreads();
