@@ -323,9 +323,11 @@ int me_result_digest(me_result* r, uint64_t digest[2]);
  * than k result rows has index = UINT64_MAX in the rest.  Each row carries its
  * decoded configuration and the 1F1B schedule statistics:
  * microbatches m = gbs/(d*b) (0 when gbs = 0: the paper mode has no global
- * batch) and the bubble fraction (p-1)/m as bubble_num / bubble_den.  Sharded
- * multi-GPU results must have been gathered.  Synchronous; scratch from the
- * result's allocator. */
+ * batch) and the bubble fraction (p-1)/m as bubble_num / bubble_den.  A
+ * sharded comm result (ME_PART_EVEN without gather): COLLECTIVE -- every rank
+ * ranks its own rows, the candidates are allgathered (NCCL) and merged per
+ * segment, and every rank receives the global top k.  Synchronous; scratch
+ * from the result's allocator. */
 #define ME_RANK_NONE 0xFFFFFFFFu
 typedef struct {
     uint32_t green_cap, yellow_cap; /* capacity slots (yellow_cap may be ME_RANK_NONE) */

@@ -801,32 +801,63 @@ extern "C" int me_result_rank(me_result* R, const me_rank_opts* o, me_rank_row* 
     if (o->green_cap >= R->n_cap || (o->yellow_cap != ME_RANK_NONE && o->yellow_cap >= R->n_cap))
         return err(ME_EINVAL, "capacity slot out of range");
     if (R->mode == ME_OUT_COUNT) return err(ME_EINVAL, "ranking needs an INDEX, FULL or RECORDS result");
-    if (R->comm && !R->gather) return err(ME_EINVAL, "ranking a sharded result needs gather = 1");
     uint64_t* cols[ME_N_COLS];
     uint64_t rows = 0;
     int st = me_result_columns(R, cols, &rows);
     if (st) return st;
+    if (!R->gather && R->local > R->capacity) return err(ME_ERANGE, "caller columns overflowed");
     me_plan* P = R->plan;
     const HostSpace& H = P->hs;
     DeviceGuard g(P->device);
     const size_t n_seg = H.seg_prefix.size() - 1, m = n_seg * o->k;
+    // a sharded comm result: every rank ranks its own rows, the candidates of
+    // all ranks are allgathered and merged per segment (collective)
+    const int nr = R->comm && !R->gather ? R->comm->nranks : 1;
     // scratch from the result's allocator, ordered on its stream
     uint64_t* keys = (uint64_t*)R->A.get((rows ? rows : 1) * 8);
     uint64_t* sel = (uint64_t*)R->A.get(m * 8);
-    uint64_t* dout = (uint64_t*)R->A.get(m * 16);
-    std::vector<uint64_t> h(2 * m);
+    uint64_t* dout = (uint64_t*)R->A.get(m * 16 * (size_t)(nr > 1 ? nr + 1 : 1));
+    std::vector<uint64_t> h(2 * m * (size_t)nr);
     cudaError_t ce = keys && sel && dout ? cudaSuccess : cudaErrorMemoryAllocation;
     if (ce == cudaSuccess)
         ce = launch_rank(P->ds, cols[0], (uint32_t)words_of(R->mode), rows, o->green_cap,
                          o->yellow_cap == ME_RANK_NONE ? 8u : o->yellow_cap, o->gpus_per_node, o->k, keys, sel, dout,
                          R->stream);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(h.data(), dout, m * 16, cudaMemcpyDeviceToHost, R->stream);
+    ncclResult_t ncr = ncclSuccess;
+    if (ce == cudaSuccess && nr > 1)
+        ncr = ncclAllGather(dout, dout + 2 * m, 2 * m, ncclUint64, R->comm->nccl, R->stream);
+    if (ce == cudaSuccess && ncr == ncclSuccess)
+        ce = cudaMemcpyAsync(h.data(), nr > 1 ? dout + 2 * m : dout, h.size() * 8, cudaMemcpyDeviceToHost, R->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(R->stream);
     R->A.put(keys);
     R->A.put(sel);
     R->A.put(dout);
+    if (ncr != ncclSuccess) return err(ME_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(ncr));
     if (ce == cudaErrorMemoryAllocation) return err(ME_ENOMEM, "rank scratch");
     if (ce != cudaSuccess) return cuda_err(ce, "me_result_rank");
+    if (nr > 1) {
+        // per segment the k smallest (key, flat index) of the nr * k candidates
+        std::vector<uint64_t> merged(2 * m);
+        std::vector<std::pair<uint64_t, uint64_t>> cand;
+        for (size_t sgi = 0; sgi < n_seg; sgi++) {
+            cand.clear();
+            for (int r = 0; r < nr; r++)
+                for (uint32_t q = 0; q < o->k; q++) {
+                    const uint64_t* x = &h[2 * ((size_t)r * m + sgi * o->k + q)];
+                    if (x[0] != ~0ull) cand.emplace_back(x[1], x[0]);
+                }
+            std::sort(cand.begin(), cand.end(), [](const std::pair<uint64_t, uint64_t>& a,
+                                                  const std::pair<uint64_t, uint64_t>& b) {
+                return a.first != b.first ? a.first < b.first
+                                          : (a.second & ((1ull << 56) - 1)) < (b.second & ((1ull << 56) - 1));
+            });
+            for (uint32_t q = 0; q < o->k; q++) {
+                merged[2 * (sgi * o->k + q)] = q < cand.size() ? cand[q].second : ~0ull;
+                merged[2 * (sgi * o->k + q) + 1] = q < cand.size() ? cand[q].first : ~0ull;
+            }
+        }
+        h.swap(merged);
+    }
     // decode the selected rows on the host (n_seg * k of them)
     for (size_t i = 0; i < m; i++) {
         me_rank_row x{};

@@ -61,6 +61,11 @@ def main():
                     ok &= o == len(cat)
                     cat += l
                 ok &= np.array_equal(np.array(cat, dtype=np.uint64), ridx)
+            # the collective rank of the sharded result = the gathered result's
+            if len(sp.cap_bytes) >= 2:
+                top_sharded = r2.rank(green_cap=0, yellow_cap=1, gpus_per_node=8, k=3)
+                top_gathered = r.rank(green_cap=0, yellow_cap=1, gpus_per_node=8, k=3)
+                ok &= top_sharded == top_gathered
             # the collective digest of the sharded result = the global result's
             dg = r2.digest()
             if rank == 0:
