@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-modes", action="store_true", help="skip the INDEX / COUNT extra keys")
+    ap.add_argument("--chunk-log2", type=int, default=28, help="configs per sweep call / cyclic block: 2^k")
     ap.add_argument("--partition", default="cyclic", choices=["cyclic", "even"],
                     help="N>1: cyclic = libme's cyclic deal: rank r sweeps blocks r, r+N, ... of CHUNK configs "
                          "on its own and me_result_join joins every block's counts with one NCCL allgather per "
@@ -285,6 +286,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    global CHUNK
+    CHUNK = 1 << args.chunk_log2
     import torch
     import torch.distributed as dist
 

@@ -130,6 +130,13 @@ struct me_plan {
     uint32_t turn = 0;
     cudaStream_t cstream = nullptr;     // K0 + scan
     cudaEvent_t ready_ev = nullptr;     // tables uploaded
+    // K3 of successive sub-ranges of one call alternate between two streams so
+    // that the next K3 fills the tail of the previous one; the caller's stream
+    // is ordered before the first and after the last of a call's K3s
+    // (ME_K3_STREAMS=1: K3 on the caller's stream)
+    cudaStream_t k3s[2] = {nullptr, nullptr};
+    cudaEvent_t k3_ev[2] = {nullptr, nullptr};  // the last K3 queued on each
+    int k3_streams = 2;
     // Survivor counts of a sweep are accumulated on the plan stream in a
     // plan-owned slot (the result's own stats block comes from the caller's
     // allocator on the caller's stream, so the plan stream may not touch it
@@ -178,6 +185,7 @@ struct me_result {
     // stream), ev[5] entry (caller's stream)
     cudaEvent_t ev[6] = {};
     std::vector<cudaEvent_t> tev;  // per sub-range: rows start/end, scan end, output start/end
+    std::vector<cudaEvent_t> xev;  // other events of the call (destroyed with the result)
     bool ran_count = false, ran_write = false;
     JoinState* join = nullptr;     // set by me_result_join
     uint32_t join_k = 0;           // this result's position in the join
@@ -351,6 +359,13 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         me_plan_free(P);
         return cuda_err(cudaGetLastError(), "plan stream");
     }
+    if (const char* e = getenv("ME_K3_STREAMS")) P->k3_streams = atoi(e) >= 2 ? 2 : 1;
+    for (int i = 0; i < 2 && P->k3_streams == 2; i++)
+        if (cudaStreamCreateWithFlags(&P->k3s[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&P->k3_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+            me_plan_free(P);
+            return cuda_err(cudaGetLastError(), "K3 stream");
+        }
     cudaEventRecord(P->ready_ev, (cudaStream_t)stream);
     if (cudaError_t ce = cudaGetLastError()) {
         me_plan_free(P);
@@ -400,6 +415,10 @@ extern "C" void me_plan_free(me_plan* P) {
             if (x) cudaEventDestroy(x);
         if (P->ready_ev) cudaEventDestroy(P->ready_ev);
         if (P->cstream) cudaStreamDestroy(P->cstream);
+        for (int i = 0; i < 2; i++) {
+            if (P->k3s[i]) cudaStreamSynchronize(P->k3s[i]), cudaStreamDestroy(P->k3s[i]);
+            if (P->k3_ev[i]) cudaEventDestroy(P->k3_ev[i]);
+        }
     }
     delete P;
 }
@@ -451,6 +470,19 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
     const auto seg_of = [&](uint64_t g) {
         return (uint32_t)(std::upper_bound(H.seg_row.begin(), H.seg_row.end(), g) - H.seg_row.begin() - 1);
     };
+    // K3 streams: ordered after the caller's stream at the call's entry
+    const bool alt = write && P->k3_streams == 2 && !P->serial;
+    bool used[2] = {false, false};
+    uint32_t n_sub = 0;
+    if (alt) {
+        cudaEvent_t entry = nullptr;
+        if (cudaEventCreateWithFlags(&entry, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_err(cudaGetLastError(), "cudaEventCreate");
+        R->xev.push_back(entry);
+        cudaEventRecord(entry, st);
+        cudaStreamWaitEvent(P->k3s[0], entry, 0);
+        cudaStreamWaitEvent(P->k3s[1], entry, 0);
+    }
     for (uint64_t lo = b, hi = b; lo < e; lo = hi) {
         hi = e - lo < kMaxSub ? e : lo + kMaxSub;
         // sub-ranges end at row boundaries: only the call's own first and last
@@ -485,19 +517,28 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
         if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
         cudaEventRecord(tev[2], cs);
         if (write) {
-            cudaStreamWaitEvent(st, tev[2], 0);
-            cudaEventRecord(tev[3], st);
+            cudaStream_t ks = alt ? P->k3s[n_sub & 1] : st;
+            if (alt) used[n_sub & 1] = true;
+            n_sub++;
+            cudaStreamWaitEvent(ks, tev[2], 0);
+            cudaEventRecord(tev[3], ks);
             ce = launch_fused(P->ds, sc.rows, sc.st, sc.rcnt, sc.ucnt, sc.uoff, n_rows, lo, hi, mode, cols, capacity,
-                              (uint32_t)(P->sms * P->fused_bps[mode]), P->fused_minb[mode], sc.rnext, stats, st);
+                              (uint32_t)(P->sms * P->fused_bps[mode]), P->fused_minb[mode], sc.rnext, stats, ks);
             if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
-            cudaEventRecord(tev[4], st);
-            cudaEventRecord(sc.free_ev, st);
+            cudaEventRecord(tev[4], ks);
+            cudaEventRecord(sc.free_ev, ks);
         } else {
             cudaEventRecord(tev[3], cs);
             cudaEventRecord(tev[4], cs);
             cudaEventRecord(sc.free_ev, cs);
         }
     }
+    // the caller's stream waits for the call's K3s (output rows, capacity counts)
+    for (int i = 0; i < 2; i++)
+        if (used[i]) {
+            cudaEventRecord(P->k3_ev[i], P->k3s[i]);
+            cudaStreamWaitEvent(st, P->k3_ev[i], 0);
+        }
     return ME_OK;
 }
 
