@@ -284,8 +284,9 @@ int me_result_copy_to_host(me_result* r, uint64_t first, uint64_t n, uint64_t* c
 int me_result_status(me_result* r);
 /* wait for the result's work on its stream to finish */
 int me_result_wait(me_result* r);
-/* device time in ms from CUDA events on the sweep's stream: [0] whole sweep,
- * [1] count pass, [2] scan, [3] write pass (0 when not run).  Waits. */
+/* device time in ms from CUDA events: [0] whole sweep, [1] K0 rows + counts
+ * (plan stream), [2] scan, [3] K3 output kernel (0 when not run), summed over
+ * the sub-ranges.  Waits. */
 int me_result_timing(me_result* r, float* ms4);
 void me_result_free(me_result* r);
 

@@ -285,17 +285,13 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         D.gb = Q.gb;
         D.ob = Q.ob;
     }
-    for (int q = 0; q < 8; q++) D.thr[q] = 0, D.thr1[q] = 1, D.cslot[q] = (uint32_t)q;
+    for (int q = 0; q < 8; q++) D.thr[q] = 0, D.thr1[q] = 1;
     D.thr_max = 0;
-    uint32_t q_max = 0;
     for (size_t q = 0; q < H.caps.size(); q++) {
         D.thr[q] = threshold_of(H.caps[q], thr);
         D.thr1[q] = (D.thr[q] < (1ull << 62) ? D.thr[q] : (1ull << 62)) + 1;
-        if (q == 0 || D.thr[q] > D.thr_max) D.thr_max = D.thr[q], q_max = (uint32_t)q;
+        if (q == 0 || D.thr[q] > D.thr_max) D.thr_max = D.thr[q];
     }
-    D.cslot[0] = q_max;  // slot 0 holds thr_max (survivor test of the stage kernel)
-    D.cslot[q_max] = 0;
-    for (int k = 0; k < 8; k++) D.thr1c[k] = D.thr1[D.cslot[k]];
     cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device);
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
     D.sparse = 2;  // measured on C5 (records, list-based two-phase path): 2 -> 346 ms/step, 4 -> 348, 8 -> 352

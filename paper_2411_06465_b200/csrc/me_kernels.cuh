@@ -51,10 +51,6 @@ struct DevSpace {
     // thr_j + 1 with thr_j clamped to 2^62 (every total is < 2^58): the sweep
     // tests total <= thr_j as the carry out of (thr_j + 1) + ~total
     uint64_t thr1[8];
-    // count pass order of the slots: slot 0 holds thr_max (its counter is the
-    // survivor count), count slot k is capacity cslot[k]
-    uint64_t thr1c[8];
-    uint32_t cslot[8];
 };
 
 // The estimator's variant policy of a configuration (the paper: all zero /
@@ -249,7 +245,7 @@ struct __align__(16) RowEnt {
 struct __align__(16) StEnt {
     uint64_t msL, kL, parL, graL, optimL, layL, hcL, _pad;
 };
-constexpr uint32_t kMaxRows = 1u << 21;  // rows of one sub-range (descriptor row field: 24 bits)
+constexpr uint32_t kMaxRows = 1u << 21;  // rows of one sub-range (scratch: 128 B + 4 B per row per set)
 
 // ---- launch wrappers (me_kernels.cu) ------------------------------------
 struct Cols {
