@@ -42,10 +42,10 @@ def done_chunks(path: Path):
         return {int(r["chunk"]) for r in csv.DictReader(fh)}
 
 
-def run(name: str, chunks, threads: int):
+def run(name: str, chunks, threads: int, path: Path = None):
     sp = mi.config(name)
     size = oracle.space_size(sp)
-    path = HERE / f"{name.lower()}_chunks.csv"
+    path = path or HERE / f"{name.lower()}_chunks.csv"
     have = done_chunks(path)
     new = not path.exists()
     with path.open("a", newline="") as fh:
@@ -66,8 +66,14 @@ def run(name: str, chunks, threads: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=oracle.default_threads())
-    ap.add_argument("--only", default="all", choices=["c4", "c5-sample", "all"])
+    ap.add_argument("--only", default="all", choices=["c4", "c5-sample", "all", "c5-range"])
+    ap.add_argument("--range", default="", help="c5-range: first:last chunks (inclusive)")
+    ap.add_argument("--out", default="", help="c5-range: output CSV (default: tests/golden/c5_chunks.csv)")
     a = ap.parse_args()
+    if a.only == "c5-range":
+        lo, hi = (int(x) for x in a.range.split(":"))
+        run("C5", range(lo, hi + 1), a.threads, Path(a.out) if a.out else None)
+        return
     n5 = -(-oracle.space_size(mi.config("C5")) // CHUNK)
     n4 = -(-oracle.space_size(mi.config("C4")) // CHUNK)
     if a.only in ("c5-sample", "all"):
