@@ -221,7 +221,7 @@ int me_estimate(const me_model* model, const me_parallel* cfg, me_breakdown* out
  * such stage) and stores its index in *which (may be NULL).  Stage 0 equals
  * me_estimate.  Layers: stage 0 holds L0 (see me_parallel), the other stages
  * split L - L0 as evenly as possible, earlier stages first.  ME_EINVAL for
- * stage >= p. */
+ * stage >= p and for interleaved 1F1B (vpp >= 2: no per-stage view). */
 int me_estimate_stage(const me_model* model, const me_parallel* cfg, uint32_t stage, me_breakdown* out,
                       uint32_t* which);
 
@@ -250,7 +250,8 @@ int me_decode(const me_model_range* models, const me_cluster* cluster, const me_
  * host, uploaded once) plus reusable scratch.  Domain of exact u64 evaluation
  * (ME_EINVAL outside it): h <= 2^15, h_ffn <= 2^17, L <= 2^8, v <= 2^19,
  * s <= 2^20, b <= 2^6, N <= 2^20 and < 2^56 configurations; then every term
- * is < 2^58. */
+ * is < 2^58 (with the NEXT-4 variants too: at most 32 bytes per parameter,
+ * and interleaving keeps the first GPU's layer-microbatches below 2L). */
 int me_plan_create(const me_model_range* models, const me_cluster* cluster,
                    const me_cfg_range* cfg, me_threshold thr, int device, void* stream,
                    me_alloc_fn alloc, me_free_fn free, void* alloc_ctx, me_plan** out);
