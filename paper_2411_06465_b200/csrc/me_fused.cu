@@ -546,22 +546,26 @@ __device__ __forceinline__ void fused_units(const DevSpace& S, const RowEnt* __r
         const uint32_t k0 = unit * kUnit;
         ME_CHECK(k0 < n_rows);
         const uint32_t nr = min(kUnit, n_rows - k0);
+        // the unit's rows into the warp's shared copy: asynchronous 16-byte
+        // copies (cp.async), in flight while the counts and the offset load
+        __syncwarp();  // the previous unit's readers are done with srow
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(rows + k0);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(srow);
+            const uint32_t n16 = nr * (uint32_t)(sizeof(RowEnt) / 16);
+            for (uint32_t i = lane; i < n16; i += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + i * 16), "l"(src + i) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         const uint32_t c = lane < nr ? __ldg(rcnt + k0 + lane) : 0u;
+        const uint64_t base = __ldg(uoff + unit);
         uint32_t inc = c;  // inclusive warp scan of the row counts
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= (uint32_t)o) inc += y;
         }
-        const uint64_t base = __ldg(uoff + unit);
-        // the unit's rows into the warp's shared copy (coalesced 16-byte loads)
-        __syncwarp();
-        {
-            const uint4* src = reinterpret_cast<const uint4*>(rows + k0);
-            uint4* dst = reinterpret_cast<uint4*>(srow);
-            const uint32_t n16 = nr * (uint32_t)(sizeof(RowEnt) / 16);
-            for (uint32_t i = lane; i < n16; i += 32) dst[i] = __ldg(src + i);
-        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         uint32_t nz = __ballot_sync(0xffffffffu, c != 0);
         CapPack<NCAP> pk;  // <= 32 rows x w / 32 survivors per lane per unit: fits 16 bits
