@@ -123,6 +123,7 @@ struct me_plan {
     uint32_t n_sets = 2;                // scratch sets in rotation (ME_SETS, 2..kMaxSets)
     uint32_t max_rows = 0;              // rows per sub-range
     int fused_bps[4] = {0, 0, 0, 0};    // resident K3 blocks per SM per output mode
+    int k3_caps[4] = {1, 1, 1, 1};      // per output mode: per-capacity counts in K3 (1) or K0 (0) (ME_K3_CAPS)
     int fused_minb[4] = {2, 3, 2, 3};   // K3 register budget per output mode: 2 or 3 blocks per SM
                                         // (measured on C5: records 3 -> 351 ms/step, 2 -> 358; INDEX
                                         // 3 -> 193, 2 -> 220 despite a few spilled registers; FULL
@@ -298,6 +299,8 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_SPARSE")) D.sparse = (uint32_t)atoi(e);
     D.k0_smem = 1;
     if (const char* e = getenv("ME_K0_SMEM")) D.k0_smem = (uint32_t)atoi(e);
+    if (const char* e = getenv("ME_K3_CAPS"))
+        for (int& x : P->k3_caps) x = atoi(e) ? 1 : 0;
     P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
     // (tests: a small cap exercises the cutting of sub-ranges by rows)
     if (const char* e = getenv("ME_MAX_ROWS")) P->max_rows = std::min(P->max_rows, (uint32_t)std::max(1, atoi(e)));
@@ -506,7 +509,7 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
         cudaEventRecord(tev[0], cs);
         cudaError_t ce;
         ce = launch_rowcount(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.rows, sc.st, sc.rcnt, sc.ucnt,
-                             stats, !write, cs);
+                             stats, !write || !P->k3_caps[mode], cs);
         if (ce != cudaSuccess) return cuda_err(ce, "row kernel");
         cudaEventRecord(tev[1], cs);
         ce = launch_scan(sc.ucnt, nullptr, fused_units_of(n_rows), 0, sc.uoff, stats, cs);
@@ -518,7 +521,9 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
             n_sub++;
             cudaStreamWaitEvent(ks, tev[2], 0);
             cudaEventRecord(tev[3], ks);
-            ce = launch_fused(P->ds, sc.rows, sc.st, sc.rcnt, sc.ucnt, sc.uoff, n_rows, lo, hi, mode, cols, capacity,
+            DevSpace dsk = P->ds;
+            dsk.k3_caps = (uint32_t)P->k3_caps[mode];
+            ce = launch_fused(dsk, sc.rows, sc.st, sc.rcnt, sc.ucnt, sc.uoff, n_rows, lo, hi, mode, cols, capacity,
                               (uint32_t)(P->sms * P->fused_bps[mode]), P->fused_minb[mode], sc.rnext, stats, ks);
             if (ce != cudaSuccess) return cuda_err(ce, "fused kernel");
             cudaEventRecord(tev[4], ks);

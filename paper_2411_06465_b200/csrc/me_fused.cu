@@ -388,7 +388,7 @@ __device__ __forceinline__ void fused_row(const DevSpace& S, const RowEnt& R, co
                 }
             }
             const uint32_t mask = cap_mask_n<NCAP>(S, ~v[7]);
-            pk.add(mask);
+            if (S.k3_caps) pk.add(mask);
             v[0] = (rs + pos) | ((uint64_t)mask << 56);
             const uint64_t o = off + done + __popc(bal & lanes_lt);
             if (o < capacity) {
@@ -509,7 +509,7 @@ __device__ __forceinline__ void fused_row_pairs(const DevSpace& S, const RowEnt&
                 }
             }
             const uint32_t mask = cap_mask_n<NCAP>(S, ~v[7]);
-            pk.add(mask);
+            if (S.k3_caps) pk.add(mask);
             v[0] = (R.rs + (j << lg | sel)) | ((uint64_t)mask << 56);
             const uint64_t o = off + k;
             if (o < capacity) {

@@ -44,6 +44,7 @@ struct DevSpace {
     uint32_t sp_off, vpp;         // NEXT-4: sequence parallelism off (R28); virtual pipeline stages (R29)
     uint32_t wb, gb, ob;          // NEXT-4: bytes per parameter of weights / gradients / optimizer states (R30)
     uint32_t k0_smem;             // K0 stages the sorted-u lists in shared memory (ME_K0_SMEM)
+    uint32_t k3_caps;             // per-capacity counts from K3's masks (1) or K0's searches (0)
     uint32_t sparse;              // K3: a row with survivors * sparse < configurations takes the
                                   // two-phase (pair mask) path; 0 = never (ME_SPARSE)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
