@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-modes", action="store_true", help="skip the INDEX / COUNT extra keys")
     ap.add_argument("--chunk-log2", type=int, default=28, help="configs per sweep call / cyclic block: 2^k")
+    ap.add_argument("--no-verify", action="store_true", help="skip the untimed feasible-set digest check")
     ap.add_argument("--partition", default="cyclic", choices=["cyclic", "even"],
                     help="N>1: cyclic = libme's cyclic deal: rank r sweeps blocks r, r+N, ... of CHUNK configs "
                          "on its own and me_result_join joins every block's counts with one NCCL allgather per "
@@ -273,6 +274,48 @@ def run_steps(torch, dist, me, plan, calls, mode, ring, flush, stream, steps, wa
     return float(t.item()), timings, n_local // steps, n_global // steps
 
 
+def verify_feasible_set(torch, dist, me, plan, calls, ring, stream, world, rank, workload):
+    """Untimed: one more pass over this rank's calls in RECORDS mode, the
+    order-dependent digest of each call's feasible set (me_result_digest),
+    gathered and merged in index order (me_digest_merge) into the digest of
+    the whole step's feasible set, compared with the oracle's per-chunk
+    digests (tests/golden/<workload>_chunks.csv, written by
+    tests/golden/gen_chunk_digests.py from oracle/)."""
+    mine = []
+    with torch.cuda.stream(stream):
+        for q, (b, e) in enumerate(calls):
+            r = plan.sweep(b, e, mode=me.ME_OUT_RECORDS, out_cols=ring[q & 1])
+            if r.status() != 0:
+                raise RuntimeError("caller columns overflowed")
+            mine.append((b, r.counts()[0], r.cap_counts(), r.digest()))
+            r.free()
+    parts = [mine]
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+    if rank != 0:
+        return None
+    allp = sorted(x for p_ in parts for x in p_)
+    counts = [x[1] for x in allp]
+    dig = me.digest_merge(counts, [x[3] for x in allp])
+    out = {"survivors": sum(counts), "digest_index": f"{dig[0]:016x}", "digest_record": f"{dig[1]:016x}",
+           "calls": len(allp)}
+    gold = ROOT / "tests" / "golden" / f"{workload.lower()}_chunks.csv"
+    if gold.exists():
+        import csv
+        with gold.open() as fh:
+            g = {int(r["begin"]): r for r in csv.DictReader(fh)}
+        if all(x[0] in g for x in allp) and len(g) == len(allp):
+            rows = [g[x[0]] for x in allp]
+            ref = me.digest_merge([int(r["count"]) for r in rows],
+                                  [(int(r["digest_index"], 16), int(r["digest_record"], 16)) for r in rows])
+            out["oracle_golden"] = str(gold.relative_to(ROOT))
+            out["equal_to_oracle"] = (ref == dig and [int(r["count"]) for r in rows] == counts
+                                      and all([int(r[f"cap{j}"]) for j in range(len(allp[0][2]))] == x[2]
+                                              for r, x in zip(rows, allp)))
+    return out
+
+
 def ncu_summary():
     """per-kernel ncu figures of one C5 chunk at HEAD (scripts/ncu_summary.py)"""
     for name in ("r2_final", "r2b"):
@@ -419,6 +462,15 @@ def main():
                                                   "scan": sum(x[2] for x in tm) / args.steps,
                                                   "output_K3": sum(x[3] for x in tm) / args.steps}}
         line["modes"] = extra
+
+    # the step's feasible set against the oracle (untimed; bench calls of 2^28
+    # configs = the golden chunks)
+    if not args.no_verify and CHUNK == 1 << 28 and (world == 1 or cyclic):
+        ring = ring_for(me.ME_OUT_RECORDS)
+        fs = verify_feasible_set(torch, dist, me, plan, calls, ring, stream, world, rank, args.workload)
+        del ring
+        if fs is not None:
+            line["feasible_set"] = fs
 
     # e2e: the public API with host buffers -- plan creation (host tables +
     # H2D) and a D2H of every survivor row inside the timed region

@@ -306,6 +306,10 @@ void me_result_free(me_result* r);
  * ME_EINVAL for COUNT results, ME_ERANGE if caller columns overflowed.
  * Synchronous. */
 int me_result_digest(me_result* r, uint64_t digest[2]);
+/* The digest of consecutive pieces of a result from the pieces' digests:
+ * piece i has counts[i] rows and digests[2i], digests[2i+1] (index, record);
+ * out = sum_i M^(rows before piece i) D_i.  Host-only. */
+int me_digest_merge(uint64_t n, const uint64_t* counts, const uint64_t* digests, uint64_t out[2]);
 
 /* NEXT-2 planner (the search heuristics of
  * P:552-593).  For every (model, N) segment of the plan (n_models * n_world

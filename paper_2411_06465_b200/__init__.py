@@ -372,3 +372,14 @@ def result_join(results: Sequence["Result"], n_blocks: int, comm: "Comm"):
     counts and the exclusive scan on the device; collective over comm."""
     arr = (ctypes.c_void_p * max(1, len(results)))(*[r.h.value for r in results])
     check(lib().me_result_join(arr, len(results), n_blocks, comm.h), "me_result_join")
+
+
+def digest_merge(counts, digests):
+    """me_digest_merge: the digest of consecutive pieces (counts[i] rows,
+    digests[i] = (index, record)) of one result.  Host-only."""
+    n = len(counts)
+    c = (ctypes.c_uint64 * max(1, n))(*[int(x) for x in counts])
+    d = (ctypes.c_uint64 * max(2, 2 * n))(*[int(x) for pair in digests for x in pair])
+    out = (ctypes.c_uint64 * 2)()
+    check(lib().me_digest_merge(n, c, d, out), "me_digest_merge")
+    return out[0], out[1]

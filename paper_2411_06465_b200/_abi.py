@@ -122,6 +122,7 @@ def lib() -> ctypes.CDLL:
             "me_result_free": ([ctypes.c_void_p], None),
             "me_result_rank": ([ctypes.c_void_p, P(me_rank_opts), P(me_rank_row)], ctypes.c_int),
             "me_result_digest": ([ctypes.c_void_p, P(u64)], ctypes.c_int),
+            "me_digest_merge": ([u64, P(u64), P(u64), P(u64)], ctypes.c_int),
             "me_comm_check": ([ctypes.c_void_p], ctypes.c_int),
             "me_cyclic_block": ([u64, u64, u64, ctypes.c_int, ctypes.c_int, u64, P(u64), P(u64), P(u64)], ctypes.c_int),
             "me_result_join": ([P(ctypes.c_void_p), u32, u64, ctypes.c_void_p], ctypes.c_int),
@@ -147,7 +148,7 @@ def lib() -> ctypes.CDLL:
 EXPORTS = ("me_estimate", "me_estimate_stage", "me_estimate_batch", "me_space_size", "me_decode", "me_plan_create", "me_plan_size", "me_plan_table_bytes",
            "me_plan_sweep", "me_plan_free", "me_sweep", "me_result_counts", "me_result_cap_counts",
            "me_result_columns", "me_result_copy_to_host", "me_result_status", "me_result_wait",
-           "me_result_timing", "me_result_free", "me_result_rank", "me_result_digest", "me_comm_check", "me_cyclic_block", "me_result_join", "me_partition", "me_join_counts", "me_comm_unique_id", "me_comm_init", "me_comm_rank",
+           "me_result_timing", "me_result_free", "me_result_rank", "me_result_digest", "me_digest_merge", "me_comm_check", "me_cyclic_block", "me_result_join", "me_partition", "me_join_counts", "me_comm_unique_id", "me_comm_init", "me_comm_rank",
            "me_comm_destroy", "me_strerror", "me_last_error_detail", "me_version")
 
 

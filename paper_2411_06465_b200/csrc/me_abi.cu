@@ -969,6 +969,20 @@ extern "C" int me_result_digest(me_result* R, uint64_t* digest) {
     return ME_OK;
 }
 
+extern "C" int me_digest_merge(uint64_t n, const uint64_t* counts, const uint64_t* digests, uint64_t out[2]) {
+    if (!out || (n && (!counts || !digests))) return err(ME_EINVAL, "null argument");
+    uint64_t off = 0, di = 0, dr = 0;
+    for (uint64_t i = 0; i < n; i++) {
+        const uint64_t sh = digest_pow_host(off);
+        di += sh * digests[2 * i];
+        dr += sh * digests[2 * i + 1];
+        off += counts[i];
+    }
+    out[0] = di;
+    out[1] = dr;
+    return ME_OK;
+}
+
 extern "C" int me_comm_check(me_comm* c) {
     if (!c) return err(ME_EINVAL, "null comm");
     ncclResult_t a = ncclSuccess;

@@ -90,3 +90,15 @@ def test_invalid_inputs(me):
         me.me_space_size(mi.Space(models=sp.models, world=[8], caps_gb=[1] * 9, mbs=[1], seq=[8]))
     with pytest.raises(me.MEError):
         me.me_space_size(mi.Space(models=sp.models, world=[8], caps_gb=[1], mbs=[1], seq=[8], rc_mask=0))
+
+
+def test_digest_merge_matches_oracle(me, oracle_mod):
+    """me_digest_merge (host-only): the digest of a result from its pieces'
+    digests equals the oracle's digest of the whole (or_digest in one piece)"""
+    import me_inputs as mi
+    sp = mi.config("C3", uneven=1)
+    whole = oracle_mod.digest(sp, chunk=1 << 40, threads=4)[0]
+    parts = oracle_mod.digest(sp, chunk=7777, threads=4)
+    got = me.digest_merge([int(r[0]) for r in parts], [(int(r[9]), int(r[10])) for r in parts])
+    assert got == (int(whole[9]), int(whole[10]))
+    assert me.digest_merge([], []) == (0, 0)
