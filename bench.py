@@ -411,18 +411,30 @@ def main():
                 "achieved": None, "peak": None, "unit": "warp-instr/s", "frac": None, "traffic": 0}
     # integer-issue roofline (ncu, each kernel alone on the GPU: 148 SMs x 4
     # SMSPs x 1 warp-instruction / cycle)
+    # integer-issue roofline per output mode (ncu --set full of C5 chunk 40,
+    # each kernel alone on the GPU; 148 SMs x 4 SMSPs x 1 warp-instruction /
+    # cycle): K0 and K3 of RECORDS, K3 of INDEX, K0 of COUNT
     issue = None
     if ncu:
-        issue = {"source": ncu_src, "chunk": ncu["chunk"], "configs": ncu["configs"],
+        issue = {"chunk": ncu["chunk"], "configs": ncu["configs"],
                  "peak": "1 warp-instr / cycle / SMSP (148 x 4 x clock)"}
-        for k in ("rowcount_kernel", "fused_kernel"):
-            v = ncu["kernels"].get(k)
-            if v:
-                issue[k] = {"issue_frac": v.get("issue_frac"), "warp_instr": v.get("warp_instr"),
-                            "warp_instr_per_config": v.get("warp_instr_per_config"),
-                            "pipe_alu_pct": v.get("pipe_alu_pct"), "pipe_fma_pct": v.get("pipe_fma_pct")}
-        if mode == me.ME_OUT_COUNT and issue.get("rowcount_kernel"):
-            roof.update({"frac": issue["rowcount_kernel"]["issue_frac"], "traffic_note": "issue fraction from ncu"})
+        for m_name in ("records", "index", "count"):
+            f = ROOT / "profiles" / "r2_final" / f"ncu_chunk40_{m_name}.json"
+            if not f.exists():
+                continue
+            d = json.loads(f.read_text())
+            issue[m_name] = {"source": str(f.relative_to(ROOT))}
+            for k in ("rowcount_kernel", "fused_kernel"):
+                v = d["kernels"].get(k)
+                if v:
+                    issue[m_name][k] = {"issue_frac": v.get("issue_frac"), "warp_instr": v.get("warp_instr"),
+                                        "warp_instr_per_config": v.get("warp_instr_per_config"),
+                                        "pipe_alu_pct": v.get("pipe_alu_pct"), "pipe_fma_pct": v.get("pipe_fma_pct"),
+                                        "duration_ms": v.get("duration_ms")}
+        k0 = issue.get("count", {}).get("rowcount_kernel")
+        if mode == me.ME_OUT_COUNT and k0:
+            roof.update({"achieved": k0["warp_instr"] / (k0["duration_ms"] / 1e3), "unit": "warp-instr/s",
+                         "frac": k0["issue_frac"], "traffic_note": "K0 alone (ncu, chunk 40, COUNT mode)"})
     line = {
         "metric": "estimator configs/sec", "value": value, "unit": "configs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
