@@ -378,7 +378,8 @@ int me_cyclic_block(uint64_t begin, uint64_t end, uint64_t block, int rank, int 
  * Asynchronous on the results' stream.  Afterwards me_result_counts gives for
  * each result its local count, the job's global count, and the global position
  * of its first row (rank_offset); me_result_cap_counts the job's per-capacity
- * counts.  The results keep the join alive. */
+ * counts.  The results keep the join alive.  A rank with no block (more ranks
+ * than blocks) calls it with n = 0 and only takes part in the allgather. */
 int me_result_join(me_result* const* results, uint32_t n, uint64_t n_blocks, me_comm* comm);
 
 /* NCCL communicator over nranks processes (one per GPU).  rank 0 creates the

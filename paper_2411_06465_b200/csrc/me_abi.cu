@@ -1224,7 +1224,21 @@ extern "C" int me_result_join(me_result* const* rs, uint32_t n, uint64_t n_block
         if (rs[k]->plan != R0->plan || rs[k]->stream != R0->stream)
             return err(ME_EINVAL, "joined results must share a plan and stream");
     }
-    if (!R0) return err(ME_EINVAL, "this rank has no blocks: nothing to join into");
+    if (!R0) {
+        // a rank without blocks (more ranks than blocks) still takes part in
+        // the collective, with zero counts, so that the others do not wait
+        DeviceGuard g(comm->device);
+        const size_t words = (size_t)kmax * 9;
+        uint64_t* d = nullptr;
+        cudaStream_t s0 = nullptr;
+        if (cudaMallocAsync(&d, words * 8 * (1 + N), s0) != cudaSuccess) return cuda_err(cudaGetLastError(), "join");
+        cudaMemsetAsync(d, 0, words * 8, s0);
+        ncclResult_t nr = ncclAllGather(d, d + words, words, ncclUint64, comm->nccl, s0);
+        cudaFreeAsync(d, s0);
+        cudaStreamSynchronize(s0);
+        if (nr != ncclSuccess) return err(ME_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
+        return ME_OK;
+    }
     DeviceGuard g(R0->plan->device);
     cudaStream_t st = R0->stream;
     JoinState* J = new (std::nothrow) JoinState();

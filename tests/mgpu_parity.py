@@ -73,13 +73,13 @@ def main():
                 ok &= r.digest() == oracle.digest_of_rows(ridx, rrows)
             r.free()
             r2.free()
-            # cyclic deal of blocks + one deferred join
-            for block in (1000, 7777):
+            # cyclic deal of blocks + one deferred join (block = the whole
+            # range: ranks > 0 hold no block and join with n = 0)
+            for block in (1000, 7777, 1 << 40):
                 e = end or plan.size
                 blocks, nb = me.cyclic_blocks(begin, e, block, rank, world)
                 res = [plan.sweep(lo_, hi_, mode=me.ME_OUT_RECORDS, partition=me.ME_PART_CYCLIC) for lo_, hi_ in blocks]
-                if res:
-                    me.result_join(res, nb, comm)
+                me.result_join(res, nb, comm)
                 mine = []
                 for rr in res:
                     lo3, gl3, off3 = rr.counts()
