@@ -60,5 +60,6 @@ def test_golden_files_cover_the_required_chunks(oracle_mod):
             caps = [int(r[f"cap{q}"]) for q in range(4)]
             assert caps == sorted(caps) and caps[-1] == int(r["count"])  # 40 <= 80 <= 94 <= 192 GiB
         nc = -(-n // CHUNK)
-        assert {0, 40, nc - 1} | set(range(0, nc, 16)) <= set(rows)
+        if name == "C5":
+            assert {0, 40, nc - 1} | set(range(0, nc, 16)) <= set(rows)
         assert set(rows) == set(range(nc))
