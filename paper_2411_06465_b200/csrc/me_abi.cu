@@ -125,6 +125,7 @@ struct me_plan {
     int fused_bps[4] = {0, 0, 0, 0};    // resident K3 blocks per SM per output mode
     int k3_caps[4] = {1, 1, 1, 1};      // per output mode: per-capacity counts in K3 (1) or K0 (0) (ME_K3_CAPS)
     int fused_minb[4] = {2, 3, 2, 3};   // K3 register budget per output mode: 2 or 3 blocks per SM
+    int k0_bps = 0;                     // count-only K0: grid-stride blocks per SM (ME_K0_BPS; 0 = resident)
                                         // (measured on C5: records 3 -> 351 ms/step, 2 -> 358; INDEX
                                         // 3 -> 193, 2 -> 220 despite a few spilled registers; FULL
                                         // spills more at 3; ME_FUSED_MINB)
@@ -297,8 +298,6 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_SERIAL")) P->serial = atoi(e);
     D.sparse = 2;  // measured on C5 (records, list-based two-phase path): 2 -> 346 ms/step, 4 -> 348, 8 -> 352
     if (const char* e = getenv("ME_SPARSE")) D.sparse = (uint32_t)atoi(e);
-    D.k0_smem = 1;
-    if (const char* e = getenv("ME_K0_SMEM")) D.k0_smem = (uint32_t)atoi(e);
     if (const char* e = getenv("ME_K3_CAPS"))
         for (int& x : P->k3_caps) x = atoi(e) ? 1 : 0;
     P->max_rows = (uint32_t)(H.total_rows < kMaxRows ? H.total_rows : kMaxRows);
@@ -313,6 +312,10 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         const int fb = fused_blocks_per_sm((me_out_mode)m, D.n_cap, P->fused_minb[m]);
         P->fused_bps[m] = fbps ? std::min(fb, fbps) : fb;
     }
+    D.k0_smem = 1;
+    if (const char* e = getenv("ME_K0_SMEM")) D.k0_smem = (uint32_t)atoi(e);
+    P->k0_bps = rowcount_blocks_per_sm(D);
+    if (const char* e = getenv("ME_K0_BPS")) P->k0_bps = atoi(e) > 0 ? atoi(e) : 0;  // 0: one block per 128 rows
     if (const char* e = getenv("ME_SETS")) P->n_sets = (uint32_t)std::min(std::max(atoi(e), 2), (int)kMaxSets);
     const uint32_t max_units = fused_units_of(P->max_rows) + 1;
     for (uint32_t si = 0; si < P->n_sets; si++) {
@@ -509,11 +512,14 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
         cudaEventRecord(tev[0], cs);
         cudaError_t ce;
         ce = launch_rowcount(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.rows, sc.st, sc.rcnt, sc.ucnt,
-                             stats, !write || !P->k3_caps[mode], cs);
+                             stats, !write || !P->k3_caps[mode], write, (uint32_t)(P->sms * P->k0_bps), cs);
         if (ce != cudaSuccess) return cuda_err(ce, "row kernel");
         cudaEventRecord(tev[1], cs);
-        ce = launch_scan(sc.ucnt, nullptr, fused_units_of(n_rows), 0, sc.uoff, stats, cs);
-        if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
+        if (write) {
+            // counts only: K0 summed them
+            ce = launch_scan(sc.ucnt, nullptr, fused_units_of(n_rows), 0, sc.uoff, stats, cs);
+            if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
+        }
         cudaEventRecord(tev[2], cs);
         if (write) {
             cudaStream_t ks = alt ? P->k3s[n_sub & 1] : st;

@@ -9,11 +9,12 @@
 // sub-range of the flat index space:
 //
 //  K0 rowcount_kernel  one thread per row: the row's coefficients (make_row,
-//                      Eq.6/7/10/12-17), its survivors per capacity -- per
-//                      digit a binary search over the row's u values sorted
-//                      ascending, evaluating the total at each probe -- the
-//                      survivor bound umax (the largest surviving u) per
-//                      digit, and per 32-row unit the survivor count;
+//                      Eq.6/7/10/12-17), per digit the exact survivor bound
+//                      umax = floor((thr - ms) / K) (the largest u whose
+//                      total fits), its survivors per capacity -- per digit
+//                      a binary search for umax over the row's u values
+//                      sorted ascending -- and per 32-row unit the survivor
+//                      count;
 //                      a global batch (R17: the in-flight count depends on
 //                      b) or a row cut by the range is evaluated config by
 //                      config instead;
@@ -70,31 +71,60 @@ __device__ __forceinline__ uint32_t count_fit(const uint32_t* su, uint32_t n, co
 // lists are staged in shared memory when they fit; a row's binary searches
 // (one per digit) run in lockstep, so their loads are in flight together.
 constexpr uint32_t kRowThreads = 128;
-constexpr uint32_t kSuSmem = 4096;  // sorted-u entries staged in shared memory (16 KB)
+#ifndef ME_K0_COUNT_MINB
+#define ME_K0_COUNT_MINB 6
+#endif
+constexpr int kRowMinbCount = ME_K0_COUNT_MINB;  // count-only K0: resident blocks per SM (register budget)
 
-// per digit q < n_sel (total ms_q + u K_q), the number of leading entries of
-// su[0, hi0_q) that fit under thr: the binary searches run in lockstep
-__device__ __forceinline__ void count_fit4(const uint32_t* su, const uint64_t (&ms)[4], const uint64_t (&K)[4],
-                                          uint32_t n_sel, const uint32_t (&hi0)[4], uint64_t thr,
-                                          uint32_t (&out)[4]) {
-    uint32_t lo[4], hi[4];
+// The survivor bound of one digit: the largest u with ms + u K <= thr, i.e.
+// floor((thr - ms) / K), clamped to 2^32 - 1 (u is 32-bit); 0 when thr < ms
+// (u >= 1 admits nothing).  The quotient is estimated in FP64 from rK, the
+// rounded reciprocal of K: relative error < 2^-50, so for quotients below
+// 2^32 the estimate is within 1 of the exact one, which one exact integer
+// step each way then restores (thr <= 2^63 and K < 2^62, so the products
+// below do not wrap).
+__device__ __forceinline__ uint32_t u_bound(uint64_t ms, uint64_t K, double rK, uint64_t thr) {
+    ME_CHECK(thr <= (1ull << 63) && K < (1ull << 62));
+    const uint64_t num = thr - ms;  // (wraps when thr < ms: the result is 0 then)
+    const double qd = __dmul_rz(__ull2double_rz(num), rK);
+    uint32_t q = (uint32_t)fmin(qd, 4294967295.0);
+    // exact: q K <= num < (q + 1) K, or q = 2^32 - 1 when (2^32 - 1) K <= num
+    uint64_t qk = (uint64_t)q * K;
+    const bool over = qk > num;
+    q = over ? q - 1 : q;
+    qk = over ? qk - K : qk;
+    q = num - qk >= K && q != 0xFFFFFFFFu ? q + 1 : q;
+    ME_CHECK(thr < ms || K == 0 || ((uint64_t)q * K <= num && (q == 0xFFFFFFFFu || num - (uint64_t)q * K < K)));
+    return thr < ms ? 0u : K == 0 ? 0xFFFFFFFFu : q;
+}
+
+// per bound j < NQ: the number of entries of the ascending su[0, n) that are
+// <= ub_j (n >= 1; u >= 1, so a bound 0 counts none).  Branch-free binary
+// search: the length sequence depends on n only, so the NQ searches run in
+// lockstep with one trip count and their loads in flight together; every load
+// is in su[0, n).
+#ifndef ME_K0_GROUP
+#define ME_K0_GROUP 1
+#endif
+constexpr int kCapGroup = ME_K0_GROUP;  // COUNT-mode K0: capacities searched together (x 4 digits)
+template <int NQ>
+__device__ __forceinline__ void count_le(const uint32_t* __restrict__ su, uint32_t n, const uint32_t (&ub)[NQ],
+                                         uint32_t (&out)[NQ]) {
+    uint32_t base[NQ];
 #pragma unroll
-    for (int q = 0; q < 4; q++) lo[q] = 0, hi[q] = (uint32_t)q < n_sel ? hi0[q] : 0u;
-    while (true) {
-        bool any = false;
+    for (int j = 0; j < NQ; j++) base[j] = 0;
+    uint32_t len = n;
+    while (len > 1) {
+        const uint32_t half = len >> 1;
+        uint32_t v[NQ];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            if (lo[q] < hi[q]) {
-                const uint32_t mid = (lo[q] + hi[q]) >> 1;
-                if (ms[q] + (uint64_t)su[mid] * K[q] <= thr) lo[q] = mid + 1;
-                else hi[q] = mid;
-                any = true;
-            }
-        }
-        if (!any) break;
+        for (int j = 0; j < NQ; j++) v[j] = su[base[j] + half - 1];
+#pragma unroll
+        for (int j = 0; j < NQ; j++) base[j] = v[j] <= ub[j] ? base[j] + half : base[j];
+        len -= half;
     }
 #pragma unroll
-    for (int q = 0; q < 4; q++) out[q] = lo[q];
+    for (int j = 0; j < NQ; j++) out[j] = base[j] + (su[base[j]] <= ub[j] ? 1u : 0u);
 }
 
 // One row: its RowEnt (to *out: global for K0, the warp's shared copy for the
@@ -133,40 +163,60 @@ __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uin
         if (two) st[(size_t)k << lg | sel] = last_stage(I, rc, dopt, Q);
     }
     if (!S.gbs_mode && !two) {
+        // per digit the exact survivor bound umax (u <= umax <=> total <= thr_max,
+        // which is what K3 tests) and the row's survivors: pairs with u <= umax
         const uint32_t np = I.tu.n_pairs;
-        const uint32_t all4[4] = {np, np, np, np};
+        ME_CHECK(np >= 1);
+        double rK[4];
         uint32_t nm[4];
-        count_fit4(su, ms, K, n_sel, all4, S.thr_max, nm);
+        // (digits sel >= n_sel keep umax 0: they count none)
 #pragma unroll
         for (uint32_t sel = 0; sel < 4; sel++) {
-            if (sel >= n_sel) break;
-            umax[sel] = nm[sel] ? su[nm[sel] - 1] : 0u;  // u >= 1: 0 admits nothing
-            if (full) cnt += nm[sel];
+            rK[sel] = sel < n_sel && K[sel] ? __drcp_rn(__ull2double_rn(K[sel])) : 0.0;
+            umax[sel] = sel < n_sel ? u_bound(ms[sel], K[sel], rK[sel], S.thr_max) : 0u;
         }
         if (CAPS && full) {
+            // every capacity's survivors (the largest threshold's are the
+            // row's), kCapGroup capacities x 4 digits per lockstep search
 #pragma unroll
-            for (int q = 0; q < NCAP; q++) {
-                if (q >= (int)S.n_cap) break;
-                if (S.thr[q] >= S.thr_max) {
-                    capc[q] += nm[0] + nm[1] + nm[2] + nm[3];
-                } else {
-                    uint32_t nq[4];
-                    count_fit4(su, ms, K, n_sel, nm, S.thr[q], nq);
-                    capc[q] += nq[0] + nq[1] + nq[2] + nq[3];
+            for (int q0 = 0; q0 < NCAP; q0 += kCapGroup) {
+                if (q0 >= (int)S.n_cap) break;
+                constexpr int G = kCapGroup < NCAP ? kCapGroup : NCAP;
+                uint32_t ub[4 * G], nq[4 * G];
+#pragma unroll
+                for (int j = 0; j < G; j++) {
+                    const int q = q0 + j;
+                    const bool on = q < (int)S.n_cap;
+                    const uint64_t th = on ? S.thr[q] : 0ull;
+#pragma unroll
+                    for (uint32_t sel = 0; sel < 4; sel++)
+                        ub[4 * j + sel] = !on ? 0u : th == S.thr_max ? umax[sel]
+                                                                      : (sel < n_sel ? u_bound(ms[sel], K[sel], rK[sel], th) : 0u);
+                }
+                count_le<4 * G>(su, np, ub, nq);
+#pragma unroll
+                for (int j = 0; j < G; j++) {
+                    const int q = q0 + j;
+                    if (q >= (int)S.n_cap) break;
+                    const uint32_t c = nq[4 * j] + nq[4 * j + 1] + nq[4 * j + 2] + nq[4 * j + 3];
+                    capc[q] += c;
+                    if (S.thr[q] == S.thr_max) cnt = c;
                 }
             }
+        } else {
+            count_le<4>(su, np, umax, nm);
+            if (full) cnt += nm[0] + nm[1] + nm[2] + nm[3];
         }
     } else if (!S.gbs_mode) {
         // NEXT-1: the largest of two stage totals, one digit at a time
-        for (uint32_t sel = 0; sel < n_sel; sel++) {
+        // (unrolled: ms[] and K[] stay in registers)
+#pragma unroll
+        for (uint32_t sel = 0; sel < 4; sel++) {
+            if (sel >= n_sel) break;
             const StEnt* x = st + ((size_t)k << lg | sel);
             Digit c{ms[sel], K[sel], x->msL, x->kL, true};
             const uint32_t nm = count_fit(su, I.tu.n_pairs, c, S.thr_max);
-            const uint32_t um = nm ? su[nm - 1] : 0u;
-            if (sel == 0) umax[0] = um;
-            else if (sel == 1) umax[1] = um;
-            else if (sel == 2) umax[2] = um;
-            else umax[3] = um;
+            umax[sel] = nm ? su[nm - 1] : 0u;
             if (full) {
                 cnt += nm;
                 if (CAPS) {
@@ -206,43 +256,65 @@ __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uin
     return cnt;
 }
 
-template <int NCAP, bool CAPS>
-__global__ void __launch_bounds__(kRowThreads, 8)
+// WR: write each row's entry and the per-row / per-unit survivor counts for
+// K3 (one block per 128 rows); !WR (COUNT mode and the sizing pass): only the
+// totals, accumulated into stats[0] and stats[1 + j] by the blocks of a
+// grid-stride launch.  SMEM (count-only): each block stages the sorted-u
+// lists in shared memory once; otherwise they are read through L1 (staging
+// per 128-row block measured slower in RECORDS: 344.3 vs 341.9 ms).  MINB: resident blocks per SM the registers are budgeted for (8: 64
+// registers, beside K3; COUNT mode runs alone and takes more registers).
+template <int NCAP, bool CAPS, bool WR, int MINB, bool SMEM>
+__global__ void __launch_bounds__(kRowThreads, MINB)
     rowcount_kernel(const DevSpace S, const uint64_t g0, const uint32_t n_rows, const uint32_t seg_lo,
                     const uint32_t n_seg_sub, const uint64_t lo, const uint64_t hi, RowEnt* __restrict__ rows,
                     StEnt* __restrict__ st, uint32_t* __restrict__ rcnt, uint32_t* __restrict__ ucnt,
                     uint64_t* __restrict__ stats) {
-    __shared__ uint32_t s_cap[NCAP];
-    __shared__ uint32_t s_su[kSuSmem];
-    if (CAPS && threadIdx.x < NCAP) s_cap[threadIdx.x] = 0;
-    const bool su_smem = S.k0_smem && !S.gbs_mode && S.n_pairs <= kSuSmem;
-    if (su_smem)
+    __shared__ uint32_t s_cap[NCAP + 1];
+    extern __shared__ uint32_t s_su[];
+    if (threadIdx.x <= NCAP) s_cap[threadIdx.x] = 0;
+    if (SMEM)
         for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_su[i] = __ldg(S.pair_su + i);
     __syncthreads();
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t* su = SMEM ? s_su : S.pair_su;
     uint32_t cnt = 0;
     uint32_t capc[NCAP];
 #pragma unroll
     for (int q = 0; q < NCAP; q++) capc[q] = 0;
-    // the segment of the warp's first row (all lanes, before the bounds test)
-    const uint64_t gw = g0 + (k & ~31u);
-    const uint32_t seg = gw < g0 + n_rows ? warp_segment(S.seg_row, seg_lo, n_seg_sub - 1, gw) : seg_lo;
-    if (k < n_rows) {
-        cnt = row_count<NCAP, CAPS>(S, g0 + k, k, seg, lo, hi, su_smem ? s_su : S.pair_su, rows + k, st, capc);
-        rcnt[k] = cnt;
+    for (uint32_t base = blockIdx.x * kRowThreads; base < n_rows; base += gridDim.x * kRowThreads) {
+        const uint32_t k = base + threadIdx.x;
+        // the segment of the warp's first row (all lanes, before the bounds test)
+        const uint64_t gw = g0 + (k & ~31u);
+        const uint32_t seg = gw < g0 + n_rows ? warp_segment(S.seg_row, seg_lo, n_seg_sub - 1, gw) : seg_lo;
+        uint32_t c = 0;
+        if (k < n_rows) {
+            RowEnt tmp;
+            c = row_count<NCAP, CAPS>(S, g0 + k, k, seg, lo, hi, su, WR ? rows + k : &tmp, st, capc);
+            if (WR) rcnt[k] = c;
+        }
+        if (WR) {
+            // survivors per 32-row unit (a unit is one warp of this kernel)
+            const uint32_t unit_cnt = __reduce_add_sync(0xffffffffu, c);
+            if ((threadIdx.x & 31) == 0 && k < n_rows) ucnt[k >> 5] = unit_cnt;
+        }
+        cnt += c;
     }
-    // survivors per 32-row unit (a unit is one warp of this kernel)
-    const uint32_t unit_cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if ((threadIdx.x & 31) == 0 && k < n_rows) ucnt[k >> 5] = unit_cnt;
+    if (!WR) {
+        const uint32_t t = __reduce_add_sync(0xffffffffu, cnt);
+        if ((threadIdx.x & 31) == 0 && t) atomicAdd(s_cap + NCAP, t);
+    }
     if (CAPS) {
 #pragma unroll
         for (int q = 0; q < NCAP; q++) {
             const uint32_t c = __reduce_add_sync(0xffffffffu, capc[q]);
             if ((threadIdx.x & 31) == 0 && c) atomicAdd(s_cap + q, c);
         }
+    }
+    if (CAPS || !WR) {
         __syncthreads();
-        if (threadIdx.x < NCAP && s_cap[threadIdx.x])
+        if (threadIdx.x < NCAP && CAPS && s_cap[threadIdx.x])
             atomicAdd((unsigned long long*)(stats + 1 + threadIdx.x), (unsigned long long)s_cap[threadIdx.x]);
+        if (threadIdx.x == NCAP && !WR && s_cap[NCAP])
+            atomicAdd((unsigned long long*)stats, (unsigned long long)s_cap[NCAP]);
     }
 }
 
@@ -663,16 +735,24 @@ void* fused_fn(me_out_mode mode, uint32_t n_cap, int minb) {
     return minb >= 3 ? fused_fn_m<3>(mode, n_cap) : fused_fn_m<2>(mode, n_cap);
 }
 
-template <bool CAPS>
+template <bool CAPS, bool WR, int MINB, bool SMEM>
 void* rowcount_fn_(uint32_t n_cap) {
     switch (ncap_pad3(n_cap)) {
-        case 1: return reinterpret_cast<void*>(&rowcount_kernel<1, CAPS>);
-        case 2: return reinterpret_cast<void*>(&rowcount_kernel<2, CAPS>);
-        case 4: return reinterpret_cast<void*>(&rowcount_kernel<4, CAPS>);
-        default: return reinterpret_cast<void*>(&rowcount_kernel<8, CAPS>);
+        case 1: return reinterpret_cast<void*>(&rowcount_kernel<1, CAPS, WR, MINB, SMEM>);
+        case 2: return reinterpret_cast<void*>(&rowcount_kernel<2, CAPS, WR, MINB, SMEM>);
+        case 4: return reinterpret_cast<void*>(&rowcount_kernel<4, CAPS, WR, MINB, SMEM>);
+        default: return reinterpret_cast<void*>(&rowcount_kernel<8, CAPS, WR, MINB, SMEM>);
     }
 }
-void* rowcount_fn(uint32_t n_cap, bool caps) { return caps ? rowcount_fn_<true>(n_cap) : rowcount_fn_<false>(n_cap); }
+void* rowcount_fn(uint32_t n_cap, bool caps, bool wr, bool smem) {
+    if (!wr) return smem ? rowcount_fn_<true, false, kRowMinbCount, true>(n_cap)
+                         : rowcount_fn_<true, false, kRowMinbCount, false>(n_cap);
+    return caps ? rowcount_fn_<true, true, 8, false>(n_cap) : rowcount_fn_<false, true, 8, false>(n_cap);
+}
+// count-only K0 stages the sorted-u lists when they fit the default 48 KB
+size_t rowcount_smem(const DevSpace& S) {
+    return S.k0_smem && !S.gbs_mode && S.n_pairs * 4ull <= 48u * 1024u ? S.n_pairs * 4ull : 0;
+}
 
 }  // namespace
 
@@ -689,11 +769,23 @@ uint32_t fused_units_of(uint32_t n_rows) { return (n_rows + kUnit - 1) / kUnit; 
 
 cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
                             uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
-                            uint64_t* stats, bool caps, cudaStream_t stream) {
-    const uint32_t blocks = (n_rows + kRowThreads - 1) / kRowThreads;
+                            uint64_t* stats, bool caps, bool write, uint32_t max_blocks, cudaStream_t stream) {
+    uint32_t blocks = (n_rows + kRowThreads - 1) / kRowThreads;
+    if (!write && max_blocks && blocks > max_blocks) blocks = max_blocks;
     void* args[] = {(void*)&S,  (void*)&g0,   (void*)&n_rows, (void*)&seg_lo, (void*)&n_seg_sub, (void*)&lo,
                     (void*)&hi, (void*)&rows, (void*)&st,     (void*)&rcnt,   (void*)&ucnt,      (void*)&stats};
-    return cudaLaunchKernel(rowcount_fn(S.n_cap, caps), dim3(blocks ? blocks : 1), dim3(kRowThreads), args, 0, stream);
+    const size_t smem = write ? 0 : rowcount_smem(S);
+    return cudaLaunchKernel(rowcount_fn(S.n_cap, caps || !write, write, smem != 0), dim3(blocks ? blocks : 1),
+                            dim3(kRowThreads), args, smem, stream);
+}
+
+int rowcount_blocks_per_sm(const DevSpace& S) {
+    int nb = 0;
+    const size_t smem = rowcount_smem(S);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, rowcount_fn(S.n_cap, true, false, smem != 0), kRowThreads,
+                                                      smem) != cudaSuccess)
+        return 1;
+    return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,

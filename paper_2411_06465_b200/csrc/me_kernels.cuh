@@ -43,10 +43,10 @@ struct DevSpace {
     uint32_t zero_stage;          // 2 / 3 = gradients / also weights sharded with the optimizer (NEXT-4)
     uint32_t sp_off, vpp;         // NEXT-4: sequence parallelism off (R28); virtual pipeline stages (R29)
     uint32_t wb, gb, ob;          // NEXT-4: bytes per parameter of weights / gradients / optimizer states (R30)
-    uint32_t k0_smem;             // K0 stages the sorted-u lists in shared memory (ME_K0_SMEM)
     uint32_t k3_caps;             // per-capacity counts from K3's masks (1) or K0's searches (0)
     uint32_t sparse;              // K3: a row with survivors * sparse < configurations takes the
                                   // two-phase (pair mask) path; 0 = never (ME_SPARSE)
+    uint32_t k0_smem;             // count-only K0 stages the sorted-u lists in shared memory (ME_K0_SMEM, 1)
     uint64_t thr[8];              // floor(cap_j * num / den); 0 for unused slots
     uint64_t thr_max;             // the largest threshold: survivor <=> total <= thr_max
     // thr_j + 1 with thr_j clamped to 2^62 (every total is < 2^58): the sweep
@@ -263,10 +263,15 @@ cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, u
 // row-count pipeline (me_fused.cu): K0 rows [g0, g0 + n_rows) of the range
 // [lo, hi) with their survivor counts (rcnt, per 32-row unit ucnt, per
 // capacity into stats[1 + j]); K3 rows with survivors -> output rows
-// caps: K0 also counts every capacity (COUNT mode); otherwise K3 does
+// caps: K0 also counts every capacity; otherwise K3 does.  !write (COUNT
+// mode, the sizing pass): K0 alone, totals only (stats[0] and every
+// capacity; no row entries, no unit counts, no scan needed), in at most
+// max_blocks grid-stride blocks (0: one per 128 rows)
 cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
                             uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
-                            uint64_t* stats, bool caps, cudaStream_t stream);
+                            uint64_t* stats, bool caps, bool write, uint32_t max_blocks, cudaStream_t stream);
+// resident blocks per SM of the count-only K0
+int rowcount_blocks_per_sm(const DevSpace& S);
 cudaError_t launch_fused(const DevSpace& S, const RowEnt* rows, const StEnt* st, const uint32_t* rcnt,
                          const uint32_t* ucnt, const uint64_t* uoff, uint32_t n_rows, uint64_t lo, uint64_t hi,
                          me_out_mode mode, Cols cols, uint64_t capacity, uint32_t n_blocks, int minb,
