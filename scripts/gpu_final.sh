@@ -19,7 +19,7 @@ mkdir -p profiles/r2_final && cp $O/ncu_chunk*.json profiles/r2_final/
 timeout 1200 python bench.py --steps 20 --warmup 5 > $O/bench.log 2>&1; echo "rc=$?" >> $O/bench.log
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref.log 2>&1; echo "rc=$?" >> $O/bench_ref.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches.csv \
-  python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-modes > $O/ncu_launch.log 2>&1; echo "ncu rc=$?" >> $O/ncu_launch.log
+  python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-modes --no-verify > $O/ncu_launch.log 2>&1; echo "ncu rc=$?" >> $O/ncu_launch.log
 python scripts/launch_summary.py $O/launches.csv > $O/launch_summary.txt 2>&1
 tail -n 3 $O/pytest_gpu.log $O/pytest_gpu_checked.log $O/smoke.log; cat $O/launch_summary.txt | head -8
 grep "^{" $O/bench.log | head -c 3000; echo; grep "^{" $O/bench_ref.log | head -c 600
