@@ -597,12 +597,15 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     // sub-range i+1 (or of the next call) runs while the caller's stream still
     // writes the rows of sub-range i.  Counts go to a plan-owned slot (see
     // me_plan::pstats) that the caller's stream copies into the result.
-    cudaStream_t cs = P->serial ? st : P->cstream;
-    const uint32_t slot = P->stat_turn++ % me_plan::kStatSlots;
-    uint64_t* pst = P->pstats + (size_t)slot * 16;
-    cudaStreamWaitEvent(cs, P->stat_ev[slot], 0);
-    cudaStreamWaitEvent(cs, P->ready_ev, 0);
+    // COUNT: K0 alone, nothing to overlap -- it runs on the caller's stream
+    // and counts straight into the result (no stream hand-offs per call).
     const int nc = n_cols_of(o->mode);
+    const bool direct = nc == 0;
+    cudaStream_t cs = P->serial || direct ? st : P->cstream;
+    const uint32_t slot = direct ? 0u : P->stat_turn++ % me_plan::kStatSlots;
+    uint64_t* pst = direct ? R->stats : P->pstats + (size_t)slot * 16;
+    if (!direct) cudaStreamWaitEvent(cs, P->stat_ev[slot], 0);
+    cudaStreamWaitEvent(cs, P->ready_ev, 0);
     const uint64_t len = e - b;
     cudaEventRecord(R->ev[0], cs);
     Cols cols{};
@@ -638,9 +641,11 @@ static int plan_sweep(me_plan* P, const me_sweep_opts* o, bool own_plan, me_resu
     R->ran_write = nc && len;
     cudaEventRecord(R->ev[2], cs);
     cudaStreamWaitEvent(st, R->ev[2], 0);  // counts complete before the caller's stream reads them
-    if (cudaMemcpyAsync(R->stats, pst, 9 * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-        return fail(cuda_err(cudaGetLastError(), "stats copy"));
-    cudaEventRecord(P->stat_ev[slot], st);
+    if (!direct) {
+        if (cudaMemcpyAsync(R->stats, pst, 9 * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return fail(cuda_err(cudaGetLastError(), "stats copy"));
+        cudaEventRecord(P->stat_ev[slot], st);
+    }
     cudaEventRecord(R->ev[3], st);
     if (o->comm && o->partition == ME_PART_EVEN) {
         R->gathered = (uint64_t*)R->A.get((size_t)o->comm->nranks * 9 * 8);
