@@ -364,6 +364,32 @@ def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
             assert_same(me, res, *ref, mode)
 
 
+@pytest.mark.parametrize("env", [{}, {"ME_K0_BPS": "0"}, {"ME_K0_BPS": "1"}, {"ME_K0_SMEM": "0"},
+                                 {"ME_MAX_ROWS": "7"}, {"ME_SERIAL": "1"}],
+                         ids=["default", "one-block-per-128-rows", "1bps", "l1", "maxrows7", "serial"])
+def test_count_mode_variants(me, oracle_mod, monkeypatch, env):
+    """COUNT mode runs K0 alone (grid-stride blocks that stage the sorted u
+    lists, totals by atomics): survivor and per-capacity counts equal the
+    oracle's for each launch variant, on the whole space and on ragged ranges
+    (cut first / last rows go config by config), in paper mode, with a global
+    batch, with NEXT-1 and with 8 capacities."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    spaces = [mi.config("C3", uneven=1),
+              mi.Space(models=mi.random_models(12, seed=5), world=[24, 64, 96], caps_gb=[40, 80, 192],
+                       mbs=[1, 2, 4], seq=[4096, 8192], uneven=1, gbs=768),
+              mi.Space(models=mi.random_models(8, seed=7), world=[16, 64], caps_gb=[40, 80, 192], mbs=[1, 2, 4],
+                       seq=[4096, 8192], uneven=1, stage_max=1),
+              mi.Space(models=mi.random_models(10, seed=11), world=[8, 32, 128], mbs=[1, 2, 3, 5, 8],
+                       seq=[2048, 4096, 16384], caps_gb=[16, 24, 40, 48, 80, 94, 141, 192], uneven=1)]
+    for sp in spaces:
+        plan = me.Plan(sp)
+        for b, e in ((0, 0), (13, plan.size - 31), (plan.size // 2, plan.size // 2 + 777)):
+            res = plan.sweep(b, e, mode=me.ME_OUT_COUNT)
+            assert res.status() == 0
+            assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), me.ME_OUT_COUNT)
+
+
 @pytest.mark.parametrize("max_rows", [1, 64, 1000])
 def test_subranges_cut_by_rows(me, oracle_mod, monkeypatch, max_rows):
     """Sub-ranges are also cut at max_rows rows (2^21 in production; a small
