@@ -529,21 +529,20 @@ __device__ __forceinline__ void fused_row_pairs(const DevSpace& S, const RowEnt&
                 m4 |= (sv ? 1u : 0u) << sel;
             }
         }
+        // the lanes' survivor counts (0..4) bit-sliced into three ballots:
+        // exclusive prefix and warp total by popcounts (no shuffle chain)
         const uint32_t c = __popc(m4);
-        uint32_t inc = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= (uint32_t)o) inc += y;
-        }
-        uint32_t at = run + inc - c;
+        const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c & 2u),
+                       b2 = __ballot_sync(0xffffffffu, c & 4u);
+        const uint32_t lt = (1u << lane) - 1u;
+        uint32_t at = run + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
         while (m4) {
             const uint32_t sel = __ffs(m4) - 1;
             m4 &= m4 - 1;
             ME_CHECK(at < kRowPairs * 4);
             slist[at++] = (uint16_t)(j << 2 | sel);
         }
-        run += __shfl_sync(0xffffffffu, inc, 31);
+        run += __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
     }
     __syncwarp();
     ME_CHECK(run == cnt);
