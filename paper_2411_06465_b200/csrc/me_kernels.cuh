@@ -239,7 +239,8 @@ struct __align__(16) RowEnt {
     uint64_t optim1, rs;           // rs = flat index of the row's first config
     // survivor bound per (rc, do) digit: total <= thr_max  <=>  u <= umax
     // (paper mode; with the largest stage when stage_max); unused with gbs.
-    // Row-count pipeline: the largest surviving u of the row (0 = none)
+    // Paper mode: floor((thr_max - ms) / K) clamped to 2^32 - 1 (0 = none);
+    // NEXT-1: the largest surviving u of the row (0 = none)
     uint32_t umax[4];
 };
 // NEXT-1: last-stage terms of one row for one (rc, do) digit (64 B)
