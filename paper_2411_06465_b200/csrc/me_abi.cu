@@ -240,7 +240,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     DevModel* dm;
     std::vector<DevModel> dmodels;
     for (const me_model& m : H.models) dmodels.push_back(dev_model(m));
-    uint32_t *dcls, *dlo, *dlt, *dpb, *dsu;
+    uint32_t *dcls, *dlo, *dlt, *dpb, *dsu, *dfe;
     uint64_t *dsp, *dlp, *dsr;
     DevTuple* dtu;
     DevPair* dpr;
@@ -254,7 +254,8 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
         (st = upload(P->A, H.tuples, &dtu)) || (P->owned.push_back(dtu), false) ||
         (st = upload(P->A, H.pairs, &dpr)) || (P->owned.push_back(dpr), false) ||
         (st = upload(P->A, H.pair_b, &dpb)) || (P->owned.push_back(dpb), false) ||
-        (st = upload(P->A, H.pair_su, &dsu)) || (P->owned.push_back(dsu), false)) {
+        (st = upload(P->A, H.pair_su, &dsu)) || (P->owned.push_back(dsu), false) ||
+        (st = upload(P->A, H.pair_fence, &dfe)) || (P->owned.push_back(dfe), false)) {
         me_plan_free(P);
         return st;
     }
@@ -269,6 +270,10 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     D.pairs = dpr;
     D.pair_b = dpb;
     D.pair_su = dsu;
+    D.pair_fence = dfe;
+    D.n_fence = (uint32_t)H.pair_fence.size();
+    D.fenced = H.fenced ? 1u : 0u;
+    if (const char* e = getenv("ME_K0_FENCE")) D.fenced = D.fenced && atoi(e) ? 1u : 0u;
     D.n_seg = (uint32_t)(H.seg_prefix.size() - 1);
     D.n_world = (uint32_t)H.world.size();
     D.n_pairs = (uint32_t)H.pairs.size();
@@ -395,7 +400,7 @@ extern "C" int me_plan_table_bytes(const me_plan* plan, uint64_t* bytes) {
     *bytes = H.models.size() * sizeof(DevModel) + H.model_class.size() * 4 + H.seg_prefix.size() * 8 +
              H.seg_row.size() * 8 + H.list_off.size() * 4 + H.list_tuple.size() * 4 + H.list_prefix.size() * 8 +
              H.tuples.size() * sizeof(DevTuple) + H.pairs.size() * sizeof(DevPair) + H.pair_b.size() * 4 +
-             H.pair_su.size() * 4;
+             H.pair_su.size() * 4 + H.pair_fence.size() * 4;
     return ME_OK;
 }
 

@@ -104,7 +104,7 @@ __device__ __forceinline__ uint32_t u_bound(uint64_t ms, uint64_t K, double rK, 
 // lockstep with one trip count and their loads in flight together; every load
 // is in su[0, n).
 #ifndef ME_K0_GROUP
-#define ME_K0_GROUP 1
+#define ME_K0_GROUP 4
 #endif
 constexpr int kCapGroup = ME_K0_GROUP;  // COUNT-mode K0: capacities searched together (x 4 digits)
 template <int NQ>
@@ -127,13 +127,47 @@ __device__ __forceinline__ void count_le(const uint32_t* __restrict__ su, uint32
     for (int j = 0; j < NQ; j++) out[j] = base[j] + (su[base[j]] <= ub[j] ? 1u : 0u);
 }
 
+// The same counts through the pool's fences (n <= 128): fe[0, 4) = the
+// largest u of each 32-entry group, fe[4, 20) = of each 8-entry block
+// (0xFFFFFFFF past the pool).  Groups, then blocks, whose largest u is <= ub
+// form a prefix, so per bound: g = full groups (4 compares), b = full blocks
+// of group g (3 compares on one 16-byte load), then a 3-step search inside
+// block 4g + b.  4 scattered 4-byte loads per bound instead of log2(n) + 1:
+// fewer shared-memory bank conflicts / L1 wavefronts, the dominant stall of
+// the plain search.
+template <int NQ>
+__device__ __forceinline__ void count_le_f(const uint32_t* __restrict__ su, uint32_t n,
+                                           const uint32_t* __restrict__ fe, const uint32_t (&ub)[NQ],
+                                           uint32_t (&out)[NQ]) {
+    const uint4 g4 = *reinterpret_cast<const uint4*>(fe);
+#pragma unroll
+    for (int j = 0; j < NQ; j++) {
+        const uint32_t x = ub[j];
+        const uint32_t g = (g4.x <= x) + (g4.y <= x) + (g4.z <= x) + (g4.w <= x);
+        const uint4 b4 = *reinterpret_cast<const uint4*>(fe + 4 + 4 * (g & 3u));
+        const uint32_t blk = 4 * g + (g < 4 ? (b4.x <= x) + (b4.y <= x) + (b4.z <= x) : 0u);
+        const uint32_t lo = 8 * blk;
+        uint32_t len = lo < n ? min(8u, n - lo) : 1u, base = 0;
+#pragma unroll
+        for (int it = 0; it < 3; it++) {
+            const uint32_t half = len >> 1;
+            const uint32_t at = lo + base + half;
+            const uint32_t v = su[min(at ? at - 1 : 0u, n - 1)];  // (half = 0: unused)
+            base = half && v <= x ? base + half : base;
+            len -= half;
+        }
+        out[j] = lo < n ? lo + base + (su[lo + base] <= x ? 1u : 0u) : n;
+        ME_CHECK(out[j] <= n);
+    }
+}
+
 // One row: its RowEnt (to *out: global for K0, the warp's shared copy for the
 // one-pass kernel), its last-stage terms (NEXT-1, to st[k]), its survivors in
 // the window [lo, hi) (returned) and, CAPS, per capacity (into capc).
 // su_base: the sorted-u lists (shared memory when staged).
 template <int NCAP, bool CAPS>
 __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uint32_t k, uint32_t seg,
-                                              uint64_t lo, uint64_t hi, const uint32_t* su_base, RowEnt* out,
+                                              uint64_t lo, uint64_t hi, const uint32_t* su_base, const uint32_t* fe_base, RowEnt* out,
                                               StEnt* __restrict__ st, uint32_t (&capc)[NCAP]) {
     uint32_t cnt = 0;
     const RowId I = row_id_from(S, g, seg);
@@ -149,6 +183,7 @@ __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uin
     const uint32_t b = I.rs + I.tu.w > hi ? (uint32_t)(hi - I.rs) : I.tu.w;
     const bool full = a == 0 && b == I.tu.w;
     const uint32_t* su = su_base + I.tu.pair_off;
+    const uint32_t* fe = fe_base + I.tu.fence_off;
     const DevPair* pp = S.pairs + I.tu.pair_off;
     // per digit: stage-0 total = ms + u K in paper mode
     uint64_t ms[4], K[4];
@@ -177,11 +212,13 @@ __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uin
         }
         if (CAPS && full) {
             // every capacity's survivors (the largest threshold's are the
-            // row's), kCapGroup capacities x 4 digits per lockstep search
+            // row's): up to kCapGroup capacities x 4 digits per lockstep
+            // search (all of them when they fit; else one at a time, which
+            // keeps 8 capacities free of spills)
+            constexpr int G = NCAP <= kCapGroup ? NCAP : 1;
 #pragma unroll
-            for (int q0 = 0; q0 < NCAP; q0 += kCapGroup) {
+            for (int q0 = 0; q0 < NCAP; q0 += G) {
                 if (q0 >= (int)S.n_cap) break;
-                constexpr int G = kCapGroup < NCAP ? kCapGroup : NCAP;
                 uint32_t ub[4 * G], nq[4 * G];
 #pragma unroll
                 for (int j = 0; j < G; j++) {
@@ -193,7 +230,8 @@ __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uin
                         ub[4 * j + sel] = !on ? 0u : th == S.thr_max ? umax[sel]
                                                                       : (sel < n_sel ? u_bound(ms[sel], K[sel], rK[sel], th) : 0u);
                 }
-                count_le<4 * G>(su, np, ub, nq);
+                if (S.fenced) count_le_f<4 * G>(su, np, fe, ub, nq);
+                else count_le<4 * G>(su, np, ub, nq);
 #pragma unroll
                 for (int j = 0; j < G; j++) {
                     const int q = q0 + j;
@@ -203,9 +241,46 @@ __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uin
                     if (S.thr[q] == S.thr_max) cnt = c;
                 }
             }
+        } else if (full) {
+            if (S.fenced) count_le_f<4>(su, np, fe, umax, nm);
+            else count_le<4>(su, np, umax, nm);
+            cnt += nm[0] + nm[1] + nm[2] + nm[3];
         } else {
-            count_le<4>(su, np, umax, nm);
-            if (full) cnt += nm[0] + nm[1] + nm[2] + nm[3];
+            // a row cut by the range: its window [a, b) configuration by
+            // configuration, one compare each against the digit's bound(s)
+            // (a single thread walks it: the per-configuration total would
+            // keep it running long after the rest of the launch)
+            for (uint32_t sel = 0; sel < n_sel; sel++) {
+                const uint32_t um = sel == 0 ? umax[0] : sel == 1 ? umax[1] : sel == 2 ? umax[2] : umax[3];
+                const uint64_t msq = sel == 0 ? ms[0] : sel == 1 ? ms[1] : sel == 2 ? ms[2] : ms[3];
+                const uint64_t Kq = sel == 0 ? K[0] : sel == 1 ? K[1] : sel == 2 ? K[2] : K[3];
+                const double rq = sel == 0 ? rK[0] : sel == 1 ? rK[1] : sel == 2 ? rK[2] : rK[3];
+                uint32_t ubc[NCAP];
+#pragma unroll
+                for (int q = 0; q < NCAP; q++)
+                    ubc[q] = !CAPS || q >= (int)S.n_cap ? 0u
+                             : S.thr[q] == S.thr_max    ? um
+                                                        : u_bound(msq, Kq, rq, S.thr[q]);
+                // eight independent loads in flight per step
+                constexpr uint32_t kW = 8;
+                for (uint32_t p0 = a + ((sel - a) & (n_sel - 1u)); p0 < b; p0 += kW * n_sel) {
+                    uint32_t u[kW];
+#pragma unroll
+                    for (uint32_t i = 0; i < kW; i++) {
+                        const uint32_t pos = p0 + i * n_sel;
+                        u[i] = pos < b ? __ldg(&pp[pos >> lg].u) : 0u;  // u >= 1: 0 marks "outside"
+                    }
+#pragma unroll
+                    for (uint32_t i = 0; i < kW; i++) {
+                        const bool in = u[i] != 0;
+                        cnt += in && u[i] <= um ? 1u : 0u;
+                        if (CAPS) {
+#pragma unroll
+                            for (int q = 0; q < NCAP; q++) capc[q] += in && u[i] <= ubc[q] ? 1u : 0u;
+                        }
+                    }
+                }
+            }
         }
     } else if (!S.gbs_mode) {
         // NEXT-1: the largest of two stage totals, one digit at a time
@@ -227,7 +302,7 @@ __device__ __forceinline__ uint32_t row_count(const DevSpace& S, uint64_t g, uin
             }
         }
     }
-    if (!full || S.gbs_mode) {
+    if (S.gbs_mode || (two && !full)) {
         // config by config over the window: in-flight counts of each
         // pair's m microbatches (R17, R29), or a cut row
 #pragma unroll
@@ -270,12 +345,18 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
                     StEnt* __restrict__ st, uint32_t* __restrict__ rcnt, uint32_t* __restrict__ ucnt,
                     uint64_t* __restrict__ stats) {
     __shared__ uint32_t s_cap[NCAP + 1];
-    extern __shared__ uint32_t s_su[];
+    extern __shared__ __align__(16) uint32_t s_su[];
+    // (SMEM: the sorted lists, then the fences from a 16-byte boundary)
+    const uint32_t fe_at = (S.n_pairs + 3u) & ~3u;
     if (threadIdx.x <= NCAP) s_cap[threadIdx.x] = 0;
-    if (SMEM)
+    if (SMEM) {
         for (uint32_t i = threadIdx.x; i < S.n_pairs; i += blockDim.x) s_su[i] = __ldg(S.pair_su + i);
+        if (S.fenced)
+            for (uint32_t i = threadIdx.x; i < S.n_fence; i += blockDim.x) s_su[fe_at + i] = __ldg(S.pair_fence + i);
+    }
     __syncthreads();
     const uint32_t* su = SMEM ? s_su : S.pair_su;
+    const uint32_t* fe = SMEM ? s_su + fe_at : S.pair_fence;
     uint32_t cnt = 0;
     uint32_t capc[NCAP];
 #pragma unroll
@@ -288,7 +369,7 @@ __global__ void __launch_bounds__(kRowThreads, MINB)
         uint32_t c = 0;
         if (k < n_rows) {
             RowEnt tmp;
-            c = row_count<NCAP, CAPS>(S, g0 + k, k, seg, lo, hi, su, WR ? rows + k : &tmp, st, capc);
+            c = row_count<NCAP, CAPS>(S, g0 + k, k, seg, lo, hi, su, fe, WR ? rows + k : &tmp, st, capc);
             if (WR) rcnt[k] = c;
         }
         if (WR) {
@@ -750,7 +831,8 @@ void* rowcount_fn(uint32_t n_cap, bool caps, bool wr, bool smem) {
 }
 // count-only K0 stages the sorted-u lists when they fit the default 48 KB
 size_t rowcount_smem(const DevSpace& S) {
-    return S.k0_smem && !S.gbs_mode && S.n_pairs * 4ull <= 48u * 1024u ? S.n_pairs * 4ull : 0;
+    const size_t b = (((S.n_pairs + 3ull) & ~3ull) + (S.fenced ? S.n_fence : 0u)) * 4ull;
+    return S.k0_smem && !S.gbs_mode && b <= 48u * 1024u ? b : 0;
 }
 
 }  // namespace

@@ -34,6 +34,9 @@ struct DevSpace {
     const DevPair* pairs;
     const uint32_t* pair_b;       // micro-batch size of each pair (planner only)
     const uint32_t* pair_su;      // per pair list: its u values sorted ascending (row-count pipeline)
+    const uint32_t* pair_fence;   // per pool: 4 + 16 fences over pair_su (DevTuple::fence_off)
+    uint32_t n_fence;             // entries of pair_fence
+    uint32_t fenced;              // K0 searches through the fences (every pool <= 128 pairs; ME_K0_FENCE)
     uint32_t n_seg, n_world;
     uint32_t n_pairs;             // pooled (b, s) pairs
     uint32_t lg_rcdo, rcdo_rc, rcdo_do;

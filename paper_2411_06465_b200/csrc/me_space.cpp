@@ -96,8 +96,11 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
     pairs.clear();
     pair_b.clear();
     pair_su.clear();
+    pair_fence.clear();
+    fenced = true;
     tup_begin.assign(1, 0);
-    std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::pair<uint32_t, uint32_t>> pool;  // (c, d|0, p|0) -> (off, n)
+    // (c, d|0, p|0) -> (off, n, fence offset)
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::tuple<uint32_t, uint32_t, uint32_t>> pool;
     std::vector<uint32_t> tvals, pvals;
     for (uint32_t N : world) {
         for (uint32_t t = 1; t <= N; t++) {
@@ -124,16 +127,25 @@ int HostSpace::build(const me_model_range* mr, const me_cluster* cl, const me_cf
                                 pairs.push_back(pr);
                                 pair_b.push_back(b);
                             }
-                        it = pool.emplace(key, std::make_pair(off, (uint32_t)pairs.size() - off)).first;
+                        const uint32_t n = (uint32_t)pairs.size() - off;
+                        it = pool.emplace(key, std::make_tuple(off, n, (uint32_t)pair_fence.size())).first;
                         for (size_t q = off; q < pairs.size(); q++) pair_su.push_back(pairs[q].u);
                         std::sort(pair_su.begin() + off, pair_su.end());
+                        // the pool's search index (K0): the largest u of each
+                        // 32-entry group (4), then of each 8-entry block (16);
+                        // past the pool's end 0xFFFFFFFF
+                        if (n > 128) fenced = false;
+                        for (uint32_t span : {32u, 8u})
+                            for (uint32_t i = 0; i < 128 / span; i++)
+                                pair_fence.push_back(n && i * span < n ? pair_su[off + std::min(n, (i + 1) * span) - 1]
+                                                                       : 0xFFFFFFFFu);
                     }
                     DevTuple tu;
                     tu.t = t; tu.c = c; tu.p = p; tu.d = d;
-                    tu.pair_off = it->second.first;
-                    tu.n_pairs = it->second.second;
+                    tu.pair_off = std::get<0>(it->second);
+                    tu.n_pairs = std::get<1>(it->second);
+                    tu.fence_off = std::get<2>(it->second);
                     tu.w = tu.n_pairs * n_rcdo;
-                    tu.n_world = N;
                     if (tu.w == 0) continue;  // no (b, s) pair survives: consumes no index
                     tuples.push_back(tu);
                     tvals.push_back(t);

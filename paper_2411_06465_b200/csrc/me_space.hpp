@@ -26,7 +26,7 @@ struct DevTuple {          // 32 B
     uint32_t w;            // configs in this tuple's row: n_pairs * n_rcdo
     uint32_t pair_off;     // first pair in the pool
     uint32_t n_pairs;
-    uint32_t n_world;      // N
+    uint32_t fence_off;    // the pool's fences in pair_fence (20 u32)
 };
 
 struct DevPair {           // 8 B
@@ -75,6 +75,8 @@ class HostSpace {
     std::vector<DevPair> pairs;
     std::vector<uint32_t> pair_b;       // micro-batch size of each pooled pair (planner)
     std::vector<uint32_t> pair_su;      // per pooled pair list: its u values sorted ascending
+    std::vector<uint32_t> pair_fence;   // per pool: 4 + 16 fences over its sorted u values (K0's search index)
+    bool fenced = true;                 // every pool has <= 128 pairs (the fences cover it)
     std::vector<uint32_t> model_class;  // per model
     uint32_t n_class = 0;
     std::vector<uint32_t> list_off;     // n_class * n_world + 1

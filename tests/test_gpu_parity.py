@@ -340,9 +340,9 @@ def test_sweep_zero_stages(me, oracle_mod, zero, stage_max):
 
 @pytest.mark.parametrize("env", [{"ME_SERIAL": "1"}, {"ME_SETS": "3"}, {"ME_FUSED_BPS": "1"},
                                  {"ME_SERIAL": "1", "ME_FUSED_BPS": "1"}, {"ME_SPARSE": "0"}, {"ME_SPARSE": "4"},
-                                 {"ME_FUSED_MINB": "2"}, {"ME_FUSED_MINB": "3"}],
+                                 {"ME_FUSED_MINB": "2"}, {"ME_FUSED_MINB": "3"}, {"ME_K0_FENCE": "0"}],
                          ids=["serial", "sets3", "fused-1bps", "serial-1bps", "positional", "sparse4", "minb2",
-                              "minb3"])
+                              "minb3", "no-fence"])
 def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
     """The launch variants (read at plan creation) give the same rows: serial
     streams, three scratch sets, one fused-kernel block per SM, K3's
@@ -365,8 +365,10 @@ def test_pipeline_variants(me, oracle_mod, monkeypatch, env):
 
 
 @pytest.mark.parametrize("env", [{}, {"ME_K0_BPS": "0"}, {"ME_K0_BPS": "1"}, {"ME_K0_SMEM": "0"},
-                                 {"ME_MAX_ROWS": "7"}, {"ME_SERIAL": "1"}],
-                         ids=["default", "one-block-per-128-rows", "1bps", "l1", "maxrows7", "serial"])
+                                 {"ME_MAX_ROWS": "7"}, {"ME_SERIAL": "1"}, {"ME_K0_FENCE": "0"},
+                                 {"ME_K0_FENCE": "0", "ME_K0_SMEM": "0"}],
+                         ids=["default", "one-block-per-128-rows", "1bps", "l1", "maxrows7", "serial", "no-fence",
+                              "no-fence-l1"])
 def test_count_mode_variants(me, oracle_mod, monkeypatch, env):
     """COUNT mode runs K0 alone (grid-stride blocks that stage the sorted u
     lists, totals by atomics): survivor and per-capacity counts equal the
