@@ -14,10 +14,6 @@
 #include "me_kernels.cuh"
 #include "me_space.hpp"
 
-namespace me {
-uint32_t ncap_stride(uint32_t n_cap);
-}
-
 using namespace me;
 
 extern "C" int me_partition(uint64_t, uint64_t, int, int, uint64_t*, uint64_t*);
@@ -522,7 +518,7 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
         cudaEventRecord(tev[1], cs);
         if (write) {
             // counts only: K0 summed them
-            ce = launch_scan(sc.ucnt, nullptr, fused_units_of(n_rows), 0, sc.uoff, stats, cs);
+            ce = launch_scan(sc.ucnt, fused_units_of(n_rows), sc.uoff, stats, cs);
             if (ce != cudaSuccess) return cuda_err(ce, "scan kernel");
         }
         cudaEventRecord(tev[2], cs);

@@ -15,60 +15,68 @@ namespace me {
 
 namespace {
 
-// one block: exclusive scan of the span counts into u64 offsets starting at
-// the running total stats[0]; stats[0] and stats[1 + q] accumulate the totals
-// of this sub-range
-__global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ counts, uint32_t n,
-                                                    const uint32_t* __restrict__ span_caps, uint32_t n_spans,
-                                                    uint32_t ncap_stride, uint32_t n_cap,
-                                                    uint64_t* __restrict__ offs, uint64_t* __restrict__ stats) {
+// one block: exclusive scan of the unit counts into u64 offsets starting at
+// the running total stats[0], which then holds the new running total.  Tiles
+// of 4096 counts: one coalesced 16-byte load per thread, warp and block scans,
+// 2 x 16-byte stores of the four offsets; the tile's total carries over.  (It
+// sits between K0 and K3 of every sub-range, so its latency counts.)
+constexpr uint32_t kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __restrict__ counts, uint32_t n,
+                                                           uint64_t* __restrict__ offs,
+                                                           uint64_t* __restrict__ stats) {
     __shared__ uint64_t s_warp[32];
-    __shared__ uint64_t s_caps[8][32];
-    __shared__ uint64_t s_base;
+    __shared__ uint64_t s_carry;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) s_base = stats[0];
-    const uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
-    const uint32_t lo = min(n, tid * chunk), hi = min(n, lo + chunk);
-    uint64_t sum = 0;
-    for (uint32_t i = lo; i < hi; i++) sum += counts[i];
-    uint64_t caps[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t s = tid; s < n_spans; s += blockDim.x)
-        for (uint32_t q = 0; q < n_cap; q++) caps[q] += span_caps[(size_t)s * ncap_stride + q];
-    uint64_t inc = sum;  // inclusive warp scan
-    for (int o = 1; o < 32; o <<= 1) {
-        uint64_t v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= (uint32_t)o) inc += v;
-    }
-    if (lane == 31) s_warp[wid] = inc;
-    for (uint32_t q = 0; q < n_cap; q++) {
-        uint64_t c = caps[q];
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
-        if (lane == 0) s_caps[q][wid] = c;
-    }
-    __syncthreads();
-    const uint64_t base = s_base;
-    if (wid == 0) {
-        const uint32_t nw = blockDim.x >> 5;
-        uint64_t v = lane < nw ? s_warp[lane] : 0;
-        uint64_t x = v;
+    // (vector accesses when the caller's allocator returned 16-byte-aligned blocks)
+    const bool vec = ((reinterpret_cast<uintptr_t>(counts) | reinterpret_cast<uintptr_t>(offs)) & 15u) == 0;
+    if (tid == 0) s_carry = stats[0];
+    for (uint32_t t0 = 0; t0 < n; t0 += 4 * kScanThreads) {
+        const uint32_t i0 = t0 + 4 * tid;
+        uint32_t c[4];
+        if (vec && i0 + 3 < n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(counts + i0);
+            c[0] = v.x, c[1] = v.y, c[2] = v.z, c[3] = v.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++) c[k] = i0 + k < n ? counts[i0 + k] : 0u;
+        }
+        const uint64_t sum = (uint64_t)c[0] + c[1] + c[2] + c[3];
+        uint64_t inc = sum;  // inclusive warp scan
+#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= (uint32_t)o) x += y;
+            const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
         }
-        if (lane < nw) s_warp[lane] = x - v;  // exclusive
-        if (lane == 31) stats[0] = base + x;
-        for (uint32_t q = 0; q < n_cap; q++) {
-            uint64_t c = lane < nw ? s_caps[q][lane] : 0;
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
-            if (lane == 0) stats[1 + q] += c;
+        if (lane == 31) s_warp[wid] = inc;
+        __syncthreads();  // (also orders s_carry's first write)
+        if (wid == 0) {
+            const uint64_t v = s_warp[lane];
+            uint64_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            s_warp[lane] = x - v;  // exclusive over warps
         }
+        __syncthreads();
+        uint64_t run = s_carry + s_warp[wid] + inc - sum;
+        uint64_t o4[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) o4[k] = run, run += c[k];
+        if (vec && i0 + 3 < n) {
+            reinterpret_cast<ulonglong2*>(offs + i0)[0] = make_ulonglong2(o4[0], o4[1]);
+            reinterpret_cast<ulonglong2*>(offs + i0)[1] = make_ulonglong2(o4[2], o4[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                if (i0 + k < n) offs[i0 + k] = o4[k];
+        }
+        __syncthreads();  // every thread has read s_carry and s_warp
+        if (tid == kScanThreads - 1) s_carry = run;
     }
     __syncthreads();
-    uint64_t run = base + s_warp[wid] + inc - sum;
-    for (uint32_t i = lo; i < hi; i++) {
-        offs[i] = run;
-        run += counts[i];
-    }
+    if (tid == 0) stats[0] = s_carry;
 }
 
 
@@ -241,16 +249,10 @@ __global__ void estimate_kernel(const me_model* __restrict__ models, uint32_t n_
     }
 }
 
-inline uint32_t ncap_stride_(uint32_t n_cap) { return n_cap <= 1 ? 1 : n_cap <= 2 ? 2 : n_cap <= 4 ? 4 : 8; }
-
 }  // namespace
 
-uint32_t ncap_stride(uint32_t n_cap) { return ncap_stride_(n_cap); }
-
-cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
-                        uint64_t* span_off, uint64_t* stats, cudaStream_t st) {
-    scan_kernel<<<1, 256, 0, st>>>(span_count, n_spans, span_caps, n_spans, ncap_stride(n_cap), n_cap, span_off,
-                                    stats);
+cudaError_t launch_scan(const uint32_t* counts, uint32_t n, uint64_t* offs, uint64_t* stats, cudaStream_t st) {
+    scan_kernel<<<1, kScanThreads, 0, st>>>(counts, n, offs, stats);
     return cudaGetLastError();
 }
 

@@ -260,10 +260,9 @@ struct Cols {
 constexpr int kThreads = 256;
 constexpr uint64_t kMaxSub = 1ull << 28;           // indices per sub-range of a sweep
 
-uint32_t ncap_stride(uint32_t n_cap);
-// span offsets = running total stats[0] + exclusive prefix; stats accumulate
-cudaError_t launch_scan(const uint32_t* span_count, const uint32_t* span_caps, uint32_t n_spans, uint32_t n_cap,
-                        uint64_t* span_off, uint64_t* stats, cudaStream_t st);
+// unit offsets = running total stats[0] + exclusive prefix of the unit
+// counts; stats[0] += their total (counts: 16-byte aligned)
+cudaError_t launch_scan(const uint32_t* counts, uint32_t n, uint64_t* offs, uint64_t* stats, cudaStream_t st);
 // row-count pipeline (me_fused.cu): K0 rows [g0, g0 + n_rows) of the range
 // [lo, hi) with their survivor counts (rcnt, per 32-row unit ucnt, per
 // capacity into stats[1 + j]); K3 rows with survivors -> output rows
