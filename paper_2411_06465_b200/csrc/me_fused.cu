@@ -156,7 +156,7 @@ __device__ __forceinline__ void count_le_f(const uint32_t* __restrict__ su, uint
             base = half && v <= x ? base + half : base;
             len -= half;
         }
-        out[j] = lo < n ? lo + base + (su[lo + base] <= x ? 1u : 0u) : n;
+        out[j] = lo < n ? lo + base + (su[min(lo + base, n - 1)] <= x ? 1u : 0u) : n;  // (index clamped: no load past the pool)
         ME_CHECK(out[j] <= n);
     }
 }
