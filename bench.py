@@ -433,8 +433,11 @@ def main():
                                         "duration_ms": v.get("duration_ms")}
         k0 = issue.get("count", {}).get("rowcount_kernel")
         if mode == me.ME_OUT_COUNT and k0:
-            roof.update({"achieved": k0["warp_instr"] / (k0["duration_ms"] / 1e3), "unit": "warp-instr/s",
-                         "frac": k0["issue_frac"], "traffic_note": "K0 alone (ncu, chunk 40, COUNT mode)"})
+            ach = k0["warp_instr"] / (k0["duration_ms"] / 1e3)
+            roof.update({"achieved": ach, "unit": "warp-instr/s", "frac": k0["issue_frac"],
+                         "peak": ach / k0["issue_frac"] if k0["issue_frac"] else None,
+                         "peak_source": "148 SMs x 4 SMSPs x 1 warp-instruction per cycle at the capture's clock",
+                         "traffic_note": "K0 alone (ncu, chunk 40, COUNT mode)"})
     line = {
         "metric": "estimator configs/sec", "value": value, "unit": "configs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -451,8 +454,8 @@ def main():
         "kernel_ms_per_step": {"rows_K0": rows_ms / args.steps, "scan": scan_ms / args.steps,
                                "output_K3": out_ms / args.steps},
         "roofline": roof,
-        # per call: K0 rows, scan, K3 (COUNT: K0, scan); + the join kernel per step (N > 1)
-        "gpu_launches": (3 if mode != me.ME_OUT_COUNT else 2) * n_launch + (args.steps if cyclic else 0),
+        # per call: K0 rows, scan, K3 (COUNT: K0 alone); + the join kernel per step (N > 1)
+        "gpu_launches": (3 if mode != me.ME_OUT_COUNT else 1) * n_launch + (args.steps if cyclic else 0),
         "clocks": clocks.summary(),
     }
     if issue:
