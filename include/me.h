@@ -286,8 +286,9 @@ int me_result_status(me_result* r);
 /* wait for the result's work on its stream to finish */
 int me_result_wait(me_result* r);
 /* device time in ms from CUDA events: [0] whole sweep, [1] K0 rows + counts
- * (plan stream), [2] scan, [3] K3 output kernel (0 when not run), summed over
- * the sub-ranges.  Waits. */
+ * (plan stream; COUNT mode: the caller's stream), [2] scan (~0 in COUNT mode:
+ * K0 sums the counts itself), [3] K3 output kernel (0 when not run), summed
+ * over the sub-ranges.  Waits. */
 int me_result_timing(me_result* r, float* ms4);
 void me_result_free(me_result* r);
 
