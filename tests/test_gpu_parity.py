@@ -392,6 +392,27 @@ def test_count_mode_variants(me, oracle_mod, monkeypatch, env):
             assert_same(me, res, *oracle_rows(oracle_mod, sp, b, e), me.ME_OUT_COUNT)
 
 
+@pytest.mark.parametrize("n_mbs,seq", [(1, [4096]), (7, [4096]), (8, [4096]), (9, [4096]), (31, [4096]),
+                                       (32, [4096]), (11, [4096, 8192, 16384]), (64, [4096, 8192]),
+                                       (43, [4096, 8192, 16384]), (16, [1024, 2048, 4096, 8192, 16384, 32768])],
+                         ids=["n1", "n7", "n8", "n9", "n31", "n32", "n33", "n128", "n129", "n96"])
+def test_fence_boundaries(me, oracle_mod, n_mbs, seq):
+    """K0's search index over each pool's sorted u values (groups of 32,
+    blocks of 8; pools over 128 pairs fall back to a plain binary search):
+    pools of 1, 7, 8, 9, 31, 32, 33, 96, 128 and 129 pairs, every count and
+    every row equal to the oracle's, on the whole space and on a ragged range,
+    in COUNT and RECORDS."""
+    sp = mi.Space(models=mi.random_models(3, seed=29), world=[8, 16], caps_gb=[24, 40, 80, 192],
+                  mbs=list(range(1, n_mbs + 1)), seq=seq, uneven=1)
+    plan = me.Plan(sp)
+    for b, e in ((0, 0), (5, plan.size - 3)):
+        ref = oracle_rows(oracle_mod, sp, b, e)
+        for mode in (me.ME_OUT_COUNT, me.ME_OUT_RECORDS):
+            res = plan.sweep(b, e, mode=mode)
+            assert res.status() == 0
+            assert_same(me, res, *ref, mode)
+
+
 @pytest.mark.parametrize("max_rows", [1, 64, 1000])
 def test_subranges_cut_by_rows(me, oracle_mod, monkeypatch, max_rows):
     """Sub-ranges are also cut at max_rows rows (2^21 in production; a small
