@@ -75,6 +75,10 @@ constexpr uint32_t kRowThreads = 128;
 #define ME_K0_COUNT_MINB 6
 #endif
 constexpr int kRowMinbCount = ME_K0_COUNT_MINB;  // count-only K0: resident blocks per SM (register budget)
+#ifndef ME_K0_WRITE_MINB
+#define ME_K0_WRITE_MINB 8
+#endif
+constexpr int kRowMinbWrite = ME_K0_WRITE_MINB;  // K0 with row entries: 8 = 64 registers
 
 // The survivor bound of one digit: the largest u with ms + u K <= thr, i.e.
 // floor((thr - ms) / K), clamped to 2^32 - 1 (u is 32-bit); 0 when thr < ms
@@ -827,7 +831,8 @@ void* rowcount_fn_(uint32_t n_cap) {
 void* rowcount_fn(uint32_t n_cap, bool caps, bool wr, bool smem) {
     if (!wr) return smem ? rowcount_fn_<true, false, kRowMinbCount, true>(n_cap)
                          : rowcount_fn_<true, false, kRowMinbCount, false>(n_cap);
-    return caps ? rowcount_fn_<true, true, 8, false>(n_cap) : rowcount_fn_<false, true, 8, false>(n_cap);
+    return caps ? rowcount_fn_<true, true, kRowMinbWrite, false>(n_cap)
+                : rowcount_fn_<false, true, kRowMinbWrite, false>(n_cap);
 }
 // count-only K0 stages the sorted-u lists when they fit the default 48 KB
 size_t rowcount_smem(const DevSpace& S) {
