@@ -122,6 +122,7 @@ struct me_plan {
     int k3_caps[4] = {1, 1, 1, 1};      // per output mode: per-capacity counts in K3 (1) or K0 (0) (ME_K3_CAPS)
     int fused_minb[4] = {2, 3, 2, 3};   // K3 register budget per output mode: 2 or 3 blocks per SM
     int k0_bps = 0;                     // count-only K0: grid-stride blocks per SM (ME_K0_BPS; 0 = resident)
+    int k0_wbps = 0;                    // K0 with row entries: the same (ME_K0_WBPS; 0 = one block per 128 rows)
                                         // (measured on C5: records 3 -> 351 ms/step, 2 -> 358; INDEX
                                         // 3 -> 193, 2 -> 220 despite a few spilled registers; FULL
                                         // spills more at 3; ME_FUSED_MINB)
@@ -317,6 +318,7 @@ static int plan_create(const me_model_range* models, const me_cluster* cluster, 
     if (const char* e = getenv("ME_K0_SMEM")) D.k0_smem = (uint32_t)atoi(e);
     P->k0_bps = rowcount_blocks_per_sm(D);
     if (const char* e = getenv("ME_K0_BPS")) P->k0_bps = atoi(e) > 0 ? atoi(e) : 0;  // 0: one block per 128 rows
+    if (const char* e = getenv("ME_K0_WBPS")) P->k0_wbps = std::max(0, atoi(e));
     if (const char* e = getenv("ME_SETS")) P->n_sets = (uint32_t)std::min(std::max(atoi(e), 2), (int)kMaxSets);
     const uint32_t max_units = fused_units_of(P->max_rows) + 1;
     for (uint32_t si = 0; si < P->n_sets; si++) {
@@ -513,7 +515,8 @@ static int run_pipeline(me_plan* P, me_result* R, uint64_t* stats, uint64_t b, u
         cudaEventRecord(tev[0], cs);
         cudaError_t ce;
         ce = launch_rowcount(P->ds, g0, n_rows, seg_lo, n_seg_sub, lo, hi, sc.rows, sc.st, sc.rcnt, sc.ucnt,
-                             stats, !write || !P->k3_caps[mode], write, (uint32_t)(P->sms * P->k0_bps), cs);
+                             stats, !write || !P->k3_caps[mode], write,
+                             (uint32_t)(P->sms * (write ? P->k0_wbps : P->k0_bps)), cs);
         if (ce != cudaSuccess) return cuda_err(ce, "row kernel");
         cudaEventRecord(tev[1], cs);
         if (write) {

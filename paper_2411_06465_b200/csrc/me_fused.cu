@@ -857,7 +857,7 @@ cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uin
                             uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
                             uint64_t* stats, bool caps, bool write, uint32_t max_blocks, cudaStream_t stream) {
     uint32_t blocks = (n_rows + kRowThreads - 1) / kRowThreads;
-    if (!write && max_blocks && blocks > max_blocks) blocks = max_blocks;
+    if (max_blocks && blocks > max_blocks) blocks = max_blocks;
     void* args[] = {(void*)&S,  (void*)&g0,   (void*)&n_rows, (void*)&seg_lo, (void*)&n_seg_sub, (void*)&lo,
                     (void*)&hi, (void*)&rows, (void*)&st,     (void*)&rcnt,   (void*)&ucnt,      (void*)&stats};
     const size_t smem = write ? 0 : rowcount_smem(S);

@@ -268,8 +268,8 @@ cudaError_t launch_scan(const uint32_t* counts, uint32_t n, uint64_t* offs, uint
 // capacity into stats[1 + j]); K3 rows with survivors -> output rows
 // caps: K0 also counts every capacity; otherwise K3 does.  !write (COUNT
 // mode, the sizing pass): K0 alone, totals only (stats[0] and every
-// capacity; no row entries, no unit counts, no scan needed), in at most
-// max_blocks grid-stride blocks (0: one per 128 rows)
+// capacity; no row entries, no unit counts, no scan needed); either way in
+// at most max_blocks grid-stride blocks (0: one per 128 rows)
 cudaError_t launch_rowcount(const DevSpace& S, uint64_t g0, uint32_t n_rows, uint32_t seg_lo, uint32_t n_seg_sub,
                             uint64_t lo, uint64_t hi, RowEnt* rows, StEnt* st, uint32_t* rcnt, uint32_t* ucnt,
                             uint64_t* stats, bool caps, bool write, uint32_t max_blocks, cudaStream_t stream);
