@@ -620,13 +620,14 @@ __device__ __forceinline__ void fused_row_pairs(const DevSpace& S, const RowEnt&
         const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c & 2u),
                        b2 = __ballot_sync(0xffffffffu, c & 4u);
         const uint32_t lt = (1u << lane) - 1u;
-        uint32_t at = run + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
-        while (m4) {
-            const uint32_t sel = __ffs(m4) - 1;
-            m4 &= m4 - 1;
-            ME_CHECK(at < kRowPairs * 4);
-            slist[at++] = (uint16_t)(j << 2 | sel);
-        }
+        const uint32_t at = run + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+        // the pair's survivor codes in digit order: predicated stores, no loop
+#pragma unroll
+        for (uint32_t sel = 0; sel < 4; sel++)
+            if ((m4 >> sel) & 1u) {
+                ME_CHECK(at + __popc(m4 & ((1u << sel) - 1u)) < kRowPairs * 4);
+                slist[at + __popc(m4 & ((1u << sel) - 1u))] = (uint16_t)(j << 2 | sel);
+            }
         run += __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
     }
     __syncwarp();
